@@ -1,0 +1,130 @@
+/*
+ * vm_oracle.h — C interface of the CPU ORACLE (test infrastructure only).
+ *
+ * Two libraries implement this interface with identical semantics:
+ *   vmr_*  oracle/_ref/libvoxmarch_ref.so  — the reference's own C++ sources
+ *          (the .cpp files under /root/reference/proj/src, compiled in place by oracle/Makefile)
+ *          wrapped by oracle/ref_capi.cpp;
+ *   vmo_*  oracle/_build/libvm_oracle.so   — oracle/vm_oracle.c, a plain-C
+ *          restatement of the same algorithms, pinned against vmr_* and the
+ *          reference's known-answer tests (tests/test_oracle_*.py).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+ * arm may load these libraries. The product path (paper_2210_04847_b200/) never
+ * links or calls them.
+ *
+ * All vectors are AoS doubles (x,y,z per element) exactly like std::vector<Vec3>
+ * in the reference (proj/include/voxmarch/math.hpp:9-14).
+ * Functions return VMB_* status codes (include/vmb200_types.h); the message of
+ * the last failure is available from *_last_error() and equals the reference's
+ * exception text byte for byte.
+ */
+#ifndef VM_ORACLE_H
+#define VM_ORACLE_H
+
+#include "../include/vmb200_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Owning result of march()/march_uniform(): PackedSamples (core_types.hpp:29-38)
+ * plus MarchStats. Free with *_packed_free. */
+typedef struct vmo_packed {
+    uint64_t n_rays;
+    uint64_t n_samples;
+    uint32_t* offsets;
+    uint32_t* counts;
+    double* t_starts;
+    double* t_ends;
+    uint32_t* ray_indices;
+    uint64_t samples_emitted;
+    uint64_t samples_kept;
+} vmo_packed;
+
+typedef struct vmo_grid vmo_grid;
+
+/* Host density callback for OccupancyGrid::update_over_time (occupancy_grid.hpp:16-17):
+ * fills out[0..n) for points[3*n]; returns the number of values produced
+ * (a value != n reproduces the "wrong batch size" error). */
+typedef int64_t (*vmo_density_cb)(void* user, const double* points, uint64_t n, double t,
+                                  double* out);
+/* Host sigma callback for march (ray_marching.hpp:21-24), called once per ray with
+ * that ray's emitted candidates; returns the number of sigmas written to out
+ * (capacity n + 16). */
+typedef int64_t (*vmo_sigma_cb)(void* user, const double* t_starts, const double* t_ends,
+                                const uint32_t* ray_indices, uint64_t n, double* out);
+
+#define VMO_DECLARE(P)                                                                          \
+    const char* P##_last_error(void);                                                           \
+    void P##_packed_free(vmo_packed* p);                                                        \
+    uint64_t P##_uniform_step_count(double near_, double far_, double step);                    \
+    int P##_pack(const uint32_t* counts, uint64_t n_rays, uint32_t* offsets,                    \
+                 uint32_t* ray_indices, uint64_t ray_indices_capacity, uint64_t* total);        \
+    int P##_validate(const uint32_t* offsets, uint64_t n_offsets, const uint32_t* counts,       \
+                     uint64_t n_counts, const double* t_starts, uint64_t n_ts,                  \
+                     const double* t_ends, uint64_t n_te, const uint32_t* ray_indices,          \
+                     uint64_t n_idx);                                                           \
+    int P##_contract(const vmb_contraction* c, const double* x, uint64_t n, double* out);      \
+    int P##_invert_grid_point(const vmb_contraction* c, const double* g, uint64_t n,            \
+                              double* out, uint8_t* valid);                                     \
+    int P##_grid_create(uint32_t resolution, const vmb_contraction* c, double alpha_threshold,  \
+                        double reference_step, double initial_density, vmo_grid** out);         \
+    void P##_grid_destroy(vmo_grid* g);                                                         \
+    int P##_grid_update_field(vmo_grid* g, const vmb_field* f, const double* timestamps,        \
+                              uint64_t n_timestamps, double ema_decay, int has_seed,            \
+                              uint64_t seed);                                                   \
+    int P##_grid_update_callback(vmo_grid* g, vmo_density_cb cb, void* user,                    \
+                                 const double* timestamps, uint64_t n_timestamps,               \
+                                 double ema_decay, int has_seed, uint64_t seed);                \
+    int P##_grid_seed_mask(vmo_grid* g, const uint8_t* occupied);                               \
+    int P##_grid_get(const vmo_grid* g, uint8_t* bits, double* cache);                          \
+    int P##_grid_info(const vmo_grid* g, uint32_t* resolution, double* alpha_threshold,         \
+                      double* reference_step, double* threshold_density,                        \
+                      double* occupied_fraction);                                               \
+    int P##_grid_query(const vmo_grid* g, const double* points, uint64_t n, uint8_t* out);      \
+    int P##_grid_save(const vmo_grid* g, const char* path);                                     \
+    int P##_grid_load(const char* path, vmo_grid** out);                                        \
+    int P##_march_field(const double* origins, const double* dirs, uint64_t n_rays,             \
+                        double near_, double far_, const vmo_grid* g, const vmb_field* f,       \
+                        const vmb_march_config* cfg, int n_threads, vmo_packed** out);          \
+    int P##_march_callback(const double* origins, const double* dirs, uint64_t n_rays,          \
+                           double near_, double far_, const vmo_grid* g, vmo_sigma_cb cb,       \
+                           void* user, const vmb_march_config* cfg, int n_threads,              \
+                           vmo_packed** out);                                                   \
+    int P##_march_uniform(const double* origins, const double* dirs, uint64_t n_rays,           \
+                          double near_, double far_, const vmb_march_config* cfg,               \
+                          vmo_packed** out);                                                    \
+    int P##_shade(const double* origins, const double* dirs, const uint32_t* ray_indices,       \
+                  const double* t_starts, const double* t_ends, uint64_t n_samples,             \
+                  const vmb_field* f, double* rgbs, double* sigmas);                            \
+    int P##_transmittance(const uint32_t* offsets, const uint32_t* counts, uint64_t n_rays,     \
+                          const double* t_starts, const double* t_ends, uint64_t n_samples,     \
+                          const double* sigmas, double* out);                                   \
+    int P##_render_forward(const uint32_t* offsets, const uint32_t* counts, uint64_t n_rays,    \
+                           const double* t_starts, const double* t_ends, uint64_t n_samples,    \
+                           const double* rgbs, const double* sigmas, int n_threads,             \
+                           double* color, double* opacity, double* depth);                      \
+    int P##_render_backward(const uint32_t* offsets, const uint32_t* counts, uint64_t n_rays,   \
+                            const double* t_starts, const double* t_ends, uint64_t n_samples,   \
+                            const double* rgbs, const double* sigmas, const double* d_color,    \
+                            const double* d_opacity, const double* d_depth, int n_threads,      \
+                            double* d_rgbs, double* d_sigmas);                                  \
+    int P##_render_attribute(const uint32_t* offsets, const uint32_t* counts, uint64_t n_rays,  \
+                             const double* t_starts, const double* t_ends, uint64_t n_samples,  \
+                             const double* sigmas, const double* values, uint64_t n_values,     \
+                             uint64_t dim, double* out);                                        \
+    int P##_train_step(const double* origins, const double* dirs, uint64_t n_rays,              \
+                       double near_, double far_, const vmo_grid* g, const vmb_field* f,        \
+                       const vmb_march_config* cfg, const double* d_color,                      \
+                       const double* d_opacity, const double* d_depth, int n_threads,           \
+                       double* phase_ms, uint64_t* n_samples_out, double* checksum);
+
+VMO_DECLARE(vmo)
+VMO_DECLARE(vmr)
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VM_ORACLE_H */
