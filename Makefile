@@ -1,0 +1,42 @@
+# Top-level build (invoked by __graft_entry__.build()).
+#
+#   paper_2210_04847_b200/lib/libvoxmarch_b200.so  — CUDA kernels + C ABI (sm_100a)
+#   paper_2210_04847_b200/lib/libvoxmarch_cpp.so   — C++ drop-in facade (namespace voxmarch)
+#   build/vm_cpp_tests                              — C++ facade tests (run under pytest -m gpu)
+#   oracle/_build, oracle/_ref                      — CPU oracle (test infrastructure)
+#
+# The decision path is compiled with --fmad=false (and the host side with
+# -ffp-contract=off) so every fp64 expression rounds exactly like the reference.
+NVCC     ?= /usr/local/cuda/bin/nvcc
+CXX      ?= g++
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+PKG      := paper_2210_04847_b200
+SRC      := $(PKG)/csrc
+LIB      := $(PKG)/lib
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC \
+            -Xcompiler -ffp-contract=off -Xptxas -v -Iinclude
+CU_SRCS  := $(SRC)/runtime.cu $(SRC)/scan.cu $(SRC)/grid.cu $(SRC)/march.cu $(SRC)/render.cu
+CU_OBJS  := $(patsubst $(SRC)/%.cu,build/obj/%.o,$(CU_SRCS))
+HDRS     := $(SRC)/vm_internal.h $(SRC)/vm_exact.cuh include/vmb200.h include/vmb200_types.h
+
+.PHONY: all oracle clean
+all: $(LIB)/libvoxmarch_b200.so oracle
+
+build/obj/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p build/obj
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/obj/$*.ptxas.log || (cat build/obj/$*.ptxas.log; false)
+
+build/obj/comm.o: $(SRC)/comm.cpp $(HDRS)
+	@mkdir -p build/obj
+	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@ 2> build/obj/comm.ptxas.log || (cat build/obj/comm.ptxas.log; false)
+
+$(LIB)/libvoxmarch_b200.so: $(CU_OBJS) build/obj/comm.o
+	@mkdir -p $(LIB)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -ldl -lpthread
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -C oracle clean

@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path: march + render forward + render backward.
+
+One STEP = one training-step pass of the path over one batch of synthetic rays
+(BASELINE.json config 5: 2^22 rays of the reference CLI's bench camera, 128^3
+occupancy grid warmed by 16 jittered updates, SolidSphere r=0.2 sigma=200,
+step 5e-3, alpha_thre 1e-2, early_stop_eps 1e-4):
+
+    march (fused traversal + density + alpha floor + T cut + packing)
+    -> shade (analytic field rgb/sigma at each sample; harness)
+    -> render_forward -> render_backward (upstream grads U(-1,1))
+
+Multi-GPU (torchrun): each rank marches its own 2^22-ray batch (weak scaling, its
+own camera angle) against a replicated grid; rank 0 prints one JSON line with the
+max-over-ranks device time. The grid warm-up runs the sharded probe +
+ncclAllReduce(max) path. `--impl reference` times the reference's own CPU code
+(oracle/_ref) on a bounded sample on the host cores.
+"""
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE_METRIC = "rays/sec & samples/sec (march+render fwd+bwd) at 1/2/4/8 B200; % HBM roofline"
+SCENE = dict(center=(0.5, 0.5, 0.5), radius=0.2, sigma=200.0, rgb=(0.8, 0.25, 0.25))
+KERNELS_PER_STEP = 8  # march count, scan x3, march fill, shade, forward, backward
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--width", type=int, default=2048, help="rays per side (2048 -> 2^22 rays)")
+    ap.add_argument("--resolution", type=int, default=128)
+    ap.add_argument("--step-size", type=float, default=5e-3)
+    ap.add_argument("--cpu-baseline", type=int, default=1)
+    ap.add_argument("--cpu-sample-rays", type=int, default=1 << 20)
+    ap.add_argument("--ref-sample-rays", type=int, default=1 << 18)
+    ap.add_argument("--phases", type=int, default=1, help="per-phase event timing pass")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------- plumbing
+class Dist:
+    """torch.distributed (gloo) used only as host plumbing: id exchange, barrier, max."""
+
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        if not self.dist:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v: float) -> float:
+        if not self.dist:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def bcast_bytes(self, b: bytes) -> bytes:
+        if not self.dist:
+            return b
+        obj = [b]
+        self.dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+
+class Clocks:
+    """nvidia-smi sampler (every 200 ms) around the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.rows = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 9 for i in range(4)
+                          if r[5 + i].lower().startswith("active")})
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------- CPU legs
+def reference_grid(orc, res):
+    from oracle import oracle as O
+    from paper_2210_04847_b200 import workload
+    g = orc.grid(res, O.Contraction.aabb())
+    for s in workload.grid_warmup_seeds(16, 5):
+        g.update_field(O.Field.sphere(**SCENE), 0.95, s)
+    return g
+
+
+def cpu_step(orc, grid, o, d, step_size, threads, seed=113):
+    from oracle import oracle as O
+    from paper_2210_04847_b200 import workload
+    dc, do, dd = workload.upstream_grads(len(o), seed)
+    cfg = O.MarchConfig(step_size, 1e-4, 1e-2)
+    t0 = time.perf_counter()
+    phase, ns, _ = orc.train_step(o, d, 0.2, 1.0, grid, O.Field.sphere(**SCENE), cfg, dc, do, dd, threads)
+    return time.perf_counter() - t0, ns, phase
+
+
+def cpu_baseline(args, o, d):
+    """Reference CPU path (oracle/_ref, else the C port) on a strided sample of the batch."""
+    from oracle import Oracle, available
+    kind = "reference" if available("ref") else "port"
+    orc = Oracle("ref" if kind == "reference" else "port")
+    threads = (os.cpu_count() or 1) if kind == "reference" else 1
+    grid = reference_grid(orc, args.resolution)
+    stride = max(1, len(o) // args.cpu_sample_rays)
+    so, sd = o[::stride], d[::stride]
+    times = []
+    for _ in range(3):
+        dt, ns, _ = cpu_step(orc, grid, so, sd, args.step_size, threads)
+        times.append(dt)
+    dt = statistics.median(times)
+    return {"value": len(so) / dt, "unit": "rays/s", "cores": threads, "kind": kind,
+            "samples_per_s": ns / dt,
+            "sample": f"every {stride}th ray of the {len(o)}-ray batch ({len(so)} rays), median of 3 "
+                      f"train steps (march+shade+fwd+bwd), {threads} threads, {cpu_model()}"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU implementation, rank 0 only."""
+    dist = Dist()
+    if dist.rank != 0:
+        return
+    from oracle import Oracle, available
+    from paper_2210_04847_b200 import workload
+    kind = "reference" if available("ref") else "port"
+    orc = Oracle("ref" if kind == "reference" else "port")
+    threads = (os.cpu_count() or 1) if kind == "reference" else 1
+    o, d = workload.orbit_rays(args.width)
+    grid = reference_grid(orc, args.resolution)
+    n_sample = min(args.ref_sample_rays, len(o))
+    stride = max(1, len(o) // n_sample)
+    for i in range(args.warmup):
+        cpu_step(orc, grid, o[i % stride::stride], d[i % stride::stride], args.step_size, threads)
+    tot_t, tot_rays, tot_s = 0.0, 0, 0
+    for i in range(args.steps):
+        k = (args.warmup + i) % stride
+        dt, ns, _ = cpu_step(orc, grid, o[k::stride], d[k::stride], args.step_size, threads)
+        tot_t += dt
+        tot_rays += len(o[k::stride])
+        tot_s += ns
+    v = tot_rays / tot_t
+    line = {"impl": "reference", "metric": BASELINE_METRIC, "value": v, "unit": "rays/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "samples_per_s": tot_s / tot_t,
+            "config": {"workload": f"config 5 sample: {n_sample} of {len(o)} orbit-camera rays per step, "
+                                   f"{args.resolution}^3 grid, step {args.step_size}",
+                       "global_batch": n_sample, "parallelism": "cpu threads"},
+            "cpu_baseline": {"value": v, "unit": "rays/s", "cores": threads, "kind": kind,
+                             "sample": f"every {stride}th ray per step, {threads} threads, {cpu_model()}"},
+            "e2e": {"value": v, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    from paper_2210_04847_b200 import api, workload
+    from paper_2210_04847_b200._lib import VMB_F32, Contraction, Field, MarchConfig, Rays, check
+
+    dist = Dist()
+    dev = api.Device(dist.local)
+    L = dev.lib
+    if dist.world > 1:
+        uid = (C.c_char * 128)()
+        if dist.rank == 0:
+            check(L.vmb_comm_unique_id(uid))
+        raw = dist.bcast_bytes(bytes(uid))
+        uid = (C.c_char * 128).from_buffer_copy(raw)
+        check(L.vmb_comm_init(dev.h, uid, dist.world, dist.rank))
+
+    field = Field.sphere(**SCENE)
+    cfg = MarchConfig(args.step_size, 1e-4, 1e-2)
+    R = args.resolution
+    grid = api.OccupancyGrid(R, Contraction.aabb(), dev=dev)
+    seeds = workload.grid_warmup_seeds(16, 5)
+    dev.record(10)
+    for s in seeds:
+        grid.update_field(field, 0.95, s)  # sharded probes + ncclAllReduce(max) when N > 1
+    dev.record(11)
+    grid_update_ms = dev.elapsed_ms(10, 11) / len(seeds)
+
+    angle = 2.0 * math.pi * dist.rank / max(dist.world, 1)
+    o64, d64 = workload.orbit_rays(args.width, angle=angle)
+    N = len(o64)
+    o32, d32 = o64.astype(np.float32), d64.astype(np.float32)
+    dc, do, dd = workload.upstream_grads(N, 113 + dist.rank)
+    do_, dd_ = dev.upload(o32), dev.upload(d32)
+    rays = Rays(do_.ptr, dd_.ptr, VMB_F32, 0, N, 0.2, 1.0)
+    check(L.vmb_rays_validate(dev.h, C.byref(rays)))
+    up_c, up_o, up_d = dev.upload(dc.astype(np.float32)), dev.upload(do.astype(np.float32)), \
+        dev.upload(dd.astype(np.float32))
+    packed = api.DevicePacked.allocate(dev, N, 8 * N)
+    packed = api.march_device(dev, grid, rays, field, cfg, packed)
+    S0 = packed.n_samples
+    cap = packed.capacity
+    rgb, sig = dev.empty(cap * 3, np.float32), dev.empty(cap, np.float32)
+    g_rgb, g_sig = dev.empty(cap * 3, np.float32), dev.empty(cap, np.float32)
+    col, op, dep = dev.empty(N * 3, np.float32), dev.empty(N, np.float32), dev.empty(N, np.float32)
+
+    def step():
+        api.march_device(dev, grid, rays, field, cfg, packed)
+        api.shade_device(dev, rays, field, packed, rgb, sig)
+        api.render_forward_device(dev, packed, rgb, sig, col, op, dep)
+        api.render_backward_device(dev, packed, rgb, sig, up_c, up_o, up_d, g_rgb, g_sig)
+
+    clocks = Clocks(dist.local)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    dev.sync()
+    dist.barrier()
+    dev.record(0)
+    for _ in range(args.steps):
+        step()
+    dev.record(1)
+    dev.sync()
+    dist.barrier()
+    ms_total = dev.elapsed_ms(0, 1)
+    # keep the GPU loaded ~1 s more so the clock sampler sees the steady state
+    t_end = time.time() + 1.2
+    while time.time() < t_end:
+        step()
+    dev.sync()
+    clk = clocks.stop()
+
+    S = packed.n_samples
+    ms_step = dist.max(ms_total / args.steps)
+    total_rays = dist.sum(float(N))
+    total_samples = dist.sum(float(S))
+    value = total_rays / (ms_step * 1e-3)
+
+    # per-phase device timing (one more pass, events between phases)
+    phase = {}
+    if args.phases:
+        acc = np.zeros(4)
+        for _ in range(args.steps):
+            dev.record(2)
+            api.march_device(dev, grid, rays, field, cfg, packed)
+            dev.record(3)
+            api.shade_device(dev, rays, field, packed, rgb, sig)
+            dev.record(4)
+            api.render_forward_device(dev, packed, rgb, sig, col, op, dep)
+            dev.record(5)
+            api.render_backward_device(dev, packed, rgb, sig, up_c, up_o, up_d, g_rgb, g_sig)
+            dev.record(6)
+            acc += [dev.elapsed_ms(2 + i, 3 + i) for i in range(4)]
+        acc /= args.steps
+        phase = dict(zip(["march", "shade", "render_forward", "render_backward"], acc.tolist()))
+
+    # roofline (HBM). Algorithmic bytes per SURVEY §8(d): rays f32 (24 B), packed_info
+    # 8 B/ray, t's f64 + ray index (20 B/sample), rgb+sigma f32 (16 B), outputs f32.
+    pk = peaks()
+    peak = pk.get("hbm_gbs", 6650.0)
+    peak_src = "measured" if "hbm_gbs" in pk else "fallback"
+    bytes_march = 24 * N + 8 * N + 20 * S + R ** 3 / 8
+    bytes_fwd = 8 * N + 32 * S + 20 * N
+    bytes_bwd = 8 * N + 20 * N + 32 * S + 16 * S
+    bytes_step = 88 * N + 100 * S + R ** 3 / 8
+    dom = max(phase, key=phase.get) if phase else "march"
+    dom_bytes = {"march": bytes_march, "shade": 20 * S + 24 * S + 16 * S,
+                 "render_forward": bytes_fwd, "render_backward": bytes_bwd}[dom]
+    achieved = dom_bytes / (phase.get(dom, ms_step) * 1e-3) / 1e9
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+            "algorithmic_bytes": dom_bytes,
+            "step": {"algorithmic_bytes": bytes_step,
+                     "achieved": bytes_step / (ms_step * 1e-3) / 1e9,
+                     "frac": bytes_step / (ms_step * 1e-3) / 1e9 / peak}}
+
+    # e2e: host buffers in, result out, through the C ABI (pinned host staging)
+    e2e = None
+    try:
+        hb = {}
+        for name, arr in (("o", o32), ("d", d32), ("dc", dc.astype(np.float32)),
+                          ("do", do.astype(np.float32)), ("dd", dd.astype(np.float32))):
+            p = C.c_void_p()
+            check(L.vmb_host_alloc(arr.nbytes, C.byref(p)))
+            C.memmove(p.value, arr.ctypes.data, arr.nbytes)
+            hb[name] = (p, arr.nbytes)
+        out_bytes = N * 4 * 5
+        p_out = C.c_void_p()
+        check(L.vmb_host_alloc(out_bytes, C.byref(p_out)))
+        dst = [(do_, "o"), (dd_, "d"), (up_c, "dc"), (up_o, "do"), (up_d, "dd")]
+
+        def e2e_step():
+            for darr, k in dst:
+                check(L.vmb_memcpy_h2d(dev.h, darr.ptr, hb[k][0], hb[k][1]))
+            step()
+            check(L.vmb_memcpy_d2h(dev.h, p_out, col.ptr, N * 12))
+            check(L.vmb_memcpy_d2h(dev.h, p_out.value + N * 12, op.ptr, N * 4))
+            check(L.vmb_memcpy_d2h(dev.h, p_out.value + N * 16, dep.ptr, N * 4))
+
+        for _ in range(2):
+            e2e_step()
+        dist.barrier()
+        t0 = time.perf_counter()
+        dev.record(7)
+        for _ in range(args.steps):
+            e2e_step()
+        dev.record(8)
+        dev.sync()
+        e2e_ms = dist.max(dev.elapsed_ms(7, 8) / args.steps)
+        h2d = sum(v[1] for v in hb.values())
+        e2e = {"value": total_rays / (e2e_ms * 1e-3), "unit": "rays/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": out_bytes,
+               "path": "C ABI vmb_* with pinned host rays+upstream grads in, color/opacity/depth out"}
+        for v in hb.values():
+            L.vmb_host_free(v[0])
+        L.vmb_host_free(p_out)
+    except Exception as ex:  # pragma: no cover
+        e2e = {"error": str(ex)}
+
+    cpu = None
+    if dist.rank == 0 and dist.world == 1 and args.cpu_baseline:
+        try:
+            cpu = cpu_baseline(args, o64, d64)
+        except Exception as ex:  # pragma: no cover
+            cpu = {"error": str(ex)}
+
+    if dist.rank == 0:
+        line = {"metric": BASELINE_METRIC, "value": value, "unit": "rays/s", "n_gpus": dist.world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "samples_per_s": total_samples / (ms_step * 1e-3),
+                "config": {"workload": f"config 5: {N} orbit-camera rays/GPU (W={args.width}), "
+                                       f"{R}^3 grid (16 jittered warm-up updates), SolidSphere r=0.2 "
+                                       f"sigma=200, step {args.step_size}, alpha 1e-2, eps 1e-4",
+                           "rays_per_gpu": N, "samples_per_gpu": S, "resolution": R,
+                           "storage": "rays/rgb/sigma/outputs f32, t f64, compute f64",
+                           "l2": "inputs larger than L2 (~1 GB working set per step)",
+                           "parallelism": f"dp{dist.world} (rays sharded, grid replicated)"},
+                "phases_ms": phase, "grid_update_ms": grid_update_ms,
+                "roofline": roof, "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
+                "gpu_launches": KERNELS_PER_STEP * args.steps}
+        print(json.dumps(line), flush=True)
+    if dist.world > 1:
+        L.vmb_comm_destroy(dev.h)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,238 @@
+/*
+ * vmb200.h — C ABI of the B200-native volumetric-rendering hot path
+ * (library: paper_2210_04847_b200/lib/libvoxmarch_b200.so, sm_100a).
+ *
+ * This is the drop-in boundary for the reference's hot path. The reference
+ * (voxmarch, /root/reference/proj) has no plugin registry: its boundary is the
+ * public C++ headers in namespace voxmarch. Each entry point below
+ * names the reference function it replaces; include/voxmarch/voxmarch.hpp is
+ * the C++ facade that restores the reference's exact signatures, value types
+ * and exception messages on top of these calls.
+ *
+ * Conventions
+ *  - Plain pointers + sizes only. Pointers named d_* are DEVICE pointers (from
+ *    vmb_malloc or any CUDA allocation on the context's device); h_* are host.
+ *  - Every call returns a VMB_* status (vmb200_types.h); vmb_last_error()
+ *    returns the thread-local message, which for VMB_INVALID_ARGUMENT and
+ *    VMB_RUNTIME equals the reference's exception text byte for byte.
+ *  - Work is enqueued on the context's CUDA stream. Calls that return a host
+ *    value computed on the device (totals, error checks) synchronize that stream.
+ *  - Packed samples use the reference layout (core_types.hpp:29-38): offsets,
+ *    counts (u32, per ray), t_starts, t_ends (f64, per sample), ray_indices (u32).
+ *  - Ray origins/directions are AoS xyz (like std::vector<Vec3>) in f32 or f64
+ *    (vmb_rays.dtype); attribute / output arrays are f32 or f64 (dtype args).
+ *    All arithmetic is fp64 regardless.
+ *  - n_threads of the reference API has no equivalent: results never depend on
+ *    the launch configuration (the reference's determinism contract, parallel.hpp:17-19).
+ */
+#ifndef VMB200_H
+#define VMB200_H
+
+#include "vmb200_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct vmb_ctx vmb_ctx;   /* device, stream, scratch, error record, optional NCCL comm */
+typedef struct vmb_grid vmb_grid; /* device-resident OccupancyGrid */
+
+/* Ray batch on the device; replaces voxmarch::RayBatch (core_types.hpp:15-25). */
+typedef struct vmb_rays {
+    const void* d_origins;    /* [n_rays][3] */
+    const void* d_directions; /* [n_rays][3], unit length */
+    int32_t dtype;            /* VMB_F32 | VMB_F64 */
+    int32_t pad_;
+    uint64_t n_rays;
+    double near_plane;
+    double far_plane;
+} vmb_rays;
+
+/* Caller-owned output of march(); replaces voxmarch::PackedSamples. */
+typedef struct vmb_samples {
+    uint32_t* d_offsets;      /* [n_rays] */
+    uint32_t* d_counts;       /* [n_rays] */
+    double* d_t_starts;       /* [capacity] */
+    double* d_t_ends;         /* [capacity] */
+    uint32_t* d_ray_indices;  /* [capacity] */
+    uint64_t capacity;
+} vmb_samples;
+
+/* Read-only view of packed samples (input of the rendering calls). */
+typedef struct vmb_packed_view {
+    const uint32_t* d_offsets;
+    const uint32_t* d_counts;
+    uint64_t n_rays;
+    const double* d_t_starts;
+    const double* d_t_ends;
+    uint64_t n_samples;
+} vmb_packed_view;
+
+/* ------------------------------------------------------------------ runtime */
+const char* vmb_last_error(void);
+const char* vmb_version(void);
+int vmb_device_count(int* h_count);
+int vmb_ctx_create(int device, vmb_ctx** out);
+int vmb_ctx_destroy(vmb_ctx* ctx);
+int vmb_ctx_set_stream(vmb_ctx* ctx, void* cuda_stream); /* NULL restores the owned stream */
+void* vmb_ctx_stream(vmb_ctx* ctx);
+int vmb_ctx_synchronize(vmb_ctx* ctx);
+int vmb_malloc(vmb_ctx* ctx, uint64_t bytes, void** d_out);
+int vmb_free(vmb_ctx* ctx, void* d_ptr);
+int vmb_host_alloc(uint64_t bytes, void** h_out); /* pinned */
+int vmb_host_free(void* h_ptr);
+int vmb_memcpy_h2d(vmb_ctx* ctx, void* d_dst, const void* h_src, uint64_t bytes);
+int vmb_memcpy_d2h(vmb_ctx* ctx, void* h_dst, const void* d_src, uint64_t bytes);
+int vmb_memcpy_d2d(vmb_ctx* ctx, void* d_dst, const void* d_src, uint64_t bytes);
+int vmb_memset(vmb_ctx* ctx, void* d_dst, int value, uint64_t bytes);
+/* CUDA events on the context stream (slot 0..31) for device-side timing. */
+int vmb_event_record(vmb_ctx* ctx, int slot);
+int vmb_event_elapsed_ms(vmb_ctx* ctx, int slot_begin, int slot_end, float* h_ms);
+/* Host-only helper (no device work): the contiguous shard of n units owned by
+ * rank — the static split of parallel_for (parallel.hpp:28-35). */
+int vmb_shard_range(uint64_t n, int nranks, int rank, uint64_t* h_begin, uint64_t* h_end);
+
+/* ------------------------------------------------------------------ core types */
+/* RayBatch::create validation (core_types.cpp:9-28): finite rays, |d|-1 <= 1e-6,
+ * far > near >= 0. Synchronizes; the first offending ray is reported. */
+int vmb_rays_validate(vmb_ctx* ctx, const vmb_rays* rays);
+/* uniform_step_count (ray_marching.cpp:51-55). Host-only. */
+uint64_t vmb_uniform_step_count(double near_plane, double far_plane, double step_size);
+/* pack (core_types.cpp:30-48): exclusive scan of counts + ray index expansion.
+ * Synchronizes to return the total; d_ray_indices may be NULL (scan only). */
+int vmb_pack(vmb_ctx* ctx, const uint32_t* d_counts, uint64_t n_rays, uint32_t* d_offsets,
+             uint32_t* d_ray_indices, uint64_t capacity, uint64_t* h_total);
+/* validate (core_types.cpp:50-78): 0 = consistent, else 1..6 = length mismatch,
+ * offset mismatch, non-positive interval, non-monotone t_starts, overlapping
+ * intervals, partition mismatch (first violated invariant in the reference's order). */
+int vmb_validate(vmb_ctx* ctx, const vmb_packed_view* packed, const uint32_t* d_ray_indices,
+                 uint64_t n_offsets, uint64_t n_ray_indices, uint64_t n_t_ends, int* h_result);
+
+/* ------------------------------------------------------------------ contraction */
+/* contract / invert_grid_point (contraction.cpp:24-47) over device point arrays. */
+int vmb_contract(vmb_ctx* ctx, const vmb_contraction* c, const double* d_points, uint64_t n,
+                 double* d_out);
+int vmb_invert_grid_point(vmb_ctx* ctx, const vmb_contraction* c, const double* d_points,
+                          uint64_t n, double* d_out, uint8_t* d_valid);
+
+/* ------------------------------------------------------------------ occupancy grid */
+/* OccupancyGrid ctor (occupancy_grid.cpp:41-56). */
+int vmb_grid_create(vmb_ctx* ctx, uint32_t resolution, const vmb_contraction* c,
+                    double alpha_threshold, double reference_step, double initial_density,
+                    vmb_grid** out);
+int vmb_grid_destroy(vmb_grid* g);
+int vmb_grid_clone(vmb_ctx* ctx, const vmb_grid* src, vmb_grid** out);
+int vmb_grid_info(const vmb_grid* g, uint32_t* h_resolution, vmb_contraction* h_contraction,
+                  double* h_alpha_threshold, double* h_reference_step,
+                  double* h_threshold_density);
+/* update / update_over_time with a device-evaluable analytic field
+ * (occupancy_grid.cpp:91-144; density_batch voxmarch.cpp:211-219; time shift
+ * fields.cpp:264-266). With a communicator attached (vmb_comm_init) each rank
+ * probes its shard of cells and the probes are combined with ncclAllReduce(max)
+ * before the EMA; the resulting grid is bit-identical for any rank count. */
+int vmb_grid_update_field(vmb_ctx* ctx, vmb_grid* g, const vmb_field* f,
+                          const double* h_timestamps, uint64_t n_timestamps, double ema_decay,
+                          int has_seed, uint64_t seed);
+/* Generic host-callback update, step 1: probe points of all invertible cells in
+ * cell order (occupancy_grid.cpp:108-119). d_points needs 3*n_cells doubles,
+ * d_cells n_cells u32. Synchronizes to return the count. */
+int vmb_grid_probe_points(vmb_ctx* ctx, const vmb_grid* g, int has_seed, uint64_t seed,
+                          double* d_points, uint32_t* d_cells, uint64_t* h_count);
+/* step 2 (per timestamp): validate densities and fold them into the running
+ * max (occupancy_grid.cpp:121-140). d_probed (n_cells f64) must start zeroed.
+ * Synchronizes; an invalid density yields VMB_RUNTIME with the reference text. */
+int vmb_grid_accumulate(vmb_ctx* ctx, const vmb_grid* g, const double* d_densities,
+                        const uint32_t* d_cells, uint64_t n, double* d_probed);
+/* step 3: cache = max(cache*decay, probed); refresh bits (occupancy_grid.cpp:142-143).
+ * With a communicator attached, d_probed is first all-reduced (max) across ranks. */
+int vmb_grid_apply(vmb_ctx* ctx, vmb_grid* g, double* d_probed, double ema_decay);
+/* seed_occupancy (occupancy_grid.cpp:152-165) from a per-cell mask (u8, cell order). */
+int vmb_grid_seed_mask(vmb_ctx* ctx, vmb_grid* g, const uint8_t* d_mask);
+/* occupied_fraction numerator (occupancy_grid.cpp:146-150). Synchronizes. */
+int vmb_grid_occupied_count(vmb_ctx* ctx, const vmb_grid* g, uint64_t* h_count);
+/* query (occupancy_grid.cpp:67-76) for n device points; d_out u8. Synchronizes to
+ * report a non-finite point ("non-finite coordinate", contraction.cpp:25). */
+int vmb_grid_query(vmb_ctx* ctx, const vmb_grid* g, const double* d_points, uint64_t n,
+                   uint8_t* d_out);
+/* Host copies of the state: h_bits is the OGRD bit section (ceil(n_cells/8) bytes,
+ * LSB-first, x-fastest; occupancy_grid.cpp:197-204) — identical to the device
+ * layout, so save/load are plain copies. Either pointer may be NULL. */
+int vmb_grid_read(vmb_ctx* ctx, const vmb_grid* g, uint8_t* h_bits, double* h_cache);
+int vmb_grid_write(vmb_ctx* ctx, vmb_grid* g, const uint8_t* h_bits, const double* h_cache);
+const uint32_t* vmb_grid_device_bits(const vmb_grid* g);
+const double* vmb_grid_device_cache(const vmb_grid* g);
+
+/* ------------------------------------------------------------------ ray marching */
+/* march() with the density of a device-evaluable analytic field at each midpoint
+ * (ray_marching.cpp:57-150 with sigma_fn_for, voxmarch.cpp:221-232). Fused:
+ * lattice traversal with empty-space skipping, grid test, inline density,
+ * alpha floor, transmittance cut, packing. Output is bit-identical to the
+ * reference. Synchronizes to return h_n_samples; if out->capacity is smaller,
+ * offsets/counts are still written, no samples are, and VMB_CAPACITY is
+ * returned with *h_n_samples set (call again with a larger buffer).
+ * h_stats may be NULL (then samples_emitted is not computed). */
+int vmb_march_field(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays, const vmb_field* f,
+                    const vmb_march_config* cfg, vmb_samples* out, uint64_t* h_n_samples,
+                    vmb_march_stats* h_stats);
+/* Asynchronous variant for training loops / CUDA graphs: no host round trip.
+ * The sample total is written to d_n_samples (u64, device); samples beyond
+ * out->capacity are dropped (check d_n_samples afterwards). Errors (negative or
+ * non-finite density) are recorded on the device and reported by the next
+ * vmb_march_check(). */
+int vmb_march_field_async(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,
+                          const vmb_field* f, const vmb_march_config* cfg, vmb_samples* out,
+                          uint64_t* d_n_samples);
+int vmb_march_check(vmb_ctx* ctx);
+/* Generic host-SigmaFn path, step 1: the grid-passing candidate intervals of every
+ * ray, capped at max_samples_per_ray (ray_marching.cpp:75-106). Same two-call
+ * capacity protocol as vmb_march_field. */
+int vmb_march_candidates(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,
+                         const vmb_march_config* cfg, vmb_samples* out, uint64_t* h_n);
+/* step 2: given one sigma per candidate (d_sigmas, dtype f64), apply the
+ * validation, alpha floor and transmittance cut per ray (ray_marching.cpp:118-137)
+ * and pack the kept samples. Reports the first invalid density in (ray, sample)
+ * order with the reference's message. */
+int vmb_march_filter(vmb_ctx* ctx, const vmb_packed_view* candidates, const double* d_sigmas,
+                     const vmb_march_config* cfg, vmb_samples* out, uint64_t* h_n);
+/* march_uniform (ray_marching.cpp:152-168). */
+int vmb_march_uniform(vmb_ctx* ctx, const vmb_rays* rays, const vmb_march_config* cfg,
+                      vmb_samples* out, uint64_t* h_n);
+
+/* ------------------------------------------------------------------ shading (harness) */
+/* shade_samples (voxmarch.cpp:235-251) for an analytic field (+time shift):
+ * rgb and sigma at each sample midpoint, written as dtype. */
+int vmb_shade_field(vmb_ctx* ctx, const vmb_rays* rays, const vmb_field* f, double time,
+                    const uint32_t* d_ray_indices, const double* d_t_starts,
+                    const double* d_t_ends, uint64_t n_samples, void* d_rgbs, void* d_sigmas,
+                    int dtype);
+
+/* ------------------------------------------------------------------ rendering */
+/* transmittance (rendering.cpp:19-33): exclusive per-ray T, out [n_samples]. */
+int vmb_transmittance(vmb_ctx* ctx, const vmb_packed_view* p, const void* d_sigmas,
+                      void* d_out, int dtype);
+/* render_forward (rendering.cpp:35-65): color [n_rays][3], opacity, depth. */
+int vmb_render_forward(vmb_ctx* ctx, const vmb_packed_view* p, const void* d_rgbs,
+                       const void* d_sigmas, void* d_color, void* d_opacity, void* d_depth,
+                       int dtype);
+/* render_backward (rendering.cpp:67-112): d_rgbs [n_samples][3], d_sigmas. */
+int vmb_render_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* d_rgbs,
+                        const void* d_sigmas, const void* d_color, const void* d_opacity,
+                        const void* d_depth, void* d_rgbs_grad, void* d_sigmas_grad,
+                        int dtype);
+/* render_attribute (rendering.cpp:114-134): out [n_rays][dim]. */
+int vmb_render_attribute(vmb_ctx* ctx, const vmb_packed_view* p, const void* d_sigmas,
+                         const void* d_values, uint64_t dim, void* d_out, int dtype);
+
+/* ------------------------------------------------------------------ multi-GPU (NCCL) */
+/* NCCL is loaded at run time (dlopen "libnccl.so.2") only when these are used. */
+int vmb_comm_unique_id(void* h_id128);
+int vmb_comm_init(vmb_ctx* ctx, const void* h_id128, int nranks, int rank);
+int vmb_comm_destroy(vmb_ctx* ctx);
+/* In-place max all-reduce of n f64 (IEEE order == u64 bit order for values >= 0). */
+int vmb_comm_allreduce_max_f64(vmb_ctx* ctx, double* d_buf, uint64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VMB200_H */

@@ -1,0 +1,600 @@
+// march.cu — occupancy-grid ray marching + sample packing (ray_marching.cpp:57-168).
+//
+// One thread per ray. For each ray the kernel walks the reference's candidate
+// lattice (t0 = near + i*step, t1 = min(near + (i+1)*step, far), midpoint query)
+// but only EVALUATES the lattice steps that can possibly be occupied:
+//
+//   * a coarse DDA (Amanatides-Woo, fp64) walks the 8^3-cell blocks of the grid
+//     along the ray, clipped to the domain [0,R]^3 (ray_aabb_intersect);
+//   * blocks whose 1-cell-DILATED coarse bit is 0 are skipped wholesale: a point
+//     whose ideal position lies in such a block computes (with <= 1e-15 rounding
+//     error) to a cell inside the block's halo, all of whose bits are 0, so the
+//     reference would reject it too;
+//   * every step whose interval [t0,t1] meets an occupied block's t-range (plus
+//     one step of slack each side) is evaluated with the reference's exact fp64
+//     arithmetic (vm_exact.cuh), in increasing order.
+//
+// The emitted candidate sequence is therefore identical to the reference's
+// per-step scan ("a DDA fast path is permitted but must be
+// output-identical"). The density of the analytic field is evaluated inline at
+// the same midpoint (sigma_fn_for, voxmarch.cpp:221-232), followed by the alpha
+// floor and the transmittance cut (ray_marching.cpp:118-137) — so a ray stops as
+// soon as T < eps instead of generating all candidates first.
+//
+// Packing is count -> CUB-free scan -> fill (the two passes re-walk the same
+// rays; both passes together read rays twice, write 8 B/ray + 20 B/sample).
+#include <string>
+
+#include "vm_internal.h"
+
+namespace vmb {
+
+int check_contraction(const vmb_contraction* c);
+
+namespace {
+
+enum Mode { COUNT = 0, FILL = 1 };
+
+struct MarchParams {
+    Contract k;
+    uint32_t res;
+    const uint32_t* bits;
+    const uint32_t* coarse;
+    uint32_t block, res_c;
+    double scale[3];      // R / size_k: world -> fine-cell units (approximate, DDA only)
+    double near_, far_, step;
+    uint64_t n_steps;     // lattice length after the host-side !(t1 > t0) check
+    bool skip;            // DDA empty-space skipping allowed (AABB, bounded lattice)
+    bool grows;           // SphereContract && growth > 1 (ray_marching.cpp:60-61)
+    double growth;
+    D3 ball_c;
+    double ball_r;
+    double eps, thr;
+    uint32_t max_cand;
+    bool full;            // walk to the end (stats / candidate mode), ignore the T cut
+    bool filter;          // apply inline density + alpha floor + T cut
+    vmb_field f;
+};
+
+template <typename T>
+__device__ __forceinline__ D3 load3(const T* p, uint64_t i) {
+    return d3(double(p[3 * i]), double(p[3 * i + 1]), double(p[3 * i + 2]));
+}
+
+__device__ __forceinline__ bool fine_bit(const uint32_t* bits, int64_t c) {
+    return (__ldg(bits + (uint64_t(c) >> 5)) >> (uint64_t(c) & 31)) & 1u;
+}
+
+// Per-ray consumer of candidate intervals: alpha floor + transmittance cut and
+// output (count or fill). Returns false when the ray is finished.
+struct Sink {
+    uint64_t ray;
+    uint32_t n_cand = 0;   // candidates seen (emitted)
+    uint32_t n_kept = 0;
+    double T = 1.0;
+    bool filtering = true; // false after the T cut (stats walk continues)
+    // FILL
+    double* ts = nullptr;
+    double* te = nullptr;
+    uint32_t* idx = nullptr;
+    uint64_t base = 0;
+    uint64_t cap = 0;
+};
+
+// Handles one grid-passing candidate. Mirrors ray_marching.cpp:78,111-137.
+template <int MODE>
+__device__ __forceinline__ bool on_candidate(const MarchParams& P, Sink& s, double t0, double t1,
+                                             D3 p, DevError* err) {
+    if (s.n_cand >= P.max_cand) return false;  // candidate cap (:78 / :91)
+    uint32_t ci = s.n_cand++;
+    if (!P.filter) {  // candidate mode: keep every grid-passing interval
+        if (MODE == FILL) {
+            uint64_t o = s.base + s.n_kept;
+            if (o < s.cap) {
+                s.ts[o] = t0;
+                s.te[o] = t1;
+                s.idx[o] = uint32_t(s.ray);
+            }
+        }
+        s.n_kept++;
+        return true;
+    }
+    if (!s.filtering) return true;  // after the cut only the emitted count matters
+    double sigma = field_density(P.f, p);
+    if (!isfinite(sigma) || sigma < 0.0) {
+        int kind = !isfinite(sigma) ? ERR_NONFINITE_SIGMA : ERR_NEGATIVE_SIGMA;
+        atomicMin(&err->key, march_err_key(s.ray, ci, kind));
+        s.filtering = false;
+        return false;
+    }
+    double delta = t1 - t0;
+    double alpha = 1.0 - exp(-sigma * delta);
+    if (alpha <= P.thr) return true;
+    if (MODE == FILL) {
+        uint64_t o = s.base + s.n_kept;
+        if (o < s.cap) {
+            s.ts[o] = t0;
+            s.te[o] = t1;
+            s.idx[o] = uint32_t(s.ray);
+        }
+    }
+    s.n_kept++;
+    s.T *= 1.0 - alpha;
+    if (s.T < P.eps) {
+        s.filtering = false;
+        return P.full;  // continue only to count emitted candidates
+    }
+    return true;
+}
+
+// Exact evaluation of lattice step i (ray_marching.cpp:79-86). Returns false on a
+// non-finite midpoint (query() throws "non-finite coordinate").
+template <int MODE>
+__device__ __forceinline__ bool eval_step(const MarchParams& P, Sink& s, D3 o, D3 d, uint64_t i,
+                                          DevError* err, bool* alive) {
+    double t0 = P.near_ + double(i) * P.step;
+    double t1 = min_ref(P.near_ + double(i + 1) * P.step, P.far_);
+    double m = 0.5 * (t0 + t1);
+    D3 p = o + d * m;
+    if (!finite3(p)) {
+        atomicMin(&err->key, march_err_key(s.ray, 0, ERR_NONFINITE_COORD));
+        *alive = false;
+        return false;
+    }
+    int64_t c = cell_of_point(P.k, P.res, p);
+    if (c >= 0 && fine_bit(P.bits, c)) {
+        if (!on_candidate<MODE>(P, s, t0, t1, p, err)) {
+            *alive = false;
+            return false;
+        }
+    }
+    return true;
+}
+
+__device__ __forceinline__ bool coarse_bit(const MarchParams& P, int cx, int cy, int cz) {
+    uint64_t kc = uint64_t(cx) + uint64_t(P.res_c) * (uint64_t(cy) + uint64_t(P.res_c) * uint64_t(cz));
+    return (__ldg(P.coarse + (kc >> 5)) >> (kc & 31)) & 1u;
+}
+
+// Bounded lattice with empty-space skipping (see file comment).
+template <int MODE>
+__device__ void walk_skip(const MarchParams& P, Sink& s, D3 o, D3 d, DevError* err) {
+    if (P.n_steps == 0) return;
+    const double R = double(P.res);
+    const double EPS = 1e-6;  // fine cells; >> 1e-15 rounding, << 1 cell halo
+    double A[3] = {(o.x - P.k.lo.x) * P.scale[0], (o.y - P.k.lo.y) * P.scale[1],
+                   (o.z - P.k.lo.z) * P.scale[2]};
+    double B[3] = {d.x * P.scale[0], d.y * P.scale[1], d.z * P.scale[2]};
+    double tlo = P.near_, thi = P.far_;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {  // ray_aabb_intersect against [-EPS, R+EPS]^3
+        if (B[a] == 0.0) {
+            if (A[a] < -EPS || A[a] > R + EPS) return;
+        } else {
+            double ta = (-EPS - A[a]) / B[a], tb = (R + EPS - A[a]) / B[a];
+            if (ta > tb) {
+                double x = ta;
+                ta = tb;
+                tb = x;
+            }
+            tlo = fmax(tlo, ta);
+            thi = fmin(thi, tb);
+        }
+    }
+    if (!(tlo <= thi)) return;
+    const double Bs = double(P.block);
+    const int Rc = int(P.res_c);
+    int c[3], stp[3];
+    double tmax[3], tdel[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double pa = A[a] + B[a] * tlo;
+        int ca = int(floor(pa / Bs));
+        ca = ca < 0 ? 0 : (ca >= Rc ? Rc - 1 : ca);
+        c[a] = ca;
+        if (B[a] > 0.0) {
+            stp[a] = 1;
+            tmax[a] = (double(ca + 1) * Bs - A[a]) / B[a];
+            tdel[a] = Bs / B[a];
+        } else if (B[a] < 0.0) {
+            stp[a] = -1;
+            tmax[a] = (double(ca) * Bs - A[a]) / B[a];
+            tdel[a] = -Bs / B[a];
+        } else {
+            stp[a] = 0;
+            tmax[a] = INFINITY;
+            tdel[a] = INFINITY;
+        }
+    }
+    const double inv_step = 1.0 / P.step;
+    const int64_t last = int64_t(P.n_steps) - 1;
+    int64_t next_i = 0;
+    double t = tlo;
+    bool alive = true;
+    for (int guard = 0; guard < 4 * (3 * Rc + 3); ++guard) {
+        double tn = fmin(fmin(tmax[0], tmax[1]), fmin(tmax[2], thi));
+        if (coarse_bit(P, c[0], c[1], c[2])) {
+            double tb = fmax(tn, t);
+            int64_t jlo = int64_t(floor((t - P.near_) * inv_step)) - 1;
+            int64_t jhi = int64_t(floor((tb - P.near_) * inv_step)) + 1;
+            if (jlo < next_i) jlo = next_i;
+            if (jhi > last) jhi = last;
+            for (int64_t j = jlo; j <= jhi; ++j)
+                if (!eval_step<MODE>(P, s, o, d, uint64_t(j), err, &alive)) return;
+            if (jhi + 1 > next_i) next_i = jhi + 1;
+            if (next_i > last) return;
+        }
+        if (tn >= thi) return;
+        int a = (tmax[0] <= tmax[1]) ? ((tmax[0] <= tmax[2]) ? 0 : 2) : ((tmax[1] <= tmax[2]) ? 1 : 2);
+        c[a] += stp[a];
+        if (c[a] < 0 || c[a] >= Rc) return;
+        tmax[a] += tdel[a];
+        t = tn;
+    }
+}
+
+// Bounded lattice, every step evaluated (sphere contraction / unsafe inputs).
+template <int MODE>
+__device__ void walk_dense(const MarchParams& P, Sink& s, D3 o, D3 d, DevError* err) {
+    bool alive = true;
+    for (uint64_t i = 0; i < P.n_steps; ++i)
+        if (!eval_step<MODE>(P, s, o, d, i, err, &alive)) return;
+}
+
+// Geometric step growth outside the unit ball (ray_marching.cpp:88-106).
+template <int MODE>
+__device__ void walk_growth(const MarchParams& P, Sink& s, D3 o, D3 d, DevError* err) {
+    double t = P.near_, dt = P.step;
+    while (t < P.far_ && s.n_cand < P.max_cand) {
+        double t1 = min_ref(t + dt, P.far_);
+        if (!(t1 > t)) break;
+        D3 mid = o + d * (0.5 * (t + t1));
+        if (!finite3(mid)) {
+            atomicMin(&err->key, march_err_key(s.ray, 0, ERR_NONFINITE_COORD));
+            return;
+        }
+        int64_t c = cell_of_point(P.k, P.res, mid);
+        if (c >= 0 && fine_bit(P.bits, c))
+            if (!on_candidate<MODE>(P, s, t, t1, mid, err)) return;
+        t += dt;
+        if (norm(mid - P.ball_c) > P.ball_r)
+            dt *= P.growth;
+        else
+            dt = P.step;
+    }
+}
+
+template <typename RT, int MODE>
+__global__ void __launch_bounds__(128) k_march(MarchParams P, const RT* __restrict__ orig,
+                                               const RT* __restrict__ dirs, uint64_t n_rays,
+                                               uint32_t* __restrict__ counts,
+                                               const uint32_t* __restrict__ offsets,
+                                               double* __restrict__ ts, double* __restrict__ te,
+                                               uint32_t* __restrict__ idx, uint64_t cap,
+                                               unsigned long long* emitted, DevError* err) {
+    unsigned long long emit_local = 0;
+    for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rays;
+         r += uint64_t(gridDim.x) * blockDim.x) {
+        D3 o = load3(orig, r), d = load3(dirs, r);
+        Sink s;
+        s.ray = r;
+        if (MODE == FILL) {
+            s.ts = ts;
+            s.te = te;
+            s.idx = idx;
+            s.base = offsets[r];
+            s.cap = cap;
+        }
+        // Overflowing midpoints can only occur for astronomically large inputs; such
+        // rays take the dense walk so every step is checked as the reference does.
+        double mag = fmax(fmax(fabs(o.x), fabs(o.y)), fabs(o.z)) +
+                     fmax(fmax(fabs(d.x), fabs(d.y)), fabs(d.z)) * fmax(fabs(P.near_), fabs(P.far_));
+        bool safe = mag < 1e300;
+        if (P.grows)
+            walk_growth<MODE>(P, s, o, d, err);
+        else if (P.skip && safe)
+            walk_skip<MODE>(P, s, o, d, err);
+        else
+            walk_dense<MODE>(P, s, o, d, err);
+        if (MODE == COUNT) counts[r] = s.n_kept;
+        emit_local += s.n_cand;
+    }
+    if (MODE == COUNT && emitted) {
+        for (int off = 16; off > 0; off >>= 1) emit_local += __shfl_xor_sync(0xffffffffu, emit_local, off);
+        if ((threadIdx.x & 31) == 0 && emit_local) atomicAdd(emitted, emit_local);
+    }
+}
+
+// Alpha floor + T cut over host-evaluated candidate sigmas (ray_marching.cpp:118-137).
+template <int MODE>
+__global__ void k_filter(const uint32_t* __restrict__ c_off, const uint32_t* __restrict__ c_cnt,
+                         uint64_t n_rays, const double* __restrict__ c_ts,
+                         const double* __restrict__ c_te, const double* __restrict__ sig,
+                         double eps, double thr, uint32_t* __restrict__ counts,
+                         const uint32_t* __restrict__ offsets, double* __restrict__ ts,
+                         double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,
+                         DevError* err) {
+    for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rays;
+         r += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t b = c_off[r], n = c_cnt[r];
+        uint64_t out = MODE == FILL ? offsets[r] : 0;
+        uint32_t kept = 0;
+        double T = 1.0;
+        for (uint64_t k = 0; k < n; ++k) {
+            double sigma = sig[b + k];
+            if (!isfinite(sigma) || sigma < 0.0) {
+                atomicMin(&err->key, march_err_key(r, k, !isfinite(sigma) ? ERR_NONFINITE_SIGMA
+                                                                          : ERR_NEGATIVE_SIGMA));
+                break;
+            }
+            double t0 = c_ts[b + k], t1 = c_te[b + k];
+            double alpha = 1.0 - exp(-sigma * (t1 - t0));
+            if (alpha <= thr) continue;
+            if (MODE == FILL && out + kept < cap) {
+                ts[out + kept] = t0;
+                te[out + kept] = t1;
+                idx[out + kept] = uint32_t(r);
+            }
+            ++kept;
+            T *= 1.0 - alpha;
+            if (T < eps) break;
+        }
+        if (MODE == COUNT) counts[r] = kept;
+    }
+}
+
+// march_uniform: every ray has the same lattice of n_eff steps.
+__global__ void k_uniform(uint64_t n_rays, uint64_t n_eff, double near_, double far_, double step,
+                          uint32_t* __restrict__ offsets, uint32_t* __restrict__ counts,
+                          double* __restrict__ ts, double* __restrict__ te,
+                          uint32_t* __restrict__ idx) {
+    const uint64_t total = n_rays * n_eff;
+    for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rays;
+         r += uint64_t(gridDim.x) * blockDim.x) {
+        offsets[r] = uint32_t(r * n_eff);
+        counts[r] = uint32_t(n_eff);
+    }
+    for (uint64_t s = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < total;
+         s += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t r = s / n_eff, i = s - r * n_eff;
+        ts[s] = near_ + double(i) * step;
+        te[s] = min_ref(near_ + double(i + 1) * step, far_);
+        idx[s] = uint32_t(r);
+    }
+}
+
+int validate_config(const vmb_march_config* c) {  // ray_marching.cpp:12-22
+    if (!(c->step_size > 0.0)) return fail(VMB_INVALID_ARGUMENT, "marching: step_size must be > 0");
+    if (!(c->early_stop_eps >= 0.0 && c->early_stop_eps < 1.0))
+        return fail(VMB_INVALID_ARGUMENT, "marching: early_stop_eps must be in [0,1)");
+    if (!(c->alpha_thre >= 0.0 && c->alpha_thre < 1.0))
+        return fail(VMB_INVALID_ARGUMENT, "marching: alpha_thre must be in [0,1)");
+    if (c->max_samples_per_ray < 1)
+        return fail(VMB_INVALID_ARGUMENT, "marching: max_samples_per_ray must be >= 1");
+    if (!(c->unbounded_step_growth >= 1.0))
+        return fail(VMB_INVALID_ARGUMENT, "marching: unbounded_step_growth must be >= 1");
+    return VMB_OK;
+}
+
+// Effective lattice length: the first i with !(t1 > t0) ends every ray's walk
+// (ray_marching.cpp:81), and it does not depend on the ray. Host arithmetic is
+// plain IEEE double (compiled with -ffp-contract=off), identical to the device's.
+uint64_t effective_steps(double near_, double far_, double step, uint64_t n, bool* exact) {
+    *exact = true;
+    if (n > (1ull << 26)) {  // too long to pre-check; the caller falls back to dense walks
+        *exact = false;
+        return n;
+    }
+    for (uint64_t i = 0; i < n; ++i) {
+        double t0 = near_ + double(i) * step;
+        double t1 = min_ref(near_ + double(i + 1) * step, far_);
+        if (!(t1 > t0)) return i;
+    }
+    return n;
+}
+
+int march_params(const vmb_grid* g, const vmb_rays* rays, const vmb_march_config* cfg,
+                 MarchParams* P) {
+    int rc = validate_config(cfg);
+    if (rc) return rc;
+    if (!(rays->near_plane >= 0.0) || !(rays->far_plane > rays->near_plane))
+        return fail(VMB_INVALID_ARGUMENT, "ray batch: requires far > near >= 0");
+    *P = MarchParams{};
+    P->k = g->k;
+    P->res = g->res;
+    P->bits = g->bits;
+    P->coarse = g->coarse;
+    P->block = g->block;
+    P->res_c = g->res_c;
+    P->scale[0] = double(g->res) / g->k.size.x;
+    P->scale[1] = double(g->res) / g->k.size.y;
+    P->scale[2] = double(g->res) / g->k.size.z;
+    P->near_ = rays->near_plane;
+    P->far_ = rays->far_plane;
+    P->step = cfg->step_size;
+    P->grows = g->con.kind == VMB_CONTRACT_SPHERE && cfg->unbounded_step_growth > 1.0;
+    P->growth = cfg->unbounded_step_growth;
+    P->ball_c = g->k.center;
+    P->ball_r = g->k.radius;
+    P->eps = cfg->early_stop_eps;
+    P->thr = cfg->alpha_thre;
+    P->max_cand = cfg->max_samples_per_ray;
+    bool exact = true;
+    uint64_t n = uniform_step_count(P->near_, P->far_, P->step);
+    P->n_steps = effective_steps(P->near_, P->far_, P->step, n, &exact);
+    P->skip = g->con.kind == VMB_CONTRACT_AABB && exact && !P->grows;
+    return VMB_OK;
+}
+
+template <int MODE>
+void launch_march(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, uint32_t* counts,
+                  const uint32_t* offsets, vmb_samples* out, unsigned long long* emitted) {
+    int blocks = grid_blocks(ctx, rays->n_rays, 128, 16);
+    if (rays->dtype == VMB_F32)
+        k_march<float, MODE><<<blocks, 128, 0, ctx->stream>>>(
+            P, static_cast<const float*>(rays->d_origins), static_cast<const float*>(rays->d_directions),
+            rays->n_rays, counts, offsets, out ? out->d_t_starts : nullptr,
+            out ? out->d_t_ends : nullptr, out ? out->d_ray_indices : nullptr, out ? out->capacity : 0,
+            emitted, ctx->d_err);
+    else
+        k_march<double, MODE><<<blocks, 128, 0, ctx->stream>>>(
+            P, static_cast<const double*>(rays->d_origins),
+            static_cast<const double*>(rays->d_directions), rays->n_rays, counts, offsets,
+            out ? out->d_t_starts : nullptr, out ? out->d_t_ends : nullptr,
+            out ? out->d_ray_indices : nullptr, out ? out->capacity : 0, emitted, ctx->d_err);
+}
+
+std::string march_error_text(const DevError& e) {
+    uint64_t ray = e.key >> 32, low = e.key & 0xffffffffull;
+    if (low == 0) return "non-finite coordinate";
+    uint64_t sample = (low >> 2) - 1;
+    int kind = int(low & 3);
+    return std::string(kind == ERR_NONFINITE_SIGMA ? "marching: non-finite density at ray "
+                                                   : "marching: negative density at ray ") +
+           std::to_string(ray) + " sample " + std::to_string(sample);
+}
+
+int report_march_error(vmb_ctx* ctx) {
+    DevError err;
+    int rc = read_error(ctx, &err);
+    if (rc) return rc;
+    if (err.key == ~0ull) return VMB_OK;
+    uint64_t low = err.key & 0xffffffffull;
+    return fail(low == 0 ? VMB_INVALID_ARGUMENT : VMB_RUNTIME, march_error_text(err));
+}
+
+// count -> scan -> (sync) -> fill, shared by march_field and march_candidates.
+int march_packed(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
+                 uint64_t* h_n, vmb_march_stats* stats) {
+    if (!out || !out->d_offsets || !out->d_counts)
+        return fail(VMB_INVALID_ARGUMENT, "march: output offsets/counts required");
+    int rc = reset_error(ctx);
+    if (rc) return rc;
+    cudaMemsetAsync(ctx->d_u64 + 1, 0, 8, ctx->stream);
+    if (rays->n_rays) launch_march<COUNT>(ctx, P, rays, out->d_counts, nullptr, nullptr, stats ? ctx->d_u64 + 1 : nullptr);
+    rc = scan_counts(ctx, out->d_counts, rays->n_rays, out->d_offsets, ctx->d_u64);
+    if (rc) return rc;
+    cudaMemcpyAsync(ctx->h_u64, ctx->d_u64, 16, cudaMemcpyDeviceToHost, ctx->stream);
+    rc = report_march_error(ctx);  // synchronizes
+    if (rc) return rc;
+    uint64_t total = ctx->h_u64[0];
+    *h_n = total;
+    if (stats) {
+        stats->samples_emitted = ctx->h_u64[1];
+        stats->samples_kept = total;
+    }
+    if (total > 0xffffffffull) return fail(VMB_INVALID_ARGUMENT, "pack: sample count exceeds 32-bit index range");
+    if (total > out->capacity) return fail(VMB_CAPACITY, "march: sample capacity too small");
+    if (total) launch_march<FILL>(ctx, P, rays, out->d_counts, out->d_offsets, out, nullptr);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? VMB_OK : cuda_fail(e, "march fill");
+}
+
+}  // namespace
+}  // namespace vmb
+
+using namespace vmb;
+
+extern "C" {
+
+int vmb_march_field(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays, const vmb_field* f,
+                    const vmb_march_config* cfg, vmb_samples* out, uint64_t* h_n,
+                    vmb_march_stats* stats) {
+    MarchParams P;
+    int rc = march_params(g, rays, cfg, &P);
+    if (rc) return rc;
+    if (f->kind == VMB_FIELD_UNIFORM_BOX &&
+        !(f->box_max[0] > f->box_min[0] && f->box_max[1] > f->box_min[1] && f->box_max[2] > f->box_min[2]))
+        return fail(VMB_INVALID_ARGUMENT, "aabb max must be strictly greater than min");
+    P.f = *f;
+    P.filter = true;
+    P.full = stats != nullptr;
+    return march_packed(ctx, P, rays, out, h_n, stats);
+}
+
+int vmb_march_field_async(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,
+                          const vmb_field* f, const vmb_march_config* cfg, vmb_samples* out,
+                          uint64_t* d_n) {
+    MarchParams P;
+    int rc = march_params(g, rays, cfg, &P);
+    if (rc) return rc;
+    P.f = *f;
+    P.filter = true;
+    P.full = false;
+    if (rays->n_rays) launch_march<COUNT>(ctx, P, rays, out->d_counts, nullptr, nullptr, nullptr);
+    rc = scan_counts(ctx, out->d_counts, rays->n_rays, out->d_offsets,
+                     reinterpret_cast<unsigned long long*>(d_n));
+    if (rc) return rc;
+    if (rays->n_rays) launch_march<FILL>(ctx, P, rays, out->d_counts, out->d_offsets, out, nullptr);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? VMB_OK : cuda_fail(e, "march async");
+}
+
+int vmb_march_check(vmb_ctx* ctx) {
+    int rc = report_march_error(ctx);
+    if (rc) return rc;
+    return reset_error(ctx);
+}
+
+int vmb_march_candidates(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,
+                         const vmb_march_config* cfg, vmb_samples* out, uint64_t* h_n) {
+    MarchParams P;
+    int rc = march_params(g, rays, cfg, &P);
+    if (rc) return rc;
+    P.filter = false;
+    P.full = true;
+    return march_packed(ctx, P, rays, out, h_n, nullptr);
+}
+
+int vmb_march_filter(vmb_ctx* ctx, const vmb_packed_view* c, const double* sig,
+                     const vmb_march_config* cfg, vmb_samples* out, uint64_t* h_n) {
+    int rc = validate_config(cfg);
+    if (rc) return rc;
+    rc = reset_error(ctx);
+    if (rc) return rc;
+    int blocks = grid_blocks(ctx, c->n_rays, 128, 16);
+    if (c->n_rays)
+        k_filter<COUNT><<<blocks, 128, 0, ctx->stream>>>(
+            c->d_offsets, c->d_counts, c->n_rays, c->d_t_starts, c->d_t_ends, sig, cfg->early_stop_eps,
+            cfg->alpha_thre, out->d_counts, nullptr, nullptr, nullptr, nullptr, 0, ctx->d_err);
+    rc = scan_counts(ctx, out->d_counts, c->n_rays, out->d_offsets, ctx->d_u64);
+    if (rc) return rc;
+    cudaMemcpyAsync(ctx->h_u64, ctx->d_u64, 8, cudaMemcpyDeviceToHost, ctx->stream);
+    rc = report_march_error(ctx);
+    if (rc) return rc;
+    *h_n = ctx->h_u64[0];
+    if (*h_n > out->capacity) return fail(VMB_CAPACITY, "march: sample capacity too small");
+    if (*h_n)
+        k_filter<FILL><<<blocks, 128, 0, ctx->stream>>>(
+            c->d_offsets, c->d_counts, c->n_rays, c->d_t_starts, c->d_t_ends, sig, cfg->early_stop_eps,
+            cfg->alpha_thre, nullptr, out->d_offsets, out->d_t_starts, out->d_t_ends,
+            out->d_ray_indices, out->capacity, ctx->d_err);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? VMB_OK : cuda_fail(e, "march filter");
+}
+
+int vmb_march_uniform(vmb_ctx* ctx, const vmb_rays* rays, const vmb_march_config* cfg,
+                      vmb_samples* out, uint64_t* h_n) {
+    int rc = validate_config(cfg);
+    if (rc) return rc;
+    if (!(rays->near_plane >= 0.0) || !(rays->far_plane > rays->near_plane))
+        return fail(VMB_INVALID_ARGUMENT, "ray batch: requires far > near >= 0");
+    bool exact;
+    uint64_t n = uniform_step_count(rays->near_plane, rays->far_plane, cfg->step_size);
+    uint64_t n_eff = effective_steps(rays->near_plane, rays->far_plane, cfg->step_size, n, &exact);
+    if (!exact) return fail(VMB_NOT_SUPPORTED, "march_uniform: lattice longer than 2^26 steps");
+    uint64_t total = rays->n_rays * n_eff;
+    *h_n = total;
+    if (total > 0xffffffffull) return fail(VMB_INVALID_ARGUMENT, "pack: sample count exceeds 32-bit index range");
+    if (total > out->capacity) return fail(VMB_CAPACITY, "march: sample capacity too small");
+    uint64_t work = total > rays->n_rays ? total : rays->n_rays;
+    if (work)
+        k_uniform<<<grid_blocks(ctx, work, 256), 256, 0, ctx->stream>>>(
+            rays->n_rays, n_eff, rays->near_plane, rays->far_plane, cfg->step_size, out->d_offsets,
+            out->d_counts, out->d_t_starts, out->d_t_ends, out->d_ray_indices);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    return e == cudaSuccess ? VMB_OK : cuda_fail(e, "march uniform");
+}
+
+}  // extern "C"

@@ -1,0 +1,469 @@
+// render.cu — differentiable compositing along rays (rendering.cpp:19-134).
+//
+// Layout: packed samples are ray-contiguous (offsets = exclusive scan of counts),
+// so the samples of 32 consecutive rays form one contiguous range. Each warp
+// owns 32 rays and streams their range through shared memory in chunks:
+//   1. coalesced, all-lane loads of t_starts/t_ends (f64), rgb (AoS) and sigma
+//      into the warp's smem tile (every HBM byte read exactly once);
+//   2. each lane runs its own ray's exclusive transmittance scan sequentially
+//      from smem, in the reference's operation order and in fp64
+//      (T *= 1 - alpha; fp32 accumulation is not accurate enough);
+//   3. per-sample outputs are staged back into the tile and written coalesced.
+// render_backward keeps the reference's reverse suffix-sum when a warp's range
+// fits one tile; longer ranges use two forward sweeps with suffix_k = S - P_k.
+// Warps whose rays are not contiguous (arbitrary user offsets) fall back to
+// per-lane global reads — same math, no staging.
+#include "vm_internal.h"
+
+namespace vmb {
+namespace {
+
+constexpr int kWarps = 4;  // 128 threads per CTA
+
+template <typename T> struct Tile;
+template <> struct Tile<float> { static constexpr int CH = 256; };
+template <> struct Tile<double> { static constexpr int CH = 128; };
+
+template <typename T>
+struct Smem {
+    double ts[Tile<T>::CH];
+    double te[Tile<T>::CH];
+    double tr[Tile<T>::CH];   // transmittance (backward / transmittance output)
+    double al[Tile<T>::CH];   // alpha (backward)
+    T rgb[3 * Tile<T>::CH];   // input rgb, then d_rgb
+    T sig[Tile<T>::CH];       // input sigma, then d_sigma
+};
+
+struct RayRange {
+    uint64_t r;
+    bool valid;
+    uint64_t off, end;
+    bool contiguous;  // warp-uniform
+    uint64_t s0, s1;  // warp range when contiguous
+};
+
+__device__ __forceinline__ RayRange ray_range(const uint32_t* __restrict__ offsets,
+                                              const uint32_t* __restrict__ counts, uint64_t n_rays,
+                                              uint64_t warp_id, int lane) {
+    RayRange rr;
+    rr.r = warp_id * 32 + lane;
+    rr.valid = rr.r < n_rays;
+    rr.off = rr.valid ? offsets[rr.r] : 0;
+    rr.end = rr.valid ? rr.off + counts[rr.r] : 0;
+    uint64_t next_off = __shfl_down_sync(0xffffffffu, rr.off, 1);
+    bool next_valid = __shfl_down_sync(0xffffffffu, rr.valid, 1);
+    bool ok = !(rr.valid && lane < 31 && next_valid) || rr.end == next_off;
+    rr.contiguous = __all_sync(0xffffffffu, ok);
+    rr.s0 = __shfl_sync(0xffffffffu, rr.off, 0);
+    unsigned vmask = __ballot_sync(0xffffffffu, rr.valid);
+    int last = vmask ? 31 - __clz(vmask) : 0;
+    rr.s1 = __shfl_sync(0xffffffffu, rr.end, last);
+    return rr;
+}
+
+template <typename T>
+__device__ __forceinline__ void stage_in(Smem<T>& sm, int lane, uint64_t cs, uint64_t n,
+                                         const double* __restrict__ ts, const double* __restrict__ te,
+                                         const T* __restrict__ rgb, const T* __restrict__ sig) {
+    for (uint64_t i = lane; i < n; i += 32) {
+        sm.ts[i] = __ldg(ts + cs + i);
+        sm.te[i] = __ldg(te + cs + i);
+        sm.sig[i] = __ldg(sig + cs + i);
+    }
+    if (rgb)
+        for (uint64_t i = lane; i < 3 * n; i += 32) sm.rgb[i] = __ldg(rgb + 3 * cs + i);
+}
+
+// ------------------------------------------------------------------ forward
+struct Fwd {
+    double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0, op = 0.0, dep = 0.0;
+    // rendering.cpp:51-58
+    __device__ __forceinline__ void add(double ts, double te, double r, double g, double b,
+                                        double sigma) {
+        double delta = te - ts;
+        double alpha = 1.0 - exp(-sigma * delta);
+        double w = T * alpha;
+        cr = cr + r * w;
+        cg = cg + g * w;
+        cb = cb + b * w;
+        op += w;
+        dep += w * 0.5 * (ts + te);
+        T *= 1.0 - alpha;
+    }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kWarps * 32) k_forward(
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays,
+    const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
+    const T* __restrict__ sig, T* __restrict__ color, T* __restrict__ opacity, T* __restrict__ depth) {
+    __shared__ Smem<T> smem[kWarps];
+    const int lane = threadIdx.x & 31;
+    Smem<T>& sm = smem[threadIdx.x >> 5];
+    const uint64_t n_warps = (n_rays + 31) / 32;
+    for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
+         w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
+        Fwd acc;
+        if (rr.contiguous) {
+            for (uint64_t cs = rr.s0; cs < rr.s1; cs += Tile<T>::CH) {
+                uint64_t n = min(uint64_t(Tile<T>::CH), rr.s1 - cs);
+                stage_in(sm, lane, cs, n, ts, te, rgb, sig);
+                __syncwarp();
+                uint64_t a = max(rr.off, cs), b = min(rr.end, cs + n);
+                for (uint64_t s = a; s < b; ++s) {
+                    uint64_t i = s - cs;
+                    acc.add(sm.ts[i], sm.te[i], double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
+                            double(sm.rgb[3 * i + 2]), double(sm.sig[i]));
+                }
+                __syncwarp();
+            }
+        } else {
+            for (uint64_t s = rr.off; s < rr.end; ++s)
+                acc.add(ts[s], te[s], double(rgb[3 * s]), double(rgb[3 * s + 1]), double(rgb[3 * s + 2]),
+                        double(sig[s]));
+        }
+        if (rr.valid) {
+            color[3 * rr.r] = T(acc.cr);
+            color[3 * rr.r + 1] = T(acc.cg);
+            color[3 * rr.r + 2] = T(acc.cb);
+            opacity[rr.r] = T(acc.op);
+            depth[rr.r] = T(acc.dep);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ backward
+struct Up {
+    double dcx, dcy, dcz, dop, ddep;
+    // v = dot(d_color, rgb) + d_opacity + d_depth * mid   (rendering.cpp:102)
+    __device__ __forceinline__ double value(double r, double g, double b, double mid) const {
+        return (dcx * r + dcy * g + dcz * b) + dop + ddep * mid;
+    }
+};
+
+template <typename T>
+__device__ __forceinline__ Up load_up(const T* dc, const T* dop, const T* ddep, uint64_t r, bool valid) {
+    Up u{0, 0, 0, 0, 0};
+    if (valid) {
+        u.dcx = double(dc[3 * r]);
+        u.dcy = double(dc[3 * r + 1]);
+        u.dcz = double(dc[3 * r + 2]);
+        u.dop = double(dop[r]);
+        u.ddep = double(ddep[r]);
+    }
+    return u;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kWarps * 32) k_backward(
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays,
+    const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
+    const T* __restrict__ sig, const T* __restrict__ dc, const T* __restrict__ dop,
+    const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig) {
+    __shared__ Smem<T> smem[kWarps];
+    const int lane = threadIdx.x & 31;
+    Smem<T>& sm = smem[threadIdx.x >> 5];
+    const uint64_t n_warps = (n_rays + 31) / 32;
+    for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
+         w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
+        Up u = load_up(dc, dop, ddep, rr.r, rr.valid);
+        if (rr.contiguous && rr.s1 - rr.s0 <= uint64_t(Tile<T>::CH)) {
+            // Exact reference order: forward T/alpha, then reverse suffix pass.
+            uint64_t cs = rr.s0, n = rr.s1 - rr.s0;
+            stage_in(sm, lane, cs, n, ts, te, rgb, sig);
+            __syncwarp();
+            double t = 1.0;
+            for (uint64_t s = rr.off; s < rr.end; ++s) {  // rendering.cpp:89-96
+                uint64_t i = s - cs;
+                double a = 1.0 - exp(-double(sm.sig[i]) * (sm.te[i] - sm.ts[i]));
+                sm.tr[i] = t;
+                sm.al[i] = a;
+                t *= 1.0 - a;
+            }
+            double suffix = 0.0;
+            for (uint64_t s = rr.end; s-- > rr.off;) {  // rendering.cpp:99-108
+                uint64_t i = s - cs;
+                double delta = sm.te[i] - sm.ts[i];
+                double mid = 0.5 * (sm.ts[i] + sm.te[i]);
+                double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
+                                   double(sm.rgb[3 * i + 2]), mid);
+                double wgt = sm.tr[i] * sm.al[i];
+                sm.rgb[3 * i] = T(u.dcx * wgt);
+                sm.rgb[3 * i + 1] = T(u.dcy * wgt);
+                sm.rgb[3 * i + 2] = T(u.dcz * wgt);
+                sm.sig[i] = T(delta * (sm.tr[i] * (1.0 - sm.al[i]) * v - suffix));
+                suffix += wgt * v;
+            }
+            __syncwarp();
+            for (uint64_t i = lane; i < n; i += 32) g_sig[cs + i] = sm.sig[i];
+            for (uint64_t i = lane; i < 3 * n; i += 32) g_rgb[3 * cs + i] = sm.rgb[i];
+            __syncwarp();
+            continue;
+        }
+        // Long or non-contiguous ranges: sweep 1 computes S = sum_k w_k v_k,
+        // sweep 2 emits suffix_k = S - P_k (P_k inclusive prefix).
+        const bool staged = rr.contiguous;
+        double S = 0.0;
+        {
+            double t = 1.0;
+            if (staged) {
+                for (uint64_t cs = rr.s0; cs < rr.s1; cs += Tile<T>::CH) {
+                    uint64_t n = min(uint64_t(Tile<T>::CH), rr.s1 - cs);
+                    stage_in(sm, lane, cs, n, ts, te, rgb, sig);
+                    __syncwarp();
+                    for (uint64_t s = max(rr.off, cs); s < min(rr.end, cs + n); ++s) {
+                        uint64_t i = s - cs;
+                        double a = 1.0 - exp(-double(sm.sig[i]) * (sm.te[i] - sm.ts[i]));
+                        double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
+                                           double(sm.rgb[3 * i + 2]), 0.5 * (sm.ts[i] + sm.te[i]));
+                        S += t * a * v;
+                        t *= 1.0 - a;
+                    }
+                    __syncwarp();
+                }
+            } else {
+                for (uint64_t s = rr.off; s < rr.end; ++s) {
+                    double a = 1.0 - exp(-double(sig[s]) * (te[s] - ts[s]));
+                    double v = u.value(double(rgb[3 * s]), double(rgb[3 * s + 1]), double(rgb[3 * s + 2]),
+                                       0.5 * (ts[s] + te[s]));
+                    S += t * a * v;
+                    t *= 1.0 - a;
+                }
+            }
+        }
+        {
+            double t = 1.0, P = 0.0;
+            if (staged) {
+                for (uint64_t cs = rr.s0; cs < rr.s1; cs += Tile<T>::CH) {
+                    uint64_t n = min(uint64_t(Tile<T>::CH), rr.s1 - cs);
+                    stage_in(sm, lane, cs, n, ts, te, rgb, sig);
+                    __syncwarp();
+                    for (uint64_t s = max(rr.off, cs); s < min(rr.end, cs + n); ++s) {
+                        uint64_t i = s - cs;
+                        double delta = sm.te[i] - sm.ts[i];
+                        double a = 1.0 - exp(-double(sm.sig[i]) * delta);
+                        double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
+                                           double(sm.rgb[3 * i + 2]), 0.5 * (sm.ts[i] + sm.te[i]));
+                        double wgt = t * a;
+                        P += wgt * v;
+                        sm.rgb[3 * i] = T(u.dcx * wgt);
+                        sm.rgb[3 * i + 1] = T(u.dcy * wgt);
+                        sm.rgb[3 * i + 2] = T(u.dcz * wgt);
+                        sm.sig[i] = T(delta * (t * (1.0 - a) * v - (S - P)));
+                        t *= 1.0 - a;
+                    }
+                    __syncwarp();
+                    for (uint64_t i = lane; i < n; i += 32) g_sig[cs + i] = sm.sig[i];
+                    for (uint64_t i = lane; i < 3 * n; i += 32) g_rgb[3 * cs + i] = sm.rgb[i];
+                    __syncwarp();
+                }
+            } else {
+                for (uint64_t s = rr.off; s < rr.end; ++s) {
+                    double delta = te[s] - ts[s];
+                    double a = 1.0 - exp(-double(sig[s]) * delta);
+                    double v = u.value(double(rgb[3 * s]), double(rgb[3 * s + 1]), double(rgb[3 * s + 2]),
+                                       0.5 * (ts[s] + te[s]));
+                    double wgt = t * a;
+                    P += wgt * v;
+                    g_rgb[3 * s] = T(u.dcx * wgt);
+                    g_rgb[3 * s + 1] = T(u.dcy * wgt);
+                    g_rgb[3 * s + 2] = T(u.dcz * wgt);
+                    g_sig[s] = T(delta * (t * (1.0 - a) * v - (S - P)));
+                    t *= 1.0 - a;
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ transmittance
+template <typename T>
+__global__ void __launch_bounds__(kWarps * 32) k_transmittance(
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays,
+    const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ sig,
+    T* __restrict__ out) {
+    __shared__ Smem<T> smem[kWarps];
+    const int lane = threadIdx.x & 31;
+    Smem<T>& sm = smem[threadIdx.x >> 5];
+    const uint64_t n_warps = (n_rays + 31) / 32;
+    for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
+         w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
+        double t = 1.0;  // rendering.cpp:26-31: out = T; T *= exp(-sigma * delta)
+        if (rr.contiguous) {
+            for (uint64_t cs = rr.s0; cs < rr.s1; cs += Tile<T>::CH) {
+                uint64_t n = min(uint64_t(Tile<T>::CH), rr.s1 - cs);
+                stage_in<T>(sm, lane, cs, n, ts, te, nullptr, sig);
+                __syncwarp();
+                for (uint64_t s = max(rr.off, cs); s < min(rr.end, cs + n); ++s) {
+                    uint64_t i = s - cs;
+                    sm.tr[i] = t;
+                    t *= exp(-double(sm.sig[i]) * (sm.te[i] - sm.ts[i]));
+                }
+                __syncwarp();
+                for (uint64_t i = lane; i < n; i += 32) out[cs + i] = T(sm.tr[i]);
+                __syncwarp();
+            }
+        } else {
+            for (uint64_t s = rr.off; s < rr.end; ++s) {
+                out[s] = T(t);
+                t *= exp(-double(sig[s]) * (te[s] - ts[s]));
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ attribute
+// render_attribute (rendering.cpp:114-134): dim-D values, thread per ray.
+template <typename T>
+__global__ void k_attribute(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts,
+                            uint64_t n_rays, const double* __restrict__ ts, const double* __restrict__ te,
+                            const T* __restrict__ sig, const T* __restrict__ values, uint64_t dim,
+                            T* __restrict__ out) {
+    for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rays;
+         r += uint64_t(gridDim.x) * blockDim.x) {
+        for (uint64_t k = 0; k < dim; ++k) out[r * dim + k] = T(0);
+        uint64_t b = offsets[r], e = b + counts[r];
+        double trans = 1.0;
+        for (uint64_t s = b; s < e; ++s) {
+            double alpha = 1.0 - exp(-double(sig[s]) * (te[s] - ts[s]));
+            double w = trans * alpha;
+            for (uint64_t k = 0; k < dim; ++k)
+                out[r * dim + k] = T(double(out[r * dim + k]) + w * double(values[s * dim + k]));
+            trans *= 1.0 - alpha;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ shading (harness)
+template <typename RT, typename T>
+__global__ void k_shade(const RT* __restrict__ orig, const RT* __restrict__ dirs, vmb_field f,
+                        double time, const uint32_t* __restrict__ idx, const double* __restrict__ ts,
+                        const double* __restrict__ te, uint64_t n, T* __restrict__ rgb,
+                        T* __restrict__ sig) {
+    for (uint64_t s = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < n;
+         s += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t r = idx[s];
+        D3 o = d3(double(orig[3 * r]), double(orig[3 * r + 1]), double(orig[3 * r + 2]));
+        D3 d = d3(double(dirs[3 * r]), double(dirs[3 * r + 1]), double(dirs[3 * r + 2]));
+        D3 p = o + d * (0.5 * (ts[s] + te[s]));  // voxmarch.cpp:243-244
+        D3 c;
+        double sigma = field_rgb_sigma(f, time_shift(f, p, time), &c);
+        rgb[3 * s] = T(c.x);
+        rgb[3 * s + 1] = T(c.y);
+        rgb[3 * s + 2] = T(c.z);
+        sig[s] = T(sigma);
+    }
+}
+
+int launched(const char* where) {
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? VMB_OK : cuda_fail(e, where);
+}
+
+int render_blocks(vmb_ctx* ctx, uint64_t n_rays) {
+    return grid_blocks(ctx, (n_rays + 31) / 32 * 32, kWarps * 32, 16);
+}
+
+}  // namespace
+}  // namespace vmb
+
+using namespace vmb;
+
+extern "C" {
+
+int vmb_render_forward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, const void* sig,
+                       void* color, void* opacity, void* depth, int dtype) {
+    if (!p->n_rays) return VMB_OK;
+    int blocks = render_blocks(ctx, p->n_rays);
+    if (dtype == VMB_F32)
+        k_forward<float><<<blocks, kWarps * 32, 0, ctx->stream>>>(
+            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            static_cast<const float*>(rgb), static_cast<const float*>(sig), static_cast<float*>(color),
+            static_cast<float*>(opacity), static_cast<float*>(depth));
+    else
+        k_forward<double><<<blocks, kWarps * 32, 0, ctx->stream>>>(
+            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            static_cast<const double*>(rgb), static_cast<const double*>(sig), static_cast<double*>(color),
+            static_cast<double*>(opacity), static_cast<double*>(depth));
+    return launched("render_forward");
+}
+
+int vmb_render_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, const void* sig,
+                        const void* dc, const void* dop, const void* ddep, void* g_rgb, void* g_sig,
+                        int dtype) {
+    if (!p->n_rays) return VMB_OK;
+    int blocks = render_blocks(ctx, p->n_rays);
+    if (dtype == VMB_F32)
+        k_backward<float><<<blocks, kWarps * 32, 0, ctx->stream>>>(
+            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            static_cast<const float*>(rgb), static_cast<const float*>(sig), static_cast<const float*>(dc),
+            static_cast<const float*>(dop), static_cast<const float*>(ddep), static_cast<float*>(g_rgb),
+            static_cast<float*>(g_sig));
+    else
+        k_backward<double><<<blocks, kWarps * 32, 0, ctx->stream>>>(
+            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            static_cast<const double*>(rgb), static_cast<const double*>(sig),
+            static_cast<const double*>(dc), static_cast<const double*>(dop),
+            static_cast<const double*>(ddep), static_cast<double*>(g_rgb), static_cast<double*>(g_sig));
+    return launched("render_backward");
+}
+
+int vmb_transmittance(vmb_ctx* ctx, const vmb_packed_view* p, const void* sig, void* out, int dtype) {
+    if (!p->n_rays) return VMB_OK;
+    int blocks = render_blocks(ctx, p->n_rays);
+    if (dtype == VMB_F32)
+        k_transmittance<float><<<blocks, kWarps * 32, 0, ctx->stream>>>(
+            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            static_cast<const float*>(sig), static_cast<float*>(out));
+    else
+        k_transmittance<double><<<blocks, kWarps * 32, 0, ctx->stream>>>(
+            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            static_cast<const double*>(sig), static_cast<double*>(out));
+    return launched("transmittance");
+}
+
+int vmb_render_attribute(vmb_ctx* ctx, const vmb_packed_view* p, const void* sig, const void* values,
+                         uint64_t dim, void* out, int dtype) {
+    if (dim == 0) return fail(VMB_INVALID_ARGUMENT, "rendering: value length mismatch");
+    if (!p->n_rays) return VMB_OK;
+    int blocks = grid_blocks(ctx, p->n_rays, 128, 16);
+    if (dtype == VMB_F32)
+        k_attribute<float><<<blocks, 128, 0, ctx->stream>>>(
+            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            static_cast<const float*>(sig), static_cast<const float*>(values), dim, static_cast<float*>(out));
+    else
+        k_attribute<double><<<blocks, 128, 0, ctx->stream>>>(
+            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            static_cast<const double*>(sig), static_cast<const double*>(values), dim,
+            static_cast<double*>(out));
+    return launched("render_attribute");
+}
+
+int vmb_shade_field(vmb_ctx* ctx, const vmb_rays* rays, const vmb_field* f, double time,
+                    const uint32_t* idx, const double* ts, const double* te, uint64_t n, void* rgb,
+                    void* sig, int dtype) {
+    if (!n) return VMB_OK;
+    int blocks = grid_blocks(ctx, n, 256, 8);
+    if (rays->dtype == VMB_F32 && dtype == VMB_F32)
+        k_shade<float, float><<<blocks, 256, 0, ctx->stream>>>(
+            static_cast<const float*>(rays->d_origins), static_cast<const float*>(rays->d_directions), *f,
+            time, idx, ts, te, n, static_cast<float*>(rgb), static_cast<float*>(sig));
+    else if (rays->dtype == VMB_F32)
+        k_shade<float, double><<<blocks, 256, 0, ctx->stream>>>(
+            static_cast<const float*>(rays->d_origins), static_cast<const float*>(rays->d_directions), *f,
+            time, idx, ts, te, n, static_cast<double*>(rgb), static_cast<double*>(sig));
+    else if (dtype == VMB_F32)
+        k_shade<double, float><<<blocks, 256, 0, ctx->stream>>>(
+            static_cast<const double*>(rays->d_origins), static_cast<const double*>(rays->d_directions), *f,
+            time, idx, ts, te, n, static_cast<float*>(rgb), static_cast<float*>(sig));
+    else
+        k_shade<double, double><<<blocks, 256, 0, ctx->stream>>>(
+            static_cast<const double*>(rays->d_origins), static_cast<const double*>(rays->d_directions), *f,
+            time, idx, ts, te, n, static_cast<double*>(rgb), static_cast<double*>(sig));
+    return launched("shade");
+}
+
+}  // extern "C"

@@ -1,0 +1,113 @@
+// vm_internal.h — library-private state and launcher declarations.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/vmb200.h"
+#include "vm_exact.cuh"
+
+namespace vmb {
+
+// Device-side error record: the FIRST failure in (ray, sample) / (timestamp, cell)
+// order wins via atomicMin on a packed 64-bit key, reproducing the reference's
+// "first error in sequential order" exception (parallel.hpp:43-46 rethrows the
+// lowest chunk's exception). key == UINT64_MAX means "no error".
+struct DevError {
+    unsigned long long key;
+    int kind;
+    int pad_;
+};
+
+enum ErrKind : int {
+    ERR_NONFINITE_SIGMA = 0,   // ray_marching.cpp:124-126
+    ERR_NEGATIVE_SIGMA = 1,    // ray_marching.cpp:127-129
+    ERR_NONFINITE_COORD = 2,   // contraction.cpp:25 via query()
+    ERR_INVALID_DENSITY = 3,   // occupancy_grid.cpp:127-136
+};
+
+// key layout for march errors: ray << 32 | low, low = 0 for a non-finite midpoint
+// (candidate generation runs before any density check of that ray in the
+// reference, ray_marching.cpp:77-116), else (sample + 1) << 2 | kind.
+__host__ __device__ inline unsigned long long march_err_key(uint64_t ray, uint64_t sample, int kind) {
+    if (kind == ERR_NONFINITE_COORD) return (unsigned long long)(ray << 32);
+    uint64_t s = sample >= 0x3ffffffeull ? 0x3ffffffeull : sample;
+    return (unsigned long long)((ray << 32) | ((s + 1) << 2) | uint64_t(kind));
+}
+
+int check_contraction(const vmb_contraction* c);
+
+}  // namespace vmb
+
+struct vmb_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    vmb::DevError* d_err = nullptr;     // device error record
+    vmb::DevError* h_err = nullptr;     // pinned mirror
+    unsigned long long* d_u64 = nullptr;  // 8 device scalars (totals, counters)
+    unsigned long long* h_u64 = nullptr;  // pinned mirror
+    void* scratch[4] = {};          // per-purpose growable device scratch (see scratch())
+    size_t scratch_bytes[4] = {};
+    cudaEvent_t events[32] = {};
+    // NCCL (dlopen'ed lazily; see comm.cpp)
+    void* nccl_comm = nullptr;
+    int nranks = 1;
+    int rank = 0;
+};
+
+struct vmb_grid {
+    int device = 0;
+    uint32_t res = 0;
+    vmb_contraction con{};
+    vmb::Contract k{};
+    double thr = 1e-2;
+    double ref_step = 0.0;
+    uint64_t n_cells = 0;
+    uint64_t n_words = 0;          // ceil(n_cells / 32)
+    double* cache = nullptr;       // [n_cells] f64 density EMA
+    uint32_t* bits = nullptr;      // [n_words] packed, LSB-first, x-fastest == OGRD bytes
+    // Coarse, 1-cell-dilated occupancy used by the empty-space-skipping marcher:
+    // bit(K) = OR of fine bits over block K expanded by one fine cell per side.
+    uint32_t block = 8;
+    uint32_t res_c = 0;            // ceil(res / block)
+    uint32_t* coarse = nullptr;    // [ceil(res_c^3 / 32)]
+    uint64_t coarse_words = 0;
+    double* probed = nullptr;      // [n_cells] scratch for the sharded / callback update
+};
+
+namespace vmb {
+
+// ---------------------------------------------------------------- utilities
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+// Growable device scratch, one buffer per slot so nested users never alias:
+// slot 0 = scan tile sums, 1 = march / candidates temporaries, 2 = grid update,
+// 3 = validation / misc. Growing synchronizes the stream before freeing.
+enum { SCRATCH_SCAN = 0, SCRATCH_MARCH = 1, SCRATCH_GRID = 2, SCRATCH_MISC = 3 };
+void* scratch(vmb_ctx* ctx, int slot, size_t bytes);
+inline int grid_blocks(vmb_ctx* ctx, uint64_t work, int threads, int per_sm = 8) {
+    uint64_t b = (work + threads - 1) / threads;
+    uint64_t cap = uint64_t(ctx->num_sms) * per_sm;
+    return int(b < 1 ? 1 : (b > cap ? cap : b));
+}
+int reset_error(vmb_ctx* ctx);
+int read_error(vmb_ctx* ctx, DevError* out);  // synchronizes
+
+// ---------------------------------------------------------------- scan (scan.cu)
+// Exclusive scan of u32 counts into u32 offsets; device total (u64) at d_total.
+int scan_counts(vmb_ctx* ctx, const uint32_t* counts, uint64_t n, uint32_t* offsets,
+                unsigned long long* d_total);
+// Exclusive scan of u8 flags into u32 positions (compaction), device total at d_total.
+int scan_flags(vmb_ctx* ctx, const uint8_t* flags, uint64_t n, uint32_t* pos,
+               unsigned long long* d_total);
+
+// ---------------------------------------------------------------- grid (grid.cu)
+int grid_refresh(vmb_ctx* ctx, vmb_grid* g);      // bits + coarse from cache
+int grid_rebuild_coarse(vmb_ctx* ctx, vmb_grid* g);
+
+}  // namespace vmb

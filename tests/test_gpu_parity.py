@@ -1,0 +1,387 @@
+"""Parity of the CUDA path (via the C ABI) with the CPU oracle.
+
+Bit-exact: grid bits/cache, sample counts, offsets (packed_info), ray_indices and
+t_starts/t_ends. Rendering outputs and gradients: rtol 1e-5 with an absolute floor
+of 1e-8 (close_rel of proj/tests/unit/test_rendering.cpp:67-69); in practice the
+fp64 kernels agree to ~1e-15.
+"""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+
+from oracle import Oracle, available
+from oracle import oracle as O
+from paper_2210_04847_b200 import api, workload
+from paper_2210_04847_b200._lib import Contraction, Field, MarchConfig, MarchStats
+
+pytestmark = pytest.mark.gpu
+G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+RTOL, ATOL = 1e-5, 1e-8
+
+
+@pytest.fixture(scope="module")
+def dev():
+    return api.Device(0)
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return Oracle("ref") if available("ref") else Oracle("port")
+
+
+def ofield(f: Field):
+    o = O.Field()
+    for name, _ in Field._fields_:
+        setattr(o, name, getattr(f, name))
+    return o
+
+
+def ocon(c: Contraction):
+    o = O.Contraction()
+    for name, _ in Contraction._fields_:
+        setattr(o, name, getattr(c, name))
+    return o
+
+
+def ocfg(c: MarchConfig):
+    return O.MarchConfig(c.step_size, c.early_stop_eps, c.alpha_thre, c.max_samples_per_ray,
+                         c.unbounded_step_growth)
+
+
+def close(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    assert a.shape == b.shape
+    tol = np.maximum(RTOL * np.maximum(np.abs(a), np.abs(b)), ATOL)
+    bad = np.abs(a - b) > tol
+    assert not bad.any(), f"{bad.sum()} mismatches, worst {np.abs(a - b).max()}"
+
+
+def same_packed(p, q):
+    for k in ("offsets", "counts", "t_starts", "t_ends", "ray_indices"):
+        assert np.array_equal(getattr(p, k), getattr(q, k)), k
+
+
+def both_grids(dev, orc, res, con, field, seeds, timestamps=(0.0,), thr=1e-2, init=0.0):
+    g = api.OccupancyGrid(res, con, thr, 0.0, init, dev=dev)
+    og = orc.grid(res, ocon(con), thr, 0.0, init)
+    for s in seeds:
+        g.update_field(field, 0.95, s, timestamps)
+        og.update_field(ofield(field), 0.95, s, timestamps)
+    return g, og
+
+
+# ------------------------------------------------------------------ occupancy grid
+@pytest.mark.parametrize("res", [128, 256])
+def test_grid_update_bit_exact_config5(dev, orc, res):
+    field = Field.sphere(**workload.SPHERE)
+    g, og = both_grids(dev, orc, res, Contraction.aabb(), field, workload.grid_warmup_seeds(16, 5))
+    assert np.array_equal(g.bits(), og.bits())
+    assert np.array_equal(g.density_cache(), og.cache())
+    assert g.occupied_fraction() == og.info()["occupied_fraction"]
+
+
+def test_grid_golden_config1(dev):
+    z = np.load(os.path.join(G, "c1.npz"))
+    field = Field.sphere(**workload.SPHERE)
+    g = api.OccupancyGrid(128, Contraction.aabb(), dev=dev)
+    for s in workload.grid_warmup_seeds(16, 5):
+        g.update_field(field, 0.95, s)
+    assert np.array_equal(g.packed_bits(), z["bits"])
+    assert np.array_equal(g.density_cache().astype(np.float32), z["cache"])
+
+
+@pytest.mark.parametrize("con", [Contraction.sphere((0.5, 0.5, 0.5), 0.5),
+                                 Contraction.aabb((-0.5, 0.0, 0.0), (1.5, 1.0, 2.0)),
+                                 Contraction.aabb((0.1, 0.2, 0.3), (0.9, 0.7, 1.0))])
+def test_grid_contractions_and_time(dev, orc, con):
+    field = Field.sphere(center=(0.3, 0.5, 0.5), radius=0.25, sigma=60.0, velocity=(0.3, 0.0, 0.1))
+    g, og = both_grids(dev, orc, 48, con, field, [1, 2, None, 3], timestamps=(0.0, 0.5, 1.0))
+    assert np.array_equal(g.bits(), og.bits())
+    assert np.array_equal(g.density_cache(), og.cache())
+    pts = np.random.default_rng(0).uniform(-0.6, 1.6, (20000, 3))
+    assert np.array_equal(g.query(pts), og.query(pts))
+
+
+def test_grid_callback_path_and_errors(dev, orc):
+    def fn(p, t):
+        return 30.0 * (np.sin(7 * p[:, 0] + t) > 0.3)
+
+    g = api.OccupancyGrid(24, Contraction.sphere((0.5, 0.5, 0.5), 0.6), dev=dev)
+    og = orc.grid(24, O.Contraction.sphere((0.5, 0.5, 0.5), 0.6))
+    g.update_over_time(fn, (0.0, 2.0), 0.9, 11)
+    og.update_callback(fn, 0.9, 11, (0.0, 2.0))
+    assert np.array_equal(g.density_cache(), og.cache()) and np.array_equal(g.bits(), og.bits())
+    bad = api.OccupancyGrid(4, Contraction.aabb(), dev=dev)
+    with pytest.raises(RuntimeError, match=r"^occupancy grid: invalid density at cell \(1,1,0\)$"):
+        bad.update(lambda p: np.where(np.arange(len(p)) == 5, -2.0, 1.0), 0.95)
+    with pytest.raises(ValueError, match="timestamps must be non-empty"):
+        bad.update_over_time(fn, [], 0.95)
+    with pytest.raises(ValueError, match="non-finite coordinate"):
+        bad.query([[np.nan, 0, 0]])
+
+
+def test_grid_invalid_sigma_field_names_first_cell(dev, orc):
+    f = Field.box((0.3, 0.3, 0.3), (0.6, 0.6, 0.6), sigma=-1.0)
+    g = api.OccupancyGrid(16, Contraction.aabb(), dev=dev)
+    og = orc.grid(16, O.Contraction.aabb())
+    with pytest.raises(O.OracleError) as e:
+        og.update_field(ofield(f), 0.95, 7)
+    with pytest.raises(RuntimeError) as e2:
+        g.update_field(f, 0.95, 7)
+    assert str(e2.value) == e.value.msg
+    assert np.array_equal(g.density_cache(), np.zeros(16 ** 3))  # grid untouched
+
+
+def test_grid_seed_fraction_and_ogrd(dev, orc):
+    rng = np.random.default_rng(3)
+    mask = (rng.uniform(size=32 ** 3) < 0.3).astype(np.uint8)
+    g = api.OccupancyGrid(32, Contraction.aabb(), dev=dev)
+    og = orc.grid(32, O.Contraction.aabb())
+    g.seed_mask(mask)
+    og.seed_mask(mask)
+    assert np.array_equal(g.bits(), og.bits()) and np.array_equal(g.density_cache(), og.cache())
+    with tempfile.TemporaryDirectory() as tmp:
+        gs = api.OccupancyGrid(16, Contraction.sphere((0.5, 0.5, 0.5), 0.75), 2e-2, 0.001, dev=dev)
+        gs.update_field(Field.sphere(radius=0.4, sigma=60.0), 0.95, 1234)
+        a = os.path.join(tmp, "a.ogrd")
+        gs.save(a)
+        lo = orc.grid_load(a)  # the reference reads our file
+        b = os.path.join(tmp, "b.ogrd")
+        lo.save(b)
+        assert open(a, "rb").read() == open(b, "rb").read()
+        lg = api.OccupancyGrid.load(b, dev)
+        assert np.array_equal(lg.bits(), lo.bits()) and np.array_equal(lg.density_cache(), lo.cache())
+
+
+# ------------------------------------------------------------------ marching
+def test_march_golden_config1(dev):
+    z = np.load(os.path.join(G, "c1.npz"))
+    field = Field.sphere(**workload.SPHERE)
+    g = api.OccupancyGrid(128, Contraction.aabb(), dev=dev)
+    for s in workload.grid_warmup_seeds(16, 5):
+        g.update_field(field, 0.95, s)
+    o, d = workload.orbit_rays(64)
+    st = MarchStats()
+    p = api.march(api.RayBatch.create(o, d, 0.2, 1.0, dev), g, field, MarchConfig(5e-3, 1e-4, 1e-2),
+                  stats=st)
+    for k in ("offsets", "counts", "t_starts", "t_ends", "ray_indices"):
+        assert np.array_equal(getattr(p, k), z[k]), k
+    assert st.samples_emitted == 107555 and st.samples_kept == 19362
+
+
+@pytest.mark.parametrize("cfg", [MarchConfig(5e-3, 1e-4, 1e-2), MarchConfig(1.6914558667664816e-3),
+                                 MarchConfig(0.011, 0.0, 0.0), MarchConfig(5e-3, 0.5, 0.3),
+                                 MarchConfig(0.003, 1e-3, 0.0, max_samples_per_ray=7)])
+def test_march_field_bit_exact(dev, orc, cfg):
+    field = Field.sphere(**workload.SPHERE)
+    g, og = both_grids(dev, orc, 64, Contraction.aabb(), field, workload.grid_warmup_seeds(6, 5))
+    o, d = workload.orbit_rays(96, angle=0.3)
+    rng = np.random.default_rng(1)
+    ro = rng.uniform(-0.2, 1.2, (3000, 3))
+    rd = rng.normal(size=(3000, 3))
+    rd /= np.sqrt((rd * rd).sum(1))[:, None]
+    for (oo, dd, near, far) in [(o, d, 0.2, 1.0), (ro, rd, 0.0, 1.7)]:
+        st = MarchStats()
+        p = api.march(api.RayBatch.create(oo, dd, near, far, dev), g, field, cfg, stats=st)
+        q = orc.march_field(oo, dd, near, far, og, ofield(field), ocfg(cfg), 4)
+        same_packed(p, q)
+        assert st.samples_emitted == q.samples_emitted
+
+
+def test_march_other_fields_and_boxes(dev, orc):
+    con = Contraction.aabb((-1.0, -0.5, 0.0), (1.0, 1.5, 3.0))  # non power-of-two sizes
+    for field in (Field.box((-0.5, 0.0, 0.5), (0.5, 1.0, 2.0), 30.0, (0.2, 0.3, 0.4)),
+                  Field.checker(0.3, 4.0, (0.9, 0.1, 0.2), (0.1, 0.8, 0.3))):
+        g, og = both_grids(dev, orc, 40, con, field, [5, 6])
+        rng = np.random.default_rng(2)
+        ro = rng.uniform(-1.2, 1.2, (2000, 3))
+        rd = rng.normal(size=(2000, 3))
+        rd /= np.sqrt((rd * rd).sum(1))[:, None]
+        cfg = MarchConfig(0.02, 1e-3, 1e-2)
+        p = api.march(api.RayBatch.create(ro, rd, 0.0, 4.0, dev), g, field, cfg)
+        same_packed(p, orc.march_field(ro, rd, 0.0, 4.0, og, ofield(field), ocfg(cfg), 4))
+
+
+def test_march_growth_golden(dev):
+    z = np.load(os.path.join(G, "growth.npz"))
+    con = Contraction.sphere((0.5, 0.5, 0.5), 0.5)
+    field = Field.sphere(radius=0.3, sigma=40.0)
+    g = api.OccupancyGrid(64, con, dev=dev)
+    for s in (1, 2, 3):
+        g.update_field(field, 0.95, s)
+    assert np.array_equal(g.packed_bits(), z["bits"])
+    cfg = MarchConfig(1.6914558667664816e-3, 1e-4, 1e-2, 2048, 1.01)
+    st = MarchStats()
+    p = api.march(api.RayBatch.create(z["origins"], z["dirs"], 0.01, 100.0, dev), g, field, cfg, stats=st)
+    for k in ("offsets", "counts", "t_starts", "t_ends", "ray_indices"):
+        assert np.array_equal(getattr(p, k), z[k]), k
+    assert st.samples_emitted == z["emitted"]
+
+
+def test_march_callback_and_errors(dev, orc):
+    field = Field.sphere(**workload.SPHERE)
+    g, og = both_grids(dev, orc, 32, Contraction.aabb(), field, [1, 2])
+    o, d = workload.orbit_rays(24)
+
+    def sig(ts, te, idx):
+        mid = 0.5 * (ts + te)
+        return 50.0 * (0.5 + 0.5 * np.sin(20 * mid))
+
+    cfg = MarchConfig(0.01, 1e-3, 0.0)
+    st = MarchStats()
+    p = api.march(api.RayBatch.create(o, d, 0.2, 1.0, dev), g, sig, cfg, stats=st)
+    q = orc.march_callback(o, d, 0.2, 1.0, og, sig, ocfg(cfg))
+    same_packed(p, q)
+    assert st.samples_emitted == q.samples_emitted
+    full = api.OccupancyGrid(8, Contraction.aabb(), 1e-2, 0.0, 1e6, dev=dev)
+    rays = api.RayBatch.create([[0.0, 0.5, 0.5]], [[1.0, 0.0, 0.0]], 0.2, 1.0, dev)
+    with pytest.raises(RuntimeError, match=r"^marching: non-finite density at ray 0 sample 7$"):
+        api.march(rays, full, lambda ts, te, i: np.r_[np.ones(len(ts) - 1), np.nan], MarchConfig(0.1))
+    with pytest.raises(RuntimeError, match=r"^marching: sigma_fn returned 9 values for 8 samples$"):
+        api.march(rays, full, lambda ts, te, i: np.ones(len(ts) + 1), MarchConfig(0.1))
+    with pytest.raises(RuntimeError, match=r"^marching: negative density at ray 0 sample 3$"):
+        api.march(rays, full, lambda ts, te, i: np.where(np.arange(len(ts)) == 3, -1.0, 0.5), MarchConfig(0.1))
+    def second_ray_negative(ts, te, idx):
+        return np.full(len(ts), -1.0 if idx[0] == 1 else 0.5)
+
+    two = api.RayBatch.create([[0.0, 0.5, 0.5]] * 2, [[1.0, 0.0, 0.0]] * 2, 0.2, 1.0, dev)
+    with pytest.raises(RuntimeError, match=r"^marching: negative density at ray 1 sample 0$"):
+        api.march(two, full, second_ray_negative, MarchConfig(0.1))
+    with pytest.raises(RuntimeError, match=r"^marching: negative density at ray 0 sample 0$"):
+        api.march(rays, full, Field.box((0, 0, 0), (1, 1, 1), -1.0), MarchConfig(0.1))
+    with pytest.raises(ValueError, match="step_size must be > 0"):
+        api.march(rays, full, field, MarchConfig(0.0))
+    with pytest.raises(ValueError, match="non-unit direction at index 1"):
+        api.RayBatch.create([[0, 0, 0]] * 2, [[1, 0, 0], [1, 1, 0]], 0.2, 1.0, dev)
+
+
+def test_march_uniform(dev, orc):
+    rng = np.random.default_rng(7)
+    o = rng.uniform(0, 1, (64, 3))
+    d = rng.normal(size=(64, 3))
+    d /= np.sqrt((d * d).sum(1))[:, None]
+    for near, far, step in [(0.2, 1.0, 0.1), (0.2, 0.25, 0.1), (0.0, 3.0, 0.0137)]:
+        p = api.march_uniform(api.RayBatch.create(o, d, near, far, dev), MarchConfig(step), dev)
+        same_packed(p, orc.march_uniform(o, d, near, far, O.MarchConfig(step)))
+    empty = api.march_uniform(api.RayBatch.create(np.zeros((0, 3)), np.zeros((0, 3)), 0.2, 1.0, dev),
+                              MarchConfig(0.1), dev)
+    assert empty.n_rays == 0 and empty.n_samples == 0
+
+
+def test_march_large_batch_matches_reference(dev, orc):
+    """2^20 rays of the bench camera (config 4 size) against the oracle."""
+    field = Field.sphere(**workload.SPHERE)
+    g, og = both_grids(dev, orc, 128, Contraction.aabb(), field, workload.grid_warmup_seeds(16, 5))
+    o, d = workload.orbit_rays(1024)
+    cfg = MarchConfig(5e-3, 1e-4, 1e-2)
+    p = api.march(api.RayBatch.create(o, d, 0.2, 1.0, dev), g, field, cfg)
+    q = orc.march_field(o, d, 0.2, 1.0, og, ofield(field), ocfg(cfg), os.cpu_count() or 1)
+    same_packed(p, q)
+    assert p.n_samples == 4951339
+
+
+# ------------------------------------------------------------------ packing
+def test_pack_and_validate(dev, orc):
+    off, idx = api.pack([2, 0, 3], dev)
+    assert list(off) == [0, 2, 2] and list(idx) == [0, 0, 2, 2, 2]
+    off, idx = api.pack([], dev)
+    assert len(off) == 0 and len(idx) == 0
+    rng = np.random.default_rng(4)
+    c = rng.integers(0, 9, 100000).astype(np.uint32)
+    o1, i1 = api.pack(c, dev)
+    o2, i2 = orc.pack(c)
+    assert np.array_equal(o1, o2) and np.array_equal(i1, i2)
+    with pytest.raises(ValueError, match="sample count exceeds 32-bit index range"):
+        api.pack(np.array([0x80000000, 0x80000001], np.uint32), dev)
+    counts = np.array([2, 0, 3], np.uint32)
+    off, idx = orc.pack(counts)
+    ts = np.array([0.1, 0.3, 0.0, 0.2, 0.5])
+    te = np.array([0.2, 0.4, 0.1, 0.3, 0.6])
+    cases = [(off, counts, ts, te, idx), (np.array([0, 1, 2], np.uint32), counts, ts, te, idx),
+             (off, counts, ts, np.where(np.arange(5) == 3, 0.2, te), idx),
+             (off, counts, np.array([0.1, 0.3, 0.3, 0.2, 0.5]), te, idx),
+             (off, counts, ts, np.array([0.2, 0.4, 0.1, 0.35, 0.6]), idx),
+             (off, counts, ts, te, np.array([0, 0, 2, 1, 2], np.uint32)),
+             (off, counts, ts[:4], te, idx)]
+    for c_ in cases:
+        assert api.validate(api.PackedSamples(*c_), dev) == orc.validate(*c_)
+
+
+# ------------------------------------------------------------------ rendering
+def test_render_golden_instances(dev):
+    z = np.load(os.path.join(G, "render.npz"))
+    for i in range(60):
+        k = lambda n: z[f"{i}_{n}"]  # noqa: E731
+        p = api.PackedSamples(k("offsets"), k("counts"), k("t_starts"), k("t_ends"),
+                              np.repeat(np.arange(len(k("counts")), dtype=np.uint32), k("counts")))
+        close(api.transmittance(p, k("sigmas"), dev), k("trans"))
+        c, o, d = api.render_forward(p, k("rgbs"), k("sigmas"), dev=dev)
+        close(c, k("color")), close(o, k("opacity")), close(d, k("depth"))
+        dr, ds = api.render_backward(p, k("rgbs"), k("sigmas"), k("d_color"), k("d_opacity"),
+                                     k("d_depth"), dev=dev)
+        close(dr, k("d_rgbs")), close(ds, k("d_sigmas"))
+        close(api.render_attribute(p, k("sigmas"), k("values"), 2, dev), k("attr"))
+
+
+def _instance(rng, n_rays, max_per_ray, contiguous=True):
+    counts = rng.integers(0, max_per_ray + 1, n_rays).astype(np.uint32)
+    offsets = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.uint32)
+    s = int(counts.sum())
+    ts = np.empty(s)
+    te = np.empty(s)
+    for r in range(n_rays):
+        b, c = offsets[r], counts[r]
+        w = rng.uniform(0.01, 0.2, c)
+        t0 = rng.uniform(0, 0.5) + np.concatenate([[0], np.cumsum(w)[:-1]])
+        ts[b:b + c], te[b:b + c] = t0, t0 + w
+    p = O.Packed(offsets, counts, ts, te, np.repeat(np.arange(n_rays, dtype=np.uint32), counts))
+    if not contiguous:  # reverse the ray order of the storage: offsets no longer ascending
+        perm = np.arange(n_rays)[::-1]
+        new_off = np.zeros(n_rays, np.uint32)
+        ts2, te2, at = np.empty(s), np.empty(s), 0
+        for r in perm:
+            b, c = offsets[r], counts[r]
+            ts2[at:at + c], te2[at:at + c] = ts[b:b + c], te[b:b + c]
+            new_off[r] = at
+            at += c
+        p = O.Packed(new_off, counts, ts2, te2, np.zeros(s, np.uint32))
+    return p, rng.uniform(0, 1, (s, 3)), rng.uniform(0, 8, s)
+
+
+@pytest.mark.parametrize("n_rays,max_per_ray,contiguous",
+                         [(3000, 12, True), (500, 300, True), (257, 40, False), (64, 2048, True)])
+def test_render_paths_vs_oracle(dev, orc, n_rays, max_per_ray, contiguous):
+    rng = np.random.default_rng(n_rays)
+    p, rgb, sig = _instance(rng, n_rays, max_per_ray, contiguous)
+    n = p.n_rays
+    dc, do, dd = rng.uniform(-1, 1, (n, 3)), rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    ap = api.PackedSamples(p.offsets, p.counts, p.t_starts, p.t_ends, p.ray_indices)
+    for dtype in (np.float64, np.float32):
+        r32 = rgb.astype(dtype).astype(np.float64)
+        s32 = sig.astype(dtype).astype(np.float64)
+        ref_f = orc.render_forward(p, r32, s32)
+        ref_b = orc.render_backward(p, r32, s32, dc.astype(dtype), do.astype(dtype), dd.astype(dtype))
+        got_f = api.render_forward(ap, r32, s32, dev=dev, dtype=dtype)
+        got_b = api.render_backward(ap, r32, s32, dc, do, dd, dev=dev, dtype=dtype)
+        for a, b in zip(got_f, ref_f):
+            close(a, b)
+        for a, b in zip(got_b, ref_b):
+            close(a, b)
+    close(api.transmittance(ap, sig, dev), orc.transmittance(p, sig))
+
+
+def test_render_closed_forms(dev):
+    p = api.PackedSamples(np.array([0], np.uint32), np.array([2], np.uint32), np.array([0.0, 1.0]),
+                          np.array([1.0, 2.0]), np.array([0, 0], np.uint32))
+    c, o, _ = api.render_forward(p, [[1, 0, 0], [0, 1, 0]], [np.log(2.0)] * 2, dev=dev)
+    assert abs(c[0, 0] - 0.5) < 1e-12 and abs(c[0, 1] - 0.25) < 1e-12 and c[0, 2] == 0.0
+    assert abs(o[0] - 0.75) < 1e-12
+    t = api.transmittance(p, [np.log(2.0), 3.0], dev)
+    assert t[0] == 1.0 and abs(t[1] - 0.5) < 1e-12
+    with pytest.raises(ValueError, match="attribute length mismatch"):
+        api.render_forward(p, [[1, 1, 1]], [1.0], dev=dev)
+    z = api.PackedSamples(np.array([0, 0], np.uint32), np.array([0, 0], np.uint32))
+    _, o, _ = api.render_forward(z, np.zeros((0, 3)), np.zeros(0), dev=dev)
+    assert list(o) == [0.0, 0.0]
