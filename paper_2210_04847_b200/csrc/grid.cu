@@ -172,11 +172,20 @@ __global__ void k_coarse(const uint32_t* __restrict__ bits, uint32_t res, uint32
             int y0 = max(ky * int(block) - 1, 0), y1 = min((ky + 1) * int(block), int(res) - 1);
             int z0 = max(kz * int(block) - 1, 0), z1 = min((kz + 1) * int(block), int(res) - 1);
             for (int z = z0; z <= z1 && !any; ++z)
-                for (int y = y0; y <= y1 && !any; ++y)
-                    for (int x = x0; x <= x1; ++x) {
-                        uint64_t c = uint64_t(x) + uint64_t(res) * (uint64_t(y) + uint64_t(res) * z);
-                        if ((bits[c >> 5] >> (c & 31)) & 1u) { any = true; break; }
+                for (int y = y0; y <= y1 && !any; ++y) {
+                    // cells [row + x0, row + x1] of one x-row: OR of masked words
+                    uint64_t row = (uint64_t(y) + uint64_t(res) * uint64_t(z)) * res;
+                    uint64_t c0 = row + x0, c1 = row + x1;
+                    for (uint64_t w = c0 >> 5; w <= (c1 >> 5); ++w) {
+                        uint32_t lo = w == (c0 >> 5) ? uint32_t(c0 & 31) : 0u;
+                        uint32_t hi = w == (c1 >> 5) ? uint32_t(c1 & 31) : 31u;
+                        uint32_t mask = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
+                        if (__ldg(bits + w) & mask) {
+                            any = true;
+                            break;
+                        }
                     }
+                }
         }
         unsigned word = __ballot_sync(0xffffffffu, any);
         if (lane == 0) coarse[w] = word;

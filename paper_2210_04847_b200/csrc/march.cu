@@ -33,7 +33,7 @@ int check_contraction(const vmb_contraction* c);
 
 namespace {
 
-enum Mode { COUNT = 0, FILL = 1 };
+enum Mode { COUNT = 0, FILL = 1, BUFFER = 2 };
 
 struct MarchParams {
     Contract k;
@@ -51,6 +51,8 @@ struct MarchParams {
     double ball_r;
     double eps, thr;
     uint32_t max_cand;
+    bool fast;            // fp32 DDA + filtered fp32 cell test (walk_fast)
+    float step_f, m0_f, inv_step_f, near_f, far_f, Mf;
     bool full;            // walk to the end (stats / candidate mode), ignore the T cut
     bool filter;          // apply inline density + alpha floor + T cut
     vmb_field f;
@@ -79,12 +81,16 @@ struct Sink {
     uint32_t* idx = nullptr;
     uint64_t base = 0;
     uint64_t cap = 0;
+    // BUFFER (fused single-pass kernel): kept lattice indices go to shared memory
+    uint32_t* buf = nullptr;
+    uint32_t buf_stride = 0;
+    uint32_t buf_cap = 0;
 };
 
 // Handles one grid-passing candidate. Mirrors ray_marching.cpp:78,111-137.
 template <int MODE>
-__device__ __forceinline__ bool on_candidate(const MarchParams& P, Sink& s, double t0, double t1,
-                                             D3 p, DevError* err) {
+__device__ __forceinline__ bool on_candidate(const MarchParams& P, Sink& s, uint64_t i, double t0,
+                                             double t1, D3 p, DevError* err) {
     if (s.n_cand >= P.max_cand) return false;  // candidate cap (:78 / :91)
     uint32_t ci = s.n_cand++;
     if (!P.filter) {  // candidate mode: keep every grid-passing interval
@@ -96,6 +102,7 @@ __device__ __forceinline__ bool on_candidate(const MarchParams& P, Sink& s, doub
                 s.idx[o] = uint32_t(s.ray);
             }
         }
+        if (MODE == BUFFER && s.n_kept < s.buf_cap) s.buf[s.n_kept * s.buf_stride] = uint32_t(i);
         s.n_kept++;
         return true;
     }
@@ -118,6 +125,7 @@ __device__ __forceinline__ bool on_candidate(const MarchParams& P, Sink& s, doub
             s.idx[o] = uint32_t(s.ray);
         }
     }
+    if (MODE == BUFFER && s.n_kept < s.buf_cap) s.buf[s.n_kept * s.buf_stride] = uint32_t(i);
     s.n_kept++;
     s.T *= 1.0 - alpha;
     if (s.T < P.eps) {
@@ -143,7 +151,7 @@ __device__ __forceinline__ bool eval_step(const MarchParams& P, Sink& s, D3 o, D
     }
     int64_t c = cell_of_point(P.k, P.res, p);
     if (c >= 0 && fine_bit(P.bits, c)) {
-        if (!on_candidate<MODE>(P, s, t0, t1, p, err)) {
+        if (!on_candidate<MODE>(P, s, i, t0, t1, p, err)) {
             *alive = false;
             return false;
         }
@@ -152,7 +160,7 @@ __device__ __forceinline__ bool eval_step(const MarchParams& P, Sink& s, D3 o, D
 }
 
 __device__ __forceinline__ bool coarse_bit(const MarchParams& P, int cx, int cy, int cz) {
-    uint64_t kc = uint64_t(cx) + uint64_t(P.res_c) * (uint64_t(cy) + uint64_t(P.res_c) * uint64_t(cz));
+    uint32_t kc = uint32_t(cx) + P.res_c * (uint32_t(cy) + P.res_c * uint32_t(cz));
     return (__ldg(P.coarse + (kc >> 5)) >> (kc & 31)) & 1u;
 }
 
@@ -225,10 +233,19 @@ __device__ void walk_skip(const MarchParams& P, Sink& s, D3 o, D3 d, DevError* e
             if (next_i > last) return;
         }
         if (tn >= thi) return;
-        int a = (tmax[0] <= tmax[1]) ? ((tmax[0] <= tmax[2]) ? 0 : 2) : ((tmax[1] <= tmax[2]) ? 1 : 2);
-        c[a] += stp[a];
-        if (c[a] < 0 || c[a] >= Rc) return;
-        tmax[a] += tdel[a];
+        if (tmax[0] <= tmax[1] && tmax[0] <= tmax[2]) {
+            c[0] += stp[0];
+            if (c[0] < 0 || c[0] >= Rc) return;
+            tmax[0] += tdel[0];
+        } else if (tmax[1] <= tmax[2]) {
+            c[1] += stp[1];
+            if (c[1] < 0 || c[1] >= Rc) return;
+            tmax[1] += tdel[1];
+        } else {
+            c[2] += stp[2];
+            if (c[2] < 0 || c[2] >= Rc) return;
+            tmax[2] += tdel[2];
+        }
         t = tn;
     }
 }
@@ -255,12 +272,272 @@ __device__ void walk_growth(const MarchParams& P, Sink& s, D3 o, D3 d, DevError*
         }
         int64_t c = cell_of_point(P.k, P.res, mid);
         if (c >= 0 && fine_bit(P.bits, c))
-            if (!on_candidate<MODE>(P, s, t, t1, mid, err)) return;
+            if (!on_candidate<MODE>(P, s, s.n_cand, t, t1, mid, err)) return;
         t += dt;
         if (norm(mid - P.ball_c) > P.ball_r)
             dt *= P.growth;
         else
             dt = P.step;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Fast walk (AABB, bounded lattice): fp32 coarse DDA + FILTERED fp32 cell test.
+//
+// For lattice step j the cell coordinate along axis a is u_a = A_a + B_a * m_j
+// (fine-cell units, A = (o - lo) R / size, B = d R / size, m_j the step midpoint).
+// It is evaluated in fp32 with one FMA; the fp32 value differs from the real value
+// by at most E = 2^-22 (2 max|A| + 5 max|B| M) (a >3x over-estimate of the
+// rounding of A, B, m and the FMA; M = max(|near|, |far|)), while the reference's
+// fp64 evaluation differs from the real value by ~1e-13 cells. Hence when every
+// fp32 coordinate is more than E away from an integer, floor() of the fp32 value
+// IS the reference's cell (and its in/out-of-domain decision). Otherwise — and
+// for the last, possibly far-clamped step — the step is re-evaluated with the
+// exact fp64 code (eval_step). Candidates always get exact t0/t1/midpoint.
+// ---------------------------------------------------------------------------
+template <int MODE>
+__device__ void walk_fast(const MarchParams& P, Sink& s, D3 o, D3 d, DevError* err) {
+    if (P.n_steps == 0) return;
+    const float Rf = float(P.res);
+    float A[3] = {float((o.x - P.k.lo.x) * P.scale[0]), float((o.y - P.k.lo.y) * P.scale[1]),
+                  float((o.z - P.k.lo.z) * P.scale[2])};
+    float B[3] = {float(d.x * P.scale[0]), float(d.y * P.scale[1]), float(d.z * P.scale[2])};
+    const float amax = fmaxf(fmaxf(fabsf(A[0]), fabsf(A[1])), fabsf(A[2]));
+    const float bmax = fmaxf(fmaxf(fabsf(B[0]), fabsf(B[1])), fabsf(B[2]));
+    const float E = ldexpf(2.0f * amax + 5.0f * bmax * P.Mf, -22) + 1e-6f;
+    const bool fast_ok = E < 0.05f;
+    const float EPSD = 1e-3f + 4.0f * E;  // domain guard for the fp32 clip
+    float tlo = P.near_f, thi = P.far_f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {  // ray_aabb_intersect against the guarded domain
+        if (B[a] == 0.0f) {
+            if (A[a] < -EPSD || A[a] > Rf + EPSD) return;
+        } else {
+            float inv = __frcp_rn(B[a]);
+            float ta = (-EPSD - A[a]) * inv, tb = (Rf + EPSD - A[a]) * inv;
+            tlo = fmaxf(tlo, fminf(ta, tb));
+            thi = fminf(thi, fmaxf(ta, tb));
+        }
+    }
+    if (!(tlo <= thi)) return;
+    const float Bs = float(P.block);
+    const float inv_bs = 1.0f / Bs;  // block is a power of two
+    const int Rc = int(P.res_c);
+    int c[3], stp[3];
+    float tmax[3], tdel[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        int ca = int(floorf(fmaf(B[a], tlo, A[a]) * inv_bs));
+        ca = ca < 0 ? 0 : (ca >= Rc ? Rc - 1 : ca);
+        c[a] = ca;
+        // approximate reciprocals are fine here: the DDA only has to stay within
+        // the 1-cell dilation halo (fp32 error ~1e-5 cells)
+        if (B[a] > 0.0f) {
+            stp[a] = 1;
+            float ib = __frcp_rn(B[a]);
+            tmax[a] = (float(ca + 1) * Bs - A[a]) * ib;
+            tdel[a] = Bs * ib;
+        } else if (B[a] < 0.0f) {
+            stp[a] = -1;
+            float ib = __frcp_rn(B[a]);
+            tmax[a] = (float(ca) * Bs - A[a]) * ib;
+            tdel[a] = -Bs * ib;
+        } else {
+            stp[a] = 0;
+            tmax[a] = INFINITY;
+            tdel[a] = INFINITY;
+        }
+    }
+    const int last = int(P.n_steps) - 1;
+    int next_i = 0;
+    float t = tlo;
+    bool alive = true;
+    for (int guard = 0; guard < 4 * (3 * Rc + 3); ++guard) {
+        float tn = fminf(fminf(tmax[0], tmax[1]), fminf(tmax[2], thi));
+        if (coarse_bit(P, c[0], c[1], c[2])) {
+            int jlo = int(floorf((t - P.near_f) * P.inv_step_f)) - 2;
+            int jhi = int(floorf((fmaxf(tn, t) - P.near_f) * P.inv_step_f)) + 2;
+            if (jlo < next_i) jlo = next_i;
+            if (jhi > last) jhi = last;
+            for (int j = jlo; j <= jhi; ++j) {
+                bool exact = !fast_ok || j == last;
+                if (!exact) {
+                    float m = fmaf(float(j), P.step_f, P.m0_f);
+                    float u0 = fmaf(B[0], m, A[0]), u1 = fmaf(B[1], m, A[1]), u2 = fmaf(B[2], m, A[2]);
+                    float f0 = floorf(u0), f1 = floorf(u1), f2 = floorf(u2);
+                    float r0 = u0 - f0, r1 = u1 - f1, r2 = u2 - f2;
+                    exact = r0 < E || r0 > 1.0f - E || r1 < E || r1 > 1.0f - E || r2 < E ||
+                            r2 > 1.0f - E;
+                    if (!exact) {
+                        if (f0 < 0.0f || f0 >= Rf || f1 < 0.0f || f1 >= Rf || f2 < 0.0f || f2 >= Rf)
+                            continue;  // definitely outside the domain
+                        // 32-bit index: the fast walk is enabled only for R <= 1024
+                        uint32_t cell = uint32_t(f0) + P.res * (uint32_t(f1) + P.res * uint32_t(f2));
+                        if (!((__ldg(P.bits + (cell >> 5)) >> (cell & 31)) & 1u)) continue;
+                        double t0 = P.near_ + double(j) * P.step;
+                        double t1 = min_ref(P.near_ + double(j + 1) * P.step, P.far_);
+                        D3 p = o + d * (0.5 * (t0 + t1));
+                        if (!on_candidate<MODE>(P, s, uint64_t(j), t0, t1, p, err)) return;
+                        continue;
+                    }
+                }
+                if (!eval_step<MODE>(P, s, o, d, uint64_t(j), err, &alive)) return;
+            }
+            if (jhi + 1 > next_i) next_i = jhi + 1;
+            if (next_i > last) return;
+        }
+        if (tn >= thi) return;
+        // advance along the axis with the nearest boundary (explicit branches keep
+        // the DDA state in registers)
+        if (tmax[0] <= tmax[1] && tmax[0] <= tmax[2]) {
+            c[0] += stp[0];
+            if (c[0] < 0 || c[0] >= Rc) return;
+            tmax[0] += tdel[0];
+        } else if (tmax[1] <= tmax[2]) {
+            c[1] += stp[1];
+            if (c[1] < 0 || c[1] >= Rc) return;
+            tmax[1] += tdel[1];
+        } else {
+            c[2] += stp[2];
+            if (c[2] < 0 || c[2] >= Rc) return;
+            tmax[2] += tdel[2];
+        }
+        t = tn;
+    }
+}
+
+__device__ __forceinline__ bool ray_safe(const MarchParams& P, D3 o, D3 d) {
+    // Overflowing midpoints can only occur for astronomically large inputs; such
+    // rays take the dense walk so every step is checked as the reference does.
+    double mag = fmax(fmax(fabs(o.x), fabs(o.y)), fabs(o.z)) +
+                 fmax(fmax(fabs(d.x), fabs(d.y)), fabs(d.z)) * fmax(fabs(P.near_), fabs(P.far_));
+    return mag < 1e300;
+}
+
+template <int MODE>
+__device__ __forceinline__ void walk(const MarchParams& P, Sink& s, D3 o, D3 d, DevError* err) {
+    bool safe = ray_safe(P, o, d);
+    if (P.grows)
+        walk_growth<MODE>(P, s, o, d, err);
+    else if (P.fast && safe)
+        walk_fast<MODE>(P, s, o, d, err);
+    else if (P.skip && safe)
+        walk_skip<MODE>(P, s, o, d, err);
+    else
+        walk_dense<MODE>(P, s, o, d, err);
+}
+
+// ---------------------------------------------------------------------------
+// Packed march, walk + expand:
+//   k_march_walk   persistent warps steal 32-ray chunks from an atomic counter
+//                  (no CTA barrier, no cross-CTA waiting: a warp that finishes
+//                  early just takes the next chunk); each ray writes its kept
+//                  count and the lattice indices of its first kWalkCap kept
+//                  samples into a chunk-major scratch [chunk][k][lane] (u32).
+//   scan           counts -> offsets (scan.cu)
+//   k_march_expand warp per chunk; the chunk's samples are one contiguous output
+//                  range, written coalesced: each lane finds the owning ray of its
+//                  output slot by a shuffle binary search over the 32 offsets and
+//                  re-materialises t0/t1 from the lattice index with the exact
+//                  reference expressions.
+//   k_march_fixup  re-walks the rare rays with more than kWalkCap kept samples.
+// ---------------------------------------------------------------------------
+constexpr int kWalkCap = 24;
+
+template <typename RT>
+__global__ void __launch_bounds__(128, 6) k_march_walk(
+    MarchParams P, const RT* __restrict__ orig, const RT* __restrict__ dirs, uint64_t n_rays,
+    uint32_t* __restrict__ counts, uint32_t* __restrict__ kept_idx, unsigned int* chunk_counter,
+    uint64_t n_chunks, unsigned long long* emitted, DevError* err) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long emit_local = 0;
+    for (;;) {
+        unsigned int chunk = 0;
+        if (lane == 0) chunk = atomicAdd(chunk_counter, 1u);
+        chunk = __shfl_sync(0xffffffffu, chunk, 0);
+        if (chunk >= n_chunks) break;
+        const uint64_t r = uint64_t(chunk) * 32 + lane;
+        if (r < n_rays) {
+            Sink s;
+            s.ray = r;
+            s.buf = kept_idx + uint64_t(chunk) * (kWalkCap * 32) + lane;
+            s.buf_stride = 32;
+            s.buf_cap = kWalkCap;
+            walk<BUFFER>(P, s, load3(orig, r), load3(dirs, r), err);
+            counts[r] = s.n_kept;
+            emit_local += s.n_cand;
+        }
+        __syncwarp();
+    }
+    if (emitted) {
+        for (int o = 16; o > 0; o >>= 1) emit_local += __shfl_xor_sync(0xffffffffu, emit_local, o);
+        if (lane == 0 && emit_local) atomicAdd(emitted, emit_local);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_march_expand(
+    double near_, double far_, double step, const uint32_t* __restrict__ counts,
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ kept_idx, uint64_t n_rays,
+    double* __restrict__ ts, double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,
+    uint32_t* __restrict__ overflow, unsigned int* n_overflow) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t n_chunks = (n_rays + 31) / 32;
+    for (uint64_t chunk = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; chunk < n_chunks;
+         chunk += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const uint64_t r = chunk * 32 + lane;
+        const bool valid = r < n_rays;
+        const uint32_t cnt = valid ? counts[r] : 0u;
+        const uint32_t off = valid ? offsets[r] : 0xffffffffu;
+        if (cnt > uint32_t(kWalkCap)) overflow[atomicAdd(n_overflow, 1u)] = uint32_t(r);
+        const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+        const int last = 31 - __clz(vmask);
+        const uint64_t base = __shfl_sync(0xffffffffu, off, 0);
+        const uint64_t end = uint64_t(__shfl_sync(0xffffffffu, off, last)) +
+                             __shfl_sync(0xffffffffu, cnt, last);
+        const uint32_t* kbuf = kept_idx + chunk * (kWalkCap * 32);
+        for (uint64_t p0 = base; p0 < end; p0 += 32) {
+            const uint64_t p = p0 + lane;
+            // owner = largest lane L with off_L <= p (zero-count lanes share the
+            // next lane's offset, so the largest such lane owns the slot)
+            int L = 0;
+#pragma unroll
+            for (int stride = 16; stride > 0; stride >>= 1) {
+                int c = L + stride;
+                uint32_t v = __shfl_sync(0xffffffffu, off, c & 31);
+                if (c < 32 && uint64_t(v) <= p) L = c;
+            }
+            const uint32_t loff = __shfl_sync(0xffffffffu, off, L);
+            if (p < end && p < cap) {
+                const uint64_t k = p - loff;
+                if (k < uint64_t(kWalkCap)) {
+                    const uint64_t i = kbuf[k * 32 + L];
+                    ts[p] = near_ + double(i) * step;
+                    te[p] = min_ref(near_ + double(i + 1) * step, far_);
+                    idx[p] = uint32_t(chunk * 32 + L);
+                }
+            }
+        }
+    }
+}
+
+// Re-walks the (rare) rays whose kept samples overflowed the shared buffer.
+template <typename RT>
+__global__ void k_march_fixup(MarchParams P, const RT* __restrict__ orig, const RT* __restrict__ dirs,
+                              const uint32_t* __restrict__ offsets, double* __restrict__ ts,
+                              double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,
+                              const uint32_t* __restrict__ overflow, const unsigned int* n_overflow,
+                              DevError* err) {
+    const unsigned int n = *n_overflow;
+    for (unsigned int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        uint64_t r = overflow[k];
+        Sink s;
+        s.ray = r;
+        s.ts = ts;
+        s.te = te;
+        s.idx = idx;
+        s.base = offsets[r];
+        s.cap = cap;
+        walk<FILL>(P, s, load3(orig, r), load3(dirs, r), err);
     }
 }
 
@@ -285,17 +562,7 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, const RT* __restri
             s.base = offsets[r];
             s.cap = cap;
         }
-        // Overflowing midpoints can only occur for astronomically large inputs; such
-        // rays take the dense walk so every step is checked as the reference does.
-        double mag = fmax(fmax(fabs(o.x), fabs(o.y)), fabs(o.z)) +
-                     fmax(fmax(fabs(d.x), fabs(d.y)), fabs(d.z)) * fmax(fabs(P.near_), fabs(P.far_));
-        bool safe = mag < 1e300;
-        if (P.grows)
-            walk_growth<MODE>(P, s, o, d, err);
-        else if (P.skip && safe)
-            walk_skip<MODE>(P, s, o, d, err);
-        else
-            walk_dense<MODE>(P, s, o, d, err);
+        walk<MODE>(P, s, o, d, err);
         if (MODE == COUNT) counts[r] = s.n_kept;
         emit_local += s.n_cand;
     }
@@ -423,6 +690,15 @@ int march_params(const vmb_grid* g, const vmb_rays* rays, const vmb_march_config
     uint64_t n = uniform_step_count(P->near_, P->far_, P->step);
     P->n_steps = effective_steps(P->near_, P->far_, P->step, n, &exact);
     P->skip = g->con.kind == VMB_CONTRACT_AABB && exact && !P->grows;
+    // fp32 fast walk: lattice indices and step-range conversions stay well inside
+    // fp32 resolution for lattices up to 2^20 steps.
+    P->fast = P->skip && P->n_steps < (1ull << 20) && P->n_steps > 0 && g->res <= 1024;
+    P->step_f = float(P->step);
+    P->m0_f = float(P->near_ + 0.5 * P->step);
+    P->inv_step_f = float(1.0 / P->step);
+    P->near_f = float(P->near_);
+    P->far_f = float(P->far_);
+    P->Mf = float(fmax(fabs(P->near_), fabs(P->far_)));
     return VMB_OK;
 }
 
@@ -463,7 +739,74 @@ int report_march_error(vmb_ctx* ctx) {
     return fail(low == 0 ? VMB_INVALID_ARGUMENT : VMB_RUNTIME, march_error_text(err));
 }
 
-// count -> scan -> (sync) -> fill, shared by march_field and march_candidates.
+// VMB_MARCH_IMPL=twopass forces the count -> scan -> fill pipeline (A/B tests).
+bool use_fused(const MarchParams& P) {
+    static int forced = [] {
+        const char* v = getenv("VMB_MARCH_IMPL");
+        return v && std::string(v) == "twopass" ? 1 : 0;
+    }();
+    return !P.grows && !forced;
+}
+
+// walk -> scan -> expand -> fixup; the sample total lands in d_total.
+int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
+                 unsigned long long* d_total, unsigned long long* emitted) {
+    const uint64_t n = rays->n_rays;
+    const uint64_t n_chunks = (n + 31) / 32;
+    const size_t head = 16;
+    const size_t idx_bytes = n_chunks * kWalkCap * 32 * sizeof(uint32_t);
+    char* base = static_cast<char*>(scratch(ctx, SCRATCH_MARCH, head + idx_bytes + n * 4 + 64));
+    if (!base) return VMB_CUDA;
+    auto* counters = reinterpret_cast<unsigned int*>(base);  // [chunk, overflow]
+    auto* kept_idx = reinterpret_cast<uint32_t*>(base + head);
+    auto* overflow = reinterpret_cast<uint32_t*>(base + head + idx_bytes);
+    cudaMemsetAsync(base, 0, head, ctx->stream);
+    if (n == 0) {
+        cudaMemsetAsync(d_total, 0, 8, ctx->stream);
+        cudaError_t e = cudaGetLastError();
+        return e == cudaSuccess ? VMB_OK : cuda_fail(e, "march");
+    }
+    // persistent grid: exactly the resident capacity of the device
+    static int per_sm = 0;
+    if (!per_sm) {
+        if (rays->dtype == VMB_F32)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_march_walk<float>, 128, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_march_walk<double>, 128, 0);
+        if (per_sm < 1) per_sm = 4;
+    }
+    const int walk_blocks = ctx->num_sms * per_sm;
+    if (rays->dtype == VMB_F32)
+        k_march_walk<float><<<walk_blocks, 128, 0, ctx->stream>>>(
+            P, static_cast<const float*>(rays->d_origins), static_cast<const float*>(rays->d_directions),
+            n, out->d_counts, kept_idx, counters, n_chunks, emitted, ctx->d_err);
+    else
+        k_march_walk<double><<<walk_blocks, 128, 0, ctx->stream>>>(
+            P, static_cast<const double*>(rays->d_origins),
+            static_cast<const double*>(rays->d_directions), n, out->d_counts, kept_idx, counters,
+            n_chunks, emitted, ctx->d_err);
+    int rc = scan_counts(ctx, out->d_counts, n, out->d_offsets, d_total);
+    if (rc) return rc;
+    k_march_expand<<<grid_blocks(ctx, n_chunks * 32, 256, 8), 256, 0, ctx->stream>>>(
+        P.near_, P.far_, P.step, out->d_counts, out->d_offsets, kept_idx, n, out->d_t_starts,
+        out->d_t_ends, out->d_ray_indices, out->capacity, overflow, counters + 1);
+    const int fix_blocks = ctx->num_sms * 2;
+    if (rays->dtype == VMB_F32)
+        k_march_fixup<float><<<fix_blocks, 128, 0, ctx->stream>>>(
+            P, static_cast<const float*>(rays->d_origins), static_cast<const float*>(rays->d_directions),
+            out->d_offsets, out->d_t_starts, out->d_t_ends, out->d_ray_indices, out->capacity, overflow,
+            counters + 1, ctx->d_err);
+    else
+        k_march_fixup<double><<<fix_blocks, 128, 0, ctx->stream>>>(
+            P, static_cast<const double*>(rays->d_origins),
+            static_cast<const double*>(rays->d_directions), out->d_offsets, out->d_t_starts,
+            out->d_t_ends, out->d_ray_indices, out->capacity, overflow, counters + 1, ctx->d_err);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? VMB_OK : cuda_fail(e, "march");
+}
+
+// Packed march shared by march_field and march_candidates: the fused single-pass
+// kernel when possible, else count -> scan -> (sync) -> fill.
 int march_packed(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
                  uint64_t* h_n, vmb_march_stats* stats) {
     if (!out || !out->d_offsets || !out->d_counts)
@@ -471,6 +814,23 @@ int march_packed(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
     int rc = reset_error(ctx);
     if (rc) return rc;
     cudaMemsetAsync(ctx->d_u64 + 1, 0, 8, ctx->stream);
+    if (use_fused(P)) {
+        rc = launch_fused(ctx, P, rays, out, ctx->d_u64, stats ? ctx->d_u64 + 1 : nullptr);
+        if (rc) return rc;
+        cudaMemcpyAsync(ctx->h_u64, ctx->d_u64, 16, cudaMemcpyDeviceToHost, ctx->stream);
+        rc = report_march_error(ctx);  // synchronizes
+        if (rc) return rc;
+        uint64_t total = ctx->h_u64[0];
+        *h_n = total;
+        if (stats) {
+            stats->samples_emitted = ctx->h_u64[1];
+            stats->samples_kept = total;
+        }
+        if (total > 0xffffffffull)
+            return fail(VMB_INVALID_ARGUMENT, "pack: sample count exceeds 32-bit index range");
+        if (total > out->capacity) return fail(VMB_CAPACITY, "march: sample capacity too small");
+        return VMB_OK;
+    }
     if (rays->n_rays) launch_march<COUNT>(ctx, P, rays, out->d_counts, nullptr, nullptr, stats ? ctx->d_u64 + 1 : nullptr);
     rc = scan_counts(ctx, out->d_counts, rays->n_rays, out->d_offsets, ctx->d_u64);
     if (rc) return rc;
@@ -521,6 +881,8 @@ int vmb_march_field_async(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,
     P.f = *f;
     P.filter = true;
     P.full = false;
+    if (use_fused(P))
+        return launch_fused(ctx, P, rays, out, reinterpret_cast<unsigned long long*>(d_n), nullptr);
     if (rays->n_rays) launch_march<COUNT>(ctx, P, rays, out->d_counts, nullptr, nullptr, nullptr);
     rc = scan_counts(ctx, out->d_counts, rays->n_rays, out->d_offsets,
                      reinterpret_cast<unsigned long long*>(d_n));

@@ -61,17 +61,37 @@ __device__ __forceinline__ RayRange ray_range(const uint32_t* __restrict__ offse
     return rr;
 }
 
-template <typename T>
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES)
+                 : "memory");
+}
+
+// Stage samples [cs, cs+n) of the warp's range into its smem tile. alpha (or,
+// for the transmittance output, exp(-sigma*delta)) is computed here, sample-
+// parallel: every lane evaluates exp() for independent samples, so the per-ray
+// sequential loops that follow only multiply and add (no exp on their critical
+// path). Same expressions as rendering.cpp, so the values are the reference's.
+template <typename T, bool kTransmittanceFactor = false>
 __device__ __forceinline__ void stage_in(Smem<T>& sm, int lane, uint64_t cs, uint64_t n,
                                          const double* __restrict__ ts, const double* __restrict__ te,
                                          const T* __restrict__ rgb, const T* __restrict__ sig) {
+    // cp.async (LDGSTS): every element of the tile is in flight at once without
+    // occupying registers; then alpha is computed from shared memory.
     for (uint64_t i = lane; i < n; i += 32) {
-        sm.ts[i] = __ldg(ts + cs + i);
-        sm.te[i] = __ldg(te + cs + i);
-        sm.sig[i] = __ldg(sig + cs + i);
+        cp_async<8>(&sm.ts[i], ts + cs + i);
+        cp_async<8>(&sm.te[i], te + cs + i);
+        cp_async<sizeof(T)>(&sm.sig[i], sig + cs + i);
     }
     if (rgb)
-        for (uint64_t i = lane; i < 3 * n; i += 32) sm.rgb[i] = __ldg(rgb + 3 * cs + i);
+        for (uint64_t i = lane; i < 3 * n; i += 32) cp_async<sizeof(T)>(&sm.rgb[i], rgb + 3 * cs + i);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncwarp();
+    for (uint64_t i = lane; i < n; i += 32) {
+        double e = exp(-double(sm.sig[i]) * (sm.te[i] - sm.ts[i]));
+        sm.al[i] = kTransmittanceFactor ? e : 1.0 - e;
+    }
 }
 
 // ------------------------------------------------------------------ forward
@@ -80,8 +100,10 @@ struct Fwd {
     // rendering.cpp:51-58
     __device__ __forceinline__ void add(double ts, double te, double r, double g, double b,
                                         double sigma) {
-        double delta = te - ts;
-        double alpha = 1.0 - exp(-sigma * delta);
+        add_alpha(ts, te, r, g, b, 1.0 - exp(-sigma * (te - ts)));
+    }
+    __device__ __forceinline__ void add_alpha(double ts, double te, double r, double g, double b,
+                                              double alpha) {
         double w = T * alpha;
         cr = cr + r * w;
         cg = cg + g * w;
@@ -113,8 +135,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_forward(
                 uint64_t a = max(rr.off, cs), b = min(rr.end, cs + n);
                 for (uint64_t s = a; s < b; ++s) {
                     uint64_t i = s - cs;
-                    acc.add(sm.ts[i], sm.te[i], double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
-                            double(sm.rgb[3 * i + 2]), double(sm.sig[i]));
+                    acc.add_alpha(sm.ts[i], sm.te[i], double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
+                                  double(sm.rgb[3 * i + 2]), sm.al[i]);
                 }
                 __syncwarp();
             }
@@ -177,10 +199,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_backward(
             double t = 1.0;
             for (uint64_t s = rr.off; s < rr.end; ++s) {  // rendering.cpp:89-96
                 uint64_t i = s - cs;
-                double a = 1.0 - exp(-double(sm.sig[i]) * (sm.te[i] - sm.ts[i]));
                 sm.tr[i] = t;
-                sm.al[i] = a;
-                t *= 1.0 - a;
+                t *= 1.0 - sm.al[i];
             }
             double suffix = 0.0;
             for (uint64_t s = rr.end; s-- > rr.off;) {  // rendering.cpp:99-108
@@ -215,7 +235,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_backward(
                     __syncwarp();
                     for (uint64_t s = max(rr.off, cs); s < min(rr.end, cs + n); ++s) {
                         uint64_t i = s - cs;
-                        double a = 1.0 - exp(-double(sm.sig[i]) * (sm.te[i] - sm.ts[i]));
+                        double a = sm.al[i];
                         double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
                                            double(sm.rgb[3 * i + 2]), 0.5 * (sm.ts[i] + sm.te[i]));
                         S += t * a * v;
@@ -243,7 +263,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_backward(
                     for (uint64_t s = max(rr.off, cs); s < min(rr.end, cs + n); ++s) {
                         uint64_t i = s - cs;
                         double delta = sm.te[i] - sm.ts[i];
-                        double a = 1.0 - exp(-double(sm.sig[i]) * delta);
+                        double a = sm.al[i];
                         double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
                                            double(sm.rgb[3 * i + 2]), 0.5 * (sm.ts[i] + sm.te[i]));
                         double wgt = t * a;
@@ -295,12 +315,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_transmittance(
         if (rr.contiguous) {
             for (uint64_t cs = rr.s0; cs < rr.s1; cs += Tile<T>::CH) {
                 uint64_t n = min(uint64_t(Tile<T>::CH), rr.s1 - cs);
-                stage_in<T>(sm, lane, cs, n, ts, te, nullptr, sig);
+                stage_in<T, true>(sm, lane, cs, n, ts, te, nullptr, sig);
                 __syncwarp();
                 for (uint64_t s = max(rr.off, cs); s < min(rr.end, cs + n); ++s) {
                     uint64_t i = s - cs;
                     sm.tr[i] = t;
-                    t *= exp(-double(sm.sig[i]) * (sm.te[i] - sm.ts[i]));
+                    t *= sm.al[i];
                 }
                 __syncwarp();
                 for (uint64_t i = lane; i < n; i += 32) out[cs + i] = T(sm.tr[i]);
