@@ -40,3 +40,10 @@ oracle:
 clean:
 	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
+
+# A/B variants (experiments): make variant DEFS="-DVMB_WALK_MINB=4" NAME=minb4
+variant:
+	@mkdir -p build/var_$(NAME) $(LIB)/variants
+	for f in $(CU_SRCS); do b=$$(basename $$f .cu); $(NVCC) $(NVFLAGS) $(DEFS) -c $$f -o build/var_$(NAME)/$$b.o 2> build/var_$(NAME)/$$b.log || exit 1; done
+	$(NVCC) $(NVFLAGS) $(DEFS) -x cu -c $(SRC)/comm.cpp -o build/var_$(NAME)/comm.o 2> /dev/null
+	$(NVCC) $(ARCH) -shared -o $(LIB)/variants/libvoxmarch_b200_$(NAME).so build/var_$(NAME)/*.o -cudart static -ldl -lpthread

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libvoxmarch_b200.so")
+# VMB_LIB_PATH selects an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("VMB_LIB_PATH") or os.path.join(HERE, "lib", "libvoxmarch_b200.so")
 
 VMB_OK, VMB_INVALID_ARGUMENT, VMB_RUNTIME, VMB_CUDA, VMB_NOT_SUPPORTED, VMB_CAPACITY = range(6)
 VMB_F32, VMB_F64 = 0, 1

@@ -52,6 +52,8 @@ struct MarchParams {
     double eps, thr;
     uint32_t max_cand;
     bool fast;            // fp32 DDA + filtered fp32 cell test (walk_fast)
+    bool sphere_fast;     // SolidSphere field: filtered fp32 density decision
+    float sph_c[3], sph_r, sph_r2, sph_cmax;
     float step_f, m0_f, inv_step_f, near_f, far_f, Mf;
     bool full;            // walk to the end (stats / candidate mode), ignore the T cut
     bool filter;          // apply inline density + alpha floor + T cut
@@ -87,6 +89,10 @@ struct Sink {
     uint32_t buf_cap = 0;
 };
 
+template <int MODE>
+__device__ __forceinline__ bool filter_sample(const MarchParams& P, Sink& s, uint64_t i, uint32_t ci,
+                                              double t0, double t1, double sigma, DevError* err);
+
 // Handles one grid-passing candidate. Mirrors ray_marching.cpp:78,111-137.
 template <int MODE>
 __device__ __forceinline__ bool on_candidate(const MarchParams& P, Sink& s, uint64_t i, double t0,
@@ -107,7 +113,14 @@ __device__ __forceinline__ bool on_candidate(const MarchParams& P, Sink& s, uint
         return true;
     }
     if (!s.filtering) return true;  // after the cut only the emitted count matters
-    double sigma = field_density(P.f, p);
+    return filter_sample<MODE>(P, s, i, ci, t0, t1, field_density(P.f, p), err);
+}
+
+// Density validation, alpha floor and transmittance cut of candidate ci with
+// density sigma (ray_marching.cpp:122-137).
+template <int MODE>
+__device__ __forceinline__ bool filter_sample(const MarchParams& P, Sink& s, uint64_t i, uint32_t ci,
+                                              double t0, double t1, double sigma, DevError* err) {
     if (!isfinite(sigma) || sigma < 0.0) {
         int kind = !isfinite(sigma) ? ERR_NONFINITE_SIGMA : ERR_NEGATIVE_SIGMA;
         atomicMin(&err->key, march_err_key(s.ray, ci, kind));
@@ -295,17 +308,40 @@ __device__ void walk_growth(const MarchParams& P, Sink& s, D3 o, D3 d, DevError*
 // for the last, possibly far-clamped step — the step is re-evaluated with the
 // exact fp64 code (eval_step). Candidates always get exact t0/t1/midpoint.
 // ---------------------------------------------------------------------------
-template <int MODE>
-__device__ void walk_fast(const MarchParams& P, Sink& s, D3 o, D3 d, DevError* err) {
+template <int MODE, typename RT>
+__device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ orig,
+                          const RT* __restrict__ dirs, uint64_t r, DevError* err) {
     if (P.n_steps == 0) return;
     const float Rf = float(P.res);
-    float A[3] = {float((o.x - P.k.lo.x) * P.scale[0]), float((o.y - P.k.lo.y) * P.scale[1]),
-                  float((o.z - P.k.lo.z) * P.scale[2])};
-    float B[3] = {float(d.x * P.scale[0]), float(d.y * P.scale[1]), float(d.z * P.scale[2])};
+    // Only fp32 state stays live in the loops; the fp64 ray is re-read from
+    // global memory (L1) by the rare exact paths.
+    float A[3], B[3], of[3], df[3];
+    {
+        const D3 o = load3(orig, r), d = load3(dirs, r);
+        A[0] = float((o.x - P.k.lo.x) * P.scale[0]);
+        A[1] = float((o.y - P.k.lo.y) * P.scale[1]);
+        A[2] = float((o.z - P.k.lo.z) * P.scale[2]);
+        B[0] = float(d.x * P.scale[0]);
+        B[1] = float(d.y * P.scale[1]);
+        B[2] = float(d.z * P.scale[2]);
+        of[0] = float(o.x), of[1] = float(o.y), of[2] = float(o.z);
+        df[0] = float(d.x), df[1] = float(d.y), df[2] = float(d.z);
+    }
     const float amax = fmaxf(fmaxf(fabsf(A[0]), fabsf(A[1])), fabsf(A[2]));
     const float bmax = fmaxf(fmaxf(fabsf(B[0]), fabsf(B[1])), fabsf(B[2]));
     const float E = ldexpf(2.0f * amax + 5.0f * bmax * P.Mf, -22) + 1e-6f;
     const bool fast_ok = E < 0.05f;
+    // Error bound of the fp32 |p - c|^2 (see the filtered sphere test below):
+    // per-axis position error e <= 2^-24 (3|o| + 7|d| M + 2|c|) (rounding of o, d, c,
+    // of the fp32 midpoint and of the FMA/subtraction), squared-distance error
+    // <= 3 2^-24 r^2 + 2 sqrt(3) r e + 3 e^2; a factor 4 of headroom on top.
+    float sph_err = 0.0f;
+    if (P.sphere_fast) {
+        float omax = fmaxf(fmaxf(fabsf(of[0]), fabsf(of[1])), fabsf(of[2]));
+        float dmax = fmaxf(fmaxf(fabsf(df[0]), fabsf(df[1])), fabsf(df[2]));
+        float e = ldexpf(3.0f * omax + 7.0f * dmax * P.Mf + 2.0f * P.sph_cmax, -24);
+        sph_err = 4.0f * (ldexpf(3.0f * P.sph_r2, -24) + 3.5f * P.sph_r * e + 3.0f * e * e) + 1e-12f;
+    }
     const float EPSD = 1e-3f + 4.0f * E;  // domain guard for the fp32 clip
     float tlo = P.near_f, thi = P.far_f;
 #pragma unroll
@@ -376,12 +412,28 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, D3 o, D3 d, DevError* e
                         if (!((__ldg(P.bits + (cell >> 5)) >> (cell & 31)) & 1u)) continue;
                         double t0 = P.near_ + double(j) * P.step;
                         double t1 = min_ref(P.near_ + double(j + 1) * P.step, P.far_);
-                        D3 p = o + d * (0.5 * (t0 + t1));
+                        if (P.sphere_fast && s.filtering) {
+                            // Filtered SolidSphere test (fields.cpp:45): |p - c|^2 in fp32 with
+                            // the bound sph_err; decided cases skip the fp64 midpoint + sqrt.
+                            float qx = fmaf(df[0], m, of[0]) - P.sph_c[0];
+                            float qy = fmaf(df[1], m, of[1]) - P.sph_c[1];
+                            float qz = fmaf(df[2], m, of[2]) - P.sph_c[2];
+                            float d2 = fmaf(qx, qx, fmaf(qy, qy, qz * qz));
+                            if (d2 > P.sph_r2 + sph_err || d2 < P.sph_r2 - sph_err) {
+                                if (s.n_cand >= P.max_cand) return;  // candidate cap
+                                uint32_t ci = s.n_cand++;
+                                double sigma = d2 < P.sph_r2 ? P.f.sigma : 0.0;
+                                if (!filter_sample<MODE>(P, s, uint64_t(j), ci, t0, t1, sigma, err)) return;
+                                continue;
+                            }
+                        }
+                        D3 p = load3(orig, r) + load3(dirs, r) * (0.5 * (t0 + t1));
                         if (!on_candidate<MODE>(P, s, uint64_t(j), t0, t1, p, err)) return;
                         continue;
                     }
                 }
-                if (!eval_step<MODE>(P, s, o, d, uint64_t(j), err, &alive)) return;
+                if (!eval_step<MODE>(P, s, load3(orig, r), load3(dirs, r), uint64_t(j), err, &alive))
+                    return;
             }
             if (jhi + 1 > next_i) next_i = jhi + 1;
             if (next_i > last) return;
@@ -414,17 +466,26 @@ __device__ __forceinline__ bool ray_safe(const MarchParams& P, D3 o, D3 d) {
     return mag < 1e300;
 }
 
-template <int MODE>
-__device__ __forceinline__ void walk(const MarchParams& P, Sink& s, D3 o, D3 d, DevError* err) {
-    bool safe = ray_safe(P, o, d);
-    if (P.grows)
-        walk_growth<MODE>(P, s, o, d, err);
-    else if (P.fast && safe)
-        walk_fast<MODE>(P, s, o, d, err);
-    else if (P.skip && safe)
-        walk_skip<MODE>(P, s, o, d, err);
-    else
-        walk_dense<MODE>(P, s, o, d, err);
+template <int MODE, typename RT>
+__device__ __forceinline__ void walk(const MarchParams& P, Sink& s, const RT* __restrict__ orig,
+                                     const RT* __restrict__ dirs, uint64_t r, DevError* err) {
+    bool safe;
+    {
+        const D3 o = load3(orig, r), d = load3(dirs, r);
+        safe = ray_safe(P, o, d);
+        if (P.grows) {
+            walk_growth<MODE>(P, s, o, d, err);
+            return;
+        }
+        if (!(P.fast && safe)) {
+            if (P.skip && safe)
+                walk_skip<MODE>(P, s, o, d, err);
+            else
+                walk_dense<MODE>(P, s, o, d, err);
+            return;
+        }
+    }
+    walk_fast<MODE>(P, s, orig, dirs, r, err);
 }
 
 // ---------------------------------------------------------------------------
@@ -444,8 +505,13 @@ __device__ __forceinline__ void walk(const MarchParams& P, Sink& s, D3 o, D3 d, 
 // ---------------------------------------------------------------------------
 constexpr int kWalkCap = 24;
 
-template <typename RT>
-__global__ void __launch_bounds__(128, 6) k_march_walk(
+// FAST instantiates only walk_fast (+ its exact fallback and the dense walk for
+// unsafe rays), so its register allocation is not the union of every walk.
+#ifndef VMB_WALK_MINB
+#define VMB_WALK_MINB 6
+#endif
+template <typename RT, bool FAST>
+__global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
     MarchParams P, const RT* __restrict__ orig, const RT* __restrict__ dirs, uint64_t n_rays,
     uint32_t* __restrict__ counts, uint32_t* __restrict__ kept_idx, unsigned int* chunk_counter,
     uint64_t n_chunks, unsigned long long* emitted, DevError* err) {
@@ -463,7 +529,15 @@ __global__ void __launch_bounds__(128, 6) k_march_walk(
             s.buf = kept_idx + uint64_t(chunk) * (kWalkCap * 32) + lane;
             s.buf_stride = 32;
             s.buf_cap = kWalkCap;
-            walk<BUFFER>(P, s, load3(orig, r), load3(dirs, r), err);
+            if (FAST) {
+                const D3 o = load3(orig, r), d = load3(dirs, r);
+                if (ray_safe(P, o, d))
+                    walk_fast<BUFFER>(P, s, orig, dirs, r, err);
+                else
+                    walk_dense<BUFFER>(P, s, o, d, err);
+            } else {
+                walk<BUFFER>(P, s, orig, dirs, r, err);
+            }
             counts[r] = s.n_kept;
             emit_local += s.n_cand;
         }
@@ -537,7 +611,7 @@ __global__ void k_march_fixup(MarchParams P, const RT* __restrict__ orig, const 
         s.idx = idx;
         s.base = offsets[r];
         s.cap = cap;
-        walk<FILL>(P, s, load3(orig, r), load3(dirs, r), err);
+        walk<FILL>(P, s, orig, dirs, r, err);
     }
 }
 
@@ -552,7 +626,6 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, const RT* __restri
     unsigned long long emit_local = 0;
     for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rays;
          r += uint64_t(gridDim.x) * blockDim.x) {
-        D3 o = load3(orig, r), d = load3(dirs, r);
         Sink s;
         s.ray = r;
         if (MODE == FILL) {
@@ -562,7 +635,7 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, const RT* __restri
             s.base = offsets[r];
             s.cap = cap;
         }
-        walk<MODE>(P, s, o, d, err);
+        walk<MODE>(P, s, orig, dirs, r, err);
         if (MODE == COUNT) counts[r] = s.n_kept;
         emit_local += s.n_cand;
     }
@@ -739,6 +812,18 @@ int report_march_error(vmb_ctx* ctx) {
     return fail(low == 0 ? VMB_INVALID_ARGUMENT : VMB_RUNTIME, march_error_text(err));
 }
 
+// Filtered fp32 density decisions are used for a well-scaled SolidSphere field.
+void set_sphere_fast(MarchParams* P) {
+    const vmb_field& f = P->f;
+    double cmax = fmax(fmax(fabs(f.center[0]), fabs(f.center[1])), fabs(f.center[2]));
+    P->sphere_fast = P->fast && f.kind == VMB_FIELD_SOLID_SPHERE && f.radius > 0.0 &&
+                     f.radius < 1e6 && cmax < 1e6 && std::isfinite(f.sigma) && f.sigma >= 0.0;
+    for (int a = 0; a < 3; ++a) P->sph_c[a] = float(f.center[a]);
+    P->sph_r = float(f.radius);
+    P->sph_r2 = P->sph_r * P->sph_r;
+    P->sph_cmax = float(cmax);
+}
+
 // VMB_MARCH_IMPL=twopass forces the count -> scan -> fill pipeline (A/B tests).
 bool use_fused(const MarchParams& P) {
     static int forced = [] {
@@ -767,24 +852,28 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
         return e == cudaSuccess ? VMB_OK : cuda_fail(e, "march");
     }
     // persistent grid: exactly the resident capacity of the device
-    static int per_sm = 0;
-    if (!per_sm) {
-        if (rays->dtype == VMB_F32)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_march_walk<float>, 128, 0);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_march_walk<double>, 128, 0);
+    auto launch_walk = [&](auto kernel, auto* o, auto* d) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, 0);
         if (per_sm < 1) per_sm = 4;
+        kernel<<<ctx->num_sms * per_sm, 128, 0, ctx->stream>>>(P, o, d, n, out->d_counts, kept_idx,
+                                                              counters, n_chunks, emitted, ctx->d_err);
+    };
+    if (rays->dtype == VMB_F32) {
+        auto* o = static_cast<const float*>(rays->d_origins);
+        auto* d = static_cast<const float*>(rays->d_directions);
+        if (P.fast)
+            launch_walk(k_march_walk<float, true>, o, d);
+        else
+            launch_walk(k_march_walk<float, false>, o, d);
+    } else {
+        auto* o = static_cast<const double*>(rays->d_origins);
+        auto* d = static_cast<const double*>(rays->d_directions);
+        if (P.fast)
+            launch_walk(k_march_walk<double, true>, o, d);
+        else
+            launch_walk(k_march_walk<double, false>, o, d);
     }
-    const int walk_blocks = ctx->num_sms * per_sm;
-    if (rays->dtype == VMB_F32)
-        k_march_walk<float><<<walk_blocks, 128, 0, ctx->stream>>>(
-            P, static_cast<const float*>(rays->d_origins), static_cast<const float*>(rays->d_directions),
-            n, out->d_counts, kept_idx, counters, n_chunks, emitted, ctx->d_err);
-    else
-        k_march_walk<double><<<walk_blocks, 128, 0, ctx->stream>>>(
-            P, static_cast<const double*>(rays->d_origins),
-            static_cast<const double*>(rays->d_directions), n, out->d_counts, kept_idx, counters,
-            n_chunks, emitted, ctx->d_err);
     int rc = scan_counts(ctx, out->d_counts, n, out->d_offsets, d_total);
     if (rc) return rc;
     k_march_expand<<<grid_blocks(ctx, n_chunks * 32, 256, 8), 256, 0, ctx->stream>>>(
@@ -869,6 +958,7 @@ int vmb_march_field(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays, const
     P.f = *f;
     P.filter = true;
     P.full = stats != nullptr;
+    set_sphere_fast(&P);
     return march_packed(ctx, P, rays, out, h_n, stats);
 }
 
@@ -881,6 +971,7 @@ int vmb_march_field_async(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,
     P.f = *f;
     P.filter = true;
     P.full = false;
+    set_sphere_fast(&P);
     if (use_fused(P))
         return launch_fused(ctx, P, rays, out, reinterpret_cast<unsigned long long*>(d_n), nullptr);
     if (rays->n_rays) launch_march<COUNT>(ctx, P, rays, out->d_counts, nullptr, nullptr, nullptr);

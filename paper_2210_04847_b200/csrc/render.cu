@@ -177,6 +177,91 @@ __device__ __forceinline__ Up load_up(const T* dc, const T* dop, const T* ddep, 
     return u;
 }
 
+// Two forward sweeps for one ray range (used for a single ray longer than a tile,
+// or with per-lane global reads when the warp's rays are not contiguous):
+// sweep 1 computes S = sum_k w_k v_k, sweep 2 emits suffix_k = S - P_k.
+template <typename T>
+__device__ void bwd_two_sweep(Smem<T>& sm, int lane, bool active, bool staged, uint64_t off,
+                              uint64_t end, uint64_t s0, uint64_t s1, const Up& u,
+                              const double* __restrict__ ts, const double* __restrict__ te,
+                              const T* __restrict__ rgb, const T* __restrict__ sig,
+                              T* __restrict__ g_rgb, T* __restrict__ g_sig) {
+    double S = 0.0;
+    double t = 1.0;
+    if (staged) {
+        for (uint64_t cs = s0; cs < s1; cs += Tile<T>::CH) {
+            uint64_t n = min(uint64_t(Tile<T>::CH), s1 - cs);
+            stage_in(sm, lane, cs, n, ts, te, rgb, sig);
+            __syncwarp();
+            if (active)
+                for (uint64_t s = max(off, cs); s < min(end, cs + n); ++s) {
+                    uint64_t i = s - cs;
+                    double a = sm.al[i];
+                    double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
+                                       double(sm.rgb[3 * i + 2]), 0.5 * (sm.ts[i] + sm.te[i]));
+                    S += t * a * v;
+                    t *= 1.0 - a;
+                }
+            __syncwarp();
+        }
+    } else if (active) {
+        for (uint64_t s = off; s < end; ++s) {
+            double a = 1.0 - exp(-double(sig[s]) * (te[s] - ts[s]));
+            double v = u.value(double(rgb[3 * s]), double(rgb[3 * s + 1]), double(rgb[3 * s + 2]),
+                               0.5 * (ts[s] + te[s]));
+            S += t * a * v;
+            t *= 1.0 - a;
+        }
+    }
+    t = 1.0;
+    double P = 0.0;
+    if (staged) {
+        for (uint64_t cs = s0; cs < s1; cs += Tile<T>::CH) {
+            uint64_t n = min(uint64_t(Tile<T>::CH), s1 - cs);
+            stage_in(sm, lane, cs, n, ts, te, rgb, sig);
+            __syncwarp();
+            if (active)
+                for (uint64_t s = max(off, cs); s < min(end, cs + n); ++s) {
+                    uint64_t i = s - cs;
+                    double delta = sm.te[i] - sm.ts[i];
+                    double a = sm.al[i];
+                    double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
+                                       double(sm.rgb[3 * i + 2]), 0.5 * (sm.ts[i] + sm.te[i]));
+                    double wgt = t * a;
+                    P += wgt * v;
+                    sm.rgb[3 * i] = T(u.dcx * wgt);
+                    sm.rgb[3 * i + 1] = T(u.dcy * wgt);
+                    sm.rgb[3 * i + 2] = T(u.dcz * wgt);
+                    sm.sig[i] = T(delta * (t * (1.0 - a) * v - (S - P)));
+                    t *= 1.0 - a;
+                }
+            __syncwarp();
+            for (uint64_t i = lane; i < n; i += 32) g_sig[cs + i] = sm.sig[i];
+            for (uint64_t i = lane; i < 3 * n; i += 32) g_rgb[3 * cs + i] = sm.rgb[i];
+            __syncwarp();
+        }
+    } else if (active) {
+        for (uint64_t s = off; s < end; ++s) {
+            double delta = te[s] - ts[s];
+            double a = 1.0 - exp(-double(sig[s]) * delta);
+            double v = u.value(double(rgb[3 * s]), double(rgb[3 * s + 1]), double(rgb[3 * s + 2]),
+                               0.5 * (ts[s] + te[s]));
+            double wgt = t * a;
+            P += wgt * v;
+            g_rgb[3 * s] = T(u.dcx * wgt);
+            g_rgb[3 * s + 1] = T(u.dcy * wgt);
+            g_rgb[3 * s + 2] = T(u.dcz * wgt);
+            g_sig[s] = T(delta * (t * (1.0 - a) * v - (S - P)));
+            t *= 1.0 - a;
+        }
+    }
+}
+
+// render_backward: the warp's 32 rays are processed in greedy groups of
+// consecutive rays whose samples fit one tile; each group is staged once and every
+// lane runs the reference's exact forward-T / reverse-suffix recurrence
+// (rendering.cpp:85-108) from shared memory. Only a single ray with more samples
+// than a tile uses the two-sweep form.
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32) k_backward(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays,
@@ -191,109 +276,57 @@ __global__ void __launch_bounds__(kWarps * 32) k_backward(
          w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
         RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
         Up u = load_up(dc, dop, ddep, rr.r, rr.valid);
-        if (rr.contiguous && rr.s1 - rr.s0 <= uint64_t(Tile<T>::CH)) {
-            // Exact reference order: forward T/alpha, then reverse suffix pass.
-            uint64_t cs = rr.s0, n = rr.s1 - rr.s0;
-            stage_in(sm, lane, cs, n, ts, te, rgb, sig);
-            __syncwarp();
-            double t = 1.0;
-            for (uint64_t s = rr.off; s < rr.end; ++s) {  // rendering.cpp:89-96
-                uint64_t i = s - cs;
-                sm.tr[i] = t;
-                t *= 1.0 - sm.al[i];
-            }
-            double suffix = 0.0;
-            for (uint64_t s = rr.end; s-- > rr.off;) {  // rendering.cpp:99-108
-                uint64_t i = s - cs;
-                double delta = sm.te[i] - sm.ts[i];
-                double mid = 0.5 * (sm.ts[i] + sm.te[i]);
-                double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
-                                   double(sm.rgb[3 * i + 2]), mid);
-                double wgt = sm.tr[i] * sm.al[i];
-                sm.rgb[3 * i] = T(u.dcx * wgt);
-                sm.rgb[3 * i + 1] = T(u.dcy * wgt);
-                sm.rgb[3 * i + 2] = T(u.dcz * wgt);
-                sm.sig[i] = T(delta * (sm.tr[i] * (1.0 - sm.al[i]) * v - suffix));
-                suffix += wgt * v;
-            }
-            __syncwarp();
-            for (uint64_t i = lane; i < n; i += 32) g_sig[cs + i] = sm.sig[i];
-            for (uint64_t i = lane; i < 3 * n; i += 32) g_rgb[3 * cs + i] = sm.rgb[i];
-            __syncwarp();
+        if (!rr.contiguous) {
+            bwd_two_sweep(sm, lane, rr.valid, false, rr.off, rr.end, 0, 0, u, ts, te, rgb, sig, g_rgb,
+                          g_sig);
             continue;
         }
-        // Long or non-contiguous ranges: sweep 1 computes S = sum_k w_k v_k,
-        // sweep 2 emits suffix_k = S - P_k (P_k inclusive prefix).
-        const bool staged = rr.contiguous;
-        double S = 0.0;
-        {
-            double t = 1.0;
-            if (staged) {
-                for (uint64_t cs = rr.s0; cs < rr.s1; cs += Tile<T>::CH) {
-                    uint64_t n = min(uint64_t(Tile<T>::CH), rr.s1 - cs);
-                    stage_in(sm, lane, cs, n, ts, te, rgb, sig);
-                    __syncwarp();
-                    for (uint64_t s = max(rr.off, cs); s < min(rr.end, cs + n); ++s) {
-                        uint64_t i = s - cs;
-                        double a = sm.al[i];
-                        double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
-                                           double(sm.rgb[3 * i + 2]), 0.5 * (sm.ts[i] + sm.te[i]));
-                        S += t * a * v;
-                        t *= 1.0 - a;
-                    }
-                    __syncwarp();
-                }
-            } else {
-                for (uint64_t s = rr.off; s < rr.end; ++s) {
-                    double a = 1.0 - exp(-double(sig[s]) * (te[s] - ts[s]));
-                    double v = u.value(double(rgb[3 * s]), double(rgb[3 * s + 1]), double(rgb[3 * s + 2]),
-                                       0.5 * (ts[s] + te[s]));
-                    S += t * a * v;
-                    t *= 1.0 - a;
-                }
+        const unsigned vmask = __ballot_sync(0xffffffffu, rr.valid);  // valid lanes: a prefix
+        int g0 = 0;
+        while (g0 < 32 && ((vmask >> g0) & 1u)) {
+            const uint64_t base = __shfl_sync(0xffffffffu, rr.off, g0);
+            const bool fits = rr.valid && lane >= g0 && rr.end - base <= uint64_t(Tile<T>::CH);
+            const unsigned fm = __ballot_sync(0xffffffffu, fits);  // monotone: ends ascend
+            if (!((fm >> g0) & 1u)) {  // ray g0 alone exceeds a tile
+                const uint64_t e0 = __shfl_sync(0xffffffffu, rr.end, g0);
+                bwd_two_sweep(sm, lane, lane == g0, true, rr.off, rr.end, base, e0, u, ts, te, rgb,
+                              sig, g_rgb, g_sig);
+                ++g0;
+                continue;
             }
-        }
-        {
-            double t = 1.0, P = 0.0;
-            if (staged) {
-                for (uint64_t cs = rr.s0; cs < rr.s1; cs += Tile<T>::CH) {
-                    uint64_t n = min(uint64_t(Tile<T>::CH), rr.s1 - cs);
-                    stage_in(sm, lane, cs, n, ts, te, rgb, sig);
-                    __syncwarp();
-                    for (uint64_t s = max(rr.off, cs); s < min(rr.end, cs + n); ++s) {
-                        uint64_t i = s - cs;
+            const int g1 = 31 - __clz(fm);
+            const uint64_t n = __shfl_sync(0xffffffffu, rr.end, g1) - base;
+            if (n) {
+                stage_in(sm, lane, base, n, ts, te, rgb, sig);
+                __syncwarp();
+                if (lane >= g0 && lane <= g1) {
+                    double t = 1.0;
+                    for (uint64_t s = rr.off; s < rr.end; ++s) {  // rendering.cpp:89-96
+                        uint64_t i = s - base;
+                        sm.tr[i] = t;
+                        t *= 1.0 - sm.al[i];
+                    }
+                    double suffix = 0.0;
+                    for (uint64_t s = rr.end; s-- > rr.off;) {  // rendering.cpp:99-108
+                        uint64_t i = s - base;
                         double delta = sm.te[i] - sm.ts[i];
-                        double a = sm.al[i];
+                        double mid = 0.5 * (sm.ts[i] + sm.te[i]);
                         double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
-                                           double(sm.rgb[3 * i + 2]), 0.5 * (sm.ts[i] + sm.te[i]));
-                        double wgt = t * a;
-                        P += wgt * v;
+                                           double(sm.rgb[3 * i + 2]), mid);
+                        double wgt = sm.tr[i] * sm.al[i];
                         sm.rgb[3 * i] = T(u.dcx * wgt);
                         sm.rgb[3 * i + 1] = T(u.dcy * wgt);
                         sm.rgb[3 * i + 2] = T(u.dcz * wgt);
-                        sm.sig[i] = T(delta * (t * (1.0 - a) * v - (S - P)));
-                        t *= 1.0 - a;
+                        sm.sig[i] = T(delta * (sm.tr[i] * (1.0 - sm.al[i]) * v - suffix));
+                        suffix += wgt * v;
                     }
-                    __syncwarp();
-                    for (uint64_t i = lane; i < n; i += 32) g_sig[cs + i] = sm.sig[i];
-                    for (uint64_t i = lane; i < 3 * n; i += 32) g_rgb[3 * cs + i] = sm.rgb[i];
-                    __syncwarp();
                 }
-            } else {
-                for (uint64_t s = rr.off; s < rr.end; ++s) {
-                    double delta = te[s] - ts[s];
-                    double a = 1.0 - exp(-double(sig[s]) * delta);
-                    double v = u.value(double(rgb[3 * s]), double(rgb[3 * s + 1]), double(rgb[3 * s + 2]),
-                                       0.5 * (ts[s] + te[s]));
-                    double wgt = t * a;
-                    P += wgt * v;
-                    g_rgb[3 * s] = T(u.dcx * wgt);
-                    g_rgb[3 * s + 1] = T(u.dcy * wgt);
-                    g_rgb[3 * s + 2] = T(u.dcz * wgt);
-                    g_sig[s] = T(delta * (t * (1.0 - a) * v - (S - P)));
-                    t *= 1.0 - a;
-                }
+                __syncwarp();
+                for (uint64_t i = lane; i < n; i += 32) g_sig[base + i] = sm.sig[i];
+                for (uint64_t i = lane; i < 3 * n; i += 32) g_rgb[3 * base + i] = sm.rgb[i];
+                __syncwarp();
             }
+            g0 = g1 + 1;
         }
     }
 }
