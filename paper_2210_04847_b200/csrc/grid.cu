@@ -278,6 +278,8 @@ int grid_alloc(vmb_grid* g) {
     cudaError_t e = cudaMalloc(&g->cache, g->n_cells * sizeof(double));
     if (e == cudaSuccess) e = cudaMalloc(&g->bits, g->n_words * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMalloc(&g->coarse, g->coarse_words * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&g->dist, g->n_cells);
+    if (e == cudaSuccess) e = cudaMalloc(&g->dist_tmp, g->n_cells);
     return e == cudaSuccess ? VMB_OK : cuda_fail(e, "grid allocation");
 }
 
@@ -299,12 +301,59 @@ int make_timestamps(const double* h_ts, uint64_t n, Timestamps* ts) {
     return VMB_OK;
 }
 
+// Capped Chebyshev distance transform, separable (x, then y, then z):
+//   D_x(c)   = min |dx| over occupied cells on the x-line (cap if none within cap-1)
+//   D_y(c)   = min over |dy| < cap of max(|dy|, D_x(c + dy e_y)),  same for z.
+// The composition is exactly the L-inf distance to the nearest occupied cell,
+// capped at kDistCap. The inner searches stop once |d| reaches the best so far.
+__global__ void k_dist_x(const uint32_t* __restrict__ bits, uint32_t res, uint64_t n,
+                         uint8_t* __restrict__ out) {
+    for (uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < n;
+         c += uint64_t(gridDim.x) * blockDim.x) {
+        const int x = int(c % res);
+        int best = kDistCap;
+        for (int dd = 0; dd < best; ++dd) {
+            const int xl = x - dd, xr = x + dd;
+            bool hit = false;
+            if (xl >= 0) {
+                uint64_t q = c - dd;
+                hit |= (__ldg(bits + (q >> 5)) >> (q & 31)) & 1u;
+            }
+            if (xr < int(res)) {
+                uint64_t q = c + dd;
+                hit |= (__ldg(bits + (q >> 5)) >> (q & 31)) & 1u;
+            }
+            if (hit) best = dd;
+        }
+        out[c] = uint8_t(best);
+    }
+}
+
+__global__ void k_dist_axis(const uint8_t* __restrict__ in, uint32_t res, uint64_t n, uint64_t stride,
+                            uint8_t* __restrict__ out) {
+    for (uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < n;
+         c += uint64_t(gridDim.x) * blockDim.x) {
+        const int i = int((c / stride) % res);
+        int best = __ldg(in + c);
+        for (int dd = 1; dd < best; ++dd) {
+            if (i - dd >= 0) best = min(best, max(dd, int(__ldg(in + c - dd * stride))));
+            if (i + dd < int(res)) best = min(best, max(dd, int(__ldg(in + c + dd * stride))));
+        }
+        out[c] = uint8_t(best);
+    }
+}
+
 }  // namespace
 
 int grid_rebuild_coarse(vmb_ctx* ctx, vmb_grid* g) {
     k_coarse<<<grid_blocks(ctx, g->coarse_words * 32, 256), 256, 0, ctx->stream>>>(
         g->bits, g->res, g->block, g->res_c, g->coarse, g->coarse_words);
-    return launch_check("grid coarse");
+    const int blocks = grid_blocks(ctx, g->n_cells, 256);
+    k_dist_x<<<blocks, 256, 0, ctx->stream>>>(g->bits, g->res, g->n_cells, g->dist);
+    k_dist_axis<<<blocks, 256, 0, ctx->stream>>>(g->dist, g->res, g->n_cells, g->res, g->dist_tmp);
+    k_dist_axis<<<blocks, 256, 0, ctx->stream>>>(g->dist_tmp, g->res, g->n_cells,
+                                                 uint64_t(g->res) * g->res, g->dist);
+    return launch_check("grid coarse/dist");
 }
 
 int grid_refresh(vmb_ctx* ctx, vmb_grid* g) {
@@ -360,6 +409,8 @@ int vmb_grid_destroy(vmb_grid* g) {
     cudaFree(g->cache);
     cudaFree(g->bits);
     cudaFree(g->coarse);
+    cudaFree(g->dist);
+    cudaFree(g->dist_tmp);
     cudaFree(g->probed);
     delete g;
     return VMB_OK;
@@ -382,6 +433,7 @@ int vmb_grid_clone(vmb_ctx* ctx, const vmb_grid* src, vmb_grid** out) {
     cudaMemcpyAsync(g->cache, src->cache, g->n_cells * 8, cudaMemcpyDeviceToDevice, ctx->stream);
     cudaMemcpyAsync(g->bits, src->bits, g->n_words * 4, cudaMemcpyDeviceToDevice, ctx->stream);
     cudaMemcpyAsync(g->coarse, src->coarse, g->coarse_words * 4, cudaMemcpyDeviceToDevice, ctx->stream);
+    cudaMemcpyAsync(g->dist, src->dist, g->n_cells, cudaMemcpyDeviceToDevice, ctx->stream);
     rc = launch_check("grid clone");
     if (rc) {
         vmb_grid_destroy(g);

@@ -40,6 +40,7 @@ struct MarchParams {
     uint32_t res;
     const uint32_t* bits;
     const uint32_t* coarse;
+    const uint8_t* dist;  // capped L-inf distance to the nearest occupied cell
     uint32_t block, res_c;
     double scale[3];      // R / size_k: world -> fine-cell units (approximate, DDA only)
     double near_, far_, step;
@@ -356,105 +357,74 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
         }
     }
     if (!(tlo <= thi)) return;
-    const float Bs = float(P.block);
-    const float inv_bs = 1.0f / Bs;  // block is a power of two
-    const int Rc = int(P.res_c);
-    int c[3], stp[3];
-    float tmax[3], tdel[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        int ca = int(floorf(fmaf(B[a], tlo, A[a]) * inv_bs));
-        ca = ca < 0 ? 0 : (ca >= Rc ? Rc - 1 : ca);
-        c[a] = ca;
-        // approximate reciprocals are fine here: the DDA only has to stay within
-        // the 1-cell dilation halo (fp32 error ~1e-5 cells)
-        if (B[a] > 0.0f) {
-            stp[a] = 1;
-            float ib = __frcp_rn(B[a]);
-            tmax[a] = (float(ca + 1) * Bs - A[a]) * ib;
-            tdel[a] = Bs * ib;
-        } else if (B[a] < 0.0f) {
-            stp[a] = -1;
-            float ib = __frcp_rn(B[a]);
-            tmax[a] = (float(ca) * Bs - A[a]) * ib;
-            tdel[a] = -Bs * ib;
-        } else {
-            stp[a] = 0;
-            tmax[a] = INFINITY;
-            tdel[a] = INFINITY;
-        }
-    }
+    // Distance-map walk (replaces a coarse DDA): for lattice step j the fp32 cell
+    // coordinate of its midpoint is within E of the real one. If that cell lies in
+    // the domain and its L-inf distance to the nearest occupied cell is D >= 2,
+    // every point within L = D - 1 - 2E - 0.01 cells of it is in an empty cell, so
+    // the next floor(L / (bmax * step)) lattice steps are skipped unevaluated
+    // (bmax * step = largest per-step move along any axis, in cells).
     const int last = int(P.n_steps) - 1;
-    int next_i = 0;
-    float t = tlo;
+    const float inv_bms = 1.0f / fmaxf(bmax * P.step_f, 1e-30f);
+    const float jump_margin = 1.0f + 2.0f * E + 0.01f;
+    const int Ri = int(P.res);
+    int j = int(floorf((tlo - P.near_f) * P.inv_step_f)) - 2;
+    int jend = int(floorf((thi - P.near_f) * P.inv_step_f)) + 2;
+    if (j < 0) j = 0;
+    if (jend > last) jend = last;
     bool alive = true;
-    for (int guard = 0; guard < 4 * (3 * Rc + 3); ++guard) {
-        float tn = fminf(fminf(tmax[0], tmax[1]), fminf(tmax[2], thi));
-        if (coarse_bit(P, c[0], c[1], c[2])) {
-            int jlo = int(floorf((t - P.near_f) * P.inv_step_f)) - 2;
-            int jhi = int(floorf((fmaxf(tn, t) - P.near_f) * P.inv_step_f)) + 2;
-            if (jlo < next_i) jlo = next_i;
-            if (jhi > last) jhi = last;
-            for (int j = jlo; j <= jhi; ++j) {
-                bool exact = !fast_ok || j == last;
-                if (!exact) {
-                    float m = fmaf(float(j), P.step_f, P.m0_f);
-                    float u0 = fmaf(B[0], m, A[0]), u1 = fmaf(B[1], m, A[1]), u2 = fmaf(B[2], m, A[2]);
-                    float f0 = floorf(u0), f1 = floorf(u1), f2 = floorf(u2);
-                    float r0 = u0 - f0, r1 = u1 - f1, r2 = u2 - f2;
-                    exact = r0 < E || r0 > 1.0f - E || r1 < E || r1 > 1.0f - E || r2 < E ||
-                            r2 > 1.0f - E;
-                    if (!exact) {
-                        if (f0 < 0.0f || f0 >= Rf || f1 < 0.0f || f1 >= Rf || f2 < 0.0f || f2 >= Rf)
-                            continue;  // definitely outside the domain
-                        // 32-bit index: the fast walk is enabled only for R <= 1024
-                        uint32_t cell = uint32_t(f0) + P.res * (uint32_t(f1) + P.res * uint32_t(f2));
-                        if (!((__ldg(P.bits + (cell >> 5)) >> (cell & 31)) & 1u)) continue;
-                        double t0 = P.near_ + double(j) * P.step;
-                        double t1 = min_ref(P.near_ + double(j + 1) * P.step, P.far_);
-                        if (P.sphere_fast && s.filtering) {
-                            // Filtered SolidSphere test (fields.cpp:45): |p - c|^2 in fp32 with
-                            // the bound sph_err; decided cases skip the fp64 midpoint + sqrt.
-                            float qx = fmaf(df[0], m, of[0]) - P.sph_c[0];
-                            float qy = fmaf(df[1], m, of[1]) - P.sph_c[1];
-                            float qz = fmaf(df[2], m, of[2]) - P.sph_c[2];
-                            float d2 = fmaf(qx, qx, fmaf(qy, qy, qz * qz));
-                            if (d2 > P.sph_r2 + sph_err || d2 < P.sph_r2 - sph_err) {
-                                if (s.n_cand >= P.max_cand) return;  // candidate cap
-                                uint32_t ci = s.n_cand++;
-                                double sigma = d2 < P.sph_r2 ? P.f.sigma : 0.0;
-                                if (!filter_sample<MODE>(P, s, uint64_t(j), ci, t0, t1, sigma, err)) return;
-                                continue;
-                            }
-                        }
-                        D3 p = load3(orig, r) + load3(dirs, r) * (0.5 * (t0 + t1));
-                        if (!on_candidate<MODE>(P, s, uint64_t(j), t0, t1, p, err)) return;
-                        continue;
-                    }
-                }
-                if (!eval_step<MODE>(P, s, load3(orig, r), load3(dirs, r), uint64_t(j), err, &alive))
-                    return;
+    while (j <= jend) {
+        const float m = fmaf(float(j), P.step_f, P.m0_f);
+        const float u0 = fmaf(B[0], m, A[0]), u1 = fmaf(B[1], m, A[1]), u2 = fmaf(B[2], m, A[2]);
+        const float f0 = floorf(u0), f1 = floorf(u1), f2 = floorf(u2);
+        const bool inside = f0 >= 0.0f && f0 < Rf && f1 >= 0.0f && f1 < Rf && f2 >= 0.0f && f2 < Rf;
+        int D = kDistCap;
+        uint32_t cell = 0;
+        if (inside) {
+            cell = uint32_t(f0) + P.res * (uint32_t(f1) + P.res * uint32_t(f2));
+            D = __ldg(P.dist + cell);
+            if (D >= 2 && j != last) {
+                const float Lj = float(D) - jump_margin;
+                j += (Lj > 0.0f ? int(Lj * inv_bms * 0.99999f) : 0) + 1;
+                continue;
             }
-            if (jhi + 1 > next_i) next_i = jhi + 1;
-            if (next_i > last) return;
         }
-        if (tn >= thi) return;
-        // advance along the axis with the nearest boundary (explicit branches keep
-        // the DDA state in registers)
-        if (tmax[0] <= tmax[1] && tmax[0] <= tmax[2]) {
-            c[0] += stp[0];
-            if (c[0] < 0 || c[0] >= Rc) return;
-            tmax[0] += tdel[0];
-        } else if (tmax[1] <= tmax[2]) {
-            c[1] += stp[1];
-            if (c[1] < 0 || c[1] >= Rc) return;
-            tmax[1] += tdel[1];
-        } else {
-            c[2] += stp[2];
-            if (c[2] < 0 || c[2] >= Rc) return;
-            tmax[2] += tdel[2];
+        bool exact = !fast_ok || j == last;
+        if (!exact) {
+            const float r0 = u0 - f0, r1 = u1 - f1, r2 = u2 - f2;
+            exact = r0 < E || r0 > 1.0f - E || r1 < E || r1 > 1.0f - E || r2 < E || r2 > 1.0f - E;
         }
-        t = tn;
+        if (exact) {
+            if (!eval_step<MODE>(P, s, load3(orig, r), load3(dirs, r), uint64_t(j), err, &alive))
+                return;
+            ++j;
+            continue;
+        }
+        if (!inside || D != 0) {  // outside the domain, or an empty cell
+            ++j;
+            continue;
+        }
+        // occupied cell: a candidate, with the reference's exact interval
+        double t0 = P.near_ + double(j) * P.step;
+        double t1 = min_ref(P.near_ + double(j + 1) * P.step, P.far_);
+        if (P.sphere_fast && s.filtering) {
+            // Filtered SolidSphere test (fields.cpp:45): |p - c|^2 in fp32 with the
+            // bound sph_err; decided cases skip the fp64 midpoint + sqrt.
+            float qx = fmaf(df[0], m, of[0]) - P.sph_c[0];
+            float qy = fmaf(df[1], m, of[1]) - P.sph_c[1];
+            float qz = fmaf(df[2], m, of[2]) - P.sph_c[2];
+            float d2 = fmaf(qx, qx, fmaf(qy, qy, qz * qz));
+            if (d2 > P.sph_r2 + sph_err || d2 < P.sph_r2 - sph_err) {
+                if (s.n_cand >= P.max_cand) return;  // candidate cap
+                uint32_t ci = s.n_cand++;
+                double sigma = d2 < P.sph_r2 ? P.f.sigma : 0.0;
+                if (!filter_sample<MODE>(P, s, uint64_t(j), ci, t0, t1, sigma, err)) return;
+                ++j;
+                continue;
+            }
+        }
+        D3 p = load3(orig, r) + load3(dirs, r) * (0.5 * (t0 + t1));
+        if (!on_candidate<MODE>(P, s, uint64_t(j), t0, t1, p, err)) return;
+        ++j;
     }
 }
 
@@ -744,6 +714,7 @@ int march_params(const vmb_grid* g, const vmb_rays* rays, const vmb_march_config
     P->res = g->res;
     P->bits = g->bits;
     P->coarse = g->coarse;
+    P->dist = g->dist;
     P->block = g->block;
     P->res_c = g->res_c;
     P->scale[0] = double(g->res) / g->k.size.x;

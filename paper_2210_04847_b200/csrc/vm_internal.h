@@ -76,6 +76,10 @@ struct vmb_grid {
     uint32_t res_c = 0;            // ceil(res / block)
     uint32_t* coarse = nullptr;    // [ceil(res_c^3 / 32)]
     uint64_t coarse_words = 0;
+    // Chebyshev (L-inf) distance, in cells, from each cell to the nearest occupied
+    // cell, capped at kDistCap (0 = occupied). Lets the marcher jump D-1 cells.
+    uint8_t* dist = nullptr;       // [n_cells]
+    uint8_t* dist_tmp = nullptr;   // [n_cells] scratch of the separable transform
     double* probed = nullptr;      // [n_cells] scratch for the sharded / callback update
 };
 
@@ -108,6 +112,7 @@ int scan_flags(vmb_ctx* ctx, const uint8_t* flags, uint64_t n, uint32_t* pos,
 
 // ---------------------------------------------------------------- grid (grid.cu)
 int grid_refresh(vmb_ctx* ctx, vmb_grid* g);      // bits + coarse from cache
-int grid_rebuild_coarse(vmb_ctx* ctx, vmb_grid* g);
+int grid_rebuild_coarse(vmb_ctx* ctx, vmb_grid* g);  // coarse bits + distance map
+constexpr int kDistCap = 16;
 
 }  // namespace vmb

@@ -385,3 +385,71 @@ def test_render_closed_forms(dev):
     z = api.PackedSamples(np.array([0, 0], np.uint32), np.array([0, 0], np.uint32))
     _, o, _ = api.render_forward(z, np.zeros((0, 3)), np.zeros(0), dev=dev)
     assert list(o) == [0.0, 0.0]
+
+
+# ------------------------------------------------------------------ skipping stress tests
+def _stress_rays(rng, n):
+    o = rng.uniform(-0.6, 1.6, (n, 3))
+    d = rng.normal(size=(n, 3))
+    k = n // 4
+    # axis-aligned and single-zero-component directions; origins on cell faces
+    d[:k] = np.eye(3)[rng.integers(0, 3, k)] * rng.choice([-1.0, 1.0], (k, 1))
+    d[k:2 * k, rng.integers(0, 3)] = 0.0
+    o[2 * k:3 * k] = np.round(o[2 * k:3 * k] * 64) / 64
+    d /= np.sqrt((d * d).sum(1))[:, None]
+    return o, d
+
+
+@pytest.mark.parametrize("density", [0.002, 0.02, 0.2, 0.7])
+def test_march_skipping_random_grids(dev, orc, density):
+    rng = np.random.default_rng(int(density * 1000) + 11)
+    R = 64
+    mask = (rng.uniform(size=R ** 3) < density).astype(np.uint8)
+    g = api.OccupancyGrid(R, Contraction.aabb(), dev=dev)
+    og = orc.grid(R, O.Contraction.aabb())
+    g.seed_mask(mask)
+    og.seed_mask(mask)
+    field = Field.box((0.1, 0.2, 0.0), (0.9, 0.7, 1.0), 30.0)
+    o, d = _stress_rays(rng, 4000)
+    for step in (0.003, 0.0117, 0.0371):
+        cfg = MarchConfig(step, 1e-3, 1e-2)
+        st = MarchStats()
+        p = api.march(api.RayBatch.create(o, d, 0.0, 2.5, dev), g, field, cfg, stats=st)
+        q = orc.march_field(o, d, 0.0, 2.5, og, ofield(field), ocfg(cfg), 4)
+        same_packed(p, q)
+        assert st.samples_emitted == q.samples_emitted
+
+
+def test_march_grazing_sphere(dev, orc):
+    """Rays tangent to the sphere at distance r +- tiny: the filtered fp32 density test
+    must fall back to fp64 exactly where it matters."""
+    field = Field.sphere(center=(0.5, 0.5, 0.5), radius=0.2, sigma=200.0)
+    g, og = both_grids(dev, orc, 128, Contraction.aabb(), field, workload.grid_warmup_seeds(8, 5))
+    rng = np.random.default_rng(5)
+    n = 6000
+    d = rng.normal(size=(n, 3))
+    d /= np.sqrt((d * d).sum(1))[:, None]
+    perp = rng.normal(size=(n, 3))
+    perp -= (perp * d).sum(1)[:, None] * d
+    perp /= np.sqrt((perp * perp).sum(1))[:, None]
+    h = 0.2 + rng.choice([-1, 1], n) * 10.0 ** rng.uniform(-12, -3, n)
+    o = 0.5 + perp * h[:, None] - d * 0.6
+    for step in (5e-3, 1.6914558667664816e-3):
+        cfg = MarchConfig(step, 1e-4, 1e-2)
+        p = api.march(api.RayBatch.create(o, d, 0.2, 1.0, dev), g, field, cfg)
+        same_packed(p, orc.march_field(o, d, 0.2, 1.0, og, ofield(field), ocfg(cfg), 4))
+
+
+def test_march_float32_rays_match_widened_oracle(dev, orc):
+    """The bench path: f32 rays on the device == the same rays widened to f64 on the CPU."""
+    field = Field.sphere(**workload.SPHERE)
+    g, og = both_grids(dev, orc, 128, Contraction.aabb(), field, workload.grid_warmup_seeds(16, 5))
+    o, d = workload.orbit_rays(256, angle=1.3)
+    o32, d32 = o.astype(np.float32), d.astype(np.float32)
+    do_, dd_ = dev.upload(o32), dev.upload(d32)
+    from paper_2210_04847_b200._lib import Rays, VMB_F32
+    rays = Rays(do_.ptr, dd_.ptr, VMB_F32, 0, len(o), 0.2, 1.0)
+    cfg = MarchConfig(5e-3, 1e-4, 1e-2)
+    out = api.march_device(dev, g, rays, field, cfg, api.DevicePacked.allocate(dev, len(o), 16 * len(o)))
+    same_packed(out.to_host(), orc.march_field(o32.astype(np.float64), d32.astype(np.float64), 0.2, 1.0,
+                                               og, ofield(field), ocfg(cfg), 4))
