@@ -19,8 +19,24 @@ CU_SRCS  := $(SRC)/runtime.cu $(SRC)/scan.cu $(SRC)/grid.cu $(SRC)/march.cu $(SR
 CU_OBJS  := $(patsubst $(SRC)/%.cu,build/obj/%.o,$(CU_SRCS))
 HDRS     := $(SRC)/vm_internal.h $(SRC)/vm_exact.cuh include/vmb200.h include/vmb200_types.h
 
-.PHONY: all oracle clean
-all: $(LIB)/libvoxmarch_b200.so oracle
+CXXFLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Wextra -Iinclude -I$(SRC)
+
+.PHONY: all oracle ref_unit clean
+all: $(LIB)/libvoxmarch_b200.so $(LIB)/libvoxmarch_cpp.so build/vm_cpp_tests oracle ref_unit
+
+# the reference's own unit tests compiled against the facade (tests/ref_unit/Makefile)
+ref_unit: $(LIB)/libvoxmarch_cpp.so
+	$(MAKE) -f tests/ref_unit/Makefile
+
+# C++ drop-in facade (namespace voxmarch) over the C ABI
+$(LIB)/libvoxmarch_cpp.so: $(SRC)/facade.cpp include/voxmarch/voxmarch.hpp $(HDRS) $(LIB)/libvoxmarch_b200.so
+	$(CXX) $(CXXFLAGS) -shared -o $@ $(SRC)/facade.cpp -L$(LIB) -lvoxmarch_b200 -Wl,-rpath,'$$ORIGIN'
+
+# C++ facade tests (run on a GPU by tests/test_cpp_facade.py)
+build/vm_cpp_tests: tests/cpp/test_facade.cpp tests/cpp/mini_check.hpp include/voxmarch/voxmarch.hpp $(LIB)/libvoxmarch_cpp.so
+	@mkdir -p build
+	$(CXX) $(CXXFLAGS) -o $@ tests/cpp/test_facade.cpp -L$(LIB) -lvoxmarch_cpp -lvoxmarch_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../$(LIB)'
 
 build/obj/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p build/obj

@@ -10,6 +10,7 @@
 // threshold decision when a value sits within ~1 ulp of the threshold.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 
 #include "../../include/vmb200_types.h"
@@ -21,6 +22,12 @@
 #endif
 
 namespace vmb {
+
+#ifndef __CUDACC__
+using std::floor;
+using std::isfinite;
+using std::sqrt;
+#endif
 
 struct D3 {
     double x, y, z;
