@@ -133,6 +133,15 @@ int vmb_grid_info(const vmb_grid* g, uint32_t* h_resolution, vmb_contraction* h_
 int vmb_grid_update_field(vmb_ctx* ctx, vmb_grid* g, const vmb_field* f,
                           const double* h_timestamps, uint64_t n_timestamps, double ema_decay,
                           int has_seed, uint64_t seed);
+/* The probe half of vmb_grid_update_field for cells [cell_begin, cell_end) only
+ * (occupancy_grid.cpp:106-140): d_probed (n_cells f64) receives the max density
+ * over timestamps for those cells and 0 everywhere else. This is what each rank
+ * contributes to the all-reduce(max) of a multi-GPU update; combining the ranks'
+ * buffers with max and calling vmb_grid_apply reproduces the single-GPU grid. */
+int vmb_grid_probe_field_range(vmb_ctx* ctx, const vmb_grid* g, const vmb_field* f,
+                               const double* h_timestamps, uint64_t n_timestamps, int has_seed,
+                               uint64_t seed, uint64_t cell_begin, uint64_t cell_end,
+                               double* d_probed);
 /* Generic host-callback update, step 1: probe points of all invertible cells in
  * cell order (occupancy_grid.cpp:108-119). d_points needs 3*n_cells doubles,
  * d_cells n_cells u32. Synchronizes to return the count. */

@@ -428,6 +428,21 @@ class OracleGrid:
             self.h, cbf, None, _p(ts, C.c_double), C.c_uint64(len(ts)), C.c_double(decay),
             C.c_int(seed is not None), C.c_uint64(0 if seed is None else int(seed))))
 
+    def probe_range(self, field, c0, c1, seed=None, timestamps=(0.0,)):
+        """Port only: probes of cells [c0, c1) (0 elsewhere) — one rank's share."""
+        ts = _f64(timestamps)
+        out = np.zeros(self.resolution ** 3)
+        self.o._check(self.o.lib.vmo_grid_probe_range(
+            self.h, C.byref(field), _p(ts, C.c_double), C.c_uint64(len(ts)),
+            C.c_int(seed is not None), C.c_uint64(0 if seed is None else int(seed)),
+            C.c_uint64(c0), C.c_uint64(c1), _p(out, C.c_double)))
+        return out
+
+    def apply(self, probed, decay):
+        """Port only: cache = max(cache*decay, probed); refresh bits."""
+        p = _f64(probed)
+        self.o._check(self.o.lib.vmo_grid_apply(self.h, _p(p, C.c_double), C.c_double(decay)))
+
     def seed_mask(self, mask):
         m = np.ascontiguousarray(mask, dtype=np.uint8)
         self.o._check(self.o._f("grid_seed_mask")(self.h, _p(m, C.c_uint8)))

@@ -123,6 +123,12 @@ typedef int64_t (*vmo_sigma_cb)(void* user, const double* t_starts, const double
 VMO_DECLARE(vmo)
 VMO_DECLARE(vmr)
 
+/* Sharded grid update halves (port only; the reference has no multi-rank update). */
+int vmo_grid_probe_range(const vmo_grid* g, const vmb_field* f, const double* timestamps,
+                         uint64_t n_timestamps, int has_seed, uint64_t seed, uint64_t c0,
+                         uint64_t c1, double* probed);
+int vmo_grid_apply(vmo_grid* g, const double* probed, double ema_decay);
+
 #ifdef __cplusplus
 }
 #endif

@@ -145,6 +145,7 @@ SIGNATURES = {
     "vmb_grid_clone": (I32, [VP, VP, P(VP)]),
     "vmb_grid_info": (I32, [VP, P(C.c_uint32), P(Contraction), P(D), P(D), P(D)]),
     "vmb_grid_update_field": (I32, [VP, VP, P(Field), P(D), U64, D, I32, U64]),
+    "vmb_grid_probe_field_range": (I32, [VP, VP, P(Field), P(D), U64, I32, U64, U64, U64, VP]),
     "vmb_grid_probe_points": (I32, [VP, VP, I32, U64, VP, VP, P(U64)]),
     "vmb_grid_accumulate": (I32, [VP, VP, VP, VP, U64, VP]),
     "vmb_grid_apply": (I32, [VP, VP, VP, D]),

@@ -499,6 +499,18 @@ int vmb_grid_update_field(vmb_ctx* ctx, vmb_grid* g, const vmb_field* f, const d
     return rc ? rc : grid_rebuild_coarse(ctx, g);
 }
 
+int vmb_grid_probe_field_range(vmb_ctx* ctx, const vmb_grid* g, const vmb_field* f,
+                               const double* h_ts, uint64_t n_ts, int has_seed, uint64_t seed,
+                               uint64_t c0, uint64_t c1, double* d_probed) {
+    Timestamps ts;
+    int rc = make_timestamps(h_ts, n_ts, &ts);
+    if (rc) return rc;
+    if (c1 > g->n_cells) c1 = g->n_cells;
+    k_probe_range<<<grid_blocks(ctx, g->n_cells, 256), 256, 0, ctx->stream>>>(
+        dev_of(g), *f, ts, has_seed != 0, seed, c0, c1, d_probed);
+    return launch_check("grid probe range");
+}
+
 int vmb_grid_probe_points(vmb_ctx* ctx, const vmb_grid* g, int has_seed, uint64_t seed,
                           double* d_points, uint32_t* d_cells, uint64_t* h_count) {
     uint64_t n = g->n_cells;
