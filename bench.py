@@ -34,7 +34,9 @@ sys.path.insert(0, ROOT)
 
 BASELINE_METRIC = "rays/sec & samples/sec (march+render fwd+bwd) at 1/2/4/8 B200; % HBM roofline"
 SCENE = dict(center=(0.5, 0.5, 0.5), radius=0.2, sigma=200.0, rgb=(0.8, 0.25, 0.25))
-KERNELS_PER_STEP = 8  # march count, scan x3, march fill, shade, forward, backward
+# march = k_march_walk + k_scan_tiles + k_scan_sums + k_scan_add + k_march_expand + k_march_fixup;
+# then k_shade, k_forward, k_backward
+KERNELS_PER_STEP = 9
 
 
 def parse():
@@ -134,6 +136,22 @@ class Clocks:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(sm)}
+
+
+PHASE_KERNELS = {"march": ["k_march_walk", "k_scan_tiles", "k_scan_sums", "k_scan_add",
+                           "k_march_expand", "k_march_fixup"],
+                 "shade": ["k_shade"], "render_forward": ["k_forward"],
+                 "render_backward": ["k_backward"]}
+
+
+def traffic_of(phase):
+    """DRAM bytes (read + write) per launch of a phase's kernels, from the committed
+    ncu --set full summary of the same workload (profiles/ncu_traffic.json), or None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return sum(t["kernels"][k] for k in PHASE_KERNELS[phase] if k in t["kernels"]) or None
+    except Exception:
+        return None
 
 
 def peaks():
@@ -342,7 +360,7 @@ def main():
                  "render_forward": bytes_fwd, "render_backward": bytes_bwd}[dom]
     achieved = dom_bytes / (phase.get(dom, ms_step) * 1e-3) / 1e9
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+            "frac": achieved / peak, "traffic": traffic_of(dom), "peak_source": peak_src,
             "algorithmic_bytes": dom_bytes,
             "step": {"algorithmic_bytes": bytes_step,
                      "achieved": bytes_step / (ms_step * 1e-3) / 1e9,
