@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--cpu-sample-rays", type=int, default=1 << 20)
     ap.add_argument("--ref-sample-rays", type=int, default=1 << 18)
     ap.add_argument("--phases", type=int, default=1, help="per-phase event timing pass")
+    ap.add_argument("--shade", default="fused", choices=["fused", "separate"],
+                    help="analytic-field shading fused into the march packing, or a separate kernel")
     return ap.parse_args()
 
 
@@ -297,9 +299,15 @@ def main():
     g_rgb, g_sig = dev.empty(cap * 3, np.float32), dev.empty(cap, np.float32)
     col, op, dep = dev.empty(N * 3, np.float32), dev.empty(N, np.float32), dev.empty(N, np.float32)
 
+    def march_and_shade():
+        if args.shade == "fused":  # analytic field shaded while the samples are packed
+            api.march_shaded_device(dev, grid, rays, field, cfg, packed, rgb, sig)
+        else:
+            api.march_device(dev, grid, rays, field, cfg, packed)
+            api.shade_device(dev, rays, field, packed, rgb, sig)
+
     def step():
-        api.march_device(dev, grid, rays, field, cfg, packed)
-        api.shade_device(dev, rays, field, packed, rgb, sig)
+        march_and_shade()
         api.render_forward_device(dev, packed, rgb, sig, col, op, dep)
         api.render_backward_device(dev, packed, rgb, sig, up_c, up_o, up_d, g_rgb, g_sig)
 
@@ -334,9 +342,13 @@ def main():
         acc = np.zeros(4)
         for _ in range(args.steps):
             dev.record(2)
-            api.march_device(dev, grid, rays, field, cfg, packed)
-            dev.record(3)
-            api.shade_device(dev, rays, field, packed, rgb, sig)
+            if args.shade == "fused":
+                api.march_shaded_device(dev, grid, rays, field, cfg, packed, rgb, sig)
+                dev.record(3)
+            else:
+                api.march_device(dev, grid, rays, field, cfg, packed)
+                dev.record(3)
+                api.shade_device(dev, rays, field, packed, rgb, sig)
             dev.record(4)
             api.render_forward_device(dev, packed, rgb, sig, col, op, dep)
             dev.record(5)
@@ -426,12 +438,13 @@ def main():
                                        f"{R}^3 grid (16 jittered warm-up updates), SolidSphere r=0.2 "
                                        f"sigma=200, step {args.step_size}, alpha 1e-2, eps 1e-4",
                            "rays_per_gpu": N, "samples_per_gpu": S, "resolution": R,
+                           "shading": args.shade + " (analytic SolidSphere rgb/sigma at sample midpoints)",
                            "storage": "rays/rgb/sigma/outputs f32, t f64, compute f64",
                            "l2": "inputs larger than L2 (~1 GB working set per step)",
                            "parallelism": f"dp{dist.world} (rays sharded, grid replicated)"},
                 "phases_ms": phase, "grid_update_ms": grid_update_ms,
                 "roofline": roof, "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
-                "gpu_launches": KERNELS_PER_STEP * args.steps}
+                "gpu_launches": (KERNELS_PER_STEP - (args.shade == "fused")) * args.steps}
         print(json.dumps(line), flush=True)
     if dist.world > 1:
         L.vmb_comm_destroy(dev.h)

@@ -183,6 +183,15 @@ const double* vmb_grid_device_cache(const vmb_grid* g);
 int vmb_march_field(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays, const vmb_field* f,
                     const vmb_march_config* cfg, vmb_samples* out, uint64_t* h_n_samples,
                     vmb_march_stats* h_stats);
+/* vmb_march_field + vmb_shade_field fused: while the kept samples are packed,
+ * the field's rgb and sigma at each sample's midpoint (shade_samples,
+ * voxmarch.cpp:235-251, with the TimeConditionedField shift at `time`) are
+ * written to d_rgbs [capacity][3] / d_sigmas [capacity] in `dtype`. Same capacity
+ * protocol as vmb_march_field (the attribute buffers need the same capacity). */
+int vmb_march_field_shaded(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,
+                           const vmb_field* f, const vmb_march_config* cfg, vmb_samples* out,
+                           void* d_rgbs, void* d_sigmas, int dtype, double time,
+                           uint64_t* h_n_samples, vmb_march_stats* h_stats);
 /* Asynchronous variant for training loops / CUDA graphs: no host round trip.
  * The sample total is written to d_n_samples (u64, device); samples beyond
  * out->capacity are dropped (check d_n_samples afterwards). Errors (negative or

@@ -46,11 +46,8 @@ class Device:
             self.lib.vmb_ctx_destroy(self.h)
             self.h = C.c_void_p()
 
-    def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass
+    # No __del__: device arrays may be garbage-collected after their context (cycle
+    # collection order is arbitrary), so a context lives until close() or exit.
 
     def sync(self):
         check(self.lib.vmb_ctx_synchronize(self.h))
@@ -91,9 +88,9 @@ class DeviceArray:
         self.ptr = p.value
 
     def free(self):
-        if self.ptr:
+        if self.ptr and self.dev.h:
             self.dev.lib.vmb_free(self.dev.h, self.ptr)
-            self.ptr = None
+        self.ptr = None
 
     def __del__(self):
         try:
@@ -191,6 +188,19 @@ def march_device(dev: Device, grid: "OccupancyGrid", rays: Rays, field: Field, c
                                      C.byref(smp), C.byref(n),
                                      C.byref(stats) if stats is not None else None)
     check(rc)
+    out.n_samples = int(n.value)
+    return out
+
+
+def march_shaded_device(dev: Device, grid: "OccupancyGrid", rays: Rays, field: Field,
+                        cfg: MarchConfig, out: DevicePacked, rgbs: DeviceArray, sigmas: DeviceArray,
+                        time: float = 0.0, stats: Optional[MarchStats] = None) -> DevicePacked:
+    """vmb_march_field_shaded: march + analytic shading fused (buffers must be large enough)."""
+    n = C.c_uint64()
+    smp = out.samples_struct()
+    check(dev.lib.vmb_march_field_shaded(dev.h, grid.h, C.byref(rays), C.byref(field), C.byref(cfg),
+                                         C.byref(smp), rgbs.ptr, sigmas.ptr, _dt(rgbs.dtype), time,
+                                         C.byref(n), C.byref(stats) if stats is not None else None))
     out.n_samples = int(n.value)
     return out
 

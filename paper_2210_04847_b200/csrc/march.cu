@@ -519,11 +519,37 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
     }
 }
 
+// Optional fused shading of an analytic field (vmb_march_field_shaded): the
+// expand kernel already holds each sample's ray and exact t0/t1, so it writes the
+// field's rgb/sigma at the midpoint too — the expressions of shade_samples
+// (voxmarch.cpp:235-251) / k_shade, without re-reading the packed samples.
+template <typename RT, typename AT>
+struct ShadeOut {
+    const RT* orig;
+    const RT* dirs;
+    vmb_field f;
+    double time;
+    AT* rgb;
+    AT* sig;
+    __device__ __forceinline__ void shade(uint64_t r, uint64_t p, double t0, double t1) const {
+        D3 o = d3(double(orig[3 * r]), double(orig[3 * r + 1]), double(orig[3 * r + 2]));
+        D3 d = d3(double(dirs[3 * r]), double(dirs[3 * r + 1]), double(dirs[3 * r + 2]));
+        D3 x = o + d * (0.5 * (t0 + t1));
+        D3 c;
+        double sigma = field_rgb_sigma(f, time_shift(f, x, time), &c);
+        rgb[3 * p] = AT(c.x);
+        rgb[3 * p + 1] = AT(c.y);
+        rgb[3 * p + 2] = AT(c.z);
+        sig[p] = AT(sigma);
+    }
+};
+
+template <typename RT, typename AT, bool SHADE>
 __global__ void __launch_bounds__(256) k_march_expand(
     double near_, double far_, double step, const uint32_t* __restrict__ counts,
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ kept_idx, uint64_t n_rays,
     double* __restrict__ ts, double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,
-    uint32_t* __restrict__ overflow, unsigned int* n_overflow) {
+    uint32_t* __restrict__ overflow, unsigned int* n_overflow, ShadeOut<RT, AT> sh) {
     const int lane = threadIdx.x & 31;
     const uint64_t n_chunks = (n_rays + 31) / 32;
     for (uint64_t chunk = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; chunk < n_chunks;
@@ -555,9 +581,12 @@ __global__ void __launch_bounds__(256) k_march_expand(
                 const uint64_t k = p - loff;
                 if (k < uint64_t(kWalkCap)) {
                     const uint64_t i = kbuf[k * 32 + L];
-                    ts[p] = near_ + double(i) * step;
-                    te[p] = min_ref(near_ + double(i + 1) * step, far_);
+                    const double t0 = near_ + double(i) * step;
+                    const double t1 = min_ref(near_ + double(i + 1) * step, far_);
+                    ts[p] = t0;
+                    te[p] = t1;
                     idx[p] = uint32_t(chunk * 32 + L);
+                    if (SHADE) sh.shade(chunk * 32 + L, p, t0, t1);
                 }
             }
         }
@@ -565,12 +594,12 @@ __global__ void __launch_bounds__(256) k_march_expand(
 }
 
 // Re-walks the (rare) rays whose kept samples overflowed the shared buffer.
-template <typename RT>
+template <typename RT, typename AT, bool SHADE>
 __global__ void k_march_fixup(MarchParams P, const RT* __restrict__ orig, const RT* __restrict__ dirs,
                               const uint32_t* __restrict__ offsets, double* __restrict__ ts,
                               double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,
                               const uint32_t* __restrict__ overflow, const unsigned int* n_overflow,
-                              DevError* err) {
+                              DevError* err, ShadeOut<RT, AT> sh) {
     const unsigned int n = *n_overflow;
     for (unsigned int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         uint64_t r = overflow[k];
@@ -582,6 +611,8 @@ __global__ void k_march_fixup(MarchParams P, const RT* __restrict__ orig, const 
         s.base = offsets[r];
         s.cap = cap;
         walk<FILL>(P, s, orig, dirs, r, err);
+        if (SHADE)
+            for (uint64_t q = s.base; q < s.base + s.n_kept && q < cap; ++q) sh.shade(r, q, ts[q], te[q]);
     }
 }
 
@@ -804,9 +835,45 @@ bool use_fused(const MarchParams& P) {
     return !P.grows && !forced;
 }
 
-// walk -> scan -> expand -> fixup; the sample total lands in d_total.
+// Optional analytic-field shading fused into the packing (vmb_march_field_shaded).
+struct ShadeReq {
+    bool on = false;
+    vmb_field f{};
+    double time = 0.0;
+    void* rgb = nullptr;
+    void* sig = nullptr;
+    int dtype = VMB_F32;
+};
+
+template <typename RT, typename AT, bool SHADE>
+void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
+                         const uint32_t* kept_idx, uint32_t* overflow, unsigned int* n_overflow,
+                         uint64_t n_chunks, const ShadeReq& sr) {
+    ShadeOut<RT, AT> sh{static_cast<const RT*>(rays->d_origins), static_cast<const RT*>(rays->d_directions),
+                        sr.f, sr.time, static_cast<AT*>(sr.rgb), static_cast<AT*>(sr.sig)};
+    k_march_expand<RT, AT, SHADE><<<grid_blocks(ctx, n_chunks * 32, 256, 8), 256, 0, ctx->stream>>>(
+        P.near_, P.far_, P.step, out->d_counts, out->d_offsets, kept_idx, rays->n_rays, out->d_t_starts,
+        out->d_t_ends, out->d_ray_indices, out->capacity, overflow, n_overflow, sh);
+    k_march_fixup<RT, AT, SHADE><<<ctx->num_sms * 2, 128, 0, ctx->stream>>>(
+        P, sh.orig, sh.dirs, out->d_offsets, out->d_t_starts, out->d_t_ends, out->d_ray_indices,
+        out->capacity, overflow, n_overflow, ctx->d_err, sh);
+}
+
+template <typename RT>
+void dispatch_expand(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
+                     const uint32_t* kept_idx, uint32_t* overflow, unsigned int* n_overflow,
+                     uint64_t n_chunks, const ShadeReq& sr) {
+    if (!sr.on)
+        launch_expand_fixup<RT, float, false>(ctx, P, rays, out, kept_idx, overflow, n_overflow, n_chunks, sr);
+    else if (sr.dtype == VMB_F32)
+        launch_expand_fixup<RT, float, true>(ctx, P, rays, out, kept_idx, overflow, n_overflow, n_chunks, sr);
+    else
+        launch_expand_fixup<RT, double, true>(ctx, P, rays, out, kept_idx, overflow, n_overflow, n_chunks, sr);
+}
+
+// walk -> scan -> expand (+shade) -> fixup; the sample total lands in d_total.
 int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
-                 unsigned long long* d_total, unsigned long long* emitted) {
+                 unsigned long long* d_total, unsigned long long* emitted, const ShadeReq& sr) {
     const uint64_t n = rays->n_rays;
     const uint64_t n_chunks = (n + 31) / 32;
     const size_t head = 16;
@@ -847,20 +914,10 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
     }
     int rc = scan_counts(ctx, out->d_counts, n, out->d_offsets, d_total);
     if (rc) return rc;
-    k_march_expand<<<grid_blocks(ctx, n_chunks * 32, 256, 8), 256, 0, ctx->stream>>>(
-        P.near_, P.far_, P.step, out->d_counts, out->d_offsets, kept_idx, n, out->d_t_starts,
-        out->d_t_ends, out->d_ray_indices, out->capacity, overflow, counters + 1);
-    const int fix_blocks = ctx->num_sms * 2;
     if (rays->dtype == VMB_F32)
-        k_march_fixup<float><<<fix_blocks, 128, 0, ctx->stream>>>(
-            P, static_cast<const float*>(rays->d_origins), static_cast<const float*>(rays->d_directions),
-            out->d_offsets, out->d_t_starts, out->d_t_ends, out->d_ray_indices, out->capacity, overflow,
-            counters + 1, ctx->d_err);
+        dispatch_expand<float>(ctx, P, rays, out, kept_idx, overflow, counters + 1, n_chunks, sr);
     else
-        k_march_fixup<double><<<fix_blocks, 128, 0, ctx->stream>>>(
-            P, static_cast<const double*>(rays->d_origins),
-            static_cast<const double*>(rays->d_directions), out->d_offsets, out->d_t_starts,
-            out->d_t_ends, out->d_ray_indices, out->capacity, overflow, counters + 1, ctx->d_err);
+        dispatch_expand<double>(ctx, P, rays, out, kept_idx, overflow, counters + 1, n_chunks, sr);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? VMB_OK : cuda_fail(e, "march");
 }
@@ -868,14 +925,14 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
 // Packed march shared by march_field and march_candidates: the fused single-pass
 // kernel when possible, else count -> scan -> (sync) -> fill.
 int march_packed(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
-                 uint64_t* h_n, vmb_march_stats* stats) {
+                 uint64_t* h_n, vmb_march_stats* stats, const ShadeReq& sr = ShadeReq{}) {
     if (!out || !out->d_offsets || !out->d_counts)
         return fail(VMB_INVALID_ARGUMENT, "march: output offsets/counts required");
     int rc = reset_error(ctx);
     if (rc) return rc;
     cudaMemsetAsync(ctx->d_u64 + 1, 0, 8, ctx->stream);
     if (use_fused(P)) {
-        rc = launch_fused(ctx, P, rays, out, ctx->d_u64, stats ? ctx->d_u64 + 1 : nullptr);
+        rc = launch_fused(ctx, P, rays, out, ctx->d_u64, stats ? ctx->d_u64 + 1 : nullptr, sr);
         if (rc) return rc;
         cudaMemcpyAsync(ctx->h_u64, ctx->d_u64, 16, cudaMemcpyDeviceToHost, ctx->stream);
         rc = report_march_error(ctx);  // synchronizes
@@ -907,7 +964,11 @@ int march_packed(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
     if (total > out->capacity) return fail(VMB_CAPACITY, "march: sample capacity too small");
     if (total) launch_march<FILL>(ctx, P, rays, out->d_counts, out->d_offsets, out, nullptr);
     cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? VMB_OK : cuda_fail(e, "march fill");
+    if (e != cudaSuccess) return cuda_fail(e, "march fill");
+    if (sr.on && total)
+        return vmb_shade_field(ctx, rays, &sr.f, sr.time, out->d_ray_indices, out->d_t_starts,
+                               out->d_t_ends, total, sr.rgb, sr.sig, sr.dtype);
+    return VMB_OK;
 }
 
 }  // namespace
@@ -916,6 +977,29 @@ int march_packed(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
 using namespace vmb;
 
 extern "C" {
+
+int vmb_march_field_shaded(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays, const vmb_field* f,
+                           const vmb_march_config* cfg, vmb_samples* out, void* d_rgbs, void* d_sigmas,
+                           int dtype, double time, uint64_t* h_n, vmb_march_stats* stats) {
+    MarchParams P;
+    int rc = march_params(g, rays, cfg, &P);
+    if (rc) return rc;
+    if (f->kind == VMB_FIELD_UNIFORM_BOX &&
+        !(f->box_max[0] > f->box_min[0] && f->box_max[1] > f->box_min[1] && f->box_max[2] > f->box_min[2]))
+        return fail(VMB_INVALID_ARGUMENT, "aabb max must be strictly greater than min");
+    P.f = *f;
+    P.filter = true;
+    P.full = stats != nullptr;
+    set_sphere_fast(&P);
+    ShadeReq sr;
+    sr.on = true;
+    sr.f = *f;
+    sr.time = time;
+    sr.rgb = d_rgbs;
+    sr.sig = d_sigmas;
+    sr.dtype = dtype;
+    return march_packed(ctx, P, rays, out, h_n, stats, sr);
+}
 
 int vmb_march_field(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays, const vmb_field* f,
                     const vmb_march_config* cfg, vmb_samples* out, uint64_t* h_n,
@@ -944,7 +1028,8 @@ int vmb_march_field_async(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,
     P.full = false;
     set_sphere_fast(&P);
     if (use_fused(P))
-        return launch_fused(ctx, P, rays, out, reinterpret_cast<unsigned long long*>(d_n), nullptr);
+        return launch_fused(ctx, P, rays, out, reinterpret_cast<unsigned long long*>(d_n), nullptr,
+                            ShadeReq{});
     if (rays->n_rays) launch_march<COUNT>(ctx, P, rays, out->d_counts, nullptr, nullptr, nullptr);
     rc = scan_counts(ctx, out->d_counts, rays->n_rays, out->d_offsets,
                      reinterpret_cast<unsigned long long*>(d_n));

@@ -1,35 +1,48 @@
 // render.cu — differentiable compositing along rays (rendering.cpp:19-134).
 //
 // Layout: packed samples are ray-contiguous (offsets = exclusive scan of counts),
-// so the samples of 32 consecutive rays form one contiguous range. Each warp
-// owns 32 rays and streams their range through shared memory in chunks:
-//   1. coalesced, all-lane loads of t_starts/t_ends (f64), rgb (AoS) and sigma
-//      into the warp's smem tile (every HBM byte read exactly once);
-//   2. each lane runs its own ray's exclusive transmittance scan sequentially
-//      from smem, in the reference's operation order and in fp64
-//      (T *= 1 - alpha; fp32 accumulation is not accurate enough);
-//   3. per-sample outputs are staged back into the tile and written coalesced.
-// render_backward keeps the reference's reverse suffix-sum when a warp's range
-// fits one tile; longer ranges use two forward sweeps with suffix_k = S - P_k.
-// Warps whose rays are not contiguous (arbitrary user offsets) fall back to
-// per-lane global reads — same math, no staging.
+// so the samples of 32 consecutive rays form one contiguous range. Each warp owns
+// 32 rays and streams their range through its shared-memory tile:
+//   1. cp.async (LDGSTS) copies t_starts/t_ends (f64), sigma and rgb (AoS) of up to
+//      CH samples into the tile — every element in flight at once, no registers;
+//   2. alpha = 1 - exp(-sigma * delta) is computed sample-parallel (all lanes,
+//      independent exps), so the per-ray loops below never wait on an exp;
+//   3. each lane runs its own ray's recurrence sequentially from shared memory in
+//      the reference's operation order and in fp64 (T *= 1 - alpha; fp32 is not
+//      accurate enough);
+//   4. per-sample outputs are staged back into the tile and written coalesced.
+// render_backward groups consecutive rays whose samples fit one tile and runs
+// the reference's forward-T / reverse-suffix recurrence; only a single ray longer
+// than a tile uses two forward sweeps with suffix_k = S - P_k. Warps whose rays
+// are not contiguous (arbitrary user offsets) use per-lane global reads.
+// Sample positions are 32-bit: packed offsets are u32 by construction (pack()
+// rejects more than 2^32-1 samples, core_types.cpp:33-36).
 #include "vm_internal.h"
 
 namespace vmb {
 namespace {
 
-constexpr int kWarps = 4;  // 128 threads per CTA
+constexpr int kWarps = 8;  // 256 threads per CTA
 
 template <typename T> struct Tile;
-template <> struct Tile<float> { static constexpr int CH = 256; };
-template <> struct Tile<double> { static constexpr int CH = 128; };
+template <> struct Tile<float> { static constexpr int CH = 128; };
+template <> struct Tile<double> { static constexpr int CH = 64; };
 
 template <typename T>
-struct Smem {
+struct FwdSmem {
     double ts[Tile<T>::CH];
     double te[Tile<T>::CH];
-    double tr[Tile<T>::CH];   // transmittance (backward / transmittance output)
-    double al[Tile<T>::CH];   // alpha (backward)
+    double al[Tile<T>::CH];   // alpha (or exp(-sigma*delta) for the transmittance)
+    T rgb[3 * Tile<T>::CH];
+    T sig[Tile<T>::CH];
+};
+
+template <typename T>
+struct BwdSmem {
+    double ts[Tile<T>::CH];
+    double te[Tile<T>::CH];
+    double al[Tile<T>::CH];
+    double tr[Tile<T>::CH];   // transmittance before each sample
     T rgb[3 * Tile<T>::CH];   // input rgb, then d_rgb
     T sig[Tile<T>::CH];       // input sigma, then d_sigma
 };
@@ -37,9 +50,9 @@ struct Smem {
 struct RayRange {
     uint64_t r;
     bool valid;
-    uint64_t off, end;
+    uint32_t off, end;
     bool contiguous;  // warp-uniform
-    uint64_t s0, s1;  // warp range when contiguous
+    uint32_t s0, s1;  // warp range when contiguous
 };
 
 __device__ __forceinline__ RayRange ray_range(const uint32_t* __restrict__ offsets,
@@ -48,16 +61,15 @@ __device__ __forceinline__ RayRange ray_range(const uint32_t* __restrict__ offse
     RayRange rr;
     rr.r = warp_id * 32 + lane;
     rr.valid = rr.r < n_rays;
-    rr.off = rr.valid ? offsets[rr.r] : 0;
-    rr.end = rr.valid ? rr.off + counts[rr.r] : 0;
-    uint64_t next_off = __shfl_down_sync(0xffffffffu, rr.off, 1);
-    bool next_valid = __shfl_down_sync(0xffffffffu, rr.valid, 1);
-    bool ok = !(rr.valid && lane < 31 && next_valid) || rr.end == next_off;
+    rr.off = rr.valid ? __ldg(offsets + rr.r) : 0u;
+    rr.end = rr.valid ? rr.off + __ldg(counts + rr.r) : 0u;
+    const uint32_t next_off = __shfl_down_sync(0xffffffffu, rr.off, 1);
+    const bool next_valid = __shfl_down_sync(0xffffffffu, int(rr.valid), 1);
+    const bool ok = !(rr.valid && lane < 31 && next_valid) || rr.end == next_off;
     rr.contiguous = __all_sync(0xffffffffu, ok);
     rr.s0 = __shfl_sync(0xffffffffu, rr.off, 0);
-    unsigned vmask = __ballot_sync(0xffffffffu, rr.valid);
-    int last = vmask ? 31 - __clz(vmask) : 0;
-    rr.s1 = __shfl_sync(0xffffffffu, rr.end, last);
+    const unsigned vmask = __ballot_sync(0xffffffffu, rr.valid);
+    rr.s1 = __shfl_sync(0xffffffffu, rr.end, vmask ? 31 - __clz(vmask) : 0);
     return rr;
 }
 
@@ -68,42 +80,35 @@ __device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
                  : "memory");
 }
 
-// Stage samples [cs, cs+n) of the warp's range into its smem tile. alpha (or,
-// for the transmittance output, exp(-sigma*delta)) is computed here, sample-
-// parallel: every lane evaluates exp() for independent samples, so the per-ray
-// sequential loops that follow only multiply and add (no exp on their critical
-// path). Same expressions as rendering.cpp, so the values are the reference's.
-template <typename T, bool kTransmittanceFactor = false>
-__device__ __forceinline__ void stage_in(Smem<T>& sm, int lane, uint64_t cs, uint64_t n,
+// Stage samples [cs, cs+n) into a tile and compute alpha (kTransmittance: the
+// factor exp(-sigma*delta) of rendering.cpp:29 instead) for each of them.
+template <typename T, bool kTransmittance, typename S>
+__device__ __forceinline__ void stage_in(S& sm, int lane, uint32_t cs, uint32_t n,
                                          const double* __restrict__ ts, const double* __restrict__ te,
                                          const T* __restrict__ rgb, const T* __restrict__ sig) {
-    // cp.async (LDGSTS): every element of the tile is in flight at once without
-    // occupying registers; then alpha is computed from shared memory.
-    for (uint64_t i = lane; i < n; i += 32) {
+    for (uint32_t i = lane; i < n; i += 32) {
         cp_async<8>(&sm.ts[i], ts + cs + i);
         cp_async<8>(&sm.te[i], te + cs + i);
         cp_async<sizeof(T)>(&sm.sig[i], sig + cs + i);
     }
     if (rgb)
-        for (uint64_t i = lane; i < 3 * n; i += 32) cp_async<sizeof(T)>(&sm.rgb[i], rgb + 3 * cs + i);
+        for (uint32_t i = lane; i < 3 * n; i += 32)
+            cp_async<sizeof(T)>(&sm.rgb[i], rgb + 3 * uint64_t(cs) + i);
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncwarp();
-    for (uint64_t i = lane; i < n; i += 32) {
+    for (uint32_t i = lane; i < n; i += 32) {
         double e = exp(-double(sm.sig[i]) * (sm.te[i] - sm.ts[i]));
-        sm.al[i] = kTransmittanceFactor ? e : 1.0 - e;
+        sm.al[i] = kTransmittance ? e : 1.0 - e;
     }
+    __syncwarp();
 }
 
 // ------------------------------------------------------------------ forward
 struct Fwd {
     double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0, op = 0.0, dep = 0.0;
-    // rendering.cpp:51-58
+    // rendering.cpp:51-58 (alpha precomputed with the same expression)
     __device__ __forceinline__ void add(double ts, double te, double r, double g, double b,
-                                        double sigma) {
-        add_alpha(ts, te, r, g, b, 1.0 - exp(-sigma * (te - ts)));
-    }
-    __device__ __forceinline__ void add_alpha(double ts, double te, double r, double g, double b,
-                                              double alpha) {
+                                        double alpha) {
         double w = T * alpha;
         cr = cr + r * w;
         cg = cg + g * w;
@@ -115,35 +120,34 @@ struct Fwd {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kWarps * 32) k_forward(
+__global__ void __launch_bounds__(kWarps * 32, 4) k_forward(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays,
     const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
     const T* __restrict__ sig, T* __restrict__ color, T* __restrict__ opacity, T* __restrict__ depth) {
-    __shared__ Smem<T> smem[kWarps];
+    __shared__ FwdSmem<T> smem[kWarps];
     const int lane = threadIdx.x & 31;
-    Smem<T>& sm = smem[threadIdx.x >> 5];
+    FwdSmem<T>& sm = smem[threadIdx.x >> 5];
     const uint64_t n_warps = (n_rays + 31) / 32;
     for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
          w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-        RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
+        const RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
         Fwd acc;
         if (rr.contiguous) {
-            for (uint64_t cs = rr.s0; cs < rr.s1; cs += Tile<T>::CH) {
-                uint64_t n = min(uint64_t(Tile<T>::CH), rr.s1 - cs);
-                stage_in(sm, lane, cs, n, ts, te, rgb, sig);
-                __syncwarp();
-                uint64_t a = max(rr.off, cs), b = min(rr.end, cs + n);
-                for (uint64_t s = a; s < b; ++s) {
-                    uint64_t i = s - cs;
-                    acc.add_alpha(sm.ts[i], sm.te[i], double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
-                                  double(sm.rgb[3 * i + 2]), sm.al[i]);
+            for (uint32_t cs = rr.s0; cs < rr.s1; cs += Tile<T>::CH) {
+                const uint32_t n = min(uint32_t(Tile<T>::CH), rr.s1 - cs);
+                stage_in<T, false>(sm, lane, cs, n, ts, te, rgb, sig);
+                const uint32_t a = max(rr.off, cs), b = min(rr.end, cs + n);
+                for (uint32_t s = a; s < b; ++s) {
+                    const uint32_t i = s - cs;
+                    acc.add(sm.ts[i], sm.te[i], double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
+                            double(sm.rgb[3 * i + 2]), sm.al[i]);
                 }
                 __syncwarp();
             }
         } else {
-            for (uint64_t s = rr.off; s < rr.end; ++s)
-                acc.add(ts[s], te[s], double(rgb[3 * s]), double(rgb[3 * s + 1]), double(rgb[3 * s + 2]),
-                        double(sig[s]));
+            for (uint32_t s = rr.off; s < rr.end; ++s)
+                acc.add(ts[s], te[s], double(rgb[3 * uint64_t(s)]), double(rgb[3 * uint64_t(s) + 1]),
+                        double(rgb[3 * uint64_t(s) + 2]), 1.0 - exp(-double(sig[s]) * (te[s] - ts[s])));
         }
         if (rr.valid) {
             color[3 * rr.r] = T(acc.cr);
@@ -177,38 +181,45 @@ __device__ __forceinline__ Up load_up(const T* dc, const T* dop, const T* ddep, 
     return u;
 }
 
-// Two forward sweeps for one ray range (used for a single ray longer than a tile,
-// or with per-lane global reads when the warp's rays are not contiguous):
+template <typename T>
+__device__ __forceinline__ void write_out(BwdSmem<T>& sm, int lane, uint32_t cs, uint32_t n,
+                                          T* __restrict__ g_rgb, T* __restrict__ g_sig) {
+    __syncwarp();
+    for (uint32_t i = lane; i < n; i += 32) g_sig[cs + i] = sm.sig[i];
+    for (uint32_t i = lane; i < 3 * n; i += 32) g_rgb[3 * uint64_t(cs) + i] = sm.rgb[i];
+    __syncwarp();
+}
+
+// Two forward sweeps for one ray range (a single ray longer than a tile, or with
+// per-lane global reads when the warp's rays are not contiguous):
 // sweep 1 computes S = sum_k w_k v_k, sweep 2 emits suffix_k = S - P_k.
 template <typename T>
-__device__ void bwd_two_sweep(Smem<T>& sm, int lane, bool active, bool staged, uint64_t off,
-                              uint64_t end, uint64_t s0, uint64_t s1, const Up& u,
+__device__ void bwd_two_sweep(BwdSmem<T>& sm, int lane, bool active, bool staged, uint32_t off,
+                              uint32_t end, uint32_t s0, uint32_t s1, const Up& u,
                               const double* __restrict__ ts, const double* __restrict__ te,
                               const T* __restrict__ rgb, const T* __restrict__ sig,
                               T* __restrict__ g_rgb, T* __restrict__ g_sig) {
-    double S = 0.0;
-    double t = 1.0;
+    double S = 0.0, t = 1.0;
     if (staged) {
-        for (uint64_t cs = s0; cs < s1; cs += Tile<T>::CH) {
-            uint64_t n = min(uint64_t(Tile<T>::CH), s1 - cs);
-            stage_in(sm, lane, cs, n, ts, te, rgb, sig);
-            __syncwarp();
+        for (uint32_t cs = s0; cs < s1; cs += Tile<T>::CH) {
+            const uint32_t n = min(uint32_t(Tile<T>::CH), s1 - cs);
+            stage_in<T, false>(sm, lane, cs, n, ts, te, rgb, sig);
             if (active)
-                for (uint64_t s = max(off, cs); s < min(end, cs + n); ++s) {
-                    uint64_t i = s - cs;
-                    double a = sm.al[i];
-                    double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
-                                       double(sm.rgb[3 * i + 2]), 0.5 * (sm.ts[i] + sm.te[i]));
+                for (uint32_t s = max(off, cs); s < min(end, cs + n); ++s) {
+                    const uint32_t i = s - cs;
+                    const double a = sm.al[i];
+                    const double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
+                                             double(sm.rgb[3 * i + 2]), 0.5 * (sm.ts[i] + sm.te[i]));
                     S += t * a * v;
                     t *= 1.0 - a;
                 }
             __syncwarp();
         }
     } else if (active) {
-        for (uint64_t s = off; s < end; ++s) {
-            double a = 1.0 - exp(-double(sig[s]) * (te[s] - ts[s]));
-            double v = u.value(double(rgb[3 * s]), double(rgb[3 * s + 1]), double(rgb[3 * s + 2]),
-                               0.5 * (ts[s] + te[s]));
+        for (uint32_t s = off; s < end; ++s) {
+            const double a = 1.0 - exp(-double(sig[s]) * (te[s] - ts[s]));
+            const double v = u.value(double(rgb[3 * uint64_t(s)]), double(rgb[3 * uint64_t(s) + 1]),
+                                     double(rgb[3 * uint64_t(s) + 2]), 0.5 * (ts[s] + te[s]));
             S += t * a * v;
             t *= 1.0 - a;
         }
@@ -216,18 +227,17 @@ __device__ void bwd_two_sweep(Smem<T>& sm, int lane, bool active, bool staged, u
     t = 1.0;
     double P = 0.0;
     if (staged) {
-        for (uint64_t cs = s0; cs < s1; cs += Tile<T>::CH) {
-            uint64_t n = min(uint64_t(Tile<T>::CH), s1 - cs);
-            stage_in(sm, lane, cs, n, ts, te, rgb, sig);
-            __syncwarp();
+        for (uint32_t cs = s0; cs < s1; cs += Tile<T>::CH) {
+            const uint32_t n = min(uint32_t(Tile<T>::CH), s1 - cs);
+            stage_in<T, false>(sm, lane, cs, n, ts, te, rgb, sig);
             if (active)
-                for (uint64_t s = max(off, cs); s < min(end, cs + n); ++s) {
-                    uint64_t i = s - cs;
-                    double delta = sm.te[i] - sm.ts[i];
-                    double a = sm.al[i];
-                    double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
-                                       double(sm.rgb[3 * i + 2]), 0.5 * (sm.ts[i] + sm.te[i]));
-                    double wgt = t * a;
+                for (uint32_t s = max(off, cs); s < min(end, cs + n); ++s) {
+                    const uint32_t i = s - cs;
+                    const double delta = sm.te[i] - sm.ts[i];
+                    const double a = sm.al[i];
+                    const double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
+                                             double(sm.rgb[3 * i + 2]), 0.5 * (sm.ts[i] + sm.te[i]));
+                    const double wgt = t * a;
                     P += wgt * v;
                     sm.rgb[3 * i] = T(u.dcx * wgt);
                     sm.rgb[3 * i + 1] = T(u.dcy * wgt);
@@ -235,85 +245,77 @@ __device__ void bwd_two_sweep(Smem<T>& sm, int lane, bool active, bool staged, u
                     sm.sig[i] = T(delta * (t * (1.0 - a) * v - (S - P)));
                     t *= 1.0 - a;
                 }
-            __syncwarp();
-            for (uint64_t i = lane; i < n; i += 32) g_sig[cs + i] = sm.sig[i];
-            for (uint64_t i = lane; i < 3 * n; i += 32) g_rgb[3 * cs + i] = sm.rgb[i];
-            __syncwarp();
+            write_out(sm, lane, cs, n, g_rgb, g_sig);
         }
     } else if (active) {
-        for (uint64_t s = off; s < end; ++s) {
-            double delta = te[s] - ts[s];
-            double a = 1.0 - exp(-double(sig[s]) * delta);
-            double v = u.value(double(rgb[3 * s]), double(rgb[3 * s + 1]), double(rgb[3 * s + 2]),
-                               0.5 * (ts[s] + te[s]));
-            double wgt = t * a;
+        for (uint32_t s = off; s < end; ++s) {
+            const double delta = te[s] - ts[s];
+            const double a = 1.0 - exp(-double(sig[s]) * delta);
+            const double v = u.value(double(rgb[3 * uint64_t(s)]), double(rgb[3 * uint64_t(s) + 1]),
+                                     double(rgb[3 * uint64_t(s) + 2]), 0.5 * (ts[s] + te[s]));
+            const double wgt = t * a;
             P += wgt * v;
-            g_rgb[3 * s] = T(u.dcx * wgt);
-            g_rgb[3 * s + 1] = T(u.dcy * wgt);
-            g_rgb[3 * s + 2] = T(u.dcz * wgt);
+            g_rgb[3 * uint64_t(s)] = T(u.dcx * wgt);
+            g_rgb[3 * uint64_t(s) + 1] = T(u.dcy * wgt);
+            g_rgb[3 * uint64_t(s) + 2] = T(u.dcz * wgt);
             g_sig[s] = T(delta * (t * (1.0 - a) * v - (S - P)));
             t *= 1.0 - a;
         }
     }
 }
 
-// render_backward: the warp's 32 rays are processed in greedy groups of
-// consecutive rays whose samples fit one tile; each group is staged once and every
-// lane runs the reference's exact forward-T / reverse-suffix recurrence
-// (rendering.cpp:85-108) from shared memory. Only a single ray with more samples
-// than a tile uses the two-sweep form.
+// render_backward: greedy groups of consecutive rays whose samples fit one tile;
+// each group is staged once and every lane runs the reference's exact forward-T /
+// reverse-suffix recurrence (rendering.cpp:85-108) from shared memory.
 template <typename T>
-__global__ void __launch_bounds__(kWarps * 32) k_backward(
+__global__ void __launch_bounds__(kWarps * 32, 4) k_backward(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays,
     const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
     const T* __restrict__ sig, const T* __restrict__ dc, const T* __restrict__ dop,
     const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig) {
-    __shared__ Smem<T> smem[kWarps];
+    __shared__ BwdSmem<T> smem[kWarps];
     const int lane = threadIdx.x & 31;
-    Smem<T>& sm = smem[threadIdx.x >> 5];
+    BwdSmem<T>& sm = smem[threadIdx.x >> 5];
     const uint64_t n_warps = (n_rays + 31) / 32;
     for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
          w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-        RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
-        Up u = load_up(dc, dop, ddep, rr.r, rr.valid);
+        const RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
+        const Up u = load_up(dc, dop, ddep, rr.r, rr.valid);
         if (!rr.contiguous) {
-            bwd_two_sweep(sm, lane, rr.valid, false, rr.off, rr.end, 0, 0, u, ts, te, rgb, sig, g_rgb,
-                          g_sig);
+            bwd_two_sweep(sm, lane, rr.valid, false, rr.off, rr.end, 0u, 0u, u, ts, te, rgb, sig,
+                          g_rgb, g_sig);
             continue;
         }
         const unsigned vmask = __ballot_sync(0xffffffffu, rr.valid);  // valid lanes: a prefix
         int g0 = 0;
         while (g0 < 32 && ((vmask >> g0) & 1u)) {
-            const uint64_t base = __shfl_sync(0xffffffffu, rr.off, g0);
-            const bool fits = rr.valid && lane >= g0 && rr.end - base <= uint64_t(Tile<T>::CH);
+            const uint32_t base = __shfl_sync(0xffffffffu, rr.off, g0);
+            const bool fits = rr.valid && lane >= g0 && rr.end - base <= uint32_t(Tile<T>::CH);
             const unsigned fm = __ballot_sync(0xffffffffu, fits);  // monotone: ends ascend
             if (!((fm >> g0) & 1u)) {  // ray g0 alone exceeds a tile
-                const uint64_t e0 = __shfl_sync(0xffffffffu, rr.end, g0);
+                const uint32_t e0 = __shfl_sync(0xffffffffu, rr.end, g0);
                 bwd_two_sweep(sm, lane, lane == g0, true, rr.off, rr.end, base, e0, u, ts, te, rgb,
                               sig, g_rgb, g_sig);
                 ++g0;
                 continue;
             }
             const int g1 = 31 - __clz(fm);
-            const uint64_t n = __shfl_sync(0xffffffffu, rr.end, g1) - base;
+            const uint32_t n = __shfl_sync(0xffffffffu, rr.end, g1) - base;
             if (n) {
-                stage_in(sm, lane, base, n, ts, te, rgb, sig);
-                __syncwarp();
+                stage_in<T, false>(sm, lane, base, n, ts, te, rgb, sig);
                 if (lane >= g0 && lane <= g1) {
                     double t = 1.0;
-                    for (uint64_t s = rr.off; s < rr.end; ++s) {  // rendering.cpp:89-96
-                        uint64_t i = s - base;
+                    for (uint32_t i = rr.off - base; i < rr.end - base; ++i) {  // rendering.cpp:89-96
                         sm.tr[i] = t;
                         t *= 1.0 - sm.al[i];
                     }
                     double suffix = 0.0;
-                    for (uint64_t s = rr.end; s-- > rr.off;) {  // rendering.cpp:99-108
-                        uint64_t i = s - base;
-                        double delta = sm.te[i] - sm.ts[i];
-                        double mid = 0.5 * (sm.ts[i] + sm.te[i]);
-                        double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
-                                           double(sm.rgb[3 * i + 2]), mid);
-                        double wgt = sm.tr[i] * sm.al[i];
+                    for (uint32_t i = rr.end - base; i-- > rr.off - base;) {  // rendering.cpp:99-108
+                        const double delta = sm.te[i] - sm.ts[i];
+                        const double mid = 0.5 * (sm.ts[i] + sm.te[i]);
+                        const double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
+                                                 double(sm.rgb[3 * i + 2]), mid);
+                        const double wgt = sm.tr[i] * sm.al[i];
                         sm.rgb[3 * i] = T(u.dcx * wgt);
                         sm.rgb[3 * i + 1] = T(u.dcy * wgt);
                         sm.rgb[3 * i + 2] = T(u.dcz * wgt);
@@ -321,10 +323,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_backward(
                         suffix += wgt * v;
                     }
                 }
-                __syncwarp();
-                for (uint64_t i = lane; i < n; i += 32) g_sig[base + i] = sm.sig[i];
-                for (uint64_t i = lane; i < 3 * n; i += 32) g_rgb[3 * base + i] = sm.rgb[i];
-                __syncwarp();
+                write_out(sm, lane, base, n, g_rgb, g_sig);
             }
             g0 = g1 + 1;
         }
@@ -333,34 +332,33 @@ __global__ void __launch_bounds__(kWarps * 32) k_backward(
 
 // ------------------------------------------------------------------ transmittance
 template <typename T>
-__global__ void __launch_bounds__(kWarps * 32) k_transmittance(
+__global__ void __launch_bounds__(kWarps * 32, 4) k_transmittance(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays,
     const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ sig,
     T* __restrict__ out) {
-    __shared__ Smem<T> smem[kWarps];
+    __shared__ BwdSmem<T> smem[kWarps];
     const int lane = threadIdx.x & 31;
-    Smem<T>& sm = smem[threadIdx.x >> 5];
+    BwdSmem<T>& sm = smem[threadIdx.x >> 5];
     const uint64_t n_warps = (n_rays + 31) / 32;
     for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
          w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-        RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
+        const RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
         double t = 1.0;  // rendering.cpp:26-31: out = T; T *= exp(-sigma * delta)
         if (rr.contiguous) {
-            for (uint64_t cs = rr.s0; cs < rr.s1; cs += Tile<T>::CH) {
-                uint64_t n = min(uint64_t(Tile<T>::CH), rr.s1 - cs);
-                stage_in<T, true>(sm, lane, cs, n, ts, te, nullptr, sig);
-                __syncwarp();
-                for (uint64_t s = max(rr.off, cs); s < min(rr.end, cs + n); ++s) {
-                    uint64_t i = s - cs;
+            for (uint32_t cs = rr.s0; cs < rr.s1; cs += Tile<T>::CH) {
+                const uint32_t n = min(uint32_t(Tile<T>::CH), rr.s1 - cs);
+                stage_in<T, true>(sm, lane, cs, n, ts, te, static_cast<const T*>(nullptr), sig);
+                for (uint32_t s = max(rr.off, cs); s < min(rr.end, cs + n); ++s) {
+                    const uint32_t i = s - cs;
                     sm.tr[i] = t;
                     t *= sm.al[i];
                 }
                 __syncwarp();
-                for (uint64_t i = lane; i < n; i += 32) out[cs + i] = T(sm.tr[i]);
+                for (uint32_t i = lane; i < n; i += 32) out[cs + i] = T(sm.tr[i]);
                 __syncwarp();
             }
         } else {
-            for (uint64_t s = rr.off; s < rr.end; ++s) {
+            for (uint32_t s = rr.off; s < rr.end; ++s) {
                 out[s] = T(t);
                 t *= exp(-double(sig[s]) * (te[s] - ts[s]));
             }

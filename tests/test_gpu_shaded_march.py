@@ -1,0 +1,62 @@
+"""vmb_march_field_shaded == vmb_march_field followed by vmb_shade_field, bit for bit
+(same packed samples, same rgb/sigma), for f32/f64 attributes, the fused
+single-pass marcher, its overflow fixup and the two-pass (growth) path."""
+import numpy as np
+import pytest
+
+from paper_2210_04847_b200 import api, workload
+from paper_2210_04847_b200._lib import VMB_F32, VMB_F64, Contraction, Field, MarchConfig, Rays
+
+pytestmark = pytest.mark.gpu
+
+
+def _rays(dev, o, d, near, far, dtype):
+    do_, dd_ = dev.upload(o.astype(dtype)), dev.upload(d.astype(dtype))
+    return Rays(do_.ptr, dd_.ptr, VMB_F32 if dtype == np.float32 else VMB_F64, 0, len(o), near, far), (do_, dd_)
+
+
+def _both(dev, grid, rays, field, cfg, n, attr_dtype, time=0.0):
+    a = api.march_device(dev, grid, rays, field, cfg, api.DevicePacked.allocate(dev, n, 8 * n + 1024))
+    cap = a.capacity  # march_device grows the buffers to the exact need
+    rgb_a, sig_a = dev.empty(cap * 3, attr_dtype), dev.empty(cap, attr_dtype)
+    api.shade_device(dev, rays, field, a, rgb_a, sig_a, time)
+    b = api.DevicePacked.allocate(dev, n, cap)
+    rgb_b, sig_b = dev.empty(cap * 3, attr_dtype), dev.empty(cap, attr_dtype)
+    api.march_shaded_device(dev, grid, rays, field, cfg, b, rgb_b, sig_b, time)
+    ha, hb = a.to_host(), b.to_host()
+    for k in ("offsets", "counts", "t_starts", "t_ends", "ray_indices"):
+        assert np.array_equal(getattr(ha, k), getattr(hb, k)), k
+    s = a.n_samples
+    assert s > 0
+    assert np.array_equal(rgb_a.numpy(3 * s), rgb_b.numpy(3 * s))
+    assert np.array_equal(sig_a.numpy(s), sig_b.numpy(s))
+
+
+@pytest.mark.parametrize("ray_dtype,attr_dtype", [(np.float32, np.float32), (np.float64, np.float64),
+                                                  (np.float64, np.float32)])
+def test_shaded_march_bounded(ray_dtype, attr_dtype):
+    dev = api.Device(0)
+    field = Field.sphere(**workload.SPHERE)
+    g = api.OccupancyGrid(128, Contraction.aabb(), dev=dev)
+    for s in workload.grid_warmup_seeds(8, 5):
+        g.update_field(field, 0.95, s)
+    o, d = workload.orbit_rays(200, angle=0.4)
+    rays, keep = _rays(dev, o, d, 0.2, 1.0, ray_dtype)
+    _both(dev, g, rays, field, MarchConfig(5e-3, 1e-4, 1e-2), len(o), attr_dtype)
+    # tiny step + no early stop: many rays overflow the 24-sample buffer -> fixup path
+    _both(dev, g, rays, field, MarchConfig(1e-3, 0.0, 0.0), len(o), attr_dtype)
+
+
+def test_shaded_march_growth_and_checker():
+    dev = api.Device(0)
+    con = Contraction.sphere((0.5, 0.5, 0.5), 0.5)
+    field = Field.checker(0.2, 30.0, (0.9, 0.1, 0.2), (0.1, 0.8, 0.3))
+    g = api.OccupancyGrid(48, con, dev=dev)
+    for s in (1, 2):
+        g.update_field(field, 0.95, s)
+    rng = np.random.default_rng(3)
+    d = rng.normal(size=(500, 3))
+    d /= np.sqrt((d * d).sum(1))[:, None]
+    o = np.tile([[0.5, 0.5, 0.5]], (500, 1))
+    rays, keep = _rays(dev, o, d, 0.01, 20.0, np.float64)
+    _both(dev, g, rays, field, MarchConfig(0.01, 1e-3, 1e-2, 256, 1.02), 500, np.float64)
