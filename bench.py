@@ -52,8 +52,8 @@ def parse():
     ap.add_argument("--cpu-sample-rays", type=int, default=1 << 20)
     ap.add_argument("--ref-sample-rays", type=int, default=1 << 18)
     ap.add_argument("--phases", type=int, default=1, help="per-phase event timing pass")
-    ap.add_argument("--shade", default="fused", choices=["fused", "separate"],
-                    help="analytic-field shading fused into the march packing, or a separate kernel")
+    ap.add_argument("--fusion", default="forward", choices=["forward", "shade", "none"],
+                    help="forward: march+shade+render_forward fused; shade: march+shade fused; none: separate")
     return ap.parse_args()
 
 
@@ -299,17 +299,29 @@ def main():
     g_rgb, g_sig = dev.empty(cap * 3, np.float32), dev.empty(cap, np.float32)
     col, op, dep = dev.empty(N * 3, np.float32), dev.empty(N, np.float32), dev.empty(N, np.float32)
 
-    def march_and_shade():
-        if args.shade == "fused":  # analytic field shaded while the samples are packed
-            api.march_shaded_device(dev, grid, rays, field, cfg, packed, rgb, sig)
+    # The step, phase by phase (record(k) brackets the phases for the timing pass):
+    #   fusion=none    march | shade | render_forward | render_backward
+    #   fusion=shade   march+shade (vmb_march_field_shaded) | render_forward | render_backward
+    #   fusion=forward march+shade+render_forward (vmb_march_render_field) | render_backward
+    def step(record=None):
+        rec = record or (lambda k: None)
+        rec(2)
+        if args.fusion == "forward":
+            api.march_render_device(dev, grid, rays, field, cfg, packed, rgb, sig, col, op, dep)
+            rec(3), rec(4), rec(5)
         else:
-            api.march_device(dev, grid, rays, field, cfg, packed)
-            api.shade_device(dev, rays, field, packed, rgb, sig)
-
-    def step():
-        march_and_shade()
-        api.render_forward_device(dev, packed, rgb, sig, col, op, dep)
+            if args.fusion == "shade":
+                api.march_shaded_device(dev, grid, rays, field, cfg, packed, rgb, sig)
+                rec(3)
+            else:
+                api.march_device(dev, grid, rays, field, cfg, packed)
+                rec(3)
+                api.shade_device(dev, rays, field, packed, rgb, sig)
+            rec(4)
+            api.render_forward_device(dev, packed, rgb, sig, col, op, dep)
+            rec(5)
         api.render_backward_device(dev, packed, rgb, sig, up_c, up_o, up_d, g_rgb, g_sig)
+        rec(6)
 
     clocks = Clocks(dist.local)
     for _ in range(max(args.warmup, 3)):
@@ -341,19 +353,7 @@ def main():
     if args.phases:
         acc = np.zeros(4)
         for _ in range(args.steps):
-            dev.record(2)
-            if args.shade == "fused":
-                api.march_shaded_device(dev, grid, rays, field, cfg, packed, rgb, sig)
-                dev.record(3)
-            else:
-                api.march_device(dev, grid, rays, field, cfg, packed)
-                dev.record(3)
-                api.shade_device(dev, rays, field, packed, rgb, sig)
-            dev.record(4)
-            api.render_forward_device(dev, packed, rgb, sig, col, op, dep)
-            dev.record(5)
-            api.render_backward_device(dev, packed, rgb, sig, up_c, up_o, up_d, g_rgb, g_sig)
-            dev.record(6)
+            step(dev.record)
             acc += [dev.elapsed_ms(2 + i, 3 + i) for i in range(4)]
         acc /= args.steps
         phase = dict(zip(["march", "shade", "render_forward", "render_backward"], acc.tolist()))
@@ -363,7 +363,14 @@ def main():
     pk = peaks()
     peak = pk.get("hbm_gbs", 6650.0)
     peak_src = "measured" if "hbm_gbs" in pk else "fallback"
+    # The march phase's compulsory bytes grow with what is fused into it: shading
+    # writes rgb+sigma (16 B/sample); the fused forward writes color/opacity/depth
+    # (20 B/ray) and does not re-read the samples.
     bytes_march = 24 * N + 8 * N + 20 * S + R ** 3 / 8
+    if args.fusion in ("shade", "forward"):
+        bytes_march += 16 * S
+    if args.fusion == "forward":
+        bytes_march += 20 * N
     bytes_fwd = 8 * N + 32 * S + 20 * N
     bytes_bwd = 8 * N + 20 * N + 32 * S + 16 * S
     bytes_step = 88 * N + 100 * S + R ** 3 / 8
@@ -438,13 +445,13 @@ def main():
                                        f"{R}^3 grid (16 jittered warm-up updates), SolidSphere r=0.2 "
                                        f"sigma=200, step {args.step_size}, alpha 1e-2, eps 1e-4",
                            "rays_per_gpu": N, "samples_per_gpu": S, "resolution": R,
-                           "shading": args.shade + " (analytic SolidSphere rgb/sigma at sample midpoints)",
+                           "fusion": args.fusion + " (analytic SolidSphere rgb/sigma shaded at sample midpoints)",
                            "storage": "rays/rgb/sigma/outputs f32, t f64, compute f64",
                            "l2": "inputs larger than L2 (~1 GB working set per step)",
                            "parallelism": f"dp{dist.world} (rays sharded, grid replicated)"},
                 "phases_ms": phase, "grid_update_ms": grid_update_ms,
                 "roofline": roof, "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
-                "gpu_launches": (KERNELS_PER_STEP - (args.shade == "fused")) * args.steps}
+                "gpu_launches": (KERNELS_PER_STEP - {"none": 0, "shade": 1, "forward": 2}[args.fusion]) * args.steps}
         print(json.dumps(line), flush=True)
     if dist.world > 1:
         L.vmb_comm_destroy(dev.h)

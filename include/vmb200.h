@@ -192,6 +192,17 @@ int vmb_march_field_shaded(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays
                            const vmb_field* f, const vmb_march_config* cfg, vmb_samples* out,
                            void* d_rgbs, void* d_sigmas, int dtype, double time,
                            uint64_t* h_n_samples, vmb_march_stats* h_stats);
+/* march + shading + render_forward fused (the forward half of a training step, or
+ * inference rendering, with an analytic field): additionally writes the per-ray
+ * color [n_rays][3], opacity and depth of render_forward (rendering.cpp:35-65)
+ * over the kept samples with the shaded (dtype-rounded) attributes — bit-identical
+ * to vmb_march_field_shaded followed by vmb_render_forward, without re-reading the
+ * packed samples. */
+int vmb_march_render_field(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,
+                           const vmb_field* f, const vmb_march_config* cfg, vmb_samples* out,
+                           void* d_rgbs, void* d_sigmas, void* d_color, void* d_opacity,
+                           void* d_depth, int dtype, double time, uint64_t* h_n_samples,
+                           vmb_march_stats* h_stats);
 /* Asynchronous variant for training loops / CUDA graphs: no host round trip.
  * The sample total is written to d_n_samples (u64, device); samples beyond
  * out->capacity are dropped (check d_n_samples afterwards). Errors (negative or

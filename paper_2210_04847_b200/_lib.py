@@ -160,6 +160,8 @@ SIGNATURES = {
                               P(MarchStats)]),
     "vmb_march_field_shaded": (I32, [VP, VP, P(Rays), P(Field), P(MarchConfig), P(Samples), VP, VP,
                                      I32, D, P(U64), P(MarchStats)]),
+    "vmb_march_render_field": (I32, [VP, VP, P(Rays), P(Field), P(MarchConfig), P(Samples), VP, VP,
+                                     VP, VP, VP, I32, D, P(U64), P(MarchStats)]),
     "vmb_march_field_async": (I32, [VP, VP, P(Rays), P(Field), P(MarchConfig), P(Samples), VP]),
     "vmb_march_check": (I32, [VP]),
     "vmb_march_candidates": (I32, [VP, VP, P(Rays), P(MarchConfig), P(Samples), P(U64)]),

@@ -205,6 +205,21 @@ def march_shaded_device(dev: Device, grid: "OccupancyGrid", rays: Rays, field: F
     return out
 
 
+def march_render_device(dev: Device, grid: "OccupancyGrid", rays: Rays, field: Field,
+                        cfg: MarchConfig, out: DevicePacked, rgbs: DeviceArray, sigmas: DeviceArray,
+                        color: DeviceArray, opacity: DeviceArray, depth: DeviceArray,
+                        time: float = 0.0, stats: Optional[MarchStats] = None) -> DevicePacked:
+    """vmb_march_render_field: march + analytic shading + render_forward fused."""
+    n = C.c_uint64()
+    smp = out.samples_struct()
+    check(dev.lib.vmb_march_render_field(dev.h, grid.h, C.byref(rays), C.byref(field), C.byref(cfg),
+                                         C.byref(smp), rgbs.ptr, sigmas.ptr, color.ptr, opacity.ptr,
+                                         depth.ptr, _dt(rgbs.dtype), time, C.byref(n),
+                                         C.byref(stats) if stats is not None else None))
+    out.n_samples = int(n.value)
+    return out
+
+
 def shade_device(dev: Device, rays: Rays, field: Field, packed: DevicePacked, rgbs: DeviceArray,
                  sigmas: DeviceArray, time: float = 0.0):
     check(dev.lib.vmb_shade_field(dev.h, C.byref(rays), C.byref(field), time,

@@ -24,6 +24,7 @@
 // Packing is count -> CUB-free scan -> fill (the two passes re-walk the same
 // rays; both passes together read rays twice, write 8 B/ray + 20 B/sample).
 #include <string>
+#include <type_traits>
 
 #include "vm_internal.h"
 
@@ -480,11 +481,53 @@ constexpr int kWalkCap = 24;
 #ifndef VMB_WALK_MINB
 #define VMB_WALK_MINB 6
 #endif
-template <typename RT, bool FAST>
+// Fused render_forward (vmb_march_render_field): for an analytic field the
+// compositing of rendering.cpp:47-58 runs over exactly the kept samples, in order,
+// with alpha from the shaded sigma. FwdAcc repeats k_shade + k_forward's
+// expressions (attributes rounded to the attribute dtype first), so the outputs
+// are bit-identical to march -> shade -> render_forward.
+template <typename AT>
+struct FwdAcc {
+    double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0, op = 0.0, dep = 0.0;
+    template <typename RT>
+    __device__ __forceinline__ void kept(const MarchParams& P, const RT* orig, const RT* dirs,
+                                         uint64_t r, double t0, double t1, double time) {
+        const D3 x = load3(orig, r) + load3(dirs, r) * (0.5 * (t0 + t1));
+        D3 c;
+        const double sg = double(AT(field_rgb_sigma(P.f, time_shift(P.f, x, time), &c)));
+        const double alpha = 1.0 - exp(-sg * (t1 - t0));
+        const double w = T * alpha;
+        cr = cr + double(AT(c.x)) * w;
+        cg = cg + double(AT(c.y)) * w;
+        cb = cb + double(AT(c.z)) * w;
+        op += w;
+        dep += w * 0.5 * (t0 + t1);
+        T *= 1.0 - alpha;
+    }
+    __device__ __forceinline__ void store(uint64_t r, AT* color, AT* opacity, AT* depth) const {
+        color[3 * r] = AT(cr);
+        color[3 * r + 1] = AT(cg);
+        color[3 * r + 2] = AT(cb);
+        opacity[r] = AT(op);
+        depth[r] = AT(dep);
+    }
+};
+
+template <typename AT>
+struct FwdOut {
+    AT* color;
+    AT* opacity;
+    AT* depth;
+    double time;
+};
+
+// FAST instantiates only walk_fast (+ its exact fallback and the dense walk for
+// unsafe rays), so its register allocation is not the union of every walk.
+template <typename RT, bool FAST, typename AT, bool FWD>
 __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
     MarchParams P, const RT* __restrict__ orig, const RT* __restrict__ dirs, uint64_t n_rays,
     uint32_t* __restrict__ counts, uint32_t* __restrict__ kept_idx, unsigned int* chunk_counter,
-    uint64_t n_chunks, unsigned long long* emitted, DevError* err) {
+    uint64_t n_chunks, unsigned long long* emitted, DevError* err, FwdOut<AT> fo) {
     const int lane = threadIdx.x & 31;
     unsigned long long emit_local = 0;
     for (;;) {
@@ -510,6 +553,15 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
             }
             counts[r] = s.n_kept;
             emit_local += s.n_cand;
+            if (FWD && s.n_kept <= uint32_t(kWalkCap)) {  // longer rays: k_march_fixup
+                FwdAcc<AT> acc;
+                for (uint32_t k = 0; k < s.n_kept; ++k) {
+                    const uint64_t j = s.buf[k * 32];
+                    acc.kept(P, orig, dirs, r, P.near_ + double(j) * P.step,
+                             min_ref(P.near_ + double(j + 1) * P.step, P.far_), fo.time);
+                }
+                acc.store(r, fo.color, fo.opacity, fo.depth);
+            }
         }
         __syncwarp();
     }
@@ -594,12 +646,12 @@ __global__ void __launch_bounds__(256) k_march_expand(
 }
 
 // Re-walks the (rare) rays whose kept samples overflowed the shared buffer.
-template <typename RT, typename AT, bool SHADE>
+template <typename RT, typename AT, bool SHADE, bool FWD>
 __global__ void k_march_fixup(MarchParams P, const RT* __restrict__ orig, const RT* __restrict__ dirs,
                               const uint32_t* __restrict__ offsets, double* __restrict__ ts,
                               double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,
                               const uint32_t* __restrict__ overflow, const unsigned int* n_overflow,
-                              DevError* err, ShadeOut<RT, AT> sh) {
+                              DevError* err, ShadeOut<RT, AT> sh, FwdOut<AT> fo) {
     const unsigned int n = *n_overflow;
     for (unsigned int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         uint64_t r = overflow[k];
@@ -613,6 +665,12 @@ __global__ void k_march_fixup(MarchParams P, const RT* __restrict__ orig, const 
         walk<FILL>(P, s, orig, dirs, r, err);
         if (SHADE)
             for (uint64_t q = s.base; q < s.base + s.n_kept && q < cap; ++q) sh.shade(r, q, ts[q], te[q]);
+        if (FWD) {  // walk_fast's t0/t1 of this ray, recomputed by the FILL walk
+            FwdAcc<AT> acc;
+            for (uint64_t q = s.base; q < s.base + s.n_kept && q < cap; ++q)
+                acc.kept(P, orig, dirs, r, ts[q], te[q], fo.time);
+            acc.store(r, fo.color, fo.opacity, fo.depth);
+        }
     }
 }
 
@@ -843,9 +901,20 @@ struct ShadeReq {
     void* rgb = nullptr;
     void* sig = nullptr;
     int dtype = VMB_F32;
+    // fused render_forward (requires on): per-ray outputs in dtype
+    bool fwd = false;
+    void* color = nullptr;
+    void* opacity = nullptr;
+    void* depth = nullptr;
 };
 
-template <typename RT, typename AT, bool SHADE>
+template <typename AT>
+FwdOut<AT> fwd_out(const ShadeReq& sr) {
+    return FwdOut<AT>{static_cast<AT*>(sr.color), static_cast<AT*>(sr.opacity),
+                      static_cast<AT*>(sr.depth), sr.time};
+}
+
+template <typename RT, typename AT, bool SHADE, bool FWD>
 void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
                          const uint32_t* kept_idx, uint32_t* overflow, unsigned int* n_overflow,
                          uint64_t n_chunks, const ShadeReq& sr) {
@@ -854,21 +923,24 @@ void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* ray
     k_march_expand<RT, AT, SHADE><<<grid_blocks(ctx, n_chunks * 32, 256, 8), 256, 0, ctx->stream>>>(
         P.near_, P.far_, P.step, out->d_counts, out->d_offsets, kept_idx, rays->n_rays, out->d_t_starts,
         out->d_t_ends, out->d_ray_indices, out->capacity, overflow, n_overflow, sh);
-    k_march_fixup<RT, AT, SHADE><<<ctx->num_sms * 2, 128, 0, ctx->stream>>>(
+    k_march_fixup<RT, AT, SHADE, FWD><<<ctx->num_sms * 2, 128, 0, ctx->stream>>>(
         P, sh.orig, sh.dirs, out->d_offsets, out->d_t_starts, out->d_t_ends, out->d_ray_indices,
-        out->capacity, overflow, n_overflow, ctx->d_err, sh);
+        out->capacity, overflow, n_overflow, ctx->d_err, sh, fwd_out<AT>(sr));
 }
 
 template <typename RT>
 void dispatch_expand(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
                      const uint32_t* kept_idx, uint32_t* overflow, unsigned int* n_overflow,
                      uint64_t n_chunks, const ShadeReq& sr) {
+#define VMB_EXPAND(AT, SH, FW) \
+    launch_expand_fixup<RT, AT, SH, FW>(ctx, P, rays, out, kept_idx, overflow, n_overflow, n_chunks, sr)
     if (!sr.on)
-        launch_expand_fixup<RT, float, false>(ctx, P, rays, out, kept_idx, overflow, n_overflow, n_chunks, sr);
+        VMB_EXPAND(float, false, false);
     else if (sr.dtype == VMB_F32)
-        launch_expand_fixup<RT, float, true>(ctx, P, rays, out, kept_idx, overflow, n_overflow, n_chunks, sr);
+        sr.fwd ? VMB_EXPAND(float, true, true) : VMB_EXPAND(float, true, false);
     else
-        launch_expand_fixup<RT, double, true>(ctx, P, rays, out, kept_idx, overflow, n_overflow, n_chunks, sr);
+        sr.fwd ? VMB_EXPAND(double, true, true) : VMB_EXPAND(double, true, false);
+#undef VMB_EXPAND
 }
 
 // walk -> scan -> expand (+shade) -> fixup; the sample total lands in d_total.
@@ -890,28 +962,36 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
         return e == cudaSuccess ? VMB_OK : cuda_fail(e, "march");
     }
     // persistent grid: exactly the resident capacity of the device
-    auto launch_walk = [&](auto kernel, auto* o, auto* d) {
+    auto launch_walk = [&](auto kernel, auto* o, auto* d, auto fo) {
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, 0);
         if (per_sm < 1) per_sm = 4;
-        kernel<<<ctx->num_sms * per_sm, 128, 0, ctx->stream>>>(P, o, d, n, out->d_counts, kept_idx,
-                                                              counters, n_chunks, emitted, ctx->d_err);
+        kernel<<<ctx->num_sms * per_sm, 128, 0, ctx->stream>>>(
+            P, o, d, n, out->d_counts, kept_idx, counters, n_chunks, emitted, ctx->d_err, fo);
     };
-    if (rays->dtype == VMB_F32) {
-        auto* o = static_cast<const float*>(rays->d_origins);
-        auto* d = static_cast<const float*>(rays->d_directions);
-        if (P.fast)
-            launch_walk(k_march_walk<float, true>, o, d);
-        else
-            launch_walk(k_march_walk<float, false>, o, d);
-    } else {
-        auto* o = static_cast<const double*>(rays->d_origins);
-        auto* d = static_cast<const double*>(rays->d_directions);
-        if (P.fast)
-            launch_walk(k_march_walk<double, true>, o, d);
-        else
-            launch_walk(k_march_walk<double, false>, o, d);
-    }
+    auto walk_rt = [&](auto* o, auto* d) {
+        using RT = std::remove_const_t<std::remove_pointer_t<decltype(o)>>;
+        const bool f64 = sr.dtype == VMB_F64;
+        if (P.fast) {
+            if (!sr.fwd)
+                launch_walk(k_march_walk<RT, true, float, false>, o, d, FwdOut<float>{});
+            else if (f64)
+                launch_walk(k_march_walk<RT, true, double, true>, o, d, fwd_out<double>(sr));
+            else
+                launch_walk(k_march_walk<RT, true, float, true>, o, d, fwd_out<float>(sr));
+        } else {
+            if (!sr.fwd)
+                launch_walk(k_march_walk<RT, false, float, false>, o, d, FwdOut<float>{});
+            else if (f64)
+                launch_walk(k_march_walk<RT, false, double, true>, o, d, fwd_out<double>(sr));
+            else
+                launch_walk(k_march_walk<RT, false, float, true>, o, d, fwd_out<float>(sr));
+        }
+    };
+    if (rays->dtype == VMB_F32)
+        walk_rt(static_cast<const float*>(rays->d_origins), static_cast<const float*>(rays->d_directions));
+    else
+        walk_rt(static_cast<const double*>(rays->d_origins), static_cast<const double*>(rays->d_directions));
     int rc = scan_counts(ctx, out->d_counts, n, out->d_offsets, d_total);
     if (rc) return rc;
     if (rays->dtype == VMB_F32)
@@ -965,9 +1045,16 @@ int march_packed(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
     if (total) launch_march<FILL>(ctx, P, rays, out->d_counts, out->d_offsets, out, nullptr);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "march fill");
-    if (sr.on && total)
-        return vmb_shade_field(ctx, rays, &sr.f, sr.time, out->d_ray_indices, out->d_t_starts,
-                               out->d_t_ends, total, sr.rgb, sr.sig, sr.dtype);
+    if (sr.on && total) {
+        rc = vmb_shade_field(ctx, rays, &sr.f, sr.time, out->d_ray_indices, out->d_t_starts,
+                             out->d_t_ends, total, sr.rgb, sr.sig, sr.dtype);
+        if (rc) return rc;
+    }
+    if (sr.fwd) {  // growth walks are sequential per ray: composite with the render kernel
+        vmb_packed_view v{out->d_offsets, out->d_counts, rays->n_rays, out->d_t_starts,
+                          out->d_t_ends, total};
+        return vmb_render_forward(ctx, &v, sr.rgb, sr.sig, sr.color, sr.opacity, sr.depth, sr.dtype);
+    }
     return VMB_OK;
 }
 
@@ -998,6 +1085,34 @@ int vmb_march_field_shaded(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays
     sr.rgb = d_rgbs;
     sr.sig = d_sigmas;
     sr.dtype = dtype;
+    return march_packed(ctx, P, rays, out, h_n, stats, sr);
+}
+
+int vmb_march_render_field(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays, const vmb_field* f,
+                           const vmb_march_config* cfg, vmb_samples* out, void* d_rgbs, void* d_sigmas,
+                           void* d_color, void* d_opacity, void* d_depth, int dtype, double time,
+                           uint64_t* h_n, vmb_march_stats* stats) {
+    MarchParams P;
+    int rc = march_params(g, rays, cfg, &P);
+    if (rc) return rc;
+    if (f->kind == VMB_FIELD_UNIFORM_BOX &&
+        !(f->box_max[0] > f->box_min[0] && f->box_max[1] > f->box_min[1] && f->box_max[2] > f->box_min[2]))
+        return fail(VMB_INVALID_ARGUMENT, "aabb max must be strictly greater than min");
+    P.f = *f;
+    P.filter = true;
+    P.full = stats != nullptr;
+    set_sphere_fast(&P);
+    ShadeReq sr;
+    sr.on = true;
+    sr.f = *f;
+    sr.time = time;
+    sr.rgb = d_rgbs;
+    sr.sig = d_sigmas;
+    sr.dtype = dtype;
+    sr.fwd = true;
+    sr.color = d_color;
+    sr.opacity = d_opacity;
+    sr.depth = d_depth;
     return march_packed(ctx, P, rays, out, h_n, stats, sr);
 }
 

@@ -60,3 +60,43 @@ def test_shaded_march_growth_and_checker():
     o = np.tile([[0.5, 0.5, 0.5]], (500, 1))
     rays, keep = _rays(dev, o, d, 0.01, 20.0, np.float64)
     _both(dev, g, rays, field, MarchConfig(0.01, 1e-3, 1e-2, 256, 1.02), 500, np.float64)
+    _render_both(dev, g, rays, field, MarchConfig(0.01, 1e-3, 1e-2, 256, 1.02), 500, np.float64)
+
+
+def _render_both(dev, grid, rays, field, cfg, n, attr_dtype, time=0.0):
+    """vmb_march_render_field == march_shaded -> render_forward, bit for bit."""
+    a = api.march_device(dev, grid, rays, field, cfg, api.DevicePacked.allocate(dev, n, 8 * n + 1024))
+    cap = a.capacity
+    rgb_a, sig_a = dev.empty(cap * 3, attr_dtype), dev.empty(cap, attr_dtype)
+    api.march_shaded_device(dev, grid, rays, field, cfg, a, rgb_a, sig_a, time)
+    outs_a = [dev.empty(n * 3, attr_dtype), dev.empty(n, attr_dtype), dev.empty(n, attr_dtype)]
+    api.render_forward_device(dev, a, rgb_a, sig_a, *outs_a)
+    b = api.DevicePacked.allocate(dev, n, cap)
+    rgb_b, sig_b = dev.empty(cap * 3, attr_dtype), dev.empty(cap, attr_dtype)
+    outs_b = [dev.empty(n * 3, attr_dtype), dev.empty(n, attr_dtype), dev.empty(n, attr_dtype)]
+    api.march_render_device(dev, grid, rays, field, cfg, b, rgb_b, sig_b, *outs_b, time=time)
+    ha, hb = a.to_host(), b.to_host()
+    for k in ("offsets", "counts", "t_starts", "t_ends", "ray_indices"):
+        assert np.array_equal(getattr(ha, k), getattr(hb, k)), k
+    s = a.n_samples
+    assert np.array_equal(rgb_a.numpy(3 * s), rgb_b.numpy(3 * s))
+    assert np.array_equal(sig_a.numpy(s), sig_b.numpy(s))
+    for x, y in zip(outs_a, outs_b):
+        assert np.array_equal(x.numpy(), y.numpy())
+
+
+@pytest.mark.parametrize("ray_dtype,attr_dtype", [(np.float32, np.float32), (np.float64, np.float64)])
+def test_fused_forward_render(ray_dtype, attr_dtype):
+    dev = api.Device(0)
+    field = Field.sphere(center=(0.5, 0.5, 0.5), radius=0.2, sigma=200.0, rgb=(0.8, 0.25, 0.1))
+    g = api.OccupancyGrid(128, Contraction.aabb(), dev=dev)
+    for s in workload.grid_warmup_seeds(8, 5):
+        g.update_field(field, 0.95, s)
+    o, d = workload.orbit_rays(160, angle=2.0)
+    rays, keep = _rays(dev, o, d, 0.2, 1.0, ray_dtype)
+    _render_both(dev, g, rays, field, MarchConfig(5e-3, 1e-4, 1e-2), len(o), attr_dtype)
+    # non-f32-representable sigma, long rays (overflow -> fixup composites), a box field
+    box = Field.box((0.3, 0.2, 0.25), (0.7, 0.8, 0.75), 0.37, (0.3, 0.6, 0.9))
+    gb = api.OccupancyGrid(64, Contraction.aabb(), 1e-3, dev=dev)
+    gb.update_field(box, 0.95, 3)
+    _render_both(dev, gb, rays, box, MarchConfig(2e-3, 0.0, 1e-4), len(o), attr_dtype)
