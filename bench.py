@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--phases", type=int, default=1, help="per-phase event timing pass")
     ap.add_argument("--fusion", default="forward", choices=["forward", "shade", "none"],
                     help="forward: march+shade+render_forward fused; shade: march+shade fused; none: separate")
+    ap.add_argument("--e2e-streams", type=int, default=2)
+    ap.add_argument("--e2e-chunks", type=int, default=4)  # 2x4 measured best on B200 (r1)
     return ap.parse_args()
 
 
@@ -251,6 +253,109 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------- e2e
+def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev_out, total_rays):
+    """The same step through the C ABI from HOST memory: every step copies its rays and
+    upstream gradients host->device and reads the rendered color/opacity/depth back.
+
+    The batch is cut into `--e2e-chunks` ray chunks served round-robin by
+    `--e2e-streams` contexts (one CUDA stream each, one host thread each; the ctypes
+    calls release the GIL), so one chunk's PCIe copies overlap another chunk's
+    kernels. Timed with CUDA events on context 0, which waits for every other
+    context at the end (vmb_ctx_wait); the others wait for its start event."""
+    import ctypes as C
+    from paper_2210_04847_b200._lib import VMB_F32, Rays, check
+    L = dev.lib
+    N = len(o32)
+    n_ctx, n_chunk = max(1, args.e2e_streams), max(1, args.e2e_chunks)
+    bounds = [(N * i // n_chunk, N * (i + 1) // n_chunk) for i in range(n_chunk)]
+    cmax = max(e - b for b, e in bounds)
+    host_in = [o32, d32] + list(ups)            # per-ray: 12, 12, 12, 4, 4 bytes
+    widths = [3, 3, 3, 1, 1]
+    pinned = []
+    for arr in host_in:
+        p = C.c_void_p()
+        check(L.vmb_host_alloc(arr.nbytes, C.byref(p)))
+        C.memmove(p.value, arr.ctypes.data, arr.nbytes)
+        pinned.append(p)
+    out_w = [3, 1, 1]
+    p_out = []
+    for w in out_w:
+        p = C.c_void_p()
+        check(L.vmb_host_alloc(N * w * 4, C.byref(p)))
+        p_out.append(p)
+    ctxs = [dev] + [api.Device(dist.local) for _ in range(n_ctx - 1)]
+    ccap = cap  # the full batch's capacity bounds any chunk's sample count
+    bufs = []
+    for cx in ctxs:
+        ins = [cx.empty(cmax * w, np.float32) for w in widths]
+        outs = [cx.empty(cmax * w, np.float32) for w in out_w]
+        bufs.append(dict(ins=ins, outs=outs, packed=api.DevicePacked.allocate(cx, cmax, ccap),
+                         rgb=cx.empty(ccap * 3, np.float32), sig=cx.empty(ccap, np.float32),
+                         grgb=cx.empty(ccap * 3, np.float32), gsig=cx.empty(ccap, np.float32)))
+
+    def run_chunk(ci, b, e):
+        cx, bf = ctxs[ci], bufs[ci]
+        n = e - b
+        for arr, p, w in zip(bf["ins"], pinned, widths):
+            check(L.vmb_memcpy_h2d(cx.h, arr.ptr, p.value + b * w * 4, n * w * 4))
+        rays = Rays(bf["ins"][0].ptr, bf["ins"][1].ptr, VMB_F32, 0, n, 0.2, 1.0)
+        pk = bf["packed"]
+        api.march_render_device(cx, grid, rays, field, cfg, pk, bf["rgb"], bf["sig"], *bf["outs"])
+        api.render_backward_device(cx, pk, bf["rgb"], bf["sig"], *bf["ins"][2:], bf["grgb"], bf["gsig"])
+        for arr, p, w in zip(bf["outs"], p_out, out_w):
+            check(L.vmb_memcpy_d2h(cx.h, p.value + b * w * 4, arr.ptr, n * w * 4))
+
+    def worker(ci, steps, err):
+        try:
+            for _ in range(steps):
+                for k in range(ci, n_chunk, n_ctx):
+                    run_chunk(ci, *bounds[k])
+        except Exception as ex:  # pragma: no cover
+            err.append(ex)
+
+    def run(steps):
+        err = []
+        ts = [threading.Thread(target=worker, args=(i, steps, err)) for i in range(n_ctx)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        if err:
+            raise err[0]
+
+    run(2)  # warm-up (also grows each context's packed buffers to the chunk's need)
+    for cx in ctxs:
+        cx.sync()
+    dist.barrier()
+    dev.record(7)
+    for cx in ctxs[1:]:
+        check(L.vmb_ctx_wait(cx.h, dev.h, 9))
+    run(args.steps)
+    for i, cx in enumerate(ctxs[1:]):
+        check(L.vmb_ctx_wait(dev.h, cx.h, 9 + (i % 8)))
+    dev.record(8)
+    for cx in ctxs:
+        cx.sync()
+    e2e_ms = dist.max(dev.elapsed_ms(7, 8) / args.steps)
+    # the pipelined result must equal the resident single-stream step's
+    same = True
+    for p, w, darr in zip(p_out, out_w, dev_out):
+        h = np.empty(N * w, np.float32)
+        C.memmove(h.ctypes.data, p.value, h.nbytes)
+        same &= bool(np.array_equal(h, darr.numpy(N * w)))
+    for p in pinned + p_out:
+        L.vmb_host_free(p)
+    for cx in ctxs[1:]:
+        cx.sync()
+    return {"value": total_rays / (e2e_ms * 1e-3), "unit": "rays/s", "ms_per_step": e2e_ms,
+            "h2d_bytes_per_step": int(sum(a.nbytes for a in host_in)), "d2h_bytes_per_step": N * 20,
+            "streams": n_ctx, "chunks": n_chunk, "matches_resident_outputs": same,
+            "path": "C ABI (vmb_memcpy_h2d, vmb_march_render_field, vmb_render_backward, vmb_memcpy_d2h): "
+                    "pinned host rays + upstream grads in, color/opacity/depth out, "
+                    f"{n_chunk} chunks pipelined over {n_ctx} streams"}
+
+
 # ---------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -386,47 +491,11 @@ def main():
                      "frac": bytes_step / (ms_step * 1e-3) / 1e9 / peak}}
 
     # e2e: host buffers in, result out, through the C ABI (pinned host staging)
-    e2e = None
     try:
-        hb = {}
-        for name, arr in (("o", o32), ("d", d32), ("dc", dc.astype(np.float32)),
-                          ("do", do.astype(np.float32)), ("dd", dd.astype(np.float32))):
-            p = C.c_void_p()
-            check(L.vmb_host_alloc(arr.nbytes, C.byref(p)))
-            C.memmove(p.value, arr.ctypes.data, arr.nbytes)
-            hb[name] = (p, arr.nbytes)
-        out_bytes = N * 4 * 5
-        p_out = C.c_void_p()
-        check(L.vmb_host_alloc(out_bytes, C.byref(p_out)))
-        dst = [(do_, "o"), (dd_, "d"), (up_c, "dc"), (up_o, "do"), (up_d, "dd")]
-
-        def e2e_step():
-            for darr, k in dst:
-                check(L.vmb_memcpy_h2d(dev.h, darr.ptr, hb[k][0], hb[k][1]))
-            step()
-            check(L.vmb_memcpy_d2h(dev.h, p_out, col.ptr, N * 12))
-            check(L.vmb_memcpy_d2h(dev.h, p_out.value + N * 12, op.ptr, N * 4))
-            check(L.vmb_memcpy_d2h(dev.h, p_out.value + N * 16, dep.ptr, N * 4))
-
-        for _ in range(2):
-            e2e_step()
-        dist.barrier()
-        t0 = time.perf_counter()
-        dev.record(7)
-        for _ in range(args.steps):
-            e2e_step()
-        dev.record(8)
-        dev.sync()
-        e2e_ms = dist.max(dev.elapsed_ms(7, 8) / args.steps)
-        h2d = sum(v[1] for v in hb.values())
-        e2e = {"value": total_rays / (e2e_ms * 1e-3), "unit": "rays/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": out_bytes,
-               "path": "C ABI vmb_* with pinned host rays+upstream grads in, color/opacity/depth out"}
-        for v in hb.values():
-            L.vmb_host_free(v[0])
-        L.vmb_host_free(p_out)
+        e2e = e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32,
+                           [x.astype(np.float32) for x in (dc, do, dd)], cap, (col, op, dep), total_rays)
     except Exception as ex:  # pragma: no cover
-        e2e = {"error": str(ex)}
+        e2e = {"error": repr(ex)}
 
     cpu = None
     if dist.rank == 0 and dist.world == 1 and args.cpu_baseline:

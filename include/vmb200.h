@@ -88,6 +88,10 @@ int vmb_memset(vmb_ctx* ctx, void* d_dst, int value, uint64_t bytes);
 /* CUDA events on the context stream (slot 0..31) for device-side timing. */
 int vmb_event_record(vmb_ctx* ctx, int slot);
 int vmb_event_elapsed_ms(vmb_ctx* ctx, int slot_begin, int slot_end, float* h_ms);
+/* Make waiter's stream wait for the work queued so far on `on`'s stream (records
+ * on's event `slot`). Lets several contexts on one device pipeline host<->device
+ * copies against compute, each context being one CUDA stream. */
+int vmb_ctx_wait(vmb_ctx* waiter, vmb_ctx* on, int slot);
 /* Host-only helper (no device work): the contiguous shard of n units owned by
  * rank — the static split of parallel_for (parallel.hpp:28-35). */
 int vmb_shard_range(uint64_t n, int nranks, int rank, uint64_t* h_begin, uint64_t* h_end);

@@ -132,6 +132,7 @@ SIGNATURES = {
     "vmb_memcpy_d2d": (I32, [VP, VP, VP, U64]),
     "vmb_memset": (I32, [VP, VP, I32, U64]),
     "vmb_event_record": (I32, [VP, I32]),
+    "vmb_ctx_wait": (I32, [VP, VP, I32]),
     "vmb_event_elapsed_ms": (I32, [VP, I32, I32, P(C.c_float)]),
     "vmb_shard_range": (I32, [U64, I32, I32, P(U64), P(U64)]),
     "vmb_rays_validate": (I32, [VP, P(Rays)]),

@@ -307,6 +307,15 @@ int vmb_event_record(vmb_ctx* ctx, int slot) {
     return VMB_OK;
 }
 
+int vmb_ctx_wait(vmb_ctx* waiter, vmb_ctx* on, int slot) {
+    if (!waiter || !on) return fail(VMB_INVALID_ARGUMENT, "null context");
+    if (slot < 0 || slot >= 32) return fail(VMB_INVALID_ARGUMENT, "event slot out of range");
+    if (waiter == on || waiter->stream == on->stream) return VMB_OK;
+    VMB_CUDA_TRY(cudaEventRecord(on->events[slot], on->stream), "cudaEventRecord");
+    VMB_CUDA_TRY(cudaStreamWaitEvent(waiter->stream, on->events[slot], 0), "cudaStreamWaitEvent");
+    return VMB_OK;
+}
+
 int vmb_event_elapsed_ms(vmb_ctx* ctx, int a, int b, float* ms) {
     if (a < 0 || a >= 32 || b < 0 || b >= 32) return fail(VMB_INVALID_ARGUMENT, "event slot out of range");
     VMB_CUDA_TRY(cudaEventSynchronize(ctx->events[b]), "cudaEventSynchronize");
