@@ -34,7 +34,9 @@ int check_contraction(const vmb_contraction* c);
 
 namespace {
 
-enum Mode { COUNT = 0, FILL = 1, BUFFER = 2 };
+// BUFFER_FWD = BUFFER + the render_forward compositing of each kept sample, done
+// in filter_sample as the sample is kept (vmb_march_render_field).
+enum Mode { COUNT = 0, FILL = 1, BUFFER = 2, BUFFER_FWD = 3 };
 
 struct MarchParams {
     Contract k;
@@ -89,11 +91,37 @@ struct Sink {
     uint32_t* buf = nullptr;
     uint32_t buf_stride = 0;
     uint32_t buf_cap = 0;
+    // BUFFER_FWD: rendering.cpp:47-58 accumulators (Tf follows the attribute-dtype
+    // sigma, T the march's fp64 sigma; they differ only if sigma is not exact in it)
+    bool at32 = false;
+    double Tf = 1.0, cr = 0.0, cg = 0.0, cb = 0.0, op = 0.0, dep = 0.0;
+
+    // One kept sample, with exactly k_shade + k_forward's expressions (FwdAcc):
+    // sigma/rgb are rounded to the attribute dtype; alpha is reused when the
+    // rounding is exact (same expression, same operands).
+    __device__ __forceinline__ void composite(double sigma, D3 c, double t0, double t1, double alpha) {
+        const double sg = at32 ? double(float(sigma)) : sigma;
+        const double a = sg == sigma ? alpha : 1.0 - exp(-sg * (t1 - t0));
+        const double w = Tf * a;
+        if (at32) {
+            cr = cr + double(float(c.x)) * w;
+            cg = cg + double(float(c.y)) * w;
+            cb = cb + double(float(c.z)) * w;
+        } else {
+            cr = cr + c.x * w;
+            cg = cg + c.y * w;
+            cb = cb + c.z * w;
+        }
+        op += w;
+        dep += w * 0.5 * (t0 + t1);
+        Tf *= 1.0 - a;
+    }
 };
 
 template <int MODE>
 __device__ __forceinline__ bool filter_sample(const MarchParams& P, Sink& s, uint64_t i, uint32_t ci,
-                                              double t0, double t1, double sigma, DevError* err);
+                                              double t0, double t1, double sigma, DevError* err,
+                                              D3 rgb = D3{0.0, 0.0, 0.0});
 
 // Handles one grid-passing candidate. Mirrors ray_marching.cpp:78,111-137.
 template <int MODE>
@@ -110,11 +138,16 @@ __device__ __forceinline__ bool on_candidate(const MarchParams& P, Sink& s, uint
                 s.idx[o] = uint32_t(s.ray);
             }
         }
-        if (MODE == BUFFER && s.n_kept < s.buf_cap) s.buf[s.n_kept * s.buf_stride] = uint32_t(i);
+        if (MODE >= BUFFER && s.n_kept < s.buf_cap) s.buf[s.n_kept * s.buf_stride] = uint32_t(i);
         s.n_kept++;
         return true;
     }
     if (!s.filtering) return true;  // after the cut only the emitted count matters
+    if (MODE == BUFFER_FWD) {  // field_rgb_sigma's sigma == field_density's for finite p
+        D3 c;
+        const double sg = field_rgb_sigma(P.f, p, &c);
+        return filter_sample<MODE>(P, s, i, ci, t0, t1, sg, err, c);
+    }
     return filter_sample<MODE>(P, s, i, ci, t0, t1, field_density(P.f, p), err);
 }
 
@@ -122,7 +155,8 @@ __device__ __forceinline__ bool on_candidate(const MarchParams& P, Sink& s, uint
 // density sigma (ray_marching.cpp:122-137).
 template <int MODE>
 __device__ __forceinline__ bool filter_sample(const MarchParams& P, Sink& s, uint64_t i, uint32_t ci,
-                                              double t0, double t1, double sigma, DevError* err) {
+                                              double t0, double t1, double sigma, DevError* err,
+                                              D3 rgb) {
     if (!isfinite(sigma) || sigma < 0.0) {
         int kind = !isfinite(sigma) ? ERR_NONFINITE_SIGMA : ERR_NEGATIVE_SIGMA;
         atomicMin(&err->key, march_err_key(s.ray, ci, kind));
@@ -140,7 +174,8 @@ __device__ __forceinline__ bool filter_sample(const MarchParams& P, Sink& s, uin
             s.idx[o] = uint32_t(s.ray);
         }
     }
-    if (MODE == BUFFER && s.n_kept < s.buf_cap) s.buf[s.n_kept * s.buf_stride] = uint32_t(i);
+    if (MODE >= BUFFER && s.n_kept < s.buf_cap) s.buf[s.n_kept * s.buf_stride] = uint32_t(i);
+    if (MODE == BUFFER_FWD) s.composite(sigma, rgb, t0, t1, alpha);
     s.n_kept++;
     s.T *= 1.0 - alpha;
     if (s.T < P.eps) {
@@ -417,8 +452,10 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
             if (d2 > P.sph_r2 + sph_err || d2 < P.sph_r2 - sph_err) {
                 if (s.n_cand >= P.max_cand) return;  // candidate cap
                 uint32_t ci = s.n_cand++;
-                double sigma = d2 < P.sph_r2 ? P.f.sigma : 0.0;
-                if (!filter_sample<MODE>(P, s, uint64_t(j), ci, t0, t1, sigma, err)) return;
+                const bool in = d2 < P.sph_r2;
+                double sigma = in ? P.f.sigma : 0.0;
+                D3 rgb = in ? d3(P.f.rgb[0], P.f.rgb[1], P.f.rgb[2]) : d3(0.0, 0.0, 0.0);
+                if (!filter_sample<MODE>(P, s, uint64_t(j), ci, t0, t1, sigma, err, rgb)) return;
                 ++j;
                 continue;
             }
@@ -483,9 +520,11 @@ constexpr int kWalkCap = 24;
 #endif
 // Fused render_forward (vmb_march_render_field): for an analytic field the
 // compositing of rendering.cpp:47-58 runs over exactly the kept samples, in order,
-// with alpha from the shaded sigma. FwdAcc repeats k_shade + k_forward's
+// with alpha from the shaded sigma. FwdAcc (k_march_fixup) and Sink::composite
+// (k_march_walk, inline as samples are kept) repeat k_shade + k_forward's
 // expressions (attributes rounded to the attribute dtype first), so the outputs
-// are bit-identical to march -> shade -> render_forward.
+// are bit-identical to march -> shade -> render_forward. Inline compositing needs
+// the shading position to be the march position (time_shift == identity).
 template <typename AT>
 struct FwdAcc {
     double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0, op = 0.0, dep = 0.0;
@@ -542,25 +581,25 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
             s.buf = kept_idx + uint64_t(chunk) * (kWalkCap * 32) + lane;
             s.buf_stride = 32;
             s.buf_cap = kWalkCap;
+            s.at32 = sizeof(AT) == 4;
+            constexpr int M = FWD ? BUFFER_FWD : BUFFER;
             if (FAST) {
                 const D3 o = load3(orig, r), d = load3(dirs, r);
                 if (ray_safe(P, o, d))
-                    walk_fast<BUFFER>(P, s, orig, dirs, r, err);
+                    walk_fast<M>(P, s, orig, dirs, r, err);
                 else
-                    walk_dense<BUFFER>(P, s, o, d, err);
+                    walk_dense<M>(P, s, o, d, err);
             } else {
-                walk<BUFFER>(P, s, orig, dirs, r, err);
+                walk<M>(P, s, orig, dirs, r, err);
             }
             counts[r] = s.n_kept;
             emit_local += s.n_cand;
-            if (FWD && s.n_kept <= uint32_t(kWalkCap)) {  // longer rays: k_march_fixup
-                FwdAcc<AT> acc;
-                for (uint32_t k = 0; k < s.n_kept; ++k) {
-                    const uint64_t j = s.buf[k * 32];
-                    acc.kept(P, orig, dirs, r, P.near_ + double(j) * P.step,
-                             min_ref(P.near_ + double(j + 1) * P.step, P.far_), fo.time);
-                }
-                acc.store(r, fo.color, fo.opacity, fo.depth);
+            if (FWD) {  // every kept sample was composited (rays over kWalkCap too)
+                fo.color[3 * r] = AT(s.cr);
+                fo.color[3 * r + 1] = AT(s.cg);
+                fo.color[3 * r + 2] = AT(s.cb);
+                fo.opacity[r] = AT(s.op);
+                fo.depth[r] = AT(s.dep);
             }
         }
         __syncwarp();
@@ -1109,6 +1148,17 @@ int vmb_march_render_field(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays
     sr.rgb = d_rgbs;
     sr.sig = d_sigmas;
     sr.dtype = dtype;
+    // Inline compositing shades at the march position: p - velocity * time must be
+    // p itself (up to the sign of zero, which no field distinguishes).
+    bool ident = std::isfinite(time) && (time == 0.0 || (f->velocity[0] == 0.0 &&
+                                                          f->velocity[1] == 0.0 && f->velocity[2] == 0.0));
+    for (int a = 0; a < 3; ++a) ident = ident && std::isfinite(f->velocity[a]);
+    if (!ident) {  // shaded march, then the render kernel
+        rc = march_packed(ctx, P, rays, out, h_n, stats, sr);
+        if (rc) return rc;
+        vmb_packed_view v{out->d_offsets, out->d_counts, rays->n_rays, out->d_t_starts, out->d_t_ends, *h_n};
+        return vmb_render_forward(ctx, &v, d_rgbs, d_sigmas, d_color, d_opacity, d_depth, dtype);
+    }
     sr.fwd = true;
     sr.color = d_color;
     sr.opacity = d_opacity;
