@@ -625,6 +625,9 @@ struct ShadeOut {
     __device__ __forceinline__ void shade(uint64_t r, uint64_t p, double t0, double t1) const {
         D3 o = d3(double(orig[3 * r]), double(orig[3 * r + 1]), double(orig[3 * r + 2]));
         D3 d = d3(double(dirs[3 * r]), double(dirs[3 * r + 1]), double(dirs[3 * r + 2]));
+        shade_ray(o, d, p, t0, t1);
+    }
+    __device__ __forceinline__ void shade_ray(D3 o, D3 d, uint64_t p, double t0, double t1) const {
         D3 x = o + d * (0.5 * (t0 + t1));
         D3 c;
         double sigma = field_rgb_sigma(f, time_shift(f, x, time), &c);
@@ -635,27 +638,59 @@ struct ShadeOut {
     }
 };
 
+// Per warp and chunk: the chunk's counts/offsets are prefetched one chunk ahead,
+// its used kept-index rows (128 B each) are staged in shared memory with coalesced
+// loads, and each lane holds its own ray, handed to the sample's lane by shuffles
+// — so the per-sample work touches only registers/smem plus the coalesced writes.
+constexpr int kExpandWarps = 8;
+
 template <typename RT, typename AT, bool SHADE>
-__global__ void __launch_bounds__(256) k_march_expand(
+__global__ void __launch_bounds__(32 * kExpandWarps) k_march_expand(
     double near_, double far_, double step, const uint32_t* __restrict__ counts,
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ kept_idx, uint64_t n_rays,
     double* __restrict__ ts, double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,
     uint32_t* __restrict__ overflow, unsigned int* n_overflow, ShadeOut<RT, AT> sh) {
+    __shared__ uint32_t s_idx[kExpandWarps][kWalkCap * 32];
     const int lane = threadIdx.x & 31;
+    uint32_t* sk = s_idx[threadIdx.x >> 5];
     const uint64_t n_chunks = (n_rays + 31) / 32;
-    for (uint64_t chunk = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; chunk < n_chunks;
-         chunk += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+    const uint64_t wstride = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    uint64_t chunk = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    uint32_t cnt_n = 0u, off_n = 0xffffffffu;
+    if (chunk < n_chunks && chunk * 32 + lane < n_rays) {
+        cnt_n = counts[chunk * 32 + lane];
+        off_n = offsets[chunk * 32 + lane];
+    }
+    for (; chunk < n_chunks; chunk += wstride) {
         const uint64_t r = chunk * 32 + lane;
         const bool valid = r < n_rays;
-        const uint32_t cnt = valid ? counts[r] : 0u;
-        const uint32_t off = valid ? offsets[r] : 0xffffffffu;
+        const uint32_t cnt = cnt_n, off = off_n;
+        {  // prefetch the next chunk's counts/offsets
+            const uint64_t rn = (chunk + wstride) * 32 + lane;
+            cnt_n = 0u;
+            off_n = 0xffffffffu;
+            if (chunk + wstride < n_chunks && rn < n_rays) {
+                cnt_n = counts[rn];
+                off_n = offsets[rn];
+            }
+        }
         if (cnt > uint32_t(kWalkCap)) overflow[atomicAdd(n_overflow, 1u)] = uint32_t(r);
         const unsigned vmask = __ballot_sync(0xffffffffu, valid);
         const int last = 31 - __clz(vmask);
         const uint64_t base = __shfl_sync(0xffffffffu, off, 0);
         const uint64_t end = uint64_t(__shfl_sync(0xffffffffu, off, last)) +
                              __shfl_sync(0xffffffffu, cnt, last);
+        if (base >= end) continue;
+        const uint32_t rows = min(__reduce_max_sync(0xffffffffu, cnt), uint32_t(kWalkCap));
         const uint32_t* kbuf = kept_idx + chunk * (kWalkCap * 32);
+        double ox = 0.0, oy = 0.0, oz = 0.0, dx = 0.0, dy = 0.0, dz = 0.0;
+        if (SHADE && valid) {
+            ox = double(sh.orig[3 * r]), oy = double(sh.orig[3 * r + 1]), oz = double(sh.orig[3 * r + 2]);
+            dx = double(sh.dirs[3 * r]), dy = double(sh.dirs[3 * r + 1]), dz = double(sh.dirs[3 * r + 2]);
+        }
+#pragma unroll 4
+        for (uint32_t k = 0; k < rows; ++k) sk[k * 32 + lane] = __ldcs(kbuf + k * 32 + lane);
+        __syncwarp();
         for (uint64_t p0 = base; p0 < end; p0 += 32) {
             const uint64_t p = p0 + lane;
             // owner = largest lane L with off_L <= p (zero-count lanes share the
@@ -668,19 +703,27 @@ __global__ void __launch_bounds__(256) k_march_expand(
                 if (c < 32 && uint64_t(v) <= p) L = c;
             }
             const uint32_t loff = __shfl_sync(0xffffffffu, off, L);
+            D3 o, d;
+            if (SHADE) {
+                o = d3(__shfl_sync(0xffffffffu, ox, L), __shfl_sync(0xffffffffu, oy, L),
+                       __shfl_sync(0xffffffffu, oz, L));
+                d = d3(__shfl_sync(0xffffffffu, dx, L), __shfl_sync(0xffffffffu, dy, L),
+                       __shfl_sync(0xffffffffu, dz, L));
+            }
             if (p < end && p < cap) {
                 const uint64_t k = p - loff;
                 if (k < uint64_t(kWalkCap)) {
-                    const uint64_t i = kbuf[k * 32 + L];
+                    const uint64_t i = sk[k * 32 + L];
                     const double t0 = near_ + double(i) * step;
                     const double t1 = min_ref(near_ + double(i + 1) * step, far_);
                     ts[p] = t0;
                     te[p] = t1;
                     idx[p] = uint32_t(chunk * 32 + L);
-                    if (SHADE) sh.shade(chunk * 32 + L, p, t0, t1);
+                    if (SHADE) sh.shade_ray(o, d, p, t0, t1);
                 }
             }
         }
+        __syncwarp();
     }
 }
 
@@ -959,7 +1002,13 @@ void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* ray
                          uint64_t n_chunks, const ShadeReq& sr) {
     ShadeOut<RT, AT> sh{static_cast<const RT*>(rays->d_origins), static_cast<const RT*>(rays->d_directions),
                         sr.f, sr.time, static_cast<AT*>(sr.rgb), static_cast<AT*>(sr.sig)};
-    k_march_expand<RT, AT, SHADE><<<grid_blocks(ctx, n_chunks * 32, 256, 8), 256, 0, ctx->stream>>>(
+    static int per_sm = [] {  // persistent: exactly the resident blocks
+        int n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_march_expand<RT, AT, SHADE>, 32 * kExpandWarps, 0);
+        return n < 1 ? 4 : n;
+    }();
+    k_march_expand<RT, AT, SHADE><<<grid_blocks(ctx, n_chunks * 32, 32 * kExpandWarps, per_sm),
+                                    32 * kExpandWarps, 0, ctx->stream>>>(
         P.near_, P.far_, P.step, out->d_counts, out->d_offsets, kept_idx, rays->n_rays, out->d_t_starts,
         out->d_t_ends, out->d_ray_indices, out->capacity, overflow, n_overflow, sh);
     k_march_fixup<RT, AT, SHADE, FWD><<<ctx->num_sms * 2, 128, 0, ctx->stream>>>(
