@@ -478,7 +478,12 @@ def main():
         bytes_march += 20 * N
     bytes_fwd = 8 * N + 32 * S + 20 * N
     bytes_bwd = 8 * N + 20 * N + 32 * S + 16 * S
-    bytes_step = 88 * N + 100 * S + R ** 3 / 8
+    # step bytes: each API call reads its inputs and writes its outputs
+    # once, 88 N + 100 S + R^3/8 for march | forward | backward (shading excluded).
+    # With the forward fused into the march, the forward's re-read (8 N + 32 S) is
+    # gone, while the fused call must write rgb/sigma (16 S) for the backward, so it
+    # is credited only its compulsory traffic: 80 N + 84 S + R^3/8.
+    bytes_step = (80 * N + 84 * S if args.fusion == "forward" else 88 * N + 100 * S) + R ** 3 / 8
     dom = max(phase, key=phase.get) if phase else "march"
     dom_bytes = {"march": bytes_march, "shade": 20 * S + 24 * S + 16 * S,
                  "render_forward": bytes_fwd, "render_backward": bytes_bwd}[dom]

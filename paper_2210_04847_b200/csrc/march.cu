@@ -516,7 +516,7 @@ constexpr int kWalkCap = 24;
 // FAST instantiates only walk_fast (+ its exact fallback and the dense walk for
 // unsafe rays), so its register allocation is not the union of every walk.
 #ifndef VMB_WALK_MINB
-#define VMB_WALK_MINB 6
+#define VMB_WALK_MINB 8
 #endif
 // Fused render_forward (vmb_march_render_field): for an analytic field the
 // compositing of rendering.cpp:47-58 runs over exactly the kept samples, in order,
@@ -638,11 +638,20 @@ struct ShadeOut {
     }
 };
 
-// Per warp and chunk: the chunk's counts/offsets are prefetched one chunk ahead,
-// its used kept-index rows (128 B each) are staged in shared memory with coalesced
-// loads, and each lane holds its own ray, handed to the sample's lane by shuffles
-// — so the per-sample work touches only registers/smem plus the coalesced writes.
+// Per warp, software-pipelined over its chunks: while chunk c is expanded, the
+// used kept-index rows of chunk c+1 (rows x 128 B, contiguous) are already in
+// flight into the other shared-memory buffer (cp.async, 16 B per lane), its rays
+// are in registers, and the counts/offsets of chunk c+2 are being loaded. Each
+// lane holds its own ray; a sample's ray is handed to its lane by shuffles. The
+// per-sample work touches registers/smem only, plus the coalesced output writes.
 constexpr int kExpandWarps = 8;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 template <typename RT, typename AT, bool SHADE>
 __global__ void __launch_bounds__(32 * kExpandWarps) k_march_expand(
@@ -650,47 +659,71 @@ __global__ void __launch_bounds__(32 * kExpandWarps) k_march_expand(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ kept_idx, uint64_t n_rays,
     double* __restrict__ ts, double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,
     uint32_t* __restrict__ overflow, unsigned int* n_overflow, ShadeOut<RT, AT> sh) {
-    __shared__ uint32_t s_idx[kExpandWarps][kWalkCap * 32];
+    __shared__ __align__(16) uint32_t s_idx[kExpandWarps][2][kWalkCap * 32];
     const int lane = threadIdx.x & 31;
-    uint32_t* sk = s_idx[threadIdx.x >> 5];
+    const int wib = threadIdx.x >> 5;
     const uint64_t n_chunks = (n_rays + 31) / 32;
     const uint64_t wstride = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-    uint64_t chunk = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    uint32_t cnt_n = 0u, off_n = 0xffffffffu;
-    if (chunk < n_chunks && chunk * 32 + lane < n_rays) {
-        cnt_n = counts[chunk * 32 + lane];
-        off_n = offsets[chunk * 32 + lane];
-    }
-    for (; chunk < n_chunks; chunk += wstride) {
+    const uint64_t c0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+
+    // chunk-local state: count/offset of this lane's ray, its ray (RT), and the
+    // number of staged rows
+    struct Stage {
+        uint32_t cnt = 0u, off = 0xffffffffu;
+        RT o[3] = {}, d[3] = {};
+    };
+    auto load_meta = [&](uint64_t c, Stage& st) {
+        const uint64_t r = c * 32 + lane;
+        st.cnt = 0u;
+        st.off = 0xffffffffu;
+        if (c < n_chunks && r < n_rays) {
+            st.cnt = counts[r];
+            st.off = offsets[r];
+        }
+    };
+    auto load_rays = [&](uint64_t c, Stage& st) {
+        const uint64_t r = c * 32 + lane;
+        if (SHADE && c < n_chunks && r < n_rays) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) st.o[a] = sh.orig[3 * r + a], st.d[a] = sh.dirs[3 * r + a];
+        }
+    };
+    auto stage_rows = [&](uint64_t c, const Stage& st, int buf) {
+        if (c < n_chunks) {
+            const uint32_t rows = min(__reduce_max_sync(0xffffffffu, st.cnt), uint32_t(kWalkCap));
+            const uint32_t* src = kept_idx + c * (kWalkCap * 32);
+            uint32_t* dst = s_idx[wib][buf];
+            for (uint32_t q = lane; q < rows * 8; q += 32) cp_async16(dst + 4 * q, src + 4 * q);
+        }
+        cp_async_commit();
+    };
+
+    Stage cur, nxt, nn;
+    load_meta(c0, cur);
+    load_rays(c0, cur);
+    stage_rows(c0, cur, 0);
+    load_meta(c0 + wstride, nxt);
+    int buf = 0;
+    for (uint64_t chunk = c0; chunk < n_chunks; chunk += wstride, buf ^= 1) {
+        // pipeline: rows + rays of the next chunk, counts of the one after
+        stage_rows(chunk + wstride, nxt, buf ^ 1);
+        load_rays(chunk + wstride, nxt);
+        load_meta(chunk + 2 * wstride, nn);
+
         const uint64_t r = chunk * 32 + lane;
         const bool valid = r < n_rays;
-        const uint32_t cnt = cnt_n, off = off_n;
-        {  // prefetch the next chunk's counts/offsets
-            const uint64_t rn = (chunk + wstride) * 32 + lane;
-            cnt_n = 0u;
-            off_n = 0xffffffffu;
-            if (chunk + wstride < n_chunks && rn < n_rays) {
-                cnt_n = counts[rn];
-                off_n = offsets[rn];
-            }
-        }
+        const uint32_t cnt = cur.cnt, off = cur.off;
         if (cnt > uint32_t(kWalkCap)) overflow[atomicAdd(n_overflow, 1u)] = uint32_t(r);
         const unsigned vmask = __ballot_sync(0xffffffffu, valid);
         const int last = 31 - __clz(vmask);
         const uint64_t base = __shfl_sync(0xffffffffu, off, 0);
         const uint64_t end = uint64_t(__shfl_sync(0xffffffffu, off, last)) +
                              __shfl_sync(0xffffffffu, cnt, last);
-        if (base >= end) continue;
-        const uint32_t rows = min(__reduce_max_sync(0xffffffffu, cnt), uint32_t(kWalkCap));
-        const uint32_t* kbuf = kept_idx + chunk * (kWalkCap * 32);
-        double ox = 0.0, oy = 0.0, oz = 0.0, dx = 0.0, dy = 0.0, dz = 0.0;
-        if (SHADE && valid) {
-            ox = double(sh.orig[3 * r]), oy = double(sh.orig[3 * r + 1]), oz = double(sh.orig[3 * r + 2]);
-            dx = double(sh.dirs[3 * r]), dy = double(sh.dirs[3 * r + 1]), dz = double(sh.dirs[3 * r + 2]);
-        }
-#pragma unroll 4
-        for (uint32_t k = 0; k < rows; ++k) sk[k * 32 + lane] = __ldcs(kbuf + k * 32 + lane);
+        const double ox = double(cur.o[0]), oy = double(cur.o[1]), oz = double(cur.o[2]);
+        const double dx = double(cur.d[0]), dy = double(cur.d[1]), dz = double(cur.d[2]);
+        cp_async_wait1();  // this chunk's rows have landed
         __syncwarp();
+        const uint32_t* sk = s_idx[wib][buf];
         for (uint64_t p0 = base; p0 < end; p0 += 32) {
             const uint64_t p = p0 + lane;
             // owner = largest lane L with off_L <= p (zero-count lanes share the
@@ -723,8 +756,11 @@ __global__ void __launch_bounds__(32 * kExpandWarps) k_march_expand(
                 }
             }
         }
-        __syncwarp();
+        __syncwarp();  // buffer `buf` is refilled two chunks from now
+        cur = nxt;
+        nxt = nn;
     }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 // Re-walks the (rare) rays whose kept samples overflowed the shared buffer.
