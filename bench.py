@@ -488,7 +488,12 @@ def main():
     dom_bytes = {"march": bytes_march, "shade": 20 * S + 24 * S + 16 * S,
                  "render_forward": bytes_fwd, "render_backward": bytes_bwd}[dom]
     achieved = dom_bytes / (phase.get(dom, ms_step) * 1e-3) / 1e9
-    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+    api = {"march": {"forward": "vmb_march_render_field", "shade": "vmb_march_field_shaded",
+                     "none": "vmb_march_field"}[args.fusion],
+           "shade": "vmb_shade_field", "render_forward": "vmb_render_forward",
+           "render_backward": "vmb_render_backward"}[dom]
+    roof = {"bound": "hbm", "kernel": f"{dom} ({api}: {' + '.join(PHASE_KERNELS[dom])})",
+            "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic_of(dom), "peak_source": peak_src,
             "algorithmic_bytes": dom_bytes,
             "step": {"algorithmic_bytes": bytes_step,
