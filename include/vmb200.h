@@ -100,6 +100,40 @@ int vmb_shard_range(uint64_t n, int nranks, int rank, uint64_t* h_begin, uint64_
 /* RayBatch::create validation (core_types.cpp:9-28): finite rays, |d|-1 <= 1e-6,
  * far > near >= 0. Synchronizes; the first offending ray is reported. */
 int vmb_rays_validate(vmb_ctx* ctx, const vmb_rays* rays);
+/* ------------------------------------------------------------------ cameras
+ * validate_camera (scene_camera.cpp:10-23), look_at (:25-44): host-only, exact
+ * fp64 as the reference. generate_rays (:46-63): one ray per pixel centre,
+ * row-major, unit directions, written on the device into caller buffers of
+ * width*height*3 elements (dtype VMB_F32/VMB_F64; directions are computed in
+ * fp64 and rounded once). Fills *out_rays (near/far as given) when non-null;
+ * the batch satisfies RayBatch::create's checks by construction. */
+int vmb_camera_validate(const vmb_camera* camera);
+int vmb_camera_look_at(const double eye[3], const double target[3], const double up[3], double focal,
+                       int32_t width, int32_t height, vmb_camera* out);
+int vmb_generate_rays(vmb_ctx* ctx, const vmb_camera* camera, double near_plane, double far_plane,
+                      int dtype, void* d_origins, void* d_directions, vmb_rays* out_rays);
+
+/* ------------------------------------------------------------------ fields
+ * query_density / query_rgb_sigma for any field kind (fields.cpp:75-93 and the
+ * TrilinearVoxelField versions :142-168), at p - velocity*time: d_points [n][3]
+ * f64 -> d_sigmas [n] (+ d_rgbs [n][3] when non-null), f64. Non-finite positions
+ * fail with "field: non-finite position at index i" (first i).
+ * TrilinearVoxelField::backward (fields.cpp:170-211): accumulates the parameter
+ * gradient of the query chain into d_accum_density [R^3] / d_accum_color
+ * [R^3][3] (f64, device); gradients d_rgb_grads [n][3] / d_sigma_grads [n] in
+ * dtype. The _samples form takes the positions as packed-sample midpoints
+ * o + d*(0.5*(t0+t1)) of `rays` (voxmarch.cpp:243-244). mode: VMB_GRAD_*. */
+int vmb_field_query(vmb_ctx* ctx, const vmb_field* field, const double* d_points, uint64_t n, double time,
+                    double* d_sigmas, double* d_rgbs);
+int vmb_voxel_field_backward(vmb_ctx* ctx, const vmb_field* field, const double* d_points, uint64_t n,
+                             const void* d_rgb_grads, const void* d_sigma_grads, int dtype,
+                             double* d_accum_density, double* d_accum_color, int mode);
+int vmb_voxel_field_backward_samples(vmb_ctx* ctx, const vmb_field* field, const vmb_rays* rays,
+                                     const uint32_t* d_ray_indices, const double* d_t_starts,
+                                     const double* d_t_ends, uint64_t n_samples, double time,
+                                     const void* d_rgb_grads, const void* d_sigma_grads, int dtype,
+                                     double* d_accum_density, double* d_accum_color, int mode);
+
 /* uniform_step_count (ray_marching.cpp:51-55). Host-only. */
 uint64_t vmb_uniform_step_count(double near_plane, double far_plane, double step_size);
 /* pack (core_types.cpp:30-48): exclusive scan of counts + ray index expansion.

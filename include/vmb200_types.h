@@ -47,8 +47,14 @@ typedef struct vmb_contraction {
     double radius;
 } vmb_contraction;
 
-/* Analytic density/appearance fields (fields.hpp:17-37, fields.cpp:39-73). */
-enum { VMB_FIELD_UNIFORM_BOX = 0, VMB_FIELD_SOLID_SPHERE = 1, VMB_FIELD_CHECKER = 2 };
+/* Density/appearance fields: the analytic fields (fields.hpp:17-37,
+ * fields.cpp:39-73) and the stored TrilinearVoxelField (fields.hpp:55-111,
+ * fields.cpp:95-168) — raw density [R^3] and raw rgb [R^3][3] per lattice vertex,
+ * x-fastest, fp64, trilinear + softplus/sigmoid, zero outside box_min..box_max.
+ * The voxel pointers are device pointers for vmb_* calls (host pointers for
+ * the CPU oracle). */
+enum { VMB_FIELD_UNIFORM_BOX = 0, VMB_FIELD_SOLID_SPHERE = 1, VMB_FIELD_CHECKER = 2,
+       VMB_FIELD_VOXEL = 3 };
 
 typedef struct vmb_field {
     int32_t kind;
@@ -62,6 +68,10 @@ typedef struct vmb_field {
     double rgb_b[3];   /* Checker rgb_b */
     double period;     /* Checker period */
     double velocity[3];/* TimeConditionedField velocity (fields.cpp:264-271); zero = static */
+    const double* vox_density; /* TrilinearVoxelField::raw_density_ [R^3] */
+    const double* vox_color;   /* TrilinearVoxelField::raw_color_ [R^3][3] */
+    uint32_t vox_resolution;   /* vertices per axis (>= 2); box_min/box_max = its box */
+    uint32_t pad2_;
 } vmb_field;
 
 typedef struct vmb_march_config {
@@ -82,6 +92,22 @@ typedef struct vmb_march_stats {
  * marching and compositing always compute in fp64 (SURVEY §0.3 precision
  * hazard); this only selects the element type of the arrays in HBM. */
 enum { VMB_F32 = 0, VMB_F64 = 1 };
+
+/* TrilinearVoxelField::backward modes (fields.cpp:170-211). DETERMINISTIC folds
+ * each vertex's contributions in sample order exactly like the reference (bitwise
+ * equal); ATOMIC uses fp64 atomics (last-bit differences, faster). */
+enum { VMB_GRAD_DETERMINISTIC = 0, VMB_GRAD_ATOMIC = 1 };
+
+/* PinholeCamera (scene_camera.hpp:12-19): OpenGL convention (looks down -z, +y
+ * up, square pixels); rotation is the row-major world-from-camera Mat3
+ * (math.hpp:63-76, m[3*row+col]); position is the eye. */
+typedef struct vmb_camera {
+    double rotation[9];
+    double position[3];
+    double focal;  /* pixels */
+    int32_t width;
+    int32_t height;
+} vmb_camera;
 
 #ifdef __cplusplus
 }

@@ -57,7 +57,9 @@ class Field(C.Structure):
     _fields_ = [("kind", C.c_int32), ("pad_", C.c_int32), ("box_min", C.c_double * 3),
                 ("box_max", C.c_double * 3), ("center", C.c_double * 3), ("radius", C.c_double),
                 ("sigma", C.c_double), ("rgb", C.c_double * 3), ("rgb_b", C.c_double * 3),
-                ("period", C.c_double), ("velocity", C.c_double * 3)]
+                ("period", C.c_double), ("velocity", C.c_double * 3),
+                ("vox_density", C.c_void_p), ("vox_color", C.c_void_p), ("vox_resolution", C.c_uint32),
+                ("pad2_", C.c_uint32)]
 
     @staticmethod
     def sphere(center=(0.5, 0.5, 0.5), radius=0.2, sigma=200.0, rgb=(0.8, 0.25, 0.25),
@@ -92,6 +94,21 @@ class Field(C.Structure):
         f.rgb_b[:] = list(rgb_b)
         return f
 
+    @staticmethod
+    def voxel(resolution, box_min, box_max, density, color, velocity=(0.0, 0.0, 0.0)):
+        """TrilinearVoxelField over host arrays (kept alive on the Field object)."""
+        f = Field()
+        f.kind = 3
+        f.box_min[:] = list(box_min)
+        f.box_max[:] = list(box_max)
+        f.vox_resolution = int(resolution)
+        f._dens = np.ascontiguousarray(density, dtype=np.float64).ravel()
+        f._col = np.ascontiguousarray(color, dtype=np.float64).ravel()
+        f.vox_density = f._dens.ctypes.data
+        f.vox_color = f._col.ctypes.data
+        f.velocity[:] = list(velocity)
+        return f
+
 
 class MarchConfig(C.Structure):
     """vmb_march_config <- voxmarch::MarchingConfig (ray_marching.hpp:11-17 defaults)."""
@@ -103,6 +120,12 @@ class MarchConfig(C.Structure):
                  max_samples_per_ray=2048, unbounded_step_growth=1.0):
         super().__init__(step_size, early_stop_eps, alpha_thre, max_samples_per_ray, 0,
                          unbounded_step_growth)
+
+
+class Camera(C.Structure):
+    """vmb_camera <- voxmarch::PinholeCamera (scene_camera.hpp:12-19)."""
+    _fields_ = [("rotation", C.c_double * 9), ("position", C.c_double * 3), ("focal", C.c_double),
+                ("width", C.c_int32), ("height", C.c_int32)]
 
 
 class _Packed(C.Structure):
@@ -180,7 +203,8 @@ class Oracle:
                      "grid_update_field", "grid_update_callback", "grid_seed_mask", "grid_get",
                      "grid_info", "grid_query", "grid_save", "grid_load", "pack", "validate",
                      "contract", "invert_grid_point", "shade", "transmittance", "render_forward",
-                     "render_backward", "render_attribute", "train_step"):
+                     "render_backward", "render_attribute", "train_step", "camera_look_at",
+                     "generate_rays", "field_query", "voxel_field_backward"):
             self._f(name).restype = C.c_int
 
     # ------------------------------------------------------------ helpers
@@ -306,6 +330,44 @@ class Oracle:
                                      _p(_f64(packed.t_ends), C.c_double), C.c_uint64(s),
                                      C.byref(field), _p(rgbs, C.c_double), _p(sig, C.c_double)))
         return rgbs, sig
+
+    # ------------------------------------------------------------ cameras
+    def look_at(self, eye, target, up, focal, width, height) -> Camera:
+        cam = Camera()
+        self._check(self._f("camera_look_at")(_p(_f64(eye), C.c_double), _p(_f64(target), C.c_double),
+                                              _p(_f64(up), C.c_double), C.c_double(focal),
+                                              C.c_int32(width), C.c_int32(height), C.byref(cam)))
+        return cam
+
+    def generate_rays(self, cam: Camera, near_, far_):
+        n = max(cam.width, 0) * max(cam.height, 0)
+        o, d = np.zeros((n, 3)), np.zeros((n, 3))
+        self._check(self._f("generate_rays")(C.byref(cam), C.c_double(near_), C.c_double(far_),
+                                             _p(o, C.c_double), _p(d, C.c_double)))
+        return o, d
+
+    # ------------------------------------------------------------ fields
+    def field_query(self, field, points, time=0.0, rgb=True):
+        p = _f64(points, (-1, 3))
+        n = len(p)
+        sig = np.zeros(n)
+        col = np.zeros((n, 3)) if rgb else None
+        self._check(self._f("field_query")(C.byref(field), _p(p, C.c_double), C.c_uint64(n), C.c_double(time),
+                                           _p(sig, C.c_double), _p(col, C.c_double)))
+        return (sig, col) if rgb else sig
+
+    def voxel_field_backward(self, field, points, d_rgbs, d_sigmas, accum_density=None, accum_color=None):
+        """TrilinearVoxelField::backward; returns the accumulated (d_density, d_color)."""
+        p = _f64(points, (-1, 3))
+        n = len(p)
+        nv = int(field.vox_resolution) ** 3
+        acc_d = np.zeros(nv) if accum_density is None else _f64(accum_density).copy()
+        acc_c = np.zeros(3 * nv) if accum_color is None else _f64(accum_color).copy().ravel()
+        self._check(self._f("voxel_field_backward")(C.byref(field), _p(p, C.c_double), C.c_uint64(n),
+                                                    _p(_f64(d_rgbs, (-1, 3)), C.c_double),
+                                                    _p(_f64(d_sigmas), C.c_double), _p(acc_d, C.c_double),
+                                                    _p(acc_c, C.c_double)))
+        return acc_d, acc_c
 
     # ------------------------------------------------------------ rendering
     def _pk(self, packed):

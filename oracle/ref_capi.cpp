@@ -7,7 +7,10 @@
 // reference's value types, calls the reference function named in its comment,
 // and converts the result back. Exceptions become VMB_* codes with the exact
 // what() text available from vmr_last_error().
+#include <algorithm>
 #include <chrono>
+#include <memory>
+#include <optional>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -60,12 +63,39 @@ Contraction to_contraction(const vmb_contraction* c) {
     return Contraction::sphere(v3(c->center), c->radius);
 }
 
-AnalyticField to_field(const vmb_field* f) {
+AnalyticField to_analytic(const vmb_field* f) {
     if (f->kind == VMB_FIELD_UNIFORM_BOX)
         return UniformBox{Aabb(v3(f->box_min), v3(f->box_max)), f->sigma, v3(f->rgb)};
     if (f->kind == VMB_FIELD_SOLID_SPHERE)
         return SolidSphere{v3(f->center), f->radius, f->sigma, v3(f->rgb)};
     return Checker{f->period, f->sigma, v3(f->rgb), v3(f->rgb_b)};
+}
+
+// An analytic field or a TrilinearVoxelField (fields.hpp:55-111) built from the
+// descriptor's host arrays; both evaluated by the reference's own code.
+struct RefField {
+    std::optional<AnalyticField> analytic;
+    std::shared_ptr<TrilinearVoxelField> voxel;
+    double density(const Vec3& p) const { return voxel ? voxel->density_at(p) : density_at(*analytic, p); }
+    std::pair<Vec3, double> rgb_sigma(const Vec3& p, const Vec3& dir) const {
+        return voxel ? voxel->rgb_sigma_at(p, dir) : rgb_sigma_at(*analytic, p, dir);
+    }
+};
+
+std::shared_ptr<TrilinearVoxelField> to_voxel(const vmb_field* f) {
+    auto v = std::make_shared<TrilinearVoxelField>(f->vox_resolution, Aabb(v3(f->box_min), v3(f->box_max)));
+    v->raw_density().assign(f->vox_density, f->vox_density + v->n_vertices());
+    v->raw_color().assign(f->vox_color, f->vox_color + 3 * v->n_vertices());
+    return v;
+}
+
+RefField to_field(const vmb_field* f) {
+    RefField r;
+    if (f->kind == VMB_FIELD_VOXEL)
+        r.voxel = to_voxel(f);
+    else
+        r.analytic = to_analytic(f);
+    return r;
 }
 
 MarchingConfig to_config(const vmb_march_config* c) {
@@ -114,14 +144,14 @@ vmo_packed* to_result(const PackedSamples& p, const MarchStats& stats) {
 }
 
 // sigma_fn_for (tools/voxmarch.cpp:221-232): density of the field at each midpoint.
-SigmaFn field_sigma(const RayBatch& rays, const AnalyticField& field) {
+SigmaFn field_sigma(const RayBatch& rays, const RefField& field) {
     return [&rays, field](std::span<const double> ts, std::span<const double> te,
                           std::span<const uint32_t> idx) {
         std::vector<double> out(ts.size());
         for (size_t s = 0; s < ts.size(); ++s) {
             uint32_t r = idx[s];
             Vec3 p = rays.origins[r] + rays.directions[r] * (0.5 * (ts[s] + te[s]));
-            out[s] = density_at(field, p);
+            out[s] = field.density(p);
         }
         return out;
     };
@@ -227,13 +257,15 @@ void vmr_grid_destroy(vmo_grid* g) { delete g; }
 int vmr_grid_update_field(vmo_grid* g, const vmb_field* f, const double* ts, uint64_t n_ts,
                           double decay, int has_seed, uint64_t seed) {
     return guarded([&] {
-        TimeConditionedField tf{to_field(f), v3(f->velocity)};
+        RefField field = to_field(f);
+        const Vec3 velocity = v3(f->velocity);
         std::optional<uint64_t> s;
         if (has_seed) s = seed;
         g->grid.update_over_time(
             [&](std::span<const Vec3> pts, double t) {
                 std::vector<double> out(pts.size());
-                for (size_t i = 0; i < pts.size(); ++i) out[i] = tf.density_at(pts[i], t);
+                // TimeConditionedField::density_at (fields.cpp:264-266)
+                for (size_t i = 0; i < pts.size(); ++i) out[i] = field.density(pts[i] - velocity * t);
                 return out;
             },
             std::span<const double>(ts, n_ts), decay, s);
@@ -312,7 +344,7 @@ int vmr_march_field(const double* o, const double* d, uint64_t n, double near_, 
                     int n_threads, vmo_packed** out) {
     return guarded([&] {
         RayBatch rays = RayBatch::create(vecs(o, n), vecs(d, n), near_, far_);
-        AnalyticField field = to_field(f);
+        RefField field = to_field(f);
         MarchStats stats;
         PackedSamples p =
             march(rays, g->grid, field_sigma(rays, field), to_config(cfg), n_threads, &stats);
@@ -354,11 +386,11 @@ int vmr_shade(const double* o, const double* d, const uint32_t* idx, const doubl
               const double* te, uint64_t n_samples, const vmb_field* f, double* rgbs,
               double* sigmas) {
     return guarded([&] {
-        AnalyticField field = to_field(f);
+        RefField field = to_field(f);
         for (uint64_t s = 0; s < n_samples; ++s) {
             uint32_t r = idx[s];
             Vec3 p = v3(o + 3 * size_t(r)) + v3(d + 3 * size_t(r)) * (0.5 * (ts[s] + te[s]));
-            auto [rgb, sigma] = rgb_sigma_at(field, p, v3(d + 3 * size_t(r)));
+            auto [rgb, sigma] = field.rgb_sigma(p, v3(d + 3 * size_t(r)));
             rgbs[3 * s] = rgb.x;
             rgbs[3 * s + 1] = rgb.y;
             rgbs[3 * s + 2] = rgb.z;
@@ -447,7 +479,7 @@ int vmr_train_step(const double* o, const double* d, uint64_t n, double near_, d
             return std::chrono::duration<double, std::milli>(b - a).count();
         };
         RayBatch rays = RayBatch::create(vecs(o, n), vecs(d, n), near_, far_);
-        AnalyticField field = to_field(f);
+        RefField field = to_field(f);
         auto t0 = clock::now();
         PackedSamples p = march(rays, g->grid, field_sigma(rays, field), to_config(cfg), n_threads);
         auto t1 = clock::now();
@@ -459,7 +491,7 @@ int vmr_train_step(const double* o, const double* d, uint64_t n, double near_, d
                 uint32_t r = p.ray_indices[s];
                 Vec3 x = rays.origins[r] +
                          rays.directions[r] * (0.5 * (p.t_starts[s] + p.t_ends[s]));
-                auto [rgb, sigma] = rgb_sigma_at(field, x, rays.directions[r]);
+                auto [rgb, sigma] = field.rgb_sigma(x, rays.directions[r]);
                 a.rgbs[s] = rgb;
                 a.sigmas[s] = sigma;
             }
@@ -510,6 +542,99 @@ int vmr_orbit_rays(const double* box_min, const double* box_max, double angle, d
                 dirs[3 * i + k] = rays.directions[i][k];
             }
         }
+    });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+static PinholeCamera to_cam(const vmb_camera* c) {
+    PinholeCamera cam;
+    for (int i = 0; i < 9; ++i) cam.rotation.m[i] = c->rotation[i];
+    cam.position = v3(c->position);
+    cam.focal = c->focal;
+    cam.width = c->width;
+    cam.height = c->height;
+    return cam;
+}
+
+// look_at / generate_rays (scene_camera.cpp:25-63) of the reference, as is.
+int vmr_camera_look_at(const double* eye, const double* target, const double* up, double focal,
+                       int32_t width, int32_t height, vmb_camera* out) {
+    return guarded([&] {
+        PinholeCamera cam = look_at(v3(eye), v3(target), v3(up), focal, width, height);
+        for (int i = 0; i < 9; ++i) out->rotation[i] = cam.rotation.m[i];
+        for (int k = 0; k < 3; ++k) out->position[k] = cam.position[k];
+        out->focal = cam.focal;
+        out->width = cam.width;
+        out->height = cam.height;
+    });
+}
+
+int vmr_generate_rays(const vmb_camera* c, double near_, double far_, double* origins, double* dirs) {
+    return guarded([&] {
+        RayBatch rays = generate_rays(to_cam(c), near_, far_);
+        for (size_t i = 0; i < rays.n_rays(); ++i)
+            for (int k = 0; k < 3; ++k) {
+                origins[3 * i + k] = rays.origins[i][k];
+                dirs[3 * i + k] = rays.directions[i][k];
+            }
+    });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// query_density / query_rgb_sigma (fields.cpp:75-93, :142-168) at p - velocity*t.
+int vmr_field_query(const vmb_field* f, const double* pts, uint64_t n, double t, double* sig, double* rgb) {
+    return guarded([&] {
+        RefField field = to_field(f);
+        std::vector<Vec3> p = vecs(pts, n);
+        for (auto& x : p) x = x - v3(f->velocity) * t;
+        if (field.voxel) {
+            if (rgb) {
+                std::vector<Vec3> rgbs;
+                std::vector<double> sigmas;
+                field.voxel->query_rgb_sigma(p, {}, rgbs, sigmas);
+                for (size_t i = 0; i < n; ++i) {
+                    sig[i] = sigmas[i];
+                    for (int k = 0; k < 3; ++k) rgb[3 * i + k] = rgbs[i][k];
+                }
+            } else {
+                std::vector<double> d = field.voxel->query_density(p);
+                std::copy(d.begin(), d.end(), sig);
+            }
+        } else {
+            if (rgb) {
+                std::vector<Vec3> rgbs;
+                std::vector<double> sigmas;
+                query_rgb_sigma(*field.analytic, p, {}, rgbs, sigmas);
+                for (size_t i = 0; i < n; ++i) {
+                    sig[i] = sigmas[i];
+                    for (int k = 0; k < 3; ++k) rgb[3 * i + k] = rgbs[i][k];
+                }
+            } else {
+                std::vector<double> d = query_density(*field.analytic, p);
+                std::copy(d.begin(), d.end(), sig);
+            }
+        }
+    });
+}
+
+// TrilinearVoxelField::backward (fields.cpp:170-211), accumulating into the
+// caller's arrays.
+int vmr_voxel_field_backward(const vmb_field* f, const double* pts, uint64_t n, const double* d_rgbs,
+                             const double* d_sigmas, double* acc_d, double* acc_c) {
+    return guarded([&] {
+        auto v = to_voxel(f);
+        TrilinearVoxelField::ParamGradients g;
+        g.d_raw_density.assign(acc_d, acc_d + v->n_vertices());
+        g.d_raw_color.assign(acc_c, acc_c + 3 * v->n_vertices());
+        v->backward(vecs(pts, n), vecs(d_rgbs, n), std::span<const double>(d_sigmas, n), g);
+        std::copy(g.d_raw_density.begin(), g.d_raw_density.end(), acc_d);
+        std::copy(g.d_raw_color.begin(), g.d_raw_color.end(), acc_c);
     });
 }
 

@@ -118,7 +118,16 @@ typedef int64_t (*vmo_sigma_cb)(void* user, const double* t_starts, const double
                        double near_, double far_, const vmo_grid* g, const vmb_field* f,        \
                        const vmb_march_config* cfg, const double* d_color,                      \
                        const double* d_opacity, const double* d_depth, int n_threads,           \
-                       double* phase_ms, uint64_t* n_samples_out, double* checksum);
+                       double* phase_ms, uint64_t* n_samples_out, double* checksum);          \
+    int P##_camera_look_at(const double* eye, const double* target, const double* up,           \
+                           double focal, int32_t width, int32_t height, vmb_camera* out);       \
+    int P##_generate_rays(const vmb_camera* camera, double near_, double far_, double* origins, \
+                          double* dirs);                                                        \
+    int P##_field_query(const vmb_field* f, const double* points, uint64_t n, double time,      \
+                        double* sigmas, double* rgbs);                                          \
+    int P##_voxel_field_backward(const vmb_field* f, const double* points, uint64_t n,          \
+                                 const double* d_rgbs, const double* d_sigmas,                  \
+                                 double* accum_density, double* accum_color);
 
 VMO_DECLARE(vmo)
 VMO_DECLARE(vmr)

@@ -15,6 +15,7 @@ LIB_PATH = os.environ.get("VMB_LIB_PATH") or os.path.join(HERE, "lib", "libvoxma
 
 VMB_OK, VMB_INVALID_ARGUMENT, VMB_RUNTIME, VMB_CUDA, VMB_NOT_SUPPORTED, VMB_CAPACITY = range(6)
 VMB_F32, VMB_F64 = 0, 1
+VMB_GRAD_DETERMINISTIC, VMB_GRAD_ATOMIC = 0, 1
 
 
 class Contraction(C.Structure):
@@ -44,7 +45,9 @@ class Field(C.Structure):
     _fields_ = [("kind", C.c_int32), ("pad_", C.c_int32), ("box_min", C.c_double * 3),
                 ("box_max", C.c_double * 3), ("center", C.c_double * 3), ("radius", C.c_double),
                 ("sigma", C.c_double), ("rgb", C.c_double * 3), ("rgb_b", C.c_double * 3),
-                ("period", C.c_double), ("velocity", C.c_double * 3)]
+                ("period", C.c_double), ("velocity", C.c_double * 3),
+                ("vox_density", C.c_void_p), ("vox_color", C.c_void_p), ("vox_resolution", C.c_uint32),
+                ("pad2_", C.c_uint32)]
 
     @staticmethod
     def sphere(center=(0.5, 0.5, 0.5), radius=0.2, sigma=1.0, rgb=(1.0, 1.0, 1.0),
@@ -77,6 +80,19 @@ class Field(C.Structure):
         f.rgb_b[:] = [float(v) for v in rgb_b]
         return f
 
+    @staticmethod
+    def voxel(resolution, box_min, box_max, density_ptr, color_ptr, velocity=(0.0, 0.0, 0.0)):
+        """TrilinearVoxelField (fields.hpp:55-111): raw density [R^3] / rgb [R^3][3] arrays
+        (device pointers for the product, host pointers for the oracle)."""
+        f = Field()
+        f.kind = 3
+        f.box_min[:] = [float(v) for v in box_min]
+        f.box_max[:] = [float(v) for v in box_max]
+        f.vox_resolution = int(resolution)
+        f.vox_density, f.vox_color = density_ptr, color_ptr
+        f.velocity[:] = [float(v) for v in velocity]
+        return f
+
 
 class MarchConfig(C.Structure):
     """vmb_march_config <- voxmarch::MarchingConfig (ray_marching.hpp:11-17)."""
@@ -98,6 +114,12 @@ class Rays(C.Structure):
     _fields_ = [("d_origins", C.c_void_p), ("d_directions", C.c_void_p), ("dtype", C.c_int32),
                 ("pad_", C.c_int32), ("n_rays", C.c_uint64), ("near_plane", C.c_double),
                 ("far_plane", C.c_double)]
+
+
+class Camera(C.Structure):
+    """vmb_camera <- voxmarch::PinholeCamera (scene_camera.hpp:12-19)."""
+    _fields_ = [("rotation", C.c_double * 9), ("position", C.c_double * 3), ("focal", C.c_double),
+                ("width", C.c_int32), ("height", C.c_int32)]
 
 
 class Samples(C.Structure):
@@ -136,6 +158,14 @@ SIGNATURES = {
     "vmb_event_elapsed_ms": (I32, [VP, I32, I32, P(C.c_float)]),
     "vmb_shard_range": (I32, [U64, I32, I32, P(U64), P(U64)]),
     "vmb_rays_validate": (I32, [VP, P(Rays)]),
+    "vmb_field_query": (I32, [VP, P(Field), VP, U64, D, VP, VP]),
+    "vmb_voxel_field_backward": (I32, [VP, P(Field), VP, U64, VP, VP, I32, VP, VP, I32]),
+    "vmb_voxel_field_backward_samples": (I32, [VP, P(Field), P(Rays), VP, VP, VP, U64, D, VP, VP, I32, VP,
+                                               VP, I32]),
+    "vmb_camera_validate": (I32, [P(Camera)]),
+    "vmb_camera_look_at": (I32, [P(C.c_double), P(C.c_double), P(C.c_double), C.c_double, I32, I32,
+                                 P(Camera)]),
+    "vmb_generate_rays": (I32, [VP, P(Camera), C.c_double, C.c_double, I32, VP, VP, P(Rays)]),
     "vmb_uniform_step_count": (U64, [D, D, D]),
     "vmb_pack": (I32, [VP, VP, U64, VP, VP, U64, P(U64)]),
     "vmb_validate": (I32, [VP, P(PackedView), VP, U64, U64, U64, P(I32)]),

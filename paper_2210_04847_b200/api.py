@@ -20,15 +20,16 @@ from typing import Callable, Optional
 
 import numpy as np
 
-from ._lib import (VMB_CAPACITY, VMB_F32, VMB_F64, Contraction, Field, MarchConfig, MarchStats,
-                   PackedView, Rays, Samples, VmbError, check, lib)
+from ._lib import (VMB_CAPACITY, VMB_F32, VMB_F64, Camera, Contraction, Field, MarchConfig,
+                   MarchStats, PackedView, Rays, Samples, VmbError, check, lib)
 
 __all__ = ["Device", "DeviceArray", "default_device", "Contraction", "Field", "MarchConfig",
            "MarchStats", "RayBatch", "PackedSamples", "OccupancyGrid", "march", "march_uniform",
            "uniform_step_count", "pack", "validate", "transmittance", "render_forward",
            "render_backward", "render_attribute", "contract", "invert_grid_point",
            "DevicePacked", "march_device", "shade_device", "render_forward_device",
-           "render_backward_device", "shard_range"]
+           "render_backward_device", "shard_range", "Camera", "look_at", "generate_rays_device",
+           "generate_rays", "VoxelField", "field_query_device"]
 
 
 # ====================================================================== device layer
@@ -241,6 +242,152 @@ def render_backward_device(dev: Device, packed: DevicePacked, rgbs: DeviceArray,
     check(dev.lib.vmb_render_backward(dev.h, C.byref(v), rgbs.ptr, sigmas.ptr, d_color.ptr,
                                       d_opacity.ptr, d_depth.ptr, g_rgbs.ptr, g_sigmas.ptr,
                                       _dt(rgbs.dtype)))
+
+
+# ====================================================================== cameras
+def look_at(eye, target, up, focal: float, width: int, height: int) -> Camera:
+    """voxmarch::look_at (scene_camera.cpp:25-44), host-side, exact fp64."""
+    d3 = lambda v: (C.c_double * 3)(*[float(x) for x in v])
+    cam = Camera()
+    check(lib().vmb_camera_look_at(d3(eye), d3(target), d3(up), float(focal), int(width), int(height),
+                                   C.byref(cam)))
+    return cam
+
+
+def generate_rays_device(dev: Device, cam: Camera, near: float, far: float, dtype=np.float32,
+                         origins: Optional["DeviceArray"] = None, dirs: Optional["DeviceArray"] = None):
+    """vmb_generate_rays: one ray per pixel on the device (scene_camera.cpp:46-63).
+    Returns (Rays, origins, dirs); the arrays may be passed in to be reused."""
+    n = max(cam.width, 0) * max(cam.height, 0)
+    origins = origins if origins is not None else dev.empty(n * 3, dtype)
+    dirs = dirs if dirs is not None else dev.empty(n * 3, dtype)
+    rays = Rays()
+    check(dev.lib.vmb_generate_rays(dev.h, C.byref(cam), float(near), float(far), _dt(dtype), origins.ptr,
+                                    dirs.ptr, C.byref(rays)))
+    return rays, origins, dirs
+
+
+def generate_rays(cam: Camera, near: float, far: float, dev: Optional[Device] = None) -> "RayBatch":
+    """voxmarch::generate_rays: the batch on the device (f64), as a RayBatch."""
+    dev = dev or default_device()
+    rays, o, d = generate_rays_device(dev, cam, near, far, np.float64)
+    n = int(rays.n_rays)
+    return RayBatch(o.numpy(3 * n).reshape(n, 3), d.numpy(3 * n).reshape(n, 3), near, far)
+
+
+# ====================================================================== fields
+def field_query_device(dev: Device, field: Field, points: "DeviceArray", n: int, time: float = 0.0,
+                       rgb: bool = True):
+    """vmb_field_query: sigma [n] (and rgb [n][3]) f64 on the device."""
+    sig = dev.empty(n, np.float64)
+    col = dev.empty(n * 3, np.float64) if rgb else None
+    check(dev.lib.vmb_field_query(dev.h, C.byref(field), points.ptr, n, float(time), sig.ptr,
+                                  col.ptr if col is not None else None))
+    return sig, col
+
+
+class VoxelField:
+    """voxmarch::TrilinearVoxelField (fields.hpp:55-111) with its parameters in HBM
+    (raw density [R^3] and raw rgb [R^3][3], f64, x-fastest). `field` is the
+    vmb_field descriptor every march / shade / grid-update entry point accepts."""
+
+    MAGIC, VERSION = b"VXFD", 1
+
+    def __init__(self, resolution: int, box_min, box_max, dev: Optional[Device] = None):
+        if resolution < 2:
+            raise ValueError("voxel field: resolution must be >= 2 vertices per axis")
+        lo, hi = [float(v) for v in box_min], [float(v) for v in box_max]
+        if not all(b > a for a, b in zip(lo, hi)):
+            raise ValueError("aabb max must be strictly greater than min")
+        self.dev = dev or default_device()
+        self.resolution, self.box_min, self.box_max = int(resolution), lo, hi
+        nv = self.n_vertices
+        self.d_density = self.dev.zeros(nv, np.float64)
+        self.d_color = self.dev.zeros(3 * nv, np.float64)
+        self.field = Field.voxel(self.resolution, lo, hi, self.d_density.ptr, self.d_color.ptr)
+
+    @property
+    def n_vertices(self) -> int:
+        return self.resolution ** 3
+
+    def vertex_index(self, ix, iy, iz) -> int:
+        return int(ix) + self.resolution * (int(iy) + self.resolution * int(iz))
+
+    def set_params(self, raw_density=None, raw_color=None):
+        if raw_density is not None:
+            self.d_density.copy_from(np.asarray(raw_density, np.float64).ravel())
+        if raw_color is not None:
+            self.d_color.copy_from(np.asarray(raw_color, np.float64).ravel())
+
+    def raw_density(self) -> np.ndarray:
+        return self.d_density.numpy()
+
+    def raw_color(self) -> np.ndarray:
+        return self.d_color.numpy()
+
+    def zero_gradients(self):
+        nv = self.n_vertices
+        return self.dev.zeros(nv, np.float64), self.dev.zeros(3 * nv, np.float64)
+
+    def query_rgb_sigma(self, positions, time: float = 0.0):
+        p = _f64(positions).reshape(-1, 3)
+        dp = self.dev.upload(p)
+        sig, col = field_query_device(self.dev, self.field, dp, len(p), time, True)
+        return col.numpy().reshape(-1, 3), sig.numpy()
+
+    def query_density(self, positions, time: float = 0.0):
+        p = _f64(positions).reshape(-1, 3)
+        sig, _ = field_query_device(self.dev, self.field, self.dev.upload(p), len(p), time, False)
+        return sig.numpy()
+
+    def backward(self, positions, d_rgbs, d_sigmas, accum=None, mode: int = 0):
+        """Accumulate the parameter gradient (host arrays in, device accumulators
+        (d_density, d_color) out); mode 0 = deterministic (reference order)."""
+        p = _f64(positions).reshape(-1, 3)
+        if len(d_rgbs) != len(p) or len(d_sigmas) != len(p):
+            raise ValueError("voxel field: gradient length mismatch")
+        acc = accum if accum is not None else self.zero_gradients()
+        gr, gs = self.dev.upload(_f64(d_rgbs).reshape(-1, 3)), self.dev.upload(_f64(d_sigmas))
+        dp = self.dev.upload(p)
+        check(self.dev.lib.vmb_voxel_field_backward(self.dev.h, C.byref(self.field), dp.ptr, len(p), gr.ptr,
+                                                    gs.ptr, VMB_F64, acc[0].ptr, acc[1].ptr, int(mode)))
+        self.dev.sync()
+        return acc
+
+    # VXFD (fields.cpp:224-262): magic, u32 version, u32 resolution, box f64 x6,
+    # raw density then raw color as f32.
+    def save(self, path: str):
+        import struct
+        with open(path, "wb") as fh:
+            fh.write(self.MAGIC + struct.pack("<II", self.VERSION, self.resolution))
+            fh.write(struct.pack("<6d", *self.box_min, *self.box_max))
+            fh.write(self.raw_density().astype("<f4").tobytes())
+            fh.write(self.raw_color().astype("<f4").tobytes())
+
+    @staticmethod
+    def load(path: str, dev: Optional[Device] = None) -> "VoxelField":
+        import struct
+        with open(path, "rb") as fh:
+            if fh.read(4) != VoxelField.MAGIC:
+                raise RuntimeError("voxel field: bad magic")
+            hdr = fh.read(8)
+            if len(hdr) < 8:
+                raise RuntimeError("voxel field: truncated stream")
+            version, res = struct.unpack("<II", hdr)
+            if version != VoxelField.VERSION:
+                raise RuntimeError("voxel field: unsupported version")
+            box = fh.read(48)
+            if len(box) < 48:
+                raise RuntimeError("voxel field: truncated stream")
+            b = struct.unpack("<6d", box)
+            vf = VoxelField(res, b[:3], b[3:], dev)
+            nv = vf.n_vertices
+            dens, col = fh.read(4 * nv), fh.read(12 * nv)
+            if len(dens) < 4 * nv or len(col) < 12 * nv:
+                raise RuntimeError("voxel field: truncated stream")
+            vf.set_params(np.frombuffer(dens, "<f4").astype(np.float64),
+                          np.frombuffer(col, "<f4").astype(np.float64))
+            return vf
 
 
 # ====================================================================== reference mirror

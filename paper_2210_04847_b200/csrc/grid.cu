@@ -43,6 +43,7 @@ struct Timestamps {
 // Probe of one cell with an analytic field over all timestamps
 // (occupancy_grid.cpp:106-140). Returns the max density (0 when the cell has no
 // preimage); sets *bad to the first timestamp index with an invalid density.
+template <bool VOX>
 __device__ __forceinline__ double probe_cell(const GridDev& g, const vmb_field& f,
                                              const Timestamps& ts, uint64_t cell, bool has_seed,
                                              uint64_t seed, int* bad) {
@@ -51,7 +52,7 @@ __device__ __forceinline__ double probe_cell(const GridDev& g, const vmb_field& 
     if (!invert(g.k, probe_point(cell, g.res, has_seed, seed), &w)) return 0.0;
     double probed = 0.0;
     for (int i = 0; i < ts.n; ++i) {
-        double d = field_density(f, time_shift(f, w, ts.t[i]));
+        double d = field_density_t<VOX>(f, time_shift(f, w, ts.t[i]));
         if (!isfinite(d) || d < 0.0) {
             *bad = i;
             return probed;
@@ -62,6 +63,7 @@ __device__ __forceinline__ double probe_cell(const GridDev& g, const vmb_field& 
 }
 
 // Fused update for a field that cannot produce invalid densities.
+template <bool VOX>
 __global__ void __launch_bounds__(256) k_update_fused(GridDev g, vmb_field f, Timestamps ts,
                                                       bool has_seed, uint64_t seed, double decay,
                                                       double* __restrict__ cache,
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(256) k_update_fused(GridDev g, vmb_field f, Ti
         bool bit = false;
         if (cell < g.n) {
             int bad;
-            double probed = probe_cell(g, f, ts, cell, has_seed, seed, &bad);
+            double probed = probe_cell<VOX>(g, f, ts, cell, has_seed, seed, &bad);
             double c = max_ref(cache[cell] * decay, probed);
             cache[cell] = c;
             bit = occupied_bit(c, g.ref_step, g.thr);
@@ -85,17 +87,19 @@ __global__ void __launch_bounds__(256) k_update_fused(GridDev g, vmb_field f, Ti
 }
 
 // Error scan for fields whose sigma is invalid: first (timestamp, cell) wins.
+template <bool VOX>
 __global__ void k_update_errors(GridDev g, vmb_field f, Timestamps ts, bool has_seed,
                                 uint64_t seed, DevError* err) {
     for (uint64_t cell = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; cell < g.n;
          cell += uint64_t(gridDim.x) * blockDim.x) {
         int bad;
-        probe_cell(g, f, ts, cell, has_seed, seed, &bad);
+        probe_cell<VOX>(g, f, ts, cell, has_seed, seed, &bad);
         if (bad >= 0) atomicMin(&err->key, (unsigned long long)((uint64_t(bad) << 40) | cell));
     }
 }
 
 // Sharded probe (multi-GPU): cells [c0, c1) of this rank, zero elsewhere.
+template <bool VOX>
 __global__ void k_probe_range(GridDev g, vmb_field f, Timestamps ts, bool has_seed, uint64_t seed,
                               uint64_t c0, uint64_t c1, double* __restrict__ probed) {
     for (uint64_t cell = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; cell < g.n;
@@ -103,7 +107,7 @@ __global__ void k_probe_range(GridDev g, vmb_field f, Timestamps ts, bool has_se
         double v = 0.0;
         if (cell >= c0 && cell < c1) {
             int bad;
-            v = probe_cell(g, f, ts, cell, has_seed, seed, &bad);
+            v = probe_cell<VOX>(g, f, ts, cell, has_seed, seed, &bad);
         }
         probed[cell] = v;
     }
@@ -460,16 +464,15 @@ int vmb_grid_update_field(vmb_ctx* ctx, vmb_grid* g, const vmb_field* f, const d
     if (rc) return rc;
     if (!(decay >= 0.0 && decay <= 1.0))
         return fail(VMB_INVALID_ARGUMENT, "occupancy grid: ema_decay must be in [0,1]");
-    if (f->kind == VMB_FIELD_UNIFORM_BOX &&
-        !(f->box_max[0] > f->box_min[0] && f->box_max[1] > f->box_min[1] && f->box_max[2] > f->box_min[2]))
-        return fail(VMB_INVALID_ARGUMENT, "aabb max must be strictly greater than min");
+    if (int frc = check_field(f)) return frc;
     GridDev gd = dev_of(g);
-    if (!(std::isfinite(f->sigma) && f->sigma >= 0.0)) {
-        // Only fields with an invalid sigma can fail; find the first bad probe
+    if (f->kind == VMB_FIELD_VOXEL || !(std::isfinite(f->sigma) && f->sigma >= 0.0)) {
+        // Only analytic fields with an invalid sigma, or a voxel field (its
+        // parameters may be non-finite), can fail; find the first bad probe
         // (timestamp-major, then cell order) before touching the cache.
         rc = reset_error(ctx);
         if (rc) return rc;
-        k_update_errors<<<grid_blocks(ctx, g->n_cells, 256), 256, 0, ctx->stream>>>(
+        (f->kind == VMB_FIELD_VOXEL ? k_update_errors<true> : k_update_errors<false>)<<<grid_blocks(ctx, g->n_cells, 256), 256, 0, ctx->stream>>>(
             gd, *f, ts, has_seed != 0, seed, ctx->d_err);
         DevError err;
         rc = read_error(ctx, &err);
@@ -483,7 +486,7 @@ int vmb_grid_update_field(vmb_ctx* ctx, vmb_grid* g, const vmb_field* f, const d
         }
         uint64_t c0, c1;
         vmb_shard_range(g->n_cells, ctx->nranks, ctx->rank, &c0, &c1);
-        k_probe_range<<<grid_blocks(ctx, g->n_cells, 256), 256, 0, ctx->stream>>>(
+        (f->kind == VMB_FIELD_VOXEL ? k_probe_range<true> : k_probe_range<false>)<<<grid_blocks(ctx, g->n_cells, 256), 256, 0, ctx->stream>>>(
             gd, *f, ts, has_seed != 0, seed, c0, c1, g->probed);
         rc = launch_check("grid probe");
         if (rc) return rc;
@@ -492,7 +495,7 @@ int vmb_grid_update_field(vmb_ctx* ctx, vmb_grid* g, const vmb_field* f, const d
         k_apply<<<grid_blocks(ctx, g->n_words * 32, 256), 256, 0, ctx->stream>>>(
             gd, g->probed, decay, g->cache, g->bits, g->n_words);
     } else {
-        k_update_fused<<<grid_blocks(ctx, g->n_words * 32, 256), 256, 0, ctx->stream>>>(
+        (f->kind == VMB_FIELD_VOXEL ? k_update_fused<true> : k_update_fused<false>)<<<grid_blocks(ctx, g->n_words * 32, 256), 256, 0, ctx->stream>>>(
             gd, *f, ts, has_seed != 0, seed, decay, g->cache, g->bits, g->n_words);
     }
     rc = launch_check("grid update");
@@ -505,8 +508,9 @@ int vmb_grid_probe_field_range(vmb_ctx* ctx, const vmb_grid* g, const vmb_field*
     Timestamps ts;
     int rc = make_timestamps(h_ts, n_ts, &ts);
     if (rc) return rc;
+    if (int frc = check_field(f)) return frc;
     if (c1 > g->n_cells) c1 = g->n_cells;
-    k_probe_range<<<grid_blocks(ctx, g->n_cells, 256), 256, 0, ctx->stream>>>(
+    (f->kind == VMB_FIELD_VOXEL ? k_probe_range<true> : k_probe_range<false>)<<<grid_blocks(ctx, g->n_cells, 256), 256, 0, ctx->stream>>>(
         dev_of(g), *f, ts, has_seed != 0, seed, c0, c1, d_probed);
     return launch_check("grid probe range");
 }

@@ -37,6 +37,10 @@ namespace {
 // BUFFER_FWD = BUFFER + the render_forward compositing of each kept sample, done
 // in filter_sample as the sample is kept (vmb_march_render_field).
 enum Mode { COUNT = 0, FILL = 1, BUFFER = 2, BUFFER_FWD = 3 };
+// bit 2 of a mode: the kernel evaluates a stored voxel field (field_density_t<true>)
+constexpr int VOXM = 4;
+__host__ __device__ constexpr int mbase(int m) { return m & 3; }
+__host__ __device__ constexpr bool mvox(int m) { return (m & VOXM) != 0; }
 
 struct MarchParams {
     Contract k;
@@ -130,7 +134,7 @@ __device__ __forceinline__ bool on_candidate(const MarchParams& P, Sink& s, uint
     if (s.n_cand >= P.max_cand) return false;  // candidate cap (:78 / :91)
     uint32_t ci = s.n_cand++;
     if (!P.filter) {  // candidate mode: keep every grid-passing interval
-        if (MODE == FILL) {
+        if (mbase(MODE) == FILL) {
             uint64_t o = s.base + s.n_kept;
             if (o < s.cap) {
                 s.ts[o] = t0;
@@ -138,17 +142,17 @@ __device__ __forceinline__ bool on_candidate(const MarchParams& P, Sink& s, uint
                 s.idx[o] = uint32_t(s.ray);
             }
         }
-        if (MODE >= BUFFER && s.n_kept < s.buf_cap) s.buf[s.n_kept * s.buf_stride] = uint32_t(i);
+        if (mbase(MODE) >= BUFFER && s.n_kept < s.buf_cap) s.buf[s.n_kept * s.buf_stride] = uint32_t(i);
         s.n_kept++;
         return true;
     }
     if (!s.filtering) return true;  // after the cut only the emitted count matters
-    if (MODE == BUFFER_FWD) {  // field_rgb_sigma's sigma == field_density's for finite p
+    if (mbase(MODE) == BUFFER_FWD) {  // field_rgb_sigma's sigma == field_density's for finite p
         D3 c;
-        const double sg = field_rgb_sigma(P.f, p, &c);
+        const double sg = field_rgb_sigma_t<mvox(MODE)>(P.f, p, &c);
         return filter_sample<MODE>(P, s, i, ci, t0, t1, sg, err, c);
     }
-    return filter_sample<MODE>(P, s, i, ci, t0, t1, field_density(P.f, p), err);
+    return filter_sample<MODE>(P, s, i, ci, t0, t1, field_density_t<mvox(MODE)>(P.f, p), err);
 }
 
 // Density validation, alpha floor and transmittance cut of candidate ci with
@@ -166,7 +170,7 @@ __device__ __forceinline__ bool filter_sample(const MarchParams& P, Sink& s, uin
     double delta = t1 - t0;
     double alpha = 1.0 - exp(-sigma * delta);
     if (alpha <= P.thr) return true;
-    if (MODE == FILL) {
+    if (mbase(MODE) == FILL) {
         uint64_t o = s.base + s.n_kept;
         if (o < s.cap) {
             s.ts[o] = t0;
@@ -174,8 +178,8 @@ __device__ __forceinline__ bool filter_sample(const MarchParams& P, Sink& s, uin
             s.idx[o] = uint32_t(s.ray);
         }
     }
-    if (MODE >= BUFFER && s.n_kept < s.buf_cap) s.buf[s.n_kept * s.buf_stride] = uint32_t(i);
-    if (MODE == BUFFER_FWD) s.composite(sigma, rgb, t0, t1, alpha);
+    if (mbase(MODE) >= BUFFER && s.n_kept < s.buf_cap) s.buf[s.n_kept * s.buf_stride] = uint32_t(i);
+    if (mbase(MODE) == BUFFER_FWD) s.composite(sigma, rgb, t0, t1, alpha);
     s.n_kept++;
     s.T *= 1.0 - alpha;
     if (s.T < P.eps) {
@@ -525,7 +529,7 @@ constexpr int kWalkCap = 24;
 // expressions (attributes rounded to the attribute dtype first), so the outputs
 // are bit-identical to march -> shade -> render_forward. Inline compositing needs
 // the shading position to be the march position (time_shift == identity).
-template <typename AT>
+template <typename AT, bool VOX>
 struct FwdAcc {
     double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0, op = 0.0, dep = 0.0;
     template <typename RT>
@@ -533,7 +537,7 @@ struct FwdAcc {
                                          uint64_t r, double t0, double t1, double time) {
         const D3 x = load3(orig, r) + load3(dirs, r) * (0.5 * (t0 + t1));
         D3 c;
-        const double sg = double(AT(field_rgb_sigma(P.f, time_shift(P.f, x, time), &c)));
+        const double sg = double(AT(field_rgb_sigma_t<VOX>(P.f, time_shift(P.f, x, time), &c)));
         const double alpha = 1.0 - exp(-sg * (t1 - t0));
         const double w = T * alpha;
         cr = cr + double(AT(c.x)) * w;
@@ -562,7 +566,7 @@ struct FwdOut {
 
 // FAST instantiates only walk_fast (+ its exact fallback and the dense walk for
 // unsafe rays), so its register allocation is not the union of every walk.
-template <typename RT, bool FAST, typename AT, bool FWD>
+template <typename RT, bool FAST, typename AT, bool FWD, bool VOX>
 __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
     MarchParams P, const RT* __restrict__ orig, const RT* __restrict__ dirs, uint64_t n_rays,
     uint32_t* __restrict__ counts, uint32_t* __restrict__ kept_idx, unsigned int* chunk_counter,
@@ -582,7 +586,7 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
             s.buf_stride = 32;
             s.buf_cap = kWalkCap;
             s.at32 = sizeof(AT) == 4;
-            constexpr int M = FWD ? BUFFER_FWD : BUFFER;
+            constexpr int M = (FWD ? BUFFER_FWD : BUFFER) | (VOX ? VOXM : 0);
             if (FAST) {
                 const D3 o = load3(orig, r), d = load3(dirs, r);
                 if (ray_safe(P, o, d))
@@ -614,7 +618,7 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
 // expand kernel already holds each sample's ray and exact t0/t1, so it writes the
 // field's rgb/sigma at the midpoint too — the expressions of shade_samples
 // (voxmarch.cpp:235-251) / k_shade, without re-reading the packed samples.
-template <typename RT, typename AT>
+template <typename RT, typename AT, bool VOX = false>
 struct ShadeOut {
     const RT* orig;
     const RT* dirs;
@@ -630,7 +634,7 @@ struct ShadeOut {
     __device__ __forceinline__ void shade_ray(D3 o, D3 d, uint64_t p, double t0, double t1) const {
         D3 x = o + d * (0.5 * (t0 + t1));
         D3 c;
-        double sigma = field_rgb_sigma(f, time_shift(f, x, time), &c);
+        double sigma = field_rgb_sigma_t<VOX>(f, time_shift(f, x, time), &c);
         rgb[3 * p] = AT(c.x);
         rgb[3 * p + 1] = AT(c.y);
         rgb[3 * p + 2] = AT(c.z);
@@ -653,12 +657,12 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
-template <typename RT, typename AT, bool SHADE>
+template <typename RT, typename AT, bool SHADE, bool VOX>
 __global__ void __launch_bounds__(32 * kExpandWarps) k_march_expand(
     double near_, double far_, double step, const uint32_t* __restrict__ counts,
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ kept_idx, uint64_t n_rays,
     double* __restrict__ ts, double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,
-    uint32_t* __restrict__ overflow, unsigned int* n_overflow, ShadeOut<RT, AT> sh) {
+    uint32_t* __restrict__ overflow, unsigned int* n_overflow, ShadeOut<RT, AT, VOX> sh) {
     __shared__ __align__(16) uint32_t s_idx[kExpandWarps][2][kWalkCap * 32];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -764,12 +768,12 @@ __global__ void __launch_bounds__(32 * kExpandWarps) k_march_expand(
 }
 
 // Re-walks the (rare) rays whose kept samples overflowed the shared buffer.
-template <typename RT, typename AT, bool SHADE, bool FWD>
+template <typename RT, typename AT, bool SHADE, bool FWD, bool VOX>
 __global__ void k_march_fixup(MarchParams P, const RT* __restrict__ orig, const RT* __restrict__ dirs,
                               const uint32_t* __restrict__ offsets, double* __restrict__ ts,
                               double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,
                               const uint32_t* __restrict__ overflow, const unsigned int* n_overflow,
-                              DevError* err, ShadeOut<RT, AT> sh, FwdOut<AT> fo) {
+                              DevError* err, ShadeOut<RT, AT, VOX> sh, FwdOut<AT> fo) {
     const unsigned int n = *n_overflow;
     for (unsigned int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         uint64_t r = overflow[k];
@@ -780,11 +784,11 @@ __global__ void k_march_fixup(MarchParams P, const RT* __restrict__ orig, const 
         s.idx = idx;
         s.base = offsets[r];
         s.cap = cap;
-        walk<FILL>(P, s, orig, dirs, r, err);
+        walk<FILL | (VOX ? VOXM : 0)>(P, s, orig, dirs, r, err);
         if (SHADE)
             for (uint64_t q = s.base; q < s.base + s.n_kept && q < cap; ++q) sh.shade(r, q, ts[q], te[q]);
         if (FWD) {  // walk_fast's t0/t1 of this ray, recomputed by the FILL walk
-            FwdAcc<AT> acc;
+            FwdAcc<AT, VOX> acc;
             for (uint64_t q = s.base; q < s.base + s.n_kept && q < cap; ++q)
                 acc.kept(P, orig, dirs, r, ts[q], te[q], fo.time);
             acc.store(r, fo.color, fo.opacity, fo.depth);
@@ -805,7 +809,7 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, const RT* __restri
          r += uint64_t(gridDim.x) * blockDim.x) {
         Sink s;
         s.ray = r;
-        if (MODE == FILL) {
+        if (mbase(MODE) == FILL) {
             s.ts = ts;
             s.te = te;
             s.idx = idx;
@@ -813,10 +817,10 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, const RT* __restri
             s.cap = cap;
         }
         walk<MODE>(P, s, orig, dirs, r, err);
-        if (MODE == COUNT) counts[r] = s.n_kept;
+        if (mbase(MODE) == COUNT) counts[r] = s.n_kept;
         emit_local += s.n_cand;
     }
-    if (MODE == COUNT && emitted) {
+    if (mbase(MODE) == COUNT && emitted) {
         for (int off = 16; off > 0; off >>= 1) emit_local += __shfl_xor_sync(0xffffffffu, emit_local, off);
         if ((threadIdx.x & 31) == 0 && emit_local) atomicAdd(emitted, emit_local);
     }
@@ -834,7 +838,7 @@ __global__ void k_filter(const uint32_t* __restrict__ c_off, const uint32_t* __r
     for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rays;
          r += uint64_t(gridDim.x) * blockDim.x) {
         uint64_t b = c_off[r], n = c_cnt[r];
-        uint64_t out = MODE == FILL ? offsets[r] : 0;
+        uint64_t out = mbase(MODE) == FILL ? offsets[r] : 0;
         uint32_t kept = 0;
         double T = 1.0;
         for (uint64_t k = 0; k < n; ++k) {
@@ -847,7 +851,7 @@ __global__ void k_filter(const uint32_t* __restrict__ c_off, const uint32_t* __r
             double t0 = c_ts[b + k], t1 = c_te[b + k];
             double alpha = 1.0 - exp(-sigma * (t1 - t0));
             if (alpha <= thr) continue;
-            if (MODE == FILL && out + kept < cap) {
+            if (mbase(MODE) == FILL && out + kept < cap) {
                 ts[out + kept] = t0;
                 te[out + kept] = t1;
                 idx[out + kept] = uint32_t(r);
@@ -856,7 +860,7 @@ __global__ void k_filter(const uint32_t* __restrict__ c_off, const uint32_t* __r
             T *= 1.0 - alpha;
             if (T < eps) break;
         }
-        if (MODE == COUNT) counts[r] = kept;
+        if (mbase(MODE) == COUNT) counts[r] = kept;
     }
 }
 
@@ -955,7 +959,11 @@ int march_params(const vmb_grid* g, const vmb_rays* rays, const vmb_march_config
 
 template <int MODE>
 void launch_march(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, uint32_t* counts,
-                  const uint32_t* offsets, vmb_samples* out, unsigned long long* emitted) {
+                  const uint32_t* offsets, vmb_samples* out, unsigned long long* emitted);
+
+template <int MODE>
+void launch_march_rt(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, uint32_t* counts,
+                     const uint32_t* offsets, vmb_samples* out, unsigned long long* emitted) {
     int blocks = grid_blocks(ctx, rays->n_rays, 128, 16);
     if (rays->dtype == VMB_F32)
         k_march<float, MODE><<<blocks, 128, 0, ctx->stream>>>(
@@ -969,6 +977,15 @@ void launch_march(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, uint
             static_cast<const double*>(rays->d_directions), rays->n_rays, counts, offsets,
             out ? out->d_t_starts : nullptr, out ? out->d_t_ends : nullptr,
             out ? out->d_ray_indices : nullptr, out ? out->capacity : 0, emitted, ctx->d_err);
+}
+
+template <int MODE>
+void launch_march(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, uint32_t* counts,
+                  const uint32_t* offsets, vmb_samples* out, unsigned long long* emitted) {
+    if (P.f.kind == VMB_FIELD_VOXEL)
+        launch_march_rt<MODE | VOXM>(ctx, P, rays, counts, offsets, out, emitted);
+    else
+        launch_march_rt<MODE>(ctx, P, rays, counts, offsets, out, emitted);
 }
 
 std::string march_error_text(const DevError& e) {
@@ -1032,22 +1049,22 @@ FwdOut<AT> fwd_out(const ShadeReq& sr) {
                       static_cast<AT*>(sr.depth), sr.time};
 }
 
-template <typename RT, typename AT, bool SHADE, bool FWD>
+template <typename RT, typename AT, bool SHADE, bool FWD, bool VOX>
 void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
                          const uint32_t* kept_idx, uint32_t* overflow, unsigned int* n_overflow,
                          uint64_t n_chunks, const ShadeReq& sr) {
-    ShadeOut<RT, AT> sh{static_cast<const RT*>(rays->d_origins), static_cast<const RT*>(rays->d_directions),
+    ShadeOut<RT, AT, VOX> sh{static_cast<const RT*>(rays->d_origins), static_cast<const RT*>(rays->d_directions),
                         sr.f, sr.time, static_cast<AT*>(sr.rgb), static_cast<AT*>(sr.sig)};
     static int per_sm = [] {  // persistent: exactly the resident blocks
         int n = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_march_expand<RT, AT, SHADE>, 32 * kExpandWarps, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_march_expand<RT, AT, SHADE, VOX>, 32 * kExpandWarps, 0);
         return n < 1 ? 4 : n;
     }();
-    k_march_expand<RT, AT, SHADE><<<grid_blocks(ctx, n_chunks * 32, 32 * kExpandWarps, per_sm),
+    k_march_expand<RT, AT, SHADE, VOX><<<grid_blocks(ctx, n_chunks * 32, 32 * kExpandWarps, per_sm),
                                     32 * kExpandWarps, 0, ctx->stream>>>(
         P.near_, P.far_, P.step, out->d_counts, out->d_offsets, kept_idx, rays->n_rays, out->d_t_starts,
         out->d_t_ends, out->d_ray_indices, out->capacity, overflow, n_overflow, sh);
-    k_march_fixup<RT, AT, SHADE, FWD><<<ctx->num_sms * 2, 128, 0, ctx->stream>>>(
+    k_march_fixup<RT, AT, SHADE, FWD, VOX><<<ctx->num_sms * 2, 128, 0, ctx->stream>>>(
         P, sh.orig, sh.dirs, out->d_offsets, out->d_t_starts, out->d_t_ends, out->d_ray_indices,
         out->capacity, overflow, n_overflow, ctx->d_err, sh, fwd_out<AT>(sr));
 }
@@ -1056,14 +1073,19 @@ template <typename RT>
 void dispatch_expand(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
                      const uint32_t* kept_idx, uint32_t* overflow, unsigned int* n_overflow,
                      uint64_t n_chunks, const ShadeReq& sr) {
-#define VMB_EXPAND(AT, SH, FW) \
-    launch_expand_fixup<RT, AT, SH, FW>(ctx, P, rays, out, kept_idx, overflow, n_overflow, n_chunks, sr)
+#define VMB_EXPAND(AT, SH, FW, VX) \
+    launch_expand_fixup<RT, AT, SH, FW, VX>(ctx, P, rays, out, kept_idx, overflow, n_overflow, n_chunks, sr)
+    const bool vox = P.f.kind == VMB_FIELD_VOXEL;
     if (!sr.on)
-        VMB_EXPAND(float, false, false);
+        vox ? VMB_EXPAND(float, false, false, true) : VMB_EXPAND(float, false, false, false);
+    else if (sr.dtype == VMB_F32 && vox)
+        sr.fwd ? VMB_EXPAND(float, true, true, true) : VMB_EXPAND(float, true, false, true);
     else if (sr.dtype == VMB_F32)
-        sr.fwd ? VMB_EXPAND(float, true, true) : VMB_EXPAND(float, true, false);
+        sr.fwd ? VMB_EXPAND(float, true, true, false) : VMB_EXPAND(float, true, false, false);
+    else if (vox)
+        sr.fwd ? VMB_EXPAND(double, true, true, true) : VMB_EXPAND(double, true, false, true);
     else
-        sr.fwd ? VMB_EXPAND(double, true, true) : VMB_EXPAND(double, true, false);
+        sr.fwd ? VMB_EXPAND(double, true, true, false) : VMB_EXPAND(double, true, false, false);
 #undef VMB_EXPAND
 }
 
@@ -1093,24 +1115,31 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
         kernel<<<ctx->num_sms * per_sm, 128, 0, ctx->stream>>>(
             P, o, d, n, out->d_counts, kept_idx, counters, n_chunks, emitted, ctx->d_err, fo);
     };
-    auto walk_rt = [&](auto* o, auto* d) {
+    auto walk_vox = [&](auto* o, auto* d, auto VOXC) {
         using RT = std::remove_const_t<std::remove_pointer_t<decltype(o)>>;
+        constexpr bool VX = decltype(VOXC)::value;
         const bool f64 = sr.dtype == VMB_F64;
         if (P.fast) {
             if (!sr.fwd)
-                launch_walk(k_march_walk<RT, true, float, false>, o, d, FwdOut<float>{});
+                launch_walk(k_march_walk<RT, true, float, false, VX>, o, d, FwdOut<float>{});
             else if (f64)
-                launch_walk(k_march_walk<RT, true, double, true>, o, d, fwd_out<double>(sr));
+                launch_walk(k_march_walk<RT, true, double, true, VX>, o, d, fwd_out<double>(sr));
             else
-                launch_walk(k_march_walk<RT, true, float, true>, o, d, fwd_out<float>(sr));
+                launch_walk(k_march_walk<RT, true, float, true, VX>, o, d, fwd_out<float>(sr));
         } else {
             if (!sr.fwd)
-                launch_walk(k_march_walk<RT, false, float, false>, o, d, FwdOut<float>{});
+                launch_walk(k_march_walk<RT, false, float, false, VX>, o, d, FwdOut<float>{});
             else if (f64)
-                launch_walk(k_march_walk<RT, false, double, true>, o, d, fwd_out<double>(sr));
+                launch_walk(k_march_walk<RT, false, double, true, VX>, o, d, fwd_out<double>(sr));
             else
-                launch_walk(k_march_walk<RT, false, float, true>, o, d, fwd_out<float>(sr));
+                launch_walk(k_march_walk<RT, false, float, true, VX>, o, d, fwd_out<float>(sr));
         }
+    };
+    auto walk_rt = [&](auto* o, auto* d) {
+        if (P.f.kind == VMB_FIELD_VOXEL)
+            walk_vox(o, d, std::true_type{});
+        else
+            walk_vox(o, d, std::false_type{});
     };
     if (rays->dtype == VMB_F32)
         walk_rt(static_cast<const float*>(rays->d_origins), static_cast<const float*>(rays->d_directions));
@@ -1195,9 +1224,7 @@ int vmb_march_field_shaded(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays
     MarchParams P;
     int rc = march_params(g, rays, cfg, &P);
     if (rc) return rc;
-    if (f->kind == VMB_FIELD_UNIFORM_BOX &&
-        !(f->box_max[0] > f->box_min[0] && f->box_max[1] > f->box_min[1] && f->box_max[2] > f->box_min[2]))
-        return fail(VMB_INVALID_ARGUMENT, "aabb max must be strictly greater than min");
+    if (int frc = check_field(f)) return frc;
     P.f = *f;
     P.filter = true;
     P.full = stats != nullptr;
@@ -1219,9 +1246,7 @@ int vmb_march_render_field(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays
     MarchParams P;
     int rc = march_params(g, rays, cfg, &P);
     if (rc) return rc;
-    if (f->kind == VMB_FIELD_UNIFORM_BOX &&
-        !(f->box_max[0] > f->box_min[0] && f->box_max[1] > f->box_min[1] && f->box_max[2] > f->box_min[2]))
-        return fail(VMB_INVALID_ARGUMENT, "aabb max must be strictly greater than min");
+    if (int frc = check_field(f)) return frc;
     P.f = *f;
     P.filter = true;
     P.full = stats != nullptr;
@@ -1257,9 +1282,7 @@ int vmb_march_field(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays, const
     MarchParams P;
     int rc = march_params(g, rays, cfg, &P);
     if (rc) return rc;
-    if (f->kind == VMB_FIELD_UNIFORM_BOX &&
-        !(f->box_max[0] > f->box_min[0] && f->box_max[1] > f->box_min[1] && f->box_max[2] > f->box_min[2]))
-        return fail(VMB_INVALID_ARGUMENT, "aabb max must be strictly greater than min");
+    if (int frc = check_field(f)) return frc;
     P.f = *f;
     P.filter = true;
     P.full = stats != nullptr;
@@ -1273,6 +1296,7 @@ int vmb_march_field_async(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,
     MarchParams P;
     int rc = march_params(g, rays, cfg, &P);
     if (rc) return rc;
+    if (int frc = check_field(f)) return frc;
     P.f = *f;
     P.filter = true;
     P.full = false;

@@ -389,7 +389,7 @@ __global__ void k_attribute(const uint32_t* __restrict__ offsets, const uint32_t
 }
 
 // ------------------------------------------------------------------ shading (harness)
-template <typename RT, typename T>
+template <typename RT, typename T, bool VOX>
 __global__ void k_shade(const RT* __restrict__ orig, const RT* __restrict__ dirs, vmb_field f,
                         double time, const uint32_t* __restrict__ idx, const double* __restrict__ ts,
                         const double* __restrict__ te, uint64_t n, T* __restrict__ rgb,
@@ -401,7 +401,7 @@ __global__ void k_shade(const RT* __restrict__ orig, const RT* __restrict__ dirs
         D3 d = d3(double(dirs[3 * r]), double(dirs[3 * r + 1]), double(dirs[3 * r + 2]));
         D3 p = o + d * (0.5 * (ts[s] + te[s]));  // voxmarch.cpp:243-244
         D3 c;
-        double sigma = field_rgb_sigma(f, time_shift(f, p, time), &c);
+        double sigma = field_rgb_sigma_t<VOX>(f, time_shift(f, p, time), &c);
         rgb[3 * s] = T(c.x);
         rgb[3 * s + 1] = T(c.y);
         rgb[3 * s + 2] = T(c.z);
@@ -496,22 +496,23 @@ int vmb_render_attribute(vmb_ctx* ctx, const vmb_packed_view* p, const void* sig
 int vmb_shade_field(vmb_ctx* ctx, const vmb_rays* rays, const vmb_field* f, double time,
                     const uint32_t* idx, const double* ts, const double* te, uint64_t n, void* rgb,
                     void* sig, int dtype) {
+    if (int frc = check_field(f)) return frc;
     if (!n) return VMB_OK;
     int blocks = grid_blocks(ctx, n, 256, 8);
     if (rays->dtype == VMB_F32 && dtype == VMB_F32)
-        k_shade<float, float><<<blocks, 256, 0, ctx->stream>>>(
+        (f->kind == VMB_FIELD_VOXEL ? k_shade<float, float, true> : k_shade<float, float, false>)<<<blocks, 256, 0, ctx->stream>>>(
             static_cast<const float*>(rays->d_origins), static_cast<const float*>(rays->d_directions), *f,
             time, idx, ts, te, n, static_cast<float*>(rgb), static_cast<float*>(sig));
     else if (rays->dtype == VMB_F32)
-        k_shade<float, double><<<blocks, 256, 0, ctx->stream>>>(
+        (f->kind == VMB_FIELD_VOXEL ? k_shade<float, double, true> : k_shade<float, double, false>)<<<blocks, 256, 0, ctx->stream>>>(
             static_cast<const float*>(rays->d_origins), static_cast<const float*>(rays->d_directions), *f,
             time, idx, ts, te, n, static_cast<double*>(rgb), static_cast<double*>(sig));
     else if (dtype == VMB_F32)
-        k_shade<double, float><<<blocks, 256, 0, ctx->stream>>>(
+        (f->kind == VMB_FIELD_VOXEL ? k_shade<double, float, true> : k_shade<double, float, false>)<<<blocks, 256, 0, ctx->stream>>>(
             static_cast<const double*>(rays->d_origins), static_cast<const double*>(rays->d_directions), *f,
             time, idx, ts, te, n, static_cast<float*>(rgb), static_cast<float*>(sig));
     else
-        k_shade<double, double><<<blocks, 256, 0, ctx->stream>>>(
+        (f->kind == VMB_FIELD_VOXEL ? k_shade<double, double, true> : k_shade<double, double, false>)<<<blocks, 256, 0, ctx->stream>>>(
             static_cast<const double*>(rays->d_origins), static_cast<const double*>(rays->d_directions), *f,
             time, idx, ts, te, n, static_cast<double*>(rgb), static_cast<double*>(sig));
     return launched("shade");

@@ -174,6 +174,22 @@ using namespace vmb;
         if (e_ != cudaSuccess) return cuda_fail(e_, where); \
     } while (0)
 
+namespace vmb {
+int check_field(const vmb_field* f) {
+    if (!f) return fail(VMB_INVALID_ARGUMENT, "field: null");
+    const bool boxed = f->kind == VMB_FIELD_UNIFORM_BOX || f->kind == VMB_FIELD_VOXEL;
+    if (f->kind == VMB_FIELD_VOXEL && f->vox_resolution < 2)
+        return fail(VMB_INVALID_ARGUMENT, "voxel field: resolution must be >= 2 vertices per axis");
+    if (boxed && !(f->box_max[0] > f->box_min[0] && f->box_max[1] > f->box_min[1] && f->box_max[2] > f->box_min[2]))
+        return fail(VMB_INVALID_ARGUMENT, "aabb max must be strictly greater than min");
+    if (f->kind == VMB_FIELD_VOXEL && (!f->vox_density || !f->vox_color))
+        return fail(VMB_INVALID_ARGUMENT, "voxel field: parameter arrays required");
+    if (f->kind < VMB_FIELD_UNIFORM_BOX || f->kind > VMB_FIELD_VOXEL)
+        return fail(VMB_INVALID_ARGUMENT, "field: unknown kind");
+    return VMB_OK;
+}
+}  // namespace vmb
+
 extern "C" {
 
 const char* vmb_last_error(void) { return vmb::g_error.c_str(); }
@@ -229,6 +245,7 @@ int vmb_ctx_destroy(vmb_ctx* ctx) {
 }
 
 static cudaStream_t g_dummy;
+
 
 int vmb_ctx_set_stream(vmb_ctx* ctx, void* stream) {
     if (ctx->own_stream && stream) {

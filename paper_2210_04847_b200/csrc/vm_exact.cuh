@@ -134,14 +134,85 @@ VM_HD bool box_contains(const vmb_field& f, D3 p) {  // math.hpp:57-60
            p.y <= f.box_max[1] && p.z >= f.box_min[2] && p.z <= f.box_max[2];
 }
 
-VM_HD double field_density(const vmb_field& f, D3 p) {
+// TrilinearVoxelField (fields.hpp:47-54 activations; fields.cpp:105-168 stencil).
+VM_HD double vox_softplus(double x) { return x > 0.0 ? x + log1p(exp(-x)) : log1p(exp(x)); }
+VM_HD double vox_sigmoid(double x) {
+    if (x >= 0.0) return 1.0 / (1.0 + exp(-x));
+    double e = exp(x);
+    return e / (1.0 + e);
+}
+
+// stencil_at: cell (lower corner vertex) and fractional offsets; false outside
+// the box (Aabb::contains, inclusive).
+VM_HD bool vox_stencil(const vmb_field& f, D3 p, uint32_t c[3], double fr[3]) {
+    if (!box_contains(f, p)) return false;
+    const double r1 = double(f.vox_resolution - 1);
+    const uint32_t last_cell = f.vox_resolution - 2;
+    const double pk[3] = {p.x, p.y, p.z};
+    for (int a = 0; a < 3; ++a) {
+        // Vec3 rel = (p - min) / box.size() * double(R - 1)
+        const double rel = ((pk[a] - f.box_min[a]) / (f.box_max[a] - f.box_min[a])) * r1;
+        const double fl = floor(rel);
+        uint32_t ca = 0;
+        if (!(fl < 0.0)) {
+            ca = uint32_t(fl);
+            ca = ca > last_cell ? last_cell : ca;
+        }
+        c[a] = ca;
+        fr[a] = rel - double(ca);
+    }
+    return true;
+}
+
+// vertex k (dz outer, dy, dx inner) of cell c and its weight wx[dx]*wy[dy]*wz[dz]
+VM_HD uint64_t vox_vertex(const vmb_field& f, const uint32_t c[3], int k) {
+    const uint64_t R = f.vox_resolution;
+    return uint64_t(c[0] + (k & 1)) + R * (uint64_t(c[1] + ((k >> 1) & 1)) + R * uint64_t(c[2] + (k >> 2)));
+}
+VM_HD double vox_weight(const double fr[3], int k) {
+    const double wx = (k & 1) ? fr[0] : 1.0 - fr[0];
+    const double wy = ((k >> 1) & 1) ? fr[1] : 1.0 - fr[1];
+    const double wz = (k >> 2) ? fr[2] : 1.0 - fr[2];
+    return wx * wy * wz;
+}
+
+// interpolated raw density (and raw rgb when rgb != nullptr), in stencil order
+VM_HD bool vox_raw(const vmb_field& f, D3 p, double* raw_d, D3* raw_c) {
+    uint32_t c[3];
+    double fr[3];
+    if (!vox_stencil(f, p, c, fr)) return false;
+    double d = 0.0, r = 0.0, g = 0.0, b = 0.0;
+    for (int k = 0; k < 8; ++k) {
+        const double w = vox_weight(fr, k);
+        const uint64_t v = vox_vertex(f, c, k);
+        d += w * f.vox_density[v];
+        if (raw_c) {
+            r += w * f.vox_color[3 * v];
+            g += w * f.vox_color[3 * v + 1];
+            b += w * f.vox_color[3 * v + 2];
+        }
+    }
+    *raw_d = d;
+    if (raw_c) *raw_c = D3{r, g, b};
+    return true;
+}
+
+// Field evaluation. Kernels are instantiated with VOX = true only when the field
+// is a stored voxel field, so the analytic instantiations never carry the
+// stencil's registers; field_density / field_rgb_sigma dispatch at run time.
+template <bool VOX>
+VM_HD double field_density_t(const vmb_field& f, D3 p);
+template <bool VOX>
+VM_HD double field_rgb_sigma_t(const vmb_field& f, D3 p, D3* rgb);
+
+VM_HD double field_density_analytic(const vmb_field& f, D3 p) {
     if (f.kind == VMB_FIELD_UNIFORM_BOX) return box_contains(f, p) ? f.sigma : 0.0;
     if (f.kind == VMB_FIELD_SOLID_SPHERE)
         return norm(p - d3(f.center[0], f.center[1], f.center[2])) <= f.radius ? f.sigma : 0.0;
     return f.sigma;
 }
 
-VM_HD double field_rgb_sigma(const vmb_field& f, D3 p, D3* rgb) {
+VM_HD double field_rgb_sigma_analytic(const vmb_field& f, D3 p, D3* rgb) {
     if (f.kind == VMB_FIELD_UNIFORM_BOX || f.kind == VMB_FIELD_SOLID_SPHERE) {
         bool in = f.kind == VMB_FIELD_UNIFORM_BOX
                       ? box_contains(f, p)
@@ -159,6 +230,33 @@ VM_HD double field_rgb_sigma(const vmb_field& f, D3 p, D3* rgb) {
                                        : d3(f.rgb_b[0], f.rgb_b[1], f.rgb_b[2]);
     return f.sigma;
 }
+
+template <bool VOX>
+VM_HD double field_density_t(const vmb_field& f, D3 p) {
+    if (VOX && f.kind == VMB_FIELD_VOXEL) {
+        double raw;
+        return vox_raw(f, p, &raw, nullptr) ? vox_softplus(raw) : 0.0;
+    }
+    return field_density_analytic(f, p);
+}
+
+template <bool VOX>
+VM_HD double field_rgb_sigma_t(const vmb_field& f, D3 p, D3* rgb) {
+    if (VOX && f.kind == VMB_FIELD_VOXEL) {
+        double raw_d;
+        D3 raw_c;
+        if (!vox_raw(f, p, &raw_d, &raw_c)) {
+            *rgb = d3(0.0, 0.0, 0.0);
+            return 0.0;
+        }
+        *rgb = d3(vox_sigmoid(raw_c.x), vox_sigmoid(raw_c.y), vox_sigmoid(raw_c.z));
+        return vox_softplus(raw_d);
+    }
+    return field_rgb_sigma_analytic(f, p, rgb);
+}
+
+VM_HD double field_density(const vmb_field& f, D3 p) { return field_density_t<true>(f, p); }
+VM_HD double field_rgb_sigma(const vmb_field& f, D3 p, D3* rgb) { return field_rgb_sigma_t<true>(f, p, rgb); }
 
 VM_HD D3 time_shift(const vmb_field& f, D3 p, double t) {  // p - velocity * t
     return p - d3(f.velocity[0], f.velocity[1], f.velocity[2]) * t;

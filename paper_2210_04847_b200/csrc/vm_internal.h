@@ -50,8 +50,8 @@ struct vmb_ctx {
     vmb::DevError* h_err = nullptr;     // pinned mirror
     unsigned long long* d_u64 = nullptr;  // 8 device scalars (totals, counters)
     unsigned long long* h_u64 = nullptr;  // pinned mirror
-    void* scratch[4] = {};          // per-purpose growable device scratch (see scratch())
-    size_t scratch_bytes[4] = {};
+    void* scratch[5] = {};          // per-purpose growable device scratch (see scratch())
+    size_t scratch_bytes[5] = {};
     cudaEvent_t events[32] = {};
     // NCCL (dlopen'ed lazily; see comm.cpp)
     void* nccl_comm = nullptr;
@@ -92,13 +92,16 @@ int cuda_fail(cudaError_t e, const char* where);
 // Growable device scratch, one buffer per slot so nested users never alias:
 // slot 0 = scan tile sums, 1 = march / candidates temporaries, 2 = grid update,
 // 3 = validation / misc. Growing synchronizes the stream before freeing.
-enum { SCRATCH_SCAN = 0, SCRATCH_MARCH = 1, SCRATCH_GRID = 2, SCRATCH_MISC = 3 };
+enum { SCRATCH_SCAN = 0, SCRATCH_MARCH = 1, SCRATCH_GRID = 2, SCRATCH_MISC = 3, SCRATCH_VOXGRAD = 4, SCRATCH_SLOTS = 5 };
 void* scratch(vmb_ctx* ctx, int slot, size_t bytes);
 inline int grid_blocks(vmb_ctx* ctx, uint64_t work, int threads, int per_sm = 8) {
     uint64_t b = (work + threads - 1) / threads;
     uint64_t cap = uint64_t(ctx->num_sms) * per_sm;
     return int(b < 1 ? 1 : (b > cap ? cap : b));
 }
+// Host-side field descriptor checks (Aabb ctor math.hpp:50 for box/voxel boxes,
+// TrilinearVoxelField ctor fields.cpp:95-101).
+int check_field(const vmb_field* f);
 int reset_error(vmb_ctx* ctx);
 int read_error(vmb_ctx* ctx, DevError* out);  // synchronizes
 

@@ -35,7 +35,7 @@ def test_struct_layouts_match_oracle():
                  (_lib.MarchConfig, o.MarchConfig)]:
         assert C.sizeof(a) == C.sizeof(b)
         assert [f[0] for f in a._fields_] == [f[0] for f in b._fields_]
-    assert C.sizeof(_lib.Field) == 8 + 3 * 8 * 3 + 8 + 8 + 24 + 24 + 8 + 24
+    assert C.sizeof(_lib.Field) == 8 + 3 * 8 * 3 + 8 + 8 + 24 + 24 + 8 + 24 + 8 + 8 + 8
     assert C.sizeof(_lib.Rays) == 48 and C.sizeof(_lib.Samples) == 48
 
 
