@@ -134,6 +134,13 @@ int vmb_voxel_field_backward_samples(vmb_ctx* ctx, const vmb_field* field, const
                                      const void* d_rgb_grads, const void* d_sigma_grads, int dtype,
                                      double* d_accum_density, double* d_accum_color, int mode);
 
+/* AdamOptimizer::step (fields.cpp:279-292) on device arrays of n doubles; step =
+ * the optimizer's step count t after increment (bias corrections 1 - beta^t).
+ * A non-finite gradient fails with "adam: non-finite gradient at index i"
+ * (VMB_RUNTIME) before anything is updated. */
+int vmb_adam_step(vmb_ctx* ctx, uint64_t n, double* d_params, const double* d_grads, double* d_m, double* d_v,
+                  double lr, double beta1, double beta2, double eps, uint64_t step);
+
 /* uniform_step_count (ray_marching.cpp:51-55). Host-only. */
 uint64_t vmb_uniform_step_count(double near_plane, double far_plane, double step_size);
 /* pack (core_types.cpp:30-48): exclusive scan of counts + ray index expansion.

@@ -219,6 +219,104 @@ void query_rgb_sigma(const AnalyticField& field, std::span<const Vec3> positions
                      std::span<const Vec3> directions, std::vector<Vec3>& rgbs,
                      std::vector<double>& sigmas);
 
+inline double softplus(double x) {  // fields.hpp:47-50
+    return x > 0.0 ? x + std::log1p(std::exp(-x)) : std::log1p(std::exp(x));
+}
+inline double sigmoid(double x) {  // fields.hpp:51-54
+    if (x >= 0.0) return 1.0 / (1.0 + std::exp(-x));
+    double e = std::exp(x);
+    return e / (1.0 + e);
+}
+
+// fields.hpp:56-111. Parameters live in these host vectors (the reference's value
+// semantics: raw_density()/raw_color() are mutable references); batch queries and
+// backward upload them and run on the device (vmb_field_query,
+// vmb_voxel_field_backward in the reference's sample-order fold).
+class TrilinearVoxelField {
+public:
+    TrilinearVoxelField(uint32_t resolution, const Aabb& box);
+
+    double density_at(const Vec3& p) const;
+    std::pair<Vec3, double> rgb_sigma_at(const Vec3& p, const Vec3& dir) const;
+    std::vector<double> query_density(std::span<const Vec3> positions) const;
+    void query_rgb_sigma(std::span<const Vec3> positions, std::span<const Vec3> directions,
+                         std::vector<Vec3>& rgbs, std::vector<double>& sigmas) const;
+
+    struct ParamGradients {
+        std::vector<double> d_raw_density;  // resolution^3
+        std::vector<double> d_raw_color;    // 3 * resolution^3
+    };
+    ParamGradients zero_gradients() const;
+    void backward(std::span<const Vec3> positions, std::span<const Vec3> d_rgbs,
+                  std::span<const double> d_sigmas, ParamGradients& accum) const;
+
+    std::vector<double>& raw_density() { return raw_density_; }
+    const std::vector<double>& raw_density() const { return raw_density_; }
+    std::vector<double>& raw_color() { return raw_color_; }
+    const std::vector<double>& raw_color() const { return raw_color_; }
+
+    uint32_t resolution() const { return resolution_; }
+    const Aabb& box() const { return box_; }
+    size_t n_vertices() const { return raw_density_.size(); }
+    size_t vertex_index(uint32_t ix, uint32_t iy, uint32_t iz) const {
+        return size_t(ix) + size_t(resolution_) * (size_t(iy) + size_t(resolution_) * iz);
+    }
+
+    void save(std::ostream& out) const;
+    void save_file(const std::string& path) const;
+    static TrilinearVoxelField load(std::istream& in);
+    static TrilinearVoxelField load_file(const std::string& path);
+
+private:
+    uint32_t resolution_ = 0;
+    Aabb box_;
+    std::vector<double> raw_density_;
+    std::vector<double> raw_color_;
+};
+
+// fields.hpp:113-121
+struct TimeConditionedField {
+    AnalyticField base;
+    Vec3 velocity{0.0, 0.0, 0.0};
+
+    double density_at(const Vec3& p, double t) const;
+    std::pair<Vec3, double> rgb_sigma_at(const Vec3& p, const Vec3& dir, double t) const;
+};
+
+// fields.hpp:123-142; the update runs on the device (vmb_adam_step).
+class AdamOptimizer {
+public:
+    explicit AdamOptimizer(size_t n_params, double lr = 1e-2, double beta1 = 0.9,
+                           double beta2 = 0.999, double eps = 1e-8);
+
+    void step(std::span<double> params, std::span<const double> grads);
+
+    double learning_rate() const { return lr_; }
+    void set_learning_rate(double lr) { lr_ = lr; }
+
+private:
+    double lr_, beta1_, beta2_, eps_;
+    uint64_t t_ = 0;
+    std::vector<double> m_, v_;
+};
+
+// ------------------------------------------------------------------ scene_camera.hpp:10-38
+struct PinholeCamera {
+    Mat3 rotation;
+    Vec3 position;
+    double focal = 1.0;  // pixels
+    int width = 0;
+    int height = 0;
+};
+
+void validate_camera(const PinholeCamera& camera);
+PinholeCamera look_at(const Vec3& eye, const Vec3& target, const Vec3& up, double focal,
+                      int width, int height);
+// one ray per pixel centre, generated on the device (vmb_generate_rays)
+RayBatch generate_rays(const PinholeCamera& camera, double near, double far);
+PinholeCamera load_camera_json(const std::string& path);
+void save_camera_json(const PinholeCamera& camera, const std::string& path);
+
 // ------------------------------------------------------------------ occupancy_grid.hpp:16-89
 using DensityBatchFn = std::function<std::vector<double>(std::span<const Vec3>)>;
 using TimeDensityBatchFn = std::function<std::vector<double>(std::span<const Vec3>, double)>;

@@ -11,7 +11,10 @@
 #include <istream>
 #include <mutex>
 #include <ostream>
+#include <cstdio>
+#include <cstdlib>
 #include <fstream>
+#include <iterator>
 
 #include "vm_exact.cuh"
 #include "vmb200.h"
@@ -301,28 +304,35 @@ std::pair<Vec3, double> rgb_sigma_at(const AnalyticField& field, const Vec3& p, 
     return {v3d(rgb), s};
 }
 
-std::vector<double> query_density(const AnalyticField& field, std::span<const Vec3> positions) {
-    std::vector<double> out(positions.size());
-    for (size_t i = 0; i < positions.size(); ++i) {
-        if (!is_finite(positions[i]))
-            throw std::invalid_argument("field: non-finite position at index " + std::to_string(i));
-        out[i] = density_at(field, positions[i]);
+namespace {
+// Batch field query on the device (vmb_field_query); rgbs == nullptr: density only.
+void device_query(const vmb_field& f, std::span<const Vec3> positions, std::vector<double>& sigmas,
+                  std::vector<Vec3>* rgbs) {
+    const size_t n = positions.size();
+    sigmas.resize(n);
+    if (rgbs) rgbs->resize(n);
+    if (!n) {
+        check(vmb_field_query(ctx(), &f, nullptr, 0, 0.0, nullptr, nullptr));  // descriptor checks
+        return;
     }
+    std::lock_guard<std::recursive_mutex> lock(g_mu);
+    Dev dp = upload(reinterpret_cast<const double*>(positions.data()), 3 * n);
+    Dev ds(n * 8), dc(rgbs ? n * 24 : 0);
+    check(vmb_field_query(ctx(), &f, dp.as<double>(), n, 0.0, ds.as<double>(), rgbs ? dc.as<double>() : nullptr));
+    check(vmb_memcpy_d2h(ctx(), sigmas.data(), ds.p, n * 8));
+    if (rgbs) check(vmb_memcpy_d2h(ctx(), rgbs->data(), dc.p, n * 24));
+}
+}  // namespace
+
+std::vector<double> query_density(const AnalyticField& field, std::span<const Vec3> positions) {
+    std::vector<double> out;
+    device_query(to_f(field), positions, out, nullptr);
     return out;
 }
 
-void query_rgb_sigma(const AnalyticField& field, std::span<const Vec3> positions,
-                     std::span<const Vec3> directions, std::vector<Vec3>& rgbs,
-                     std::vector<double>& sigmas) {
-    rgbs.resize(positions.size());
-    sigmas.resize(positions.size());
-    for (size_t i = 0; i < positions.size(); ++i) {
-        if (!is_finite(positions[i]))
-            throw std::invalid_argument("field: non-finite position at index " + std::to_string(i));
-        auto [rgb, s] = rgb_sigma_at(field, positions[i], directions.empty() ? Vec3{} : directions[i]);
-        rgbs[i] = rgb;
-        sigmas[i] = s;
-    }
+void query_rgb_sigma(const AnalyticField& field, std::span<const Vec3> positions, std::span<const Vec3>,
+                     std::vector<Vec3>& rgbs, std::vector<double>& sigmas) {
+    device_query(to_f(field), positions, sigmas, &rgbs);
 }
 
 // ================================================================== occupancy grid
@@ -706,6 +716,298 @@ std::vector<double> render_attribute(const PackedSamples& packed, std::span<cons
     Dev out(packed.n_rays() * dim * 8);
     check(vmb_render_attribute(ctx(), &dv.v, ds.p, dvals.p, dim, out.p, VMB_F64));
     return download<double>(out, packed.n_rays() * dim);
+}
+
+// ================================================================== TrilinearVoxelField
+// fields.cpp:95-262. Host vectors hold the parameters (value semantics); batch
+// queries and the backward upload them and run on the device.
+namespace {
+vmb_field voxel_desc(uint32_t res, const Aabb& box, const double* dens, const double* col) {
+    vmb_field f{};
+    f.kind = VMB_FIELD_VOXEL;
+    for (int a = 0; a < 3; ++a) {
+        f.box_min[a] = box.min[a];
+        f.box_max[a] = box.max[a];
+    }
+    f.vox_resolution = res;
+    f.vox_density = dens;
+    f.vox_color = col;
+    return f;
+}
+
+struct DevVoxel {  // the parameters on the device + the descriptor pointing at them
+    Dev d, c;
+    vmb_field f;
+    explicit DevVoxel(const TrilinearVoxelField& v)
+        : d(upload(v.raw_density())), c(upload(v.raw_color())),
+          f(voxel_desc(v.resolution(), v.box(), d.as<double>(), c.as<double>())) {}
+};
+
+constexpr char kVxfdMagic[4] = {'V', 'X', 'F', 'D'};
+constexpr uint32_t kVxfdVersion = 1;
+
+template <typename T>
+T vget(std::istream& in) {
+    T v;
+    in.read(reinterpret_cast<char*>(&v), sizeof(T));
+    if (!in) throw std::runtime_error("voxel field: truncated stream");
+    return v;
+}
+}  // namespace
+
+TrilinearVoxelField::TrilinearVoxelField(uint32_t resolution, const Aabb& box)
+    : resolution_(resolution), box_(box) {
+    if (resolution < 2) throw std::invalid_argument("voxel field: resolution must be >= 2 vertices per axis");
+    size_t n = size_t(resolution) * resolution * resolution;
+    raw_density_.assign(n, 0.0);
+    raw_color_.assign(3 * n, 0.0);
+}
+
+// Single-point queries evaluate the kernels' own __host__ __device__ stencil.
+double TrilinearVoxelField::density_at(const Vec3& p) const {
+    return vmb::field_density(voxel_desc(resolution_, box_, raw_density_.data(), raw_color_.data()), d3v(p));
+}
+
+std::pair<Vec3, double> TrilinearVoxelField::rgb_sigma_at(const Vec3& p, const Vec3&) const {
+    vmb::D3 rgb;
+    double s = vmb::field_rgb_sigma(voxel_desc(resolution_, box_, raw_density_.data(), raw_color_.data()),
+                                    d3v(p), &rgb);
+    return {v3d(rgb), s};
+}
+
+std::vector<double> TrilinearVoxelField::query_density(std::span<const Vec3> positions) const {
+    std::lock_guard<std::recursive_mutex> lock(g_mu);
+    DevVoxel dv(*this);
+    std::vector<double> out;
+    device_query(dv.f, positions, out, nullptr);
+    return out;
+}
+
+void TrilinearVoxelField::query_rgb_sigma(std::span<const Vec3> positions, std::span<const Vec3>,
+                                          std::vector<Vec3>& rgbs, std::vector<double>& sigmas) const {
+    std::lock_guard<std::recursive_mutex> lock(g_mu);
+    DevVoxel dv(*this);
+    device_query(dv.f, positions, sigmas, &rgbs);
+}
+
+TrilinearVoxelField::ParamGradients TrilinearVoxelField::zero_gradients() const {
+    ParamGradients g;
+    g.d_raw_density.assign(raw_density_.size(), 0.0);
+    g.d_raw_color.assign(raw_color_.size(), 0.0);
+    return g;
+}
+
+void TrilinearVoxelField::backward(std::span<const Vec3> positions, std::span<const Vec3> d_rgbs,
+                                   std::span<const double> d_sigmas, ParamGradients& accum) const {
+    if (d_rgbs.size() != positions.size() || d_sigmas.size() != positions.size())
+        throw std::invalid_argument("voxel field: gradient length mismatch");
+    if (accum.d_raw_density.size() != raw_density_.size() || accum.d_raw_color.size() != raw_color_.size())
+        throw std::invalid_argument("voxel field: gradient buffer size mismatch");
+    const size_t n = positions.size();
+    if (!n) return;
+    std::lock_guard<std::recursive_mutex> lock(g_mu);
+    DevVoxel dv(*this);
+    Dev dp = upload(reinterpret_cast<const double*>(positions.data()), 3 * n);
+    Dev dr = upload(reinterpret_cast<const double*>(d_rgbs.data()), 3 * n);
+    Dev ds = upload(d_sigmas.data(), n);
+    Dev ad = upload(accum.d_raw_density), ac = upload(accum.d_raw_color);
+    check(vmb_voxel_field_backward(ctx(), &dv.f, dp.as<double>(), n, dr.p, ds.p, VMB_F64, ad.as<double>(),
+                                   ac.as<double>(), VMB_GRAD_DETERMINISTIC));
+    check(vmb_memcpy_d2h(ctx(), accum.d_raw_density.data(), ad.p, ad.bytes));
+    check(vmb_memcpy_d2h(ctx(), accum.d_raw_color.data(), ac.p, ac.bytes));
+}
+
+void TrilinearVoxelField::save(std::ostream& out) const {  // fields.cpp:224-233
+    out.write(kVxfdMagic, 4);
+    put(out, kVxfdVersion);
+    put(out, resolution_);
+    for (int i = 0; i < 3; ++i) put(out, box_.min[i]);
+    for (int i = 0; i < 3; ++i) put(out, box_.max[i]);
+    for (double d : raw_density_) put(out, float(d));
+    for (double d : raw_color_) put(out, float(d));
+    if (!out) throw std::runtime_error("voxel field: write failed");
+}
+
+TrilinearVoxelField TrilinearVoxelField::load(std::istream& in) {  // fields.cpp:235-250
+    char magic[4];
+    in.read(magic, 4);
+    if (!in || std::memcmp(magic, kVxfdMagic, 4) != 0) throw std::runtime_error("voxel field: bad magic");
+    if (vget<uint32_t>(in) != kVxfdVersion) throw std::runtime_error("voxel field: unsupported version");
+    uint32_t resolution = vget<uint32_t>(in);
+    Vec3 lo, hi;
+    for (int i = 0; i < 3; ++i) lo[i] = vget<double>(in);
+    for (int i = 0; i < 3; ++i) hi[i] = vget<double>(in);
+    TrilinearVoxelField field(resolution, Aabb(lo, hi));
+    for (double& d : field.raw_density_) d = vget<float>(in);
+    for (double& d : field.raw_color_) d = vget<float>(in);
+    return field;
+}
+
+void TrilinearVoxelField::save_file(const std::string& path) const {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw std::runtime_error("voxel field: cannot open " + path);
+    save(out);
+}
+
+TrilinearVoxelField TrilinearVoxelField::load_file(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error("voxel field: cannot open " + path);
+    return load(in);
+}
+
+// fields.cpp:264-271
+double TimeConditionedField::density_at(const Vec3& p, double t) const {
+    return voxmarch::density_at(base, p - velocity * t);
+}
+std::pair<Vec3, double> TimeConditionedField::rgb_sigma_at(const Vec3& p, const Vec3& dir, double t) const {
+    return voxmarch::rgb_sigma_at(base, p - velocity * t, dir);
+}
+
+// ================================================================== AdamOptimizer (fields.cpp:273-292)
+AdamOptimizer::AdamOptimizer(size_t n_params, double lr, double beta1, double beta2, double eps)
+    : lr_(lr), beta1_(beta1), beta2_(beta2), eps_(eps), m_(n_params, 0.0), v_(n_params, 0.0) {}
+
+void AdamOptimizer::step(std::span<double> params, std::span<const double> grads) {
+    if (params.size() != m_.size() || grads.size() != m_.size())
+        throw std::invalid_argument("adam: parameter/gradient size mismatch");
+    const size_t n = params.size();
+    std::lock_guard<std::recursive_mutex> lock(g_mu);
+    Dev dp = upload(params.data(), n), dg = upload(grads.data(), n), dm = upload(m_), dv = upload(v_);
+    check(vmb_adam_step(ctx(), n, dp.as<double>(), dg.as<double>(), dm.as<double>(), dv.as<double>(), lr_, beta1_,
+                        beta2_, eps_, t_ + 1));
+    ++t_;  // only after the gradients passed the finiteness check, as the reference
+    if (n) {
+        check(vmb_memcpy_d2h(ctx(), params.data(), dp.p, n * 8));
+        check(vmb_memcpy_d2h(ctx(), m_.data(), dm.p, n * 8));
+        check(vmb_memcpy_d2h(ctx(), v_.data(), dv.p, n * 8));
+    }
+}
+
+// ================================================================== cameras (scene_camera.cpp)
+namespace {
+vmb_camera to_cam(const PinholeCamera& c) {
+    vmb_camera o{};
+    for (int i = 0; i < 9; ++i) o.rotation[i] = c.rotation.m[i];
+    for (int a = 0; a < 3; ++a) o.position[a] = c.position[a];
+    o.focal = c.focal;
+    o.width = c.width;
+    o.height = c.height;
+    return o;
+}
+PinholeCamera from_cam(const vmb_camera& c) {
+    PinholeCamera o;
+    for (int i = 0; i < 9; ++i) o.rotation.m[i] = c.rotation[i];
+    for (int a = 0; a < 3; ++a) o.position[a] = c.position[a];
+    o.focal = c.focal;
+    o.width = c.width;
+    o.height = c.height;
+    return o;
+}
+}  // namespace
+
+void validate_camera(const PinholeCamera& camera) {
+    vmb_camera c = to_cam(camera);
+    check(vmb_camera_validate(&c));
+}
+
+PinholeCamera look_at(const Vec3& eye, const Vec3& target, const Vec3& up, double focal, int width, int height) {
+    const double e[3] = {eye.x, eye.y, eye.z}, t[3] = {target.x, target.y, target.z}, u[3] = {up.x, up.y, up.z};
+    vmb_camera c{};
+    check(vmb_camera_look_at(e, t, u, focal, width, height, &c));
+    return from_cam(c);
+}
+
+RayBatch generate_rays(const PinholeCamera& camera, double near, double far) {
+    vmb_camera c = to_cam(camera);
+    check(vmb_camera_validate(&c));
+    const size_t n = size_t(camera.width) * size_t(camera.height);
+    std::lock_guard<std::recursive_mutex> lock(g_mu);
+    Dev o(n * 24), d(n * 24);
+    vmb_rays r{};
+    check(vmb_generate_rays(ctx(), &c, near, far, VMB_F64, o.p, d.p, &r));
+    RayBatch b;
+    b.origins.resize(n);
+    b.directions.resize(n);
+    if (n) {
+        check(vmb_memcpy_d2h(ctx(), b.origins.data(), o.p, n * 24));
+        check(vmb_memcpy_d2h(ctx(), b.directions.data(), d.p, n * 24));
+    }
+    b.near = near;
+    b.far = far;
+    return b;
+}
+
+// {"focal": f, "width": w, "height": h, "pose": [12 numbers, row-major 3x4]}
+// (scene_camera.cpp:66-99). A small reader for exactly this schema.
+namespace {
+const char* skip_ws(const char* p) {
+    while (*p == ' ' || *p == '\n' || *p == '\r' || *p == '\t') ++p;
+    return p;
+}
+double json_number(const std::string& text, const std::string& key) {
+    size_t k = text.find("\"" + key + "\"");
+    if (k == std::string::npos) throw std::runtime_error("camera: missing key " + key);
+    const char* p = skip_ws(text.c_str() + k + key.size() + 2);
+    if (*p != ':') throw std::runtime_error("camera: malformed json");
+    char* end = nullptr;
+    double v = std::strtod(skip_ws(p + 1), &end);
+    if (end == skip_ws(p + 1)) throw std::runtime_error("camera: malformed json");
+    return v;
+}
+std::vector<double> json_array(const std::string& text, const std::string& key) {
+    size_t k = text.find("\"" + key + "\"");
+    if (k == std::string::npos) throw std::runtime_error("camera: missing key " + key);
+    const char* p = skip_ws(text.c_str() + k + key.size() + 2);
+    if (*p != ':') throw std::runtime_error("camera: malformed json");
+    p = skip_ws(p + 1);
+    if (*p != '[') throw std::runtime_error("camera: malformed json");
+    std::vector<double> out;
+    p = skip_ws(p + 1);
+    while (*p && *p != ']') {
+        char* end = nullptr;
+        out.push_back(std::strtod(p, &end));
+        if (end == p) throw std::runtime_error("camera: malformed json");
+        p = skip_ws(end);
+        if (*p == ',') p = skip_ws(p + 1);
+    }
+    return out;
+}
+}  // namespace
+
+PinholeCamera load_camera_json(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw std::runtime_error("camera: cannot open " + path);
+    std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    PinholeCamera camera;
+    camera.focal = json_number(text, "focal");
+    camera.width = int(json_number(text, "width"));
+    camera.height = int(json_number(text, "height"));
+    std::vector<double> pose = json_array(text, "pose");
+    if (pose.size() != 12) throw std::runtime_error("camera: pose must have 12 numbers");
+    for (int row = 0; row < 3; ++row) {
+        for (int col = 0; col < 3; ++col) camera.rotation.m[3 * row + col] = pose[4 * row + col];
+        camera.position[row] = pose[4 * row + 3];
+    }
+    validate_camera(camera);
+    return camera;
+}
+
+void save_camera_json(const PinholeCamera& camera, const std::string& path) {
+    validate_camera(camera);
+    std::ofstream out(path);
+    if (!out) throw std::runtime_error("camera: cannot open " + path);
+    char buf[64];
+    auto num = [&](double v) {
+        std::snprintf(buf, sizeof buf, "%.17g", v);
+        return std::string(buf);
+    };
+    out << "{\n  \"focal\": " << num(camera.focal) << ",\n  \"height\": " << camera.height << ",\n  \"pose\": [";
+    for (int row = 0; row < 3; ++row)
+        for (int col = 0; col < 4; ++col) {
+            double v = col < 3 ? camera.rotation.m[3 * row + col] : camera.position[row];
+            out << (row || col ? ",\n    " : "\n    ") << num(v);
+        }
+    out << "\n  ],\n  \"width\": " << camera.width << "\n}\n";
 }
 
 }  // namespace voxmarch

@@ -230,6 +230,30 @@ int vox_backward(vmb_ctx* ctx, const vmb_field& f, const Positions& pos, uint64_
     return e == cudaSuccess ? VMB_OK : cuda_fail(e, "voxel field backward");
 }
 
+// AdamOptimizer::step (fields.cpp:282-292): the reference's expressions per
+// element; bias corrections come from the host (std::pow, as the reference).
+__global__ void k_adam_check(const double* __restrict__ g, uint64_t n, DevError* err) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        if (!isfinite(g[i])) atomicMin(&err->key, (unsigned long long)i);
+}
+
+__global__ void k_adam(double* __restrict__ p, const double* __restrict__ g, double* __restrict__ m,
+                       double* __restrict__ v, uint64_t n, double lr, double b1, double b2, double eps,
+                       double bias1, double bias2) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const double gi = g[i];
+        const double mi = b1 * m[i] + (1.0 - b1) * gi;
+        const double vi = b2 * v[i] + (1.0 - b2) * gi * gi;
+        m[i] = mi;
+        v[i] = vi;
+        const double m_hat = mi / bias1;
+        const double v_hat = vi / bias2;
+        p[i] -= lr * m_hat / (sqrt(v_hat) + eps);
+    }
+}
+
 Positions sample_positions(const vmb_rays* rays, const uint32_t* idx, const double* ts, const double* te,
                            double time) {
     return Positions{nullptr, rays->d_origins, rays->d_directions, rays->dtype, idx, ts, te, time};
@@ -276,6 +300,25 @@ int vmb_voxel_field_backward_samples(vmb_ctx* ctx, const vmb_field* f, const vmb
                             static_cast<const float*>(d_sigma_grads), d_accum_density, d_accum_color, mode);
     return vox_backward(ctx, *f, pos, n_samples, static_cast<const double*>(d_rgb_grads),
                         static_cast<const double*>(d_sigma_grads), d_accum_density, d_accum_color, mode);
+}
+
+int vmb_adam_step(vmb_ctx* ctx, uint64_t n, double* d_params, const double* d_grads, double* d_m, double* d_v,
+                  double lr, double beta1, double beta2, double eps, uint64_t step) {
+    if (!n) return VMB_OK;
+    int rc = reset_error(ctx);
+    if (rc) return rc;
+    const int blocks = grid_blocks(ctx, n, 256, 8);
+    k_adam_check<<<blocks, 256, 0, ctx->stream>>>(d_grads, n, ctx->d_err);
+    DevError err;
+    rc = read_error(ctx, &err);
+    if (rc) return rc;
+    if (err.key != ~0ull)
+        return fail(VMB_RUNTIME, "adam: non-finite gradient at index " + std::to_string(err.key));
+    const double bias1 = 1.0 - std::pow(beta1, double(step));
+    const double bias2 = 1.0 - std::pow(beta2, double(step));
+    k_adam<<<blocks, 256, 0, ctx->stream>>>(d_params, d_grads, d_m, d_v, n, lr, beta1, beta2, eps, bias1, bias2);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? VMB_OK : cuda_fail(e, "adam");
 }
 
 }  // extern "C"

@@ -4,7 +4,7 @@
 * GPU: build/vm_cpp_tests (this repo's C++ tests of the facade) and
   build/ref_unit_tests — the REFERENCE's own hot-path unit tests
   (proj/tests/unit/test_{core_types,contraction,occupancy_grid,ray_marching,
-  rendering}.cpp, compiled unchanged against include/voxmarch/ by
+  rendering,fields,scene_camera}.cpp, compiled unchanged against include/voxmarch/ by
   tests/ref_unit/Makefile) — must pass on the B200.
 """
 import os
@@ -25,7 +25,10 @@ API = ["voxmarch::march(voxmarch::RayBatch const&, voxmarch::OccupancyGrid const
        "voxmarch::OccupancyGrid::update(", "voxmarch::OccupancyGrid::update_over_time(",
        "voxmarch::OccupancyGrid::seed_occupancy(", "voxmarch::OccupancyGrid::save(",
        "voxmarch::OccupancyGrid::load(", "voxmarch::OccupancyGrid::occupied_fraction(",
-       "voxmarch::OccupancyGrid::threshold_density("]
+       "voxmarch::OccupancyGrid::threshold_density(", "voxmarch::TrilinearVoxelField::backward(",
+       "voxmarch::TrilinearVoxelField::query_rgb_sigma(", "voxmarch::TrilinearVoxelField::load(",
+       "voxmarch::AdamOptimizer::step(", "voxmarch::generate_rays(", "voxmarch::look_at(",
+       "voxmarch::load_camera_json("]
 
 
 def test_facade_exports_reference_api():
