@@ -304,6 +304,24 @@ int vmb_comm_init(vmb_ctx* ctx, const void* h_id128, int nranks, int rank);
 int vmb_comm_destroy(vmb_ctx* ctx);
 /* In-place max all-reduce of n f64 (IEEE order == u64 bit order for values >= 0). */
 int vmb_comm_allreduce_max_f64(vmb_ctx* ctx, double* d_buf, uint64_t n);
+/* In-place sum all-reduce of n f64 (data-parallel parameter gradients). */
+int vmb_comm_allreduce_sum_f64(vmb_ctx* ctx, double* d_buf, uint64_t n);
+
+/* ------------------------------------------------------------------ training step helpers
+ * (tools/voxmarch.cpp cmd_train, :460-498 — the reference's trainer, outside its
+ * library; the B200 framework provides its per-ray pieces on the device.)
+ * Photometric MSE against a white background: err = color + (1 - opacity) - target;
+ * loss = sum |err|^2 / (3n); d_color = err * 2/(3n); d_opacity = -2/(3n) * sum(err);
+ * d_depth = 0. color/opacity/d_* in dtype, targets [n][3] in dtype; *h_loss gets
+ * the loss (fp64, fixed-order block reduction). */
+int vmb_loss_mse_background(vmb_ctx* ctx, const void* d_color, const void* d_opacity, const void* d_targets,
+                            uint64_t n, int dtype, void* d_dcolor, void* d_dopacity, void* d_ddepth,
+                            double* h_loss);
+/* Minibatch gather: out[i] = pool[idx[i]] for origins, directions (3 x dtype) and
+ * targets (3 x dtype) — one kernel. */
+int vmb_gather_rays(vmb_ctx* ctx, const void* d_pool_origins, const void* d_pool_dirs,
+                    const void* d_pool_targets, const uint32_t* d_idx, uint64_t n, int dtype,
+                    void* d_origins, void* d_dirs, void* d_targets);
 
 #ifdef __cplusplus
 }

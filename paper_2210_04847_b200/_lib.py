@@ -163,6 +163,9 @@ SIGNATURES = {
     "vmb_voxel_field_backward_samples": (I32, [VP, P(Field), P(Rays), VP, VP, VP, U64, D, VP, VP, I32, VP,
                                                VP, I32]),
     "vmb_adam_step": (I32, [VP, U64, VP, VP, VP, VP, D, D, D, D, U64]),
+    "vmb_comm_allreduce_sum_f64": (I32, [VP, VP, U64]),
+    "vmb_loss_mse_background": (I32, [VP, VP, VP, VP, U64, I32, VP, VP, VP, P(D)]),
+    "vmb_gather_rays": (I32, [VP, VP, VP, VP, VP, U64, I32, VP, VP, VP]),
     "vmb_camera_validate": (I32, [P(Camera)]),
     "vmb_camera_look_at": (I32, [P(C.c_double), P(C.c_double), P(C.c_double), C.c_double, I32, I32,
                                  P(Camera)]),

@@ -1,5 +1,6 @@
-// comm.cpp — the single collective of the path: ncclAllReduce(max) of the grid's
-// probe densities at each occupancy-grid update.
+// comm.cpp — the collectives of the path: ncclAllReduce(max) of the grid's probe
+// densities at each occupancy-grid update, and ncclAllReduce(sum)
+// of the voxel-field parameter gradients in data-parallel training (§8f rank 4).
 //
 // NCCL is resolved at run time with dlopen("libnccl.so.2") so the library loads
 // (and the single-GPU path runs) on machines without NCCL. The all-reduce runs on
@@ -102,6 +103,15 @@ int vmb_comm_allreduce_max_f64(vmb_ctx* ctx, double* buf, uint64_t count) {
     // u64 bit patterns: order-identical to f64 for non-negative values, and max
     // over integers is exact (no NaN / signed-zero corner cases).
     ncclResult_t r = n.all_reduce(buf, buf, count, ncclUint64, ncclMax,
+                                  static_cast<ncclComm_t>(ctx->nccl_comm), ctx->stream);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
+    return VMB_OK;
+}
+
+int vmb_comm_allreduce_sum_f64(vmb_ctx* ctx, double* buf, uint64_t count) {
+    if (!ctx->nccl_comm || ctx->nranks == 1) return VMB_OK;
+    Nccl& n = nccl();
+    ncclResult_t r = n.all_reduce(buf, buf, count, ncclFloat64, ncclSum,
                                   static_cast<ncclComm_t>(ctx->nccl_comm), ctx->stream);
     if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
     return VMB_OK;
