@@ -254,7 +254,7 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------- e2e
-def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev_out, total_rays):
+def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev_out, total_rays, cam=None):
     """The same step through the C ABI from HOST memory: every step copies its rays and
     upstream gradients host->device and reads the rendered color/opacity/depth back.
 
@@ -262,7 +262,11 @@ def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev
     `--e2e-streams` contexts (one CUDA stream each, one host thread each; the ctypes
     calls release the GIL), so one chunk's PCIe copies overlap another chunk's
     kernels. Timed with CUDA events on context 0, which waits for every other
-    context at the end (vmb_ctx_wait); the others wait for its start event."""
+    context at the end (vmb_ctx_wait); the others wait for its start event.
+
+    With `cam` (a vmb_camera) the rays are not copied: each chunk generates its own
+    pixels' rays on the device (vmb_generate_rays_range, scene_camera.cpp:46-63), so
+    only the upstream gradients cross PCIe."""
     import ctypes as C
     from paper_2210_04847_b200._lib import VMB_F32, Rays, check
     L = dev.lib
@@ -272,6 +276,7 @@ def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev
     cmax = max(e - b for b, e in bounds)
     host_in = [o32, d32] + list(ups)            # per-ray: 12, 12, 12, 4, 4 bytes
     widths = [3, 3, 3, 1, 1]
+    first_in = 2 if cam is not None else 0      # camera mode: rays made on the device
     pinned = []
     for arr in host_in:
         p = C.c_void_p()
@@ -297,9 +302,12 @@ def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev
     def run_chunk(ci, b, e):
         cx, bf = ctxs[ci], bufs[ci]
         n = e - b
-        for arr, p, w in zip(bf["ins"], pinned, widths):
+        for arr, p, w in list(zip(bf["ins"], pinned, widths))[first_in:]:
             check(L.vmb_memcpy_h2d(cx.h, arr.ptr, p.value + b * w * 4, n * w * 4))
         rays = Rays(bf["ins"][0].ptr, bf["ins"][1].ptr, VMB_F32, 0, n, 0.2, 1.0)
+        if cam is not None:
+            check(L.vmb_generate_rays_range(cx.h, C.byref(cam), 0.2, 1.0, VMB_F32, b, n, bf["ins"][0].ptr,
+                                            bf["ins"][1].ptr, C.byref(rays)))
         pk = bf["packed"]
         api.march_render_device(cx, grid, rays, field, cfg, pk, bf["rgb"], bf["sig"], *bf["outs"])
         api.render_backward_device(cx, pk, bf["rgb"], bf["sig"], *bf["ins"][2:], bf["grgb"], bf["gsig"])
@@ -348,6 +356,12 @@ def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev
         L.vmb_host_free(p)
     for cx in ctxs[1:]:
         cx.sync()
+    if cam is not None:
+        return {"value": total_rays / (e2e_ms * 1e-3), "unit": "rays/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": int(sum(a.nbytes for a in host_in[2:])), "d2h_bytes_per_step": N * 20,
+                "streams": n_ctx, "chunks": n_chunk, "matches_resident_outputs": same,
+                "path": "C ABI: camera in, rays generated per chunk on the device (vmb_generate_rays_range), "
+                        "pinned host upstream grads in, color/opacity/depth out"}
     return {"value": total_rays / (e2e_ms * 1e-3), "unit": "rays/s", "ms_per_step": e2e_ms,
             "h2d_bytes_per_step": int(sum(a.nbytes for a in host_in)), "d2h_bytes_per_step": N * 20,
             "streams": n_ctx, "chunks": n_chunk, "matches_resident_outputs": same,
@@ -488,11 +502,11 @@ def main():
     dom_bytes = {"march": bytes_march, "shade": 20 * S + 24 * S + 16 * S,
                  "render_forward": bytes_fwd, "render_backward": bytes_bwd}[dom]
     achieved = dom_bytes / (phase.get(dom, ms_step) * 1e-3) / 1e9
-    api = {"march": {"forward": "vmb_march_render_field", "shade": "vmb_march_field_shaded",
+    api_name = {"march": {"forward": "vmb_march_render_field", "shade": "vmb_march_field_shaded",
                      "none": "vmb_march_field"}[args.fusion],
            "shade": "vmb_shade_field", "render_forward": "vmb_render_forward",
            "render_backward": "vmb_render_backward"}[dom]
-    roof = {"bound": "hbm", "kernel": f"{dom} ({api}: {' + '.join(PHASE_KERNELS[dom])})",
+    roof = {"bound": "hbm", "kernel": f"{dom} ({api_name}: {' + '.join(PHASE_KERNELS[dom])})",
             "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic_of(dom), "peak_source": peak_src,
             "algorithmic_bytes": dom_bytes,
@@ -506,6 +520,16 @@ def main():
                            [x.astype(np.float32) for x in (dc, do, dd)], cap, (col, op, dep), total_rays)
     except Exception as ex:  # pragma: no cover
         e2e = {"error": repr(ex)}
+    try:  # the same step with the benchmark camera's rays generated on the device
+        ang = 2.0 * math.pi * dist.rank / max(dist.world, 1)
+        rad = 0.6 * math.sqrt(3.0) / math.sqrt(3.0)  # orbit_camera's radius, as workload.orbit_rays
+        eye = [0.5 + rad * math.cos(ang) * math.cos(0.4), 0.5 + rad * math.sin(ang) * math.cos(0.4),
+               0.5 + rad * math.sin(0.4)]
+        cam = api.look_at(eye, (0.5, 0.5, 0.5), (0, 0, 1), 1.1 * args.width, args.width, args.width)
+        e2e_cam = e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32,
+                               [x.astype(np.float32) for x in (dc, do, dd)], cap, (col, op, dep), total_rays, cam)
+    except Exception as ex:  # pragma: no cover
+        e2e_cam = {"error": repr(ex)}
 
     cpu = None
     if dist.rank == 0 and dist.world == 1 and args.cpu_baseline:
@@ -529,7 +553,7 @@ def main():
                            "l2": "inputs larger than L2 (~1 GB working set per step)",
                            "parallelism": f"dp{dist.world} (rays sharded, grid replicated)"},
                 "phases_ms": phase, "grid_update_ms": grid_update_ms,
-                "roofline": roof, "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
+                "roofline": roof, "e2e": e2e, "e2e_camera": e2e_cam, "cpu_baseline": cpu, "clocks": clk,
                 "gpu_launches": (KERNELS_PER_STEP - {"none": 0, "shade": 1, "forward": 2}[args.fusion]) * args.steps}
         print(json.dumps(line), flush=True)
     if dist.world > 1:

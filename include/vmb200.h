@@ -112,6 +112,11 @@ int vmb_camera_look_at(const double eye[3], const double target[3], const double
                        int32_t width, int32_t height, vmb_camera* out);
 int vmb_generate_rays(vmb_ctx* ctx, const vmb_camera* camera, double near_plane, double far_plane,
                       int dtype, void* d_origins, void* d_directions, vmb_rays* out_rays);
+/* Rays of pixels [first_ray, first_ray + n_rays) (row-major) only: a chunk of the
+ * image, for pipelined steps. */
+int vmb_generate_rays_range(vmb_ctx* ctx, const vmb_camera* camera, double near_plane, double far_plane,
+                            int dtype, uint64_t first_ray, uint64_t n_rays, void* d_origins, void* d_directions,
+                            vmb_rays* out_rays);
 
 /* ------------------------------------------------------------------ fields
  * query_density / query_rgb_sigma for any field kind (fields.cpp:75-93 and the

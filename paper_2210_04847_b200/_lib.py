@@ -170,6 +170,7 @@ SIGNATURES = {
     "vmb_camera_look_at": (I32, [P(C.c_double), P(C.c_double), P(C.c_double), C.c_double, I32, I32,
                                  P(Camera)]),
     "vmb_generate_rays": (I32, [VP, P(Camera), C.c_double, C.c_double, I32, VP, VP, P(Rays)]),
+    "vmb_generate_rays_range": (I32, [VP, P(Camera), C.c_double, C.c_double, I32, U64, U64, VP, VP, P(Rays)]),
     "vmb_uniform_step_count": (U64, [D, D, D]),
     "vmb_pack": (I32, [VP, VP, U64, VP, VP, U64, P(U64)]),
     "vmb_validate": (I32, [VP, P(PackedView), VP, U64, U64, U64, P(I32)]),

@@ -23,13 +23,15 @@ VM_HD D3 div3(D3 a, double s) { return d3(a.x / s, a.y / s, a.z / s); }
 VM_HD D3 normalize3(D3 a) { return div3(a, norm(a)); }  // math.hpp:31
 
 template <typename T>
-__global__ void k_generate_rays(vmb_camera cam, uint64_t n, T* __restrict__ o, T* __restrict__ d) {
+__global__ void k_generate_rays(vmb_camera cam, uint64_t first, uint64_t n, T* __restrict__ o,
+                                T* __restrict__ d) {
     const double cx = 0.5 * cam.width;
     const double cy = 0.5 * cam.height;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
-        const int row = int(i / uint64_t(cam.width));
-        const int col = int(i - uint64_t(row) * uint64_t(cam.width));
+        const uint64_t px = first + i;  // row-major pixel index
+        const int row = int(px / uint64_t(cam.width));
+        const int col = int(px - uint64_t(row) * uint64_t(cam.width));
         // pixel centres; image row 0 is the top of the frame (scene_camera.cpp:56-58)
         const D3 dir_cam = d3((double(col) + 0.5 - cx) / cam.focal, (cy - (double(row) + 0.5)) / cam.focal, -1.0);
         const D3 w = normalize3(mat_vec(cam.rotation, dir_cam));
@@ -88,8 +90,9 @@ int vmb_camera_look_at(const double eye[3], const double target[3], const double
     return VMB_OK;
 }
 
-int vmb_generate_rays(vmb_ctx* ctx, const vmb_camera* camera, double near_plane, double far_plane, int dtype,
-                      void* d_origins, void* d_directions, vmb_rays* out_rays) {
+int vmb_generate_rays_range(vmb_ctx* ctx, const vmb_camera* camera, double near_plane, double far_plane,
+                            int dtype, uint64_t first_ray, uint64_t n_rays, void* d_origins, void* d_directions,
+                            vmb_rays* out_rays) {
     int rc = vmb_camera_validate(camera);
     if (rc) return rc;
     // RayBatch::create (core_types.cpp:13-20). Directions are unit by construction
@@ -101,15 +104,18 @@ int vmb_generate_rays(vmb_ctx* ctx, const vmb_camera* camera, double near_plane,
           std::isfinite(camera->position[2])))
         return fail(VMB_INVALID_ARGUMENT, "ray batch: non-finite ray at index 0");
     if (dtype != VMB_F32 && dtype != VMB_F64) return fail(VMB_INVALID_ARGUMENT, "generate_rays: dtype");
-    const uint64_t n = uint64_t(camera->width) * uint64_t(camera->height);
+    const uint64_t total = uint64_t(camera->width) * uint64_t(camera->height);
+    if (first_ray > total || n_rays > total - first_ray)
+        return fail(VMB_INVALID_ARGUMENT, "generate_rays: ray range outside the image");
+    const uint64_t n = n_rays;
     if (n) {
         const int blocks = grid_blocks(ctx, n, 256, 8);
         if (dtype == VMB_F32)
-            k_generate_rays<float><<<blocks, 256, 0, ctx->stream>>>(*camera, n, static_cast<float*>(d_origins),
-                                                                     static_cast<float*>(d_directions));
+            k_generate_rays<float><<<blocks, 256, 0, ctx->stream>>>(
+                *camera, first_ray, n, static_cast<float*>(d_origins), static_cast<float*>(d_directions));
         else
             k_generate_rays<double><<<blocks, 256, 0, ctx->stream>>>(
-                *camera, n, static_cast<double*>(d_origins), static_cast<double*>(d_directions));
+                *camera, first_ray, n, static_cast<double*>(d_origins), static_cast<double*>(d_directions));
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "generate_rays");
     }
@@ -117,6 +123,15 @@ int vmb_generate_rays(vmb_ctx* ctx, const vmb_camera* camera, double near_plane,
         *out_rays = vmb_rays{d_origins, d_directions, int32_t(dtype), 0, n, near_plane, far_plane};
     }
     return VMB_OK;
+}
+
+int vmb_generate_rays(vmb_ctx* ctx, const vmb_camera* camera, double near_plane, double far_plane, int dtype,
+                      void* d_origins, void* d_directions, vmb_rays* out_rays) {
+    const uint64_t n = camera && camera->width > 0 && camera->height > 0
+                           ? uint64_t(camera->width) * uint64_t(camera->height)
+                           : 0;
+    return vmb_generate_rays_range(ctx, camera, near_plane, far_plane, dtype, 0, n, d_origins, d_directions,
+                                   out_rays);
 }
 
 }  // extern "C"
