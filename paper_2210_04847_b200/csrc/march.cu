@@ -62,6 +62,7 @@ struct MarchParams {
     bool fast;            // fp32 DDA + filtered fp32 cell test (walk_fast)
     bool sphere_fast;     // SolidSphere field: filtered fp32 density decision
     float sph_c[3], sph_r, sph_r2, sph_cmax;
+    double sph_sig32, sph_rgb32[3];  // SolidSphere sigma / rgb rounded through fp32 (fused forward)
     float step_f, m0_f, inv_step_f, near_f, far_f, Mf;
     bool full;            // walk to the end (stats / candidate mode), ignore the T cut
     bool filter;          // apply inline density + alpha floor + T cut
@@ -104,18 +105,20 @@ struct Sink {
     // sigma/rgb are rounded to the attribute dtype; alpha is reused when the
     // rounding is exact (same expression, same operands).
     __device__ __forceinline__ void composite(double sigma, D3 c, double t0, double t1, double alpha) {
-        const double sg = at32 ? double(float(sigma)) : sigma;
+        if (at32)
+            composite_rounded(sigma, double(float(sigma)), d3(double(float(c.x)), double(float(c.y)), double(float(c.z))),
+                              t0, t1, alpha);
+        else
+            composite_rounded(sigma, sigma, c, t0, t1, alpha);
+    }
+    // sg / c already rounded to the attribute dtype (constant-field fast path)
+    __device__ __forceinline__ void composite_rounded(double sigma, double sg, D3 c, double t0, double t1,
+                                                      double alpha) {
         const double a = sg == sigma ? alpha : 1.0 - exp(-sg * (t1 - t0));
         const double w = Tf * a;
-        if (at32) {
-            cr = cr + double(float(c.x)) * w;
-            cg = cg + double(float(c.y)) * w;
-            cb = cb + double(float(c.z)) * w;
-        } else {
-            cr = cr + c.x * w;
-            cg = cg + c.y * w;
-            cb = cb + c.z * w;
-        }
+        cr = cr + c.x * w;
+        cg = cg + c.y * w;
+        cb = cb + c.z * w;
         op += w;
         dep += w * 0.5 * (t0 + t1);
         Tf *= 1.0 - a;
@@ -125,7 +128,8 @@ struct Sink {
 template <int MODE>
 __device__ __forceinline__ bool filter_sample(const MarchParams& P, Sink& s, uint64_t i, uint32_t ci,
                                               double t0, double t1, double sigma, DevError* err,
-                                              D3 rgb = D3{0.0, 0.0, 0.0});
+                                              D3 rgb = D3{0.0, 0.0, 0.0}, bool rounded = false,
+                                              double sg_r = 0.0);
 
 // Handles one grid-passing candidate. Mirrors ray_marching.cpp:78,111-137.
 template <int MODE>
@@ -160,13 +164,15 @@ __device__ __forceinline__ bool on_candidate(const MarchParams& P, Sink& s, uint
 template <int MODE>
 __device__ __forceinline__ bool filter_sample(const MarchParams& P, Sink& s, uint64_t i, uint32_t ci,
                                               double t0, double t1, double sigma, DevError* err,
-                                              D3 rgb) {
+                                              D3 rgb, bool rounded, double sg_r) {
     if (!isfinite(sigma) || sigma < 0.0) {
         int kind = !isfinite(sigma) ? ERR_NONFINITE_SIGMA : ERR_NEGATIVE_SIGMA;
         atomicMin(&err->key, march_err_key(s.ray, ci, kind));
         s.filtering = false;
         return false;
     }
+    // sigma == 0: alpha = 1 - exp(-0 * delta) = 0 exactly, never above a floor >= 0
+    if (sigma == 0.0 && P.thr >= 0.0) return true;
     double delta = t1 - t0;
     double alpha = 1.0 - exp(-sigma * delta);
     if (alpha <= P.thr) return true;
@@ -179,7 +185,12 @@ __device__ __forceinline__ bool filter_sample(const MarchParams& P, Sink& s, uin
         }
     }
     if (mbase(MODE) >= BUFFER && s.n_kept < s.buf_cap) s.buf[s.n_kept * s.buf_stride] = uint32_t(i);
-    if (mbase(MODE) == BUFFER_FWD) s.composite(sigma, rgb, t0, t1, alpha);
+    if (mbase(MODE) == BUFFER_FWD) {
+        if (rounded)
+            s.composite_rounded(sigma, sg_r, rgb, t0, t1, alpha);
+        else
+            s.composite(sigma, rgb, t0, t1, alpha);
+    }
     s.n_kept++;
     s.T *= 1.0 - alpha;
     if (s.T < P.eps) {
@@ -415,12 +426,14 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
     while (j <= jend) {
         const float m = fmaf(float(j), P.step_f, P.m0_f);
         const float u0 = fmaf(B[0], m, A[0]), u1 = fmaf(B[1], m, A[1]), u2 = fmaf(B[2], m, A[2]);
-        const float f0 = floorf(u0), f1 = floorf(u1), f2 = floorf(u2);
-        const bool inside = f0 >= 0.0f && f0 < Rf && f1 >= 0.0f && f1 < Rf && f2 >= 0.0f && f2 < Rf;
+        // |u| stays within a few cells of the domain here (the loop range is the
+        // clipped lattice), so the float->int floor is exact and in range
+        const int i0 = __float2int_rd(u0), i1 = __float2int_rd(u1), i2 = __float2int_rd(u2);
+        const bool inside = unsigned(i0) < unsigned(Ri) && unsigned(i1) < unsigned(Ri) && unsigned(i2) < unsigned(Ri);
         int D = kDistCap;
         uint32_t cell = 0;
         if (inside) {
-            cell = uint32_t(f0) + P.res * (uint32_t(f1) + P.res * uint32_t(f2));
+            cell = uint32_t(i0) + P.res * (uint32_t(i1) + P.res * uint32_t(i2));
             D = __ldg(P.dist + cell);
             if (D >= 2 && j != last) {
                 const float Lj = float(D) - jump_margin;
@@ -430,7 +443,7 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
         }
         bool exact = !fast_ok || j == last;
         if (!exact) {
-            const float r0 = u0 - f0, r1 = u1 - f1, r2 = u2 - f2;
+            const float r0 = u0 - float(i0), r1 = u1 - float(i1), r2 = u2 - float(i2);
             exact = r0 < E || r0 > 1.0f - E || r1 < E || r1 > 1.0f - E || r2 < E || r2 > 1.0f - E;
         }
         if (exact) {
@@ -457,9 +470,13 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
                 if (s.n_cand >= P.max_cand) return;  // candidate cap
                 uint32_t ci = s.n_cand++;
                 const bool in = d2 < P.sph_r2;
-                double sigma = in ? P.f.sigma : 0.0;
-                D3 rgb = in ? d3(P.f.rgb[0], P.f.rgb[1], P.f.rgb[2]) : d3(0.0, 0.0, 0.0);
-                if (!filter_sample<MODE>(P, s, uint64_t(j), ci, t0, t1, sigma, err, rgb)) return;
+                const double sigma = in ? P.f.sigma : 0.0;
+                // attribute-dtype roundings precomputed on the host (k_shade's AT(rgb), AT(sigma))
+                const D3 rgb = !in ? d3(0.0, 0.0, 0.0)
+                                   : s.at32 ? d3(P.sph_rgb32[0], P.sph_rgb32[1], P.sph_rgb32[2])
+                                            : d3(P.f.rgb[0], P.f.rgb[1], P.f.rgb[2]);
+                const double sg = !in ? 0.0 : s.at32 ? P.sph_sig32 : P.f.sigma;
+                if (!filter_sample<MODE>(P, s, uint64_t(j), ci, t0, t1, sigma, err, rgb, true, sg)) return;
                 ++j;
                 continue;
             }
@@ -1017,6 +1034,8 @@ void set_sphere_fast(MarchParams* P) {
     P->sph_r = float(f.radius);
     P->sph_r2 = P->sph_r * P->sph_r;
     P->sph_cmax = float(cmax);
+    P->sph_sig32 = double(float(f.sigma));
+    for (int a = 0; a < 3; ++a) P->sph_rgb32[a] = double(float(f.rgb[a]));
 }
 
 // VMB_MARCH_IMPL=twopass forces the count -> scan -> fill pipeline (A/B tests).
