@@ -37,6 +37,7 @@ namespace {
 // BUFFER_FWD = BUFFER + the render_forward compositing of each kept sample, done
 // in filter_sample as the sample is kept (vmb_march_render_field).
 enum Mode { COUNT = 0, FILL = 1, BUFFER = 2, BUFFER_FWD = 3 };
+constexpr int kAccStride = 128;  // = the walk kernel's block size
 // bit 2 of a mode: the kernel evaluates a stored voxel field (field_density_t<true>)
 constexpr int VOXM = 4;
 __host__ __device__ constexpr int mbase(int m) { return m & 3; }
@@ -98,8 +99,11 @@ struct Sink {
     uint32_t buf_cap = 0;
     // BUFFER_FWD: rendering.cpp:47-58 accumulators (Tf follows the attribute-dtype
     // sigma, T the march's fp64 sigma; they differ only if sigma is not exact in it)
+    // The six accumulators live in shared memory (acc[k * kAccStride], k = Tf, r, g,
+    // b, opacity, depth): they are touched only per kept sample, and keeping them
+    // out of registers leaves the walk loop its 64 registers.
     bool at32 = false;
-    double Tf = 1.0, cr = 0.0, cg = 0.0, cb = 0.0, op = 0.0, dep = 0.0;
+    double* acc = nullptr;
 
     // One kept sample, with exactly k_shade + k_forward's expressions (FwdAcc):
     // sigma/rgb are rounded to the attribute dtype; alpha is reused when the
@@ -115,13 +119,14 @@ struct Sink {
     __device__ __forceinline__ void composite_rounded(double sigma, double sg, D3 c, double t0, double t1,
                                                       double alpha) {
         const double a = sg == sigma ? alpha : 1.0 - exp(-sg * (t1 - t0));
+        const double Tf = acc[0];
         const double w = Tf * a;
-        cr = cr + c.x * w;
-        cg = cg + c.y * w;
-        cb = cb + c.z * w;
-        op += w;
-        dep += w * 0.5 * (t0 + t1);
-        Tf *= 1.0 - a;
+        acc[1 * kAccStride] = acc[1 * kAccStride] + c.x * w;
+        acc[2 * kAccStride] = acc[2 * kAccStride] + c.y * w;
+        acc[3 * kAccStride] = acc[3 * kAccStride] + c.z * w;
+        acc[4 * kAccStride] += w;
+        acc[5 * kAccStride] += w * 0.5 * (t0 + t1);
+        acc[0] = Tf * (1.0 - a);
     }
 };
 
@@ -457,8 +462,9 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
             continue;
         }
         // occupied cell: a candidate, with the reference's exact interval
-        double t0 = P.near_ + double(j) * P.step;
-        double t1 = min_ref(P.near_ + double(j + 1) * P.step, P.far_);
+        const double dj = double(j);  // double(j + 1) == dj + 1.0 exactly (j < 2^20): one I2F
+        double t0 = P.near_ + dj * P.step;
+        double t1 = min_ref(P.near_ + (dj + 1.0) * P.step, P.far_);
         if (P.sphere_fast && s.filtering) {
             // Filtered SolidSphere test (fields.cpp:45): |p - c|^2 in fp32 with the
             // bound sph_err; decided cases skip the fp64 midpoint + sqrt.
@@ -588,6 +594,7 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
     MarchParams P, const RT* __restrict__ orig, const RT* __restrict__ dirs, uint64_t n_rays,
     uint32_t* __restrict__ counts, uint32_t* __restrict__ kept_idx, unsigned int* chunk_counter,
     uint64_t n_chunks, unsigned long long* emitted, DevError* err, FwdOut<AT> fo) {
+    __shared__ double s_acc[FWD ? 6 : 1][kAccStride];
     const int lane = threadIdx.x & 31;
     unsigned long long emit_local = 0;
     for (;;) {
@@ -603,6 +610,12 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
             s.buf_stride = 32;
             s.buf_cap = kWalkCap;
             s.at32 = sizeof(AT) == 4;
+            if (FWD) {
+                s.acc = &s_acc[0][threadIdx.x];
+                s.acc[0] = 1.0;
+#pragma unroll
+                for (int k = 1; k < 6; ++k) s.acc[k * kAccStride] = 0.0;
+            }
             constexpr int M = (FWD ? BUFFER_FWD : BUFFER) | (VOX ? VOXM : 0);
             if (FAST) {
                 const D3 o = load3(orig, r), d = load3(dirs, r);
@@ -616,11 +629,11 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
             counts[r] = s.n_kept;
             emit_local += s.n_cand;
             if (FWD) {  // every kept sample was composited (rays over kWalkCap too)
-                fo.color[3 * r] = AT(s.cr);
-                fo.color[3 * r + 1] = AT(s.cg);
-                fo.color[3 * r + 2] = AT(s.cb);
-                fo.opacity[r] = AT(s.op);
-                fo.depth[r] = AT(s.dep);
+                fo.color[3 * r] = AT(s.acc[1 * kAccStride]);
+                fo.color[3 * r + 1] = AT(s.acc[2 * kAccStride]);
+                fo.color[3 * r + 2] = AT(s.acc[3 * kAccStride]);
+                fo.opacity[r] = AT(s.acc[4 * kAccStride]);
+                fo.depth[r] = AT(s.acc[5 * kAccStride]);
             }
         }
         __syncwarp();
@@ -767,9 +780,10 @@ __global__ void __launch_bounds__(32 * kExpandWarps) k_march_expand(
             if (p < end && p < cap) {
                 const uint64_t k = p - loff;
                 if (k < uint64_t(kWalkCap)) {
-                    const uint64_t i = sk[k * 32 + L];
-                    const double t0 = near_ + double(i) * step;
-                    const double t1 = min_ref(near_ + double(i + 1) * step, far_);
+                    const uint32_t i = sk[k * 32 + L];
+                    const double di = double(i);  // double(i + 1) == di + 1.0 exactly
+                    const double t0 = near_ + di * step;
+                    const double t1 = min_ref(near_ + (di + 1.0) * step, far_);
                     ts[p] = t0;
                     te[p] = t1;
                     idx[p] = uint32_t(chunk * 32 + L);
