@@ -753,8 +753,8 @@ __global__ void __launch_bounds__(32 * kExpandWarps) k_march_expand(
         const uint64_t base = __shfl_sync(0xffffffffu, off, 0);
         const uint64_t end = uint64_t(__shfl_sync(0xffffffffu, off, last)) +
                              __shfl_sync(0xffffffffu, cnt, last);
-        const double ox = double(cur.o[0]), oy = double(cur.o[1]), oz = double(cur.o[2]);
-        const double dx = double(cur.d[0]), dy = double(cur.d[1]), dz = double(cur.d[2]);
+        const RT ox = cur.o[0], oy = cur.o[1], oz = cur.o[2];  // shuffled in the ray's own type
+        const RT dx = cur.d[0], dy = cur.d[1], dz = cur.d[2];
         cp_async_wait1();  // this chunk's rows have landed
         __syncwarp();
         const uint32_t* sk = s_idx[wib][buf];
@@ -772,10 +772,10 @@ __global__ void __launch_bounds__(32 * kExpandWarps) k_march_expand(
             const uint32_t loff = __shfl_sync(0xffffffffu, off, L);
             D3 o, d;
             if (SHADE) {
-                o = d3(__shfl_sync(0xffffffffu, ox, L), __shfl_sync(0xffffffffu, oy, L),
-                       __shfl_sync(0xffffffffu, oz, L));
-                d = d3(__shfl_sync(0xffffffffu, dx, L), __shfl_sync(0xffffffffu, dy, L),
-                       __shfl_sync(0xffffffffu, dz, L));
+                o = d3(double(__shfl_sync(0xffffffffu, ox, L)), double(__shfl_sync(0xffffffffu, oy, L)),
+                       double(__shfl_sync(0xffffffffu, oz, L)));
+                d = d3(double(__shfl_sync(0xffffffffu, dx, L)), double(__shfl_sync(0xffffffffu, dy, L)),
+                       double(__shfl_sync(0xffffffffu, dz, L)));
             }
             if (p < end && p < cap) {
                 const uint64_t k = p - loff;

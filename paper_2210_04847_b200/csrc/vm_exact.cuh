@@ -205,10 +205,34 @@ VM_HD double field_density_t(const vmb_field& f, D3 p);
 template <bool VOX>
 VM_HD double field_rgb_sigma_t(const vmb_field& f, D3 p, D3* rgb);
 
+// The reference's SolidSphere test compares norm(p - c) = sqrt(d2) with the
+// radius. sqrt is correctly rounded and monotone, so when d2 is more than a
+// relative 1e-12 away from r^2 the comparison of d2 with r^2 decides it the same
+// way; only the thin shell in between takes the sqrt. Returns +1 outside
+// (norm > r), -1 inside (norm < r), 0 undecided.
+VM_HD int sphere_side(const vmb_field& f, double d2) {
+    const double r2 = f.radius * f.radius;
+    if (!(r2 > 1e-200 && r2 < 1e200)) return 0;
+    if (d2 > r2 * (1.0 + 1e-12)) return 1;
+    if (d2 < r2 * (1.0 - 1e-12)) return -1;
+    return 0;
+}
+
+VM_HD bool sphere_outside(const vmb_field& f, D3 p) {  // norm(p - c) > radius (fields.cpp:45,60)
+    const D3 q = p - d3(f.center[0], f.center[1], f.center[2]);
+    const double d2 = dot(q, q);  // norm(q) == sqrt(dot(q, q)), math.hpp:30
+    const int side = sphere_side(f, d2);
+    return side != 0 ? side > 0 : sqrt(d2) > f.radius;
+}
+
 VM_HD double field_density_analytic(const vmb_field& f, D3 p) {
     if (f.kind == VMB_FIELD_UNIFORM_BOX) return box_contains(f, p) ? f.sigma : 0.0;
-    if (f.kind == VMB_FIELD_SOLID_SPHERE)
-        return norm(p - d3(f.center[0], f.center[1], f.center[2])) <= f.radius ? f.sigma : 0.0;
+    if (f.kind == VMB_FIELD_SOLID_SPHERE) {  // norm <= r; NaN midpoints never reach here
+        const D3 q = p - d3(f.center[0], f.center[1], f.center[2]);
+        const double d2 = dot(q, q);
+        const int side = sphere_side(f, d2);
+        return (side != 0 ? side < 0 : sqrt(d2) <= f.radius) ? f.sigma : 0.0;
+    }
     return f.sigma;
 }
 
@@ -216,7 +240,7 @@ VM_HD double field_rgb_sigma_analytic(const vmb_field& f, D3 p, D3* rgb) {
     if (f.kind == VMB_FIELD_UNIFORM_BOX || f.kind == VMB_FIELD_SOLID_SPHERE) {
         bool in = f.kind == VMB_FIELD_UNIFORM_BOX
                       ? box_contains(f, p)
-                      : !(norm(p - d3(f.center[0], f.center[1], f.center[2])) > f.radius);
+                      : !sphere_outside(f, p);
         if (!in) {
             *rgb = d3(0.0, 0.0, 0.0);
             return 0.0;
