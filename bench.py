@@ -56,6 +56,10 @@ def parse():
                     help="forward: march+shade+render_forward fused; shade: march+shade fused; none: separate")
     ap.add_argument("--e2e-streams", type=int, default=2)
     ap.add_argument("--e2e-chunks", type=int, default=4)  # 2x4 measured best on B200 (r1)
+    ap.add_argument("--e2e-async", type=int, default=1, help="async march (no per-chunk host sync)")
+    # device-generated rays leave PCIe to the gradients: more, smaller chunks pay (4x8 best on B200, r1)
+    ap.add_argument("--e2e-camera-streams", type=int, default=4)
+    ap.add_argument("--e2e-camera-chunks", type=int, default=8)
     return ap.parse_args()
 
 
@@ -272,6 +276,8 @@ def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev
     L = dev.lib
     N = len(o32)
     n_ctx, n_chunk = max(1, args.e2e_streams), max(1, args.e2e_chunks)
+    if cam is not None:
+        n_ctx, n_chunk = max(1, args.e2e_camera_streams), max(1, args.e2e_camera_chunks)
     bounds = [(N * i // n_chunk, N * (i + 1) // n_chunk) for i in range(n_chunk)]
     cmax = max(e - b for b, e in bounds)
     host_in = [o32, d32] + list(ups)            # per-ray: 12, 12, 12, 4, 4 bytes
@@ -296,6 +302,7 @@ def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev
         ins = [cx.empty(cmax * w, np.float32) for w in widths]
         outs = [cx.empty(cmax * w, np.float32) for w in out_w]
         bufs.append(dict(ins=ins, outs=outs, packed=api.DevicePacked.allocate(cx, cmax, ccap),
+                         n_dev=cx.zeros(n_chunk, np.uint64),
                          rgb=cx.empty(ccap * 3, np.float32), sig=cx.empty(ccap, np.float32),
                          grgb=cx.empty(ccap * 3, np.float32), gsig=cx.empty(ccap, np.float32)))
 
@@ -309,10 +316,19 @@ def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev
             check(L.vmb_generate_rays_range(cx.h, C.byref(cam), 0.2, 1.0, VMB_F32, b, n, bf["ins"][0].ptr,
                                             bf["ins"][1].ptr, C.byref(rays)))
         pk = bf["packed"]
-        api.march_render_device(cx, grid, rays, field, cfg, pk, bf["rgb"], bf["sig"], *bf["outs"])
+        if args.e2e_async:  # no host round trip: the sample total stays on the device
+            smp = pk.samples_struct()
+            check(L.vmb_march_render_field_async(cx.h, grid.h, C.byref(rays), C.byref(field), C.byref(cfg),
+                                                 C.byref(smp), bf["rgb"].ptr, bf["sig"].ptr, bf["outs"][0].ptr,
+                                                 bf["outs"][1].ptr, bf["outs"][2].ptr, VMB_F32, 0.0,
+                                                 bf["n_dev"].ptr + 8 * chunk_id[0]))
+            pk.n_samples = pk.capacity
+        else:
+            api.march_render_device(cx, grid, rays, field, cfg, pk, bf["rgb"], bf["sig"], *bf["outs"])
         api.render_backward_device(cx, pk, bf["rgb"], bf["sig"], *bf["ins"][2:], bf["grgb"], bf["gsig"])
+        d2h = L.vmb_memcpy_d2h_async if args.e2e_async else L.vmb_memcpy_d2h  # async: synced at the end
         for arr, p, w in zip(bf["outs"], p_out, out_w):
-            check(L.vmb_memcpy_d2h(cx.h, p.value + b * w * 4, arr.ptr, n * w * 4))
+            check(d2h(cx.h, p.value + b * w * 4, arr.ptr, n * w * 4))
 
     def worker(ci, steps, err):
         try:
@@ -322,7 +338,15 @@ def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev
         except Exception as ex:  # pragma: no cover
             err.append(ex)
 
+    chunk_id = [0]
+
     def run(steps):
+        if args.e2e_async:  # one host thread enqueues everything; the streams overlap
+            for _ in range(steps):
+                for k in range(n_chunk):
+                    chunk_id[0] = k
+                    run_chunk(k % n_ctx, *bounds[k])
+            return
         err = []
         ts = [threading.Thread(target=worker, args=(i, steps, err)) for i in range(n_ctx)]
         for t in ts:
@@ -346,6 +370,10 @@ def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev
     for cx in ctxs:
         cx.sync()
     e2e_ms = dist.max(dev.elapsed_ms(7, 8) / args.steps)
+    if args.e2e_async:  # deferred error report + every chunk's samples fitted the buffers
+        for cx, bf in zip(ctxs, bufs):
+            check(L.vmb_march_check(cx.h))
+            assert int(bf["n_dev"].numpy().max()) <= ccap, "e2e chunk exceeded its sample capacity"
     # the pipelined result must equal the resident single-stream step's
     same = True
     for p, w, darr in zip(p_out, out_w, dev_out):
@@ -360,12 +388,14 @@ def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev
         return {"value": total_rays / (e2e_ms * 1e-3), "unit": "rays/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(sum(a.nbytes for a in host_in[2:])), "d2h_bytes_per_step": N * 20,
                 "streams": n_ctx, "chunks": n_chunk, "matches_resident_outputs": same,
-                "path": "C ABI: camera in, rays generated per chunk on the device (vmb_generate_rays_range), "
+                "path": f"C ABI: camera in, rays generated per chunk on the device (vmb_generate_rays_range), "
+                        f"vmb_march_render_field{'_async' if args.e2e_async else ''} + vmb_render_backward, "
                         "pinned host upstream grads in, color/opacity/depth out"}
     return {"value": total_rays / (e2e_ms * 1e-3), "unit": "rays/s", "ms_per_step": e2e_ms,
             "h2d_bytes_per_step": int(sum(a.nbytes for a in host_in)), "d2h_bytes_per_step": N * 20,
             "streams": n_ctx, "chunks": n_chunk, "matches_resident_outputs": same,
-            "path": "C ABI (vmb_memcpy_h2d, vmb_march_render_field, vmb_render_backward, vmb_memcpy_d2h): "
+            "path": f"C ABI (vmb_memcpy_h2d, vmb_march_render_field{'_async' if args.e2e_async else ''}, "
+                    "vmb_render_backward, vmb_memcpy_d2h): "
                     "pinned host rays + upstream grads in, color/opacity/depth out, "
                     f"{n_chunk} chunks pipelined over {n_ctx} streams"}
 

@@ -83,6 +83,9 @@ int vmb_host_alloc(uint64_t bytes, void** h_out); /* pinned */
 int vmb_host_free(void* h_ptr);
 int vmb_memcpy_h2d(vmb_ctx* ctx, void* d_dst, const void* h_src, uint64_t bytes);
 int vmb_memcpy_d2h(vmb_ctx* ctx, void* h_dst, const void* d_src, uint64_t bytes);
+/* Stream-ordered d2h into pinned memory without waiting: the data is valid after
+ * vmb_ctx_synchronize (or an event). vmb_memcpy_d2h waits. */
+int vmb_memcpy_d2h_async(vmb_ctx* ctx, void* h_dst, const void* d_src, uint64_t bytes);
 int vmb_memcpy_d2d(vmb_ctx* ctx, void* d_dst, const void* d_src, uint64_t bytes);
 int vmb_memset(vmb_ctx* ctx, void* d_dst, int value, uint64_t bytes);
 /* CUDA events on the context stream (slot 0..31) for device-side timing. */
@@ -261,6 +264,13 @@ int vmb_march_render_field(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays
 int vmb_march_field_async(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,
                           const vmb_field* f, const vmb_march_config* cfg, vmb_samples* out,
                           uint64_t* d_n_samples);
+/* Asynchronous vmb_march_render_field (same contract as vmb_march_field_async);
+ * where the fused single pass does not apply (time-shifted fields, growth
+ * lattices) it runs the synchronous path and then publishes the total. */
+int vmb_march_render_field_async(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays, const vmb_field* f,
+                                 const vmb_march_config* cfg, vmb_samples* out, void* d_rgbs, void* d_sigmas,
+                                 void* d_color, void* d_opacity, void* d_depth, int dtype, double time,
+                                 uint64_t* d_n_samples);
 int vmb_march_check(vmb_ctx* ctx);
 /* Generic host-SigmaFn path, step 1: the grid-passing candidate intervals of every
  * ray, capped at max_samples_per_ray (ray_marching.cpp:75-106). Same two-call

@@ -151,6 +151,7 @@ SIGNATURES = {
     "vmb_host_free": (I32, [VP]),
     "vmb_memcpy_h2d": (I32, [VP, VP, VP, U64]),
     "vmb_memcpy_d2h": (I32, [VP, VP, VP, U64]),
+    "vmb_memcpy_d2h_async": (I32, [VP, VP, VP, U64]),
     "vmb_memcpy_d2d": (I32, [VP, VP, VP, U64]),
     "vmb_memset": (I32, [VP, VP, I32, U64]),
     "vmb_event_record": (I32, [VP, I32]),
@@ -199,6 +200,8 @@ SIGNATURES = {
     "vmb_march_render_field": (I32, [VP, VP, P(Rays), P(Field), P(MarchConfig), P(Samples), VP, VP,
                                      VP, VP, VP, I32, D, P(U64), P(MarchStats)]),
     "vmb_march_field_async": (I32, [VP, VP, P(Rays), P(Field), P(MarchConfig), P(Samples), VP]),
+    "vmb_march_render_field_async": (I32, [VP, VP, P(Rays), P(Field), P(MarchConfig), P(Samples), VP, VP, VP, VP,
+                                           VP, I32, D, VP]),
     "vmb_march_check": (I32, [VP]),
     "vmb_march_candidates": (I32, [VP, VP, P(Rays), P(MarchConfig), P(Samples), P(U64)]),
     "vmb_march_filter": (I32, [VP, P(PackedView), VP, P(MarchConfig), P(Samples), P(U64)]),

@@ -1346,10 +1346,48 @@ int vmb_march_field_async(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,
     return e == cudaSuccess ? VMB_OK : cuda_fail(e, "march async");
 }
 
-int vmb_march_check(vmb_ctx* ctx) {
-    int rc = report_march_error(ctx);
+int vmb_march_render_field_async(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays, const vmb_field* f,
+                                 const vmb_march_config* cfg, vmb_samples* out, void* d_rgbs, void* d_sigmas,
+                                 void* d_color, void* d_opacity, void* d_depth, int dtype, double time,
+                                 uint64_t* d_n) {
+    MarchParams P;
+    int rc = march_params(g, rays, cfg, &P);
     if (rc) return rc;
-    return reset_error(ctx);
+    if (int frc = check_field(f)) return frc;
+    P.f = *f;
+    P.filter = true;
+    P.full = false;
+    set_sphere_fast(&P);
+    bool ident = std::isfinite(time) && (time == 0.0 || (f->velocity[0] == 0.0 &&
+                                                          f->velocity[1] == 0.0 && f->velocity[2] == 0.0));
+    for (int a = 0; a < 3; ++a) ident = ident && std::isfinite(f->velocity[a]);
+    if (!ident || !use_fused(P)) {  // the synchronous path, then publish the total on the device
+        uint64_t n = 0;
+        rc = vmb_march_render_field(ctx, g, rays, f, cfg, out, d_rgbs, d_sigmas, d_color, d_opacity, d_depth,
+                                    dtype, time, &n, nullptr);
+        if (rc && rc != VMB_CAPACITY) return rc;
+        cudaError_t e = cudaMemcpyAsync(d_n, &n, 8, cudaMemcpyHostToDevice, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        return e == cudaSuccess ? VMB_OK : cuda_fail(e, "march async");
+    }
+    ShadeReq sr;
+    sr.on = true;
+    sr.f = *f;
+    sr.time = time;
+    sr.rgb = d_rgbs;
+    sr.sig = d_sigmas;
+    sr.dtype = dtype;
+    sr.fwd = true;
+    sr.color = d_color;
+    sr.opacity = d_opacity;
+    sr.depth = d_depth;
+    return launch_fused(ctx, P, rays, out, reinterpret_cast<unsigned long long*>(d_n), nullptr, sr);
+}
+
+int vmb_march_check(vmb_ctx* ctx) {  // reports the recorded error once, then clears the record
+    int rc = report_march_error(ctx);
+    int rr = reset_error(ctx);
+    return rc ? rc : rr;
 }
 
 int vmb_march_candidates(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,

@@ -222,6 +222,10 @@ int vmb_ctx_create(int device, vmb_ctx** out) {
     VMB_CUDA_TRY(cudaMalloc(&ctx->d_u64, 8 * sizeof(unsigned long long)), "cudaMalloc");
     VMB_CUDA_TRY(cudaMallocHost(&ctx->h_u64, 8 * sizeof(unsigned long long)), "cudaMallocHost");
     for (auto& ev : ctx->events) VMB_CUDA_TRY(cudaEventCreate(&ev), "cudaEventCreate");
+    // the async entry points rely on a clean error record from the start
+    if (int rc = reset_error(ctx)) return rc;
+    VMB_CUDA_TRY(cudaMemsetAsync(ctx->d_u64, 0, 8 * sizeof(unsigned long long), ctx->stream), "cudaMemset");
+    VMB_CUDA_TRY(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
     *out = ctx;
     return VMB_OK;
 }
@@ -296,6 +300,12 @@ int vmb_host_free(void* p) {
 int vmb_memcpy_h2d(vmb_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
     if (!bytes) return VMB_OK;
     VMB_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream), "h2d");
+    return VMB_OK;
+}
+
+int vmb_memcpy_d2h_async(vmb_ctx* ctx, void* dst, const void* src, uint64_t bytes) {
+    if (!bytes) return VMB_OK;
+    VMB_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
     return VMB_OK;
 }
 

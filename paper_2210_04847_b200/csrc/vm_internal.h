@@ -116,6 +116,9 @@ int scan_flags(vmb_ctx* ctx, const uint8_t* flags, uint64_t n, uint32_t* pos,
 // ---------------------------------------------------------------- grid (grid.cu)
 int grid_refresh(vmb_ctx* ctx, vmb_grid* g);      // bits + coarse from cache
 int grid_rebuild_coarse(vmb_ctx* ctx, vmb_grid* g);  // coarse bits + distance map
-constexpr int kDistCap = 16;
+#ifndef VMB_DIST_CAP
+#define VMB_DIST_CAP 16
+#endif
+constexpr int kDistCap = VMB_DIST_CAP;
 
 }  // namespace vmb

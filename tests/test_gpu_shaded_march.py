@@ -100,3 +100,52 @@ def test_fused_forward_render(ray_dtype, attr_dtype):
     gb = api.OccupancyGrid(64, Contraction.aabb(), 1e-3, dev=dev)
     gb.update_field(box, 0.95, 3)
     _render_both(dev, gb, rays, box, MarchConfig(2e-3, 0.0, 1e-4), len(o), attr_dtype)
+
+
+def test_async_fused_forward_matches_sync():
+    """vmb_march_render_field_async: same samples/attributes/outputs as the
+    synchronous call, total on the device, errors deferred to vmb_march_check."""
+    import ctypes as C
+    from paper_2210_04847_b200._lib import VMB_F32 as F32, check
+    dev = api.Device(0)
+    L = dev.lib
+    field = Field.sphere(**workload.SPHERE)
+    g = api.OccupancyGrid(128, Contraction.aabb(), dev=dev)
+    for s in workload.grid_warmup_seeds(8, 5):
+        g.update_field(field, 0.95, s)
+    o, d = workload.orbit_rays(96, angle=0.3)
+    n = len(o)
+    rays, keep = _rays(dev, o, d, 0.2, 1.0, np.float32)
+    cfg = MarchConfig(5e-3, 1e-4, 1e-2)
+    a = api.march_device(dev, g, rays, field, cfg, api.DevicePacked.allocate(dev, n, 8 * n + 1024))
+    cap = a.capacity
+    bufs = []
+    for _ in range(2):
+        bufs.append(dict(p=api.DevicePacked.allocate(dev, n, cap), rgb=dev.empty(3 * cap, np.float32),
+                         sig=dev.empty(cap, np.float32),
+                         out=[dev.empty(3 * n, np.float32), dev.empty(n, np.float32), dev.empty(n, np.float32)]))
+    x, y = bufs
+    api.march_render_device(dev, g, rays, field, cfg, x["p"], x["rgb"], x["sig"], *x["out"])
+    nd = dev.zeros(1, np.uint64)
+    smp = y["p"].samples_struct()
+    check(L.vmb_march_render_field_async(dev.h, g.h, C.byref(rays), C.byref(field), C.byref(cfg), C.byref(smp),
+                                         y["rgb"].ptr, y["sig"].ptr, y["out"][0].ptr, y["out"][1].ptr,
+                                         y["out"][2].ptr, F32, 0.0, nd.ptr))
+    check(L.vmb_march_check(dev.h))
+    s = int(nd.numpy()[0])
+    assert s == x["p"].n_samples > 0
+    y["p"].n_samples = s
+    hx, hy = x["p"].to_host(), y["p"].to_host()
+    for k in ("offsets", "counts", "t_starts", "t_ends", "ray_indices"):
+        assert np.array_equal(getattr(hx, k), getattr(hy, k)), k
+    assert np.array_equal(x["rgb"].numpy(3 * s), y["rgb"].numpy(3 * s))
+    for u, v in zip(x["out"], y["out"]):
+        assert np.array_equal(u.numpy(), v.numpy())
+    # a negative density is recorded on the device and reported by vmb_march_check
+    bad = Field.sphere(center=(0.5, 0.5, 0.5), radius=0.2, sigma=-1.0)
+    check(L.vmb_march_render_field_async(dev.h, g.h, C.byref(rays), C.byref(bad), C.byref(cfg), C.byref(smp),
+                                         y["rgb"].ptr, y["sig"].ptr, y["out"][0].ptr, y["out"][1].ptr,
+                                         y["out"][2].ptr, F32, 0.0, nd.ptr))
+    with pytest.raises(RuntimeError, match="negative density"):
+        check(L.vmb_march_check(dev.h))
+    check(L.vmb_march_check(dev.h))  # the record was reset
