@@ -149,3 +149,40 @@ def test_async_fused_forward_matches_sync():
     with pytest.raises(RuntimeError, match="negative density"):
         check(L.vmb_march_check(dev.h))
     check(L.vmb_march_check(dev.h))  # the record was reset
+
+
+def test_step_is_bitwise_reproducible_and_chunk_independent():
+    """The reference promises outputs independent of n_threads (test_ray_marching.cpp
+    :180-199, test_rendering.cpp:350-371). Here: the fused step run twice gives the
+    same bits (the walk's atomic chunk stealing does not leak into results), and
+    marching the batch in two halves gives the same per-ray outputs."""
+    dev = api.Device(0)
+    field = Field.sphere(**workload.SPHERE)
+    g = api.OccupancyGrid(128, Contraction.aabb(), dev=dev)
+    for s in workload.grid_warmup_seeds(8, 5):
+        g.update_field(field, 0.95, s)
+    o, d = workload.orbit_rays(128, angle=0.7)
+    n = len(o)
+    cfg = MarchConfig(5e-3, 1e-4, 1e-2)
+
+    def run(oo, dd):
+        rays, keep = _rays(dev, oo, dd, 0.2, 1.0, np.float32)
+        m = len(oo)
+        p = api.march_device(dev, g, rays, field, cfg, api.DevicePacked.allocate(dev, m, 8 * m + 1024))
+        cap = p.capacity
+        rgb, sig = dev.empty(3 * cap, np.float32), dev.empty(cap, np.float32)
+        outs = [dev.empty(3 * m, np.float32), dev.empty(m, np.float32), dev.empty(m, np.float32)]
+        api.march_render_device(dev, g, rays, field, cfg, p, rgb, sig, *outs)
+        return p.to_host(), [x.numpy() for x in outs]
+
+    (p1, o1), (p2, o2) = run(o, d), run(o, d)
+    for k in ("offsets", "counts", "t_starts", "t_ends", "ray_indices"):
+        assert np.array_equal(getattr(p1, k), getattr(p2, k)), k
+    for a, b in zip(o1, o2):
+        assert np.array_equal(a, b)
+    h = n // 2 + 17
+    (pa, oa), (pb, ob) = run(o[:h], d[:h]), run(o[h:], d[h:])
+    assert np.array_equal(np.concatenate([pa.counts, pb.counts]), p1.counts)
+    assert np.array_equal(np.concatenate([pa.t_starts, pb.t_starts]), p1.t_starts)
+    for a, b, full, w in zip(oa, ob, o1, (3, 1, 1)):
+        assert np.array_equal(np.concatenate([a, b]), full)
