@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--phases", type=int, default=1, help="per-phase event timing pass")
     ap.add_argument("--fusion", default="forward", choices=["forward", "shade", "none"],
                     help="forward: march+shade+render_forward fused; shade: march+shade fused; none: separate")
+    ap.add_argument("--grid-update-every", type=int, default=0,
+                    help="config 4: an occupancy-grid EMA update (sharded probe + NCCL all-reduce(max) when N > 1) "
+                         "inside the timed loop every K steps (0: none)")
     ap.add_argument("--e2e-streams", type=int, default=2)
     ap.add_argument("--e2e-chunks", type=int, default=4)  # 2x4 measured best on B200 (r1)
     ap.add_argument("--e2e-async", type=int, default=1, help="async march (no per-chunk host sync)")
@@ -452,8 +455,15 @@ def main():
     #   fusion=none    march | shade | render_forward | render_backward
     #   fusion=shade   march+shade (vmb_march_field_shaded) | render_forward | render_backward
     #   fusion=forward march+shade+render_forward (vmb_march_render_field) | render_backward
+    step_no = [0]
+    update_seeds = workload.grid_warmup_seeds(4096, 11)
+
     def step(record=None):
         rec = record or (lambda k: None)
+        step_no[0] += 1
+        if args.grid_update_every and step_no[0] % args.grid_update_every == 0:
+            # config 4's training loop (voxmarch.cpp:514-515): EMA update of the grid
+            grid.update_field(field, 0.95, update_seeds[(step_no[0] // args.grid_update_every) % 4096])
         rec(2)
         if args.fusion == "forward":
             api.march_render_device(dev, grid, rays, field, cfg, packed, rgb, sig, col, op, dep)
@@ -574,7 +584,9 @@ def main():
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
                 "samples_per_s": total_samples / (ms_step * 1e-3),
-                "config": {"workload": f"config 5: {N} orbit-camera rays/GPU (W={args.width}), "
+                "config": {"workload": (f"config 4: grid update every {args.grid_update_every} steps, "
+                                        if args.grid_update_every else "config 5: ") +
+                                       f"{N} orbit-camera rays/GPU (W={args.width}), "
                                        f"{R}^3 grid (16 jittered warm-up updates), SolidSphere r=0.2 "
                                        f"sigma=200, step {args.step_size}, alpha 1e-2, eps 1e-4",
                            "rays_per_gpu": N, "samples_per_gpu": S, "resolution": R,
