@@ -221,6 +221,9 @@ int vmb_grid_query(vmb_ctx* ctx, const vmb_grid* g, const double* d_points, uint
  * layout, so save/load are plain copies. Either pointer may be NULL. */
 int vmb_grid_read(vmb_ctx* ctx, const vmb_grid* g, uint8_t* h_bits, double* h_cache);
 int vmb_grid_write(vmb_ctx* ctx, vmb_grid* g, const uint8_t* h_bits, const double* h_cache);
+/* The marcher's acceleration structure (not in the reference): per cell the L-inf
+ * distance in cells to the nearest occupied cell, capped (*h_cap), u8 [n_cells]. */
+int vmb_grid_read_distance(vmb_ctx* ctx, const vmb_grid* g, uint8_t* h_dist, uint32_t* h_cap);
 const uint32_t* vmb_grid_device_bits(const vmb_grid* g);
 const double* vmb_grid_device_cache(const vmb_grid* g);
 

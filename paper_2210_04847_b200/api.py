@@ -570,6 +570,13 @@ class OccupancyGrid:
         check(self.dev.lib.vmb_grid_read(self.dev.h, self.h, b.ctypes.data, None))
         return np.unpackbits(b, bitorder="little")[:n]
 
+    def distance_map(self) -> np.ndarray:
+        """The marcher's capped L-inf distance map (u8 per cell) and its cap."""
+        d = np.zeros(self.n_cells, np.uint8)
+        cap = C.c_uint32()
+        check(self.dev.lib.vmb_grid_read_distance(self.dev.h, self.h, d.ctypes.data, C.byref(cap)))
+        return d, int(cap.value)
+
     def packed_bits(self) -> np.ndarray:
         b = np.zeros((self.n_cells + 7) // 8, np.uint8)
         check(self.dev.lib.vmb_grid_read(self.dev.h, self.h, b.ctypes.data, None))

@@ -309,41 +309,66 @@ int make_timestamps(const double* h_ts, uint64_t n, Timestamps* ts) {
 //   D_x(c)   = min |dx| over occupied cells on the x-line (cap if none within cap-1)
 //   D_y(c)   = min over |dy| < cap of max(|dy|, D_x(c + dy e_y)),  same for z.
 // The composition is exactly the L-inf distance to the nearest occupied cell,
-// capped at kDistCap. The inner searches stop once |d| reaches the best so far.
-__global__ void k_dist_x(const uint32_t* __restrict__ bits, uint32_t res, uint64_t n,
+// capped at kDistCap.
+static_assert(kDistCap >= 1 && kDistCap <= 16, "the x pass reads a 2 * kDistCap - 1 bit window");
+
+// bits [lo, lo + 63] of the packed bitfield (cells outside [0, n) read as 0)
+__device__ __forceinline__ uint64_t bits64(const uint32_t* __restrict__ bits, int64_t lo, uint64_t n_words) {
+    const int64_t neg = lo < 0 ? -lo : 0;  // cells before 0 read as 0 (|lo| < 16 here)
+    const uint64_t start = uint64_t(lo + neg);
+    const uint64_t q = start >> 5, sh = start & 31;
+    const uint64_t w0 = q < n_words ? __ldg(bits + q) : 0u;
+    const uint64_t w1 = q + 1 < n_words ? __ldg(bits + q + 1) : 0u;
+    const uint64_t w2 = q + 2 < n_words ? __ldg(bits + q + 2) : 0u;
+    const uint64_t w = ((w0 | (w1 << 32)) >> sh) | (sh ? (w2 << (64 - sh)) : 0ull);
+    return w << neg;
+}
+
+// x pass: the window [c - (cap-1), c + (cap-1)] of the row, clipped to the row,
+// nearest set bit on each side by clz / ffs.
+__global__ void k_dist_x(const uint32_t* __restrict__ bits, uint32_t res, uint64_t n, uint64_t n_words,
                          uint8_t* __restrict__ out) {
+    constexpr int W = kDistCap - 1;
     for (uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < n;
          c += uint64_t(gridDim.x) * blockDim.x) {
         const int x = int(c % res);
+        const int64_t lo = int64_t(c) - W;
+        uint64_t w = bits64(bits, lo, n_words);
+        // keep bit positions p <= 2W with lo + p inside this row [c - x, c - x + res)
+        const int pmin = x < W ? W - x : 0;                        // row start
+        const int pmax = min(2 * W, W + (int(res) - 1 - x));        // row end / window end
+        const uint64_t keep = (pmax >= 63 ? ~0ull : ((1ull << (pmax + 1)) - 1)) & (~0ull << pmin);
+        w &= keep;
         int best = kDistCap;
-        for (int dd = 0; dd < best; ++dd) {
-            const int xl = x - dd, xr = x + dd;
-            bool hit = false;
-            if (xl >= 0) {
-                uint64_t q = c - dd;
-                hit |= (__ldg(bits + (q >> 5)) >> (q & 31)) & 1u;
-            }
-            if (xr < int(res)) {
-                uint64_t q = c + dd;
-                hit |= (__ldg(bits + (q >> 5)) >> (q & 31)) & 1u;
-            }
-            if (hit) best = dd;
-        }
+        const uint64_t left = w & ((2ull << W) - 1);  // positions 0..W: cells c-W .. c
+        if (left) best = W - (63 - __clzll(left));
+        const uint64_t right = w >> W;                 // cell c at bit 0
+        if (right) best = min(best, __ffsll(right) - 1);
         out[c] = uint8_t(best);
     }
 }
 
-__global__ void k_dist_axis(const uint8_t* __restrict__ in, uint32_t res, uint64_t n, uint64_t stride,
-                            uint8_t* __restrict__ out) {
-    for (uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < n;
-         c += uint64_t(gridDim.x) * blockDim.x) {
-        const int i = int((c / stride) % res);
-        int best = __ldg(in + c);
+// y / z pass over shared-memory tiles: a block holds one full line of 32
+// neighbouring x columns (tile[t][x]); each cell scans |dd| < its current best.
+__global__ void k_dist_axis_tiled(const uint8_t* __restrict__ in, uint32_t res, uint64_t stride,
+                                  uint64_t ostride, uint8_t* __restrict__ out) {
+    extern __shared__ uint8_t tile[];  // [res][32]
+    const uint32_t ntx = (res + 31) / 32;
+    const uint32_t other = blockIdx.x / ntx, x0 = (blockIdx.x % ntx) * 32;
+    const int lane = threadIdx.x & 31, row = threadIdx.x >> 5, rows = blockDim.x >> 5;
+    const uint32_t x = x0 + lane;
+    const bool valid = x < res;
+    const uint64_t base = x + uint64_t(other) * ostride;
+    for (uint32_t t = row; t < res; t += rows) tile[t * 32 + lane] = valid ? __ldg(in + base + t * stride) : kDistCap;
+    __syncthreads();
+    if (!valid) return;
+    for (int t = row; t < int(res); t += rows) {
+        int best = tile[t * 32 + lane];
         for (int dd = 1; dd < best; ++dd) {
-            if (i - dd >= 0) best = min(best, max(dd, int(__ldg(in + c - dd * stride))));
-            if (i + dd < int(res)) best = min(best, max(dd, int(__ldg(in + c + dd * stride))));
+            if (t - dd >= 0) best = min(best, max(dd, int(tile[(t - dd) * 32 + lane])));
+            if (t + dd < int(res)) best = min(best, max(dd, int(tile[(t + dd) * 32 + lane])));
         }
-        out[c] = uint8_t(best);
+        out[base + t * stride] = uint8_t(best);
     }
 }
 
@@ -353,10 +378,17 @@ int grid_rebuild_coarse(vmb_ctx* ctx, vmb_grid* g) {
     k_coarse<<<grid_blocks(ctx, g->coarse_words * 32, 256), 256, 0, ctx->stream>>>(
         g->bits, g->res, g->block, g->res_c, g->coarse, g->coarse_words);
     const int blocks = grid_blocks(ctx, g->n_cells, 256);
-    k_dist_x<<<blocks, 256, 0, ctx->stream>>>(g->bits, g->res, g->n_cells, g->dist);
-    k_dist_axis<<<blocks, 256, 0, ctx->stream>>>(g->dist, g->res, g->n_cells, g->res, g->dist_tmp);
-    k_dist_axis<<<blocks, 256, 0, ctx->stream>>>(g->dist_tmp, g->res, g->n_cells,
-                                                 uint64_t(g->res) * g->res, g->dist);
+    k_dist_x<<<blocks, 256, 0, ctx->stream>>>(g->bits, g->res, g->n_cells, g->n_words, g->dist);
+    const uint64_t r = g->res, plane = r * r;
+    const uint32_t tiles = uint32_t(r * ((r + 31) / 32));
+    const size_t smem = size_t(r) * 32;  // one line of 32 columns
+    static const bool opted = [] {      // lines beyond 48 KB of shared memory (res > 1536)
+        return cudaFuncSetAttribute(k_dist_axis_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) ==
+               cudaSuccess;
+    }();
+    (void)opted;
+    k_dist_axis_tiled<<<tiles, 256, smem, ctx->stream>>>(g->dist, g->res, r, plane, g->dist_tmp);      // y
+    k_dist_axis_tiled<<<tiles, 256, smem, ctx->stream>>>(g->dist_tmp, g->res, plane, r, g->dist);      // z
     return launch_check("grid coarse/dist");
 }
 
@@ -605,6 +637,13 @@ int vmb_grid_read(vmb_ctx* ctx, const vmb_grid* g, uint8_t* h_bits, double* h_ca
         cudaMemcpyAsync(h_cache, g->cache, g->n_cells * 8, cudaMemcpyDeviceToHost, ctx->stream);
     cudaError_t e = cudaStreamSynchronize(ctx->stream);
     return e == cudaSuccess ? VMB_OK : cuda_fail(e, "grid read");
+}
+
+int vmb_grid_read_distance(vmb_ctx* ctx, const vmb_grid* g, uint8_t* h_dist, uint32_t* h_cap) {
+    if (h_cap) *h_cap = uint32_t(kDistCap);
+    if (h_dist) cudaMemcpyAsync(h_dist, g->dist, g->n_cells, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    return e == cudaSuccess ? VMB_OK : cuda_fail(e, "grid read distance");
 }
 
 int vmb_grid_write(vmb_ctx* ctx, vmb_grid* g, const uint8_t* h_bits, const double* h_cache) {

@@ -453,3 +453,26 @@ def test_march_float32_rays_match_widened_oracle(dev, orc):
     out = api.march_device(dev, g, rays, field, cfg, api.DevicePacked.allocate(dev, len(o), 16 * len(o)))
     same_packed(out.to_host(), orc.march_field(o32.astype(np.float64), d32.astype(np.float64), 0.2, 1.0,
                                                og, ofield(field), ocfg(cfg), 4))
+
+
+@pytest.mark.parametrize("res,density", [(32, 0.01), (48, 0.002), (100, 0.0005), (128, 0.0), (40, 0.3)])
+def test_distance_map_is_exact_capped_chebyshev(dev, res, density):
+    """The marcher's acceleration structure: per cell the L-inf distance to the nearest
+    occupied cell capped at 16 — exact (an over-estimate would skip candidates, an
+    under-estimate only costs speed); resolutions not multiple of 32 included."""
+    from scipy import ndimage
+    rng = np.random.default_rng(res)
+    occ = rng.random(res ** 3) < density
+    if density > 0.2:  # clustered blobs too
+        occ[: res * res * 3] = False
+    g = api.OccupancyGrid(res, Contraction.aabb(), dev=dev)
+    g.write(np.packbits(occ.astype(np.uint8), bitorder="little"))
+    assert np.array_equal(g.bits(), occ.astype(np.uint8))
+    dist, cap = g.distance_map()
+    grid = occ.reshape(res, res, res)  # [z][y][x]
+    if grid.any():
+        want = ndimage.distance_transform_cdt(~grid, metric="chessboard")
+    else:
+        want = np.full(grid.shape, cap)
+    want = np.minimum(want, cap).astype(np.uint8).ravel()
+    assert np.array_equal(dist, want), np.argwhere(dist != want)[:5]
