@@ -98,7 +98,7 @@ int vmb_comm_destroy(vmb_ctx* ctx) {
 }
 
 int vmb_comm_allreduce_max_f64(vmb_ctx* ctx, double* buf, uint64_t count) {
-    if (!ctx->nccl_comm || ctx->nranks == 1) return VMB_OK;
+    if (!ctx->nccl_comm) return VMB_OK;
     Nccl& n = nccl();
     // u64 bit patterns: order-identical to f64 for non-negative values, and max
     // over integers is exact (no NaN / signed-zero corner cases).
@@ -109,7 +109,7 @@ int vmb_comm_allreduce_max_f64(vmb_ctx* ctx, double* buf, uint64_t count) {
 }
 
 int vmb_comm_allreduce_sum_f64(vmb_ctx* ctx, double* buf, uint64_t count) {
-    if (!ctx->nccl_comm || ctx->nranks == 1) return VMB_OK;
+    if (!ctx->nccl_comm) return VMB_OK;
     Nccl& n = nccl();
     ncclResult_t r = n.all_reduce(buf, buf, count, ncclFloat64, ncclSum,
                                   static_cast<ncclComm_t>(ctx->nccl_comm), ctx->stream);

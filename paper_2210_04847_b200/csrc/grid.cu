@@ -511,7 +511,7 @@ int vmb_grid_update_field(vmb_ctx* ctx, vmb_grid* g, const vmb_field* f, const d
         if (rc) return rc;
         if (err.key != ~0ull) return fail(VMB_RUNTIME, cell_name(g, err.key & ((1ull << 40) - 1)));
     }
-    if (ctx->nranks > 1) {
+    if (ctx->nccl_comm) {  // a communicator attached (any size): sharded probe + all-reduce
         if (!g->probed) {
             cudaError_t e = cudaMalloc(&g->probed, g->n_cells * sizeof(double));
             if (e != cudaSuccess) return cuda_fail(e, "probe buffer");
@@ -589,7 +589,7 @@ int vmb_grid_accumulate(vmb_ctx* ctx, const vmb_grid* g, const double* dens, con
 int vmb_grid_apply(vmb_ctx* ctx, vmb_grid* g, double* probed, double decay) {
     if (!(decay >= 0.0 && decay <= 1.0))
         return fail(VMB_INVALID_ARGUMENT, "occupancy grid: ema_decay must be in [0,1]");
-    if (ctx->nranks > 1) {
+    if (ctx->nccl_comm) {  // a communicator attached (any size): combine the ranks' probes
         int rc = vmb_comm_allreduce_max_f64(ctx, probed, g->n_cells);
         if (rc) return rc;
     }

@@ -54,3 +54,35 @@ def test_sharded_probe_allreduce_apply_matches_fused(world):
     for s in workload.grid_warmup_seeds(5, 9):
         og.update_field(of, 0.9, s, ts)
     assert np.array_equal(fused.bits(), og.bits())
+
+
+def test_nccl_single_rank_communicator_runs_the_collective_path():
+    """With a communicator attached (here 1 rank on cuda:0) the grid update takes the
+    sharded probe + ncclAllReduce(max) + apply path through the real NCCL library, and
+    the grid equals the plain fused update bit for bit; the training all-reduce(sum)
+    of a 1-rank communicator is the identity."""
+    import ctypes as C
+    import os
+    os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+    from paper_2210_04847_b200 import api, workload
+    from paper_2210_04847_b200._lib import Contraction, Field, check
+    dev, plain = api.Device(0), api.Device(0)
+    L = dev.lib
+    uid = (C.c_char * 128)()
+    check(L.vmb_comm_unique_id(uid))
+    check(L.vmb_comm_init(dev.h, uid, 1, 0))
+    try:
+        field = Field.sphere(**workload.SPHERE)
+        g1 = api.OccupancyGrid(128, Contraction.aabb(), dev=dev)
+        g2 = api.OccupancyGrid(128, Contraction.aabb(), dev=plain)
+        for s in workload.grid_warmup_seeds(4, 5):
+            g1.update_field(field, 0.95, s)
+            g2.update_field(field, 0.95, s)
+        assert np.array_equal(g1.bits(), g2.bits())
+        assert np.array_equal(g1.density_cache(), g2.density_cache())
+        x = np.random.default_rng(0).normal(size=1000)
+        buf = dev.upload(x)
+        check(L.vmb_comm_allreduce_sum_f64(dev.h, buf.ptr, 1000))
+        assert np.array_equal(buf.numpy(), x)
+    finally:
+        check(L.vmb_comm_destroy(dev.h))
