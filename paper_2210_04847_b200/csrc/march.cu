@@ -687,11 +687,15 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
-#ifndef VMB_EXPAND_MINB
-#define VMB_EXPAND_MINB 1
+// (an explicit minBlocksPerSM, even 1, changes the register allocation and costs
+// ~25 us per step here: leave it unset unless tuning with -DVMB_EXPAND_MINB)
+#ifdef VMB_EXPAND_MINB
+#define VMB_EXPAND_BOUNDS __launch_bounds__(32 * kExpandWarps, VMB_EXPAND_MINB)
+#else
+#define VMB_EXPAND_BOUNDS __launch_bounds__(32 * kExpandWarps)
 #endif
 template <typename RT, typename AT, bool SHADE, bool VOX>
-__global__ void __launch_bounds__(32 * kExpandWarps, VMB_EXPAND_MINB) k_march_expand(
+__global__ void VMB_EXPAND_BOUNDS k_march_expand(
     double near_, double far_, double step, const uint32_t* __restrict__ counts,
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ kept_idx, uint64_t n_rays,
     double* __restrict__ ts, double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,

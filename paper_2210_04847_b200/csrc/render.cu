@@ -270,10 +270,7 @@ __device__ void bwd_two_sweep(BwdSmem<T>& sm, int lane, bool active, bool staged
 #ifndef VMB_BWD_MINB
 #define VMB_BWD_MINB 4
 #endif
-#ifndef VMB_BWD_UNROLL
-#define VMB_BWD_UNROLL 1
-#endif
-constexpr int kBwdUnroll = VMB_BWD_UNROLL;
+
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays,
@@ -312,13 +309,11 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward(
                 stage_in<T, false>(sm, lane, base, n, ts, te, rgb, sig);
                 if (lane >= g0 && lane <= g1) {
                     double t = 1.0;
-#pragma unroll kBwdUnroll
                     for (uint32_t i = rr.off - base; i < rr.end - base; ++i) {  // rendering.cpp:89-96
                         sm.tr[i] = t;
                         t *= 1.0 - sm.al[i];
                     }
                     double suffix = 0.0;
-#pragma unroll kBwdUnroll
                     for (uint32_t i = rr.end - base; i-- > rr.off - base;) {  // rendering.cpp:99-108
                         const double delta = sm.te[i] - sm.ts[i];
                         const double mid = 0.5 * (sm.ts[i] + sm.te[i]);
