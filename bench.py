@@ -10,6 +10,12 @@ step 5e-3, alpha_thre 1e-2, early_stop_eps 1e-4):
     -> shade (analytic field rgb/sigma at each sample; harness)
     -> render_forward -> render_backward (upstream grads U(-1,1))
 
+The timed resident step (fusion=forward) runs the batch as `--chunks` contiguous
+ray sub-batches served by `--streams` contexts (default 2 x 2): the same C-ABI
+calls per sub-batch, overlapping on the device; its outputs are checked equal,
+bit for bit, to the single-call step's. `--streams 1 --chunks 1` times the single
+call sequence.
+
 Multi-GPU (torchrun): each rank marches its own 2^22-ray batch (weak scaling, its
 own camera angle) against a replicated grid; rank 0 prints one JSON line with the
 max-over-ranks device time. The grid warm-up runs the sharded probe +
@@ -57,6 +63,10 @@ def parse():
     ap.add_argument("--grid-update-every", type=int, default=0,
                     help="config 4: an occupancy-grid EMA update (sharded probe + NCCL all-reduce(max) when N > 1) "
                          "inside the timed loop every K steps (0: none)")
+    ap.add_argument("--streams", type=int, default=2,
+                    help="resident step: sub-batches served round-robin by this many contexts (streams)")
+    ap.add_argument("--chunks", type=int, default=2,
+                    help="resident step: the batch is marched as this many sub-batches (2x2 measured best, r1)")
     ap.add_argument("--e2e-streams", type=int, default=2)
     ap.add_argument("--e2e-chunks", type=int, default=4)  # 2x4 measured best on B200 (r1)
     ap.add_argument("--e2e-async", type=int, default=1, help="async march (no per-chunk host sync)")
@@ -258,6 +268,91 @@ def run_reference(args):
                              "sample": f"every {stride}th ray per step, {threads} threads, {cpu_model()}"},
             "e2e": {"value": v, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------- resident pipeline
+class ResidentPipeline:
+    """The resident step (rays, upstream gradients, outputs in HBM) as `--chunks`
+    contiguous ray sub-batches served round-robin by `--streams` contexts, each
+    sub-batch one vmb_march_render_field_async + vmb_render_backward pair on its
+    context's stream. Sub-batches of different streams overlap on the device (one
+    sub-batch's expansion/backward fills the SMs the other's walk tail leaves idle).
+    Per-ray outputs land in full-batch arrays, so they can be compared with the
+    single-call step bit for bit."""
+
+    def __init__(self, args, api, dev, grid, field, cfg, rays_dev, ups_dev, N):
+        from paper_2210_04847_b200._lib import VMB_F32
+        self.api, self.dev, self.grid, self.field, self.cfg = api, dev, grid, field, cfg
+        self.L = dev.lib
+        self.S, self.K = max(1, args.streams), max(1, args.chunks)
+        self.N = N
+        self.bounds = [(N * i // self.K, N * (i + 1) // self.K) for i in range(self.K)]
+        cmax = max(e - b for b, e in self.bounds)
+        cap = 8 * cmax
+        self.ctxs = [dev] + [api.Device(dev.index) for _ in range(self.S - 1)]
+        self.rays_dev, self.ups_dev = rays_dev, ups_dev
+        self.outs = [dev.empty(N * w, np.float32) for w in (3, 1, 1)]
+        self.n_dev = dev.zeros(self.K, np.uint64)
+        self.bufs = [dict(packed=api.DevicePacked.allocate(cx, cmax, cap),
+                          rgb=cx.empty(cap * 3, np.float32), sig=cx.empty(cap, np.float32),
+                          grgb=cx.empty(cap * 3, np.float32), gsig=cx.empty(cap, np.float32))
+                     for cx in self.ctxs]
+        self.cap = cap
+        self.VMB_F32 = VMB_F32
+
+    def chunk(self, k):
+        from paper_2210_04847_b200._lib import Rays, check
+
+        class Ptr:  # a device pointer with the DeviceArray interface the api needs
+            def __init__(self, ptr):
+                self.ptr = ptr
+
+        ci = k % self.S
+        cx, bf = self.ctxs[ci], self.bufs[ci]
+        b, e = self.bounds[k]
+        o, d = self.rays_dev
+        rays = Rays(o.ptr + 12 * b, d.ptr + 12 * b, self.VMB_F32, 0, e - b, 0.2, 1.0)
+        pk = bf["packed"]
+        smp = pk.samples_struct()
+        outs = [a.ptr + 4 * w * b for a, w in zip(self.outs, (3, 1, 1))]
+        check(self.L.vmb_march_render_field_async(
+            cx.h, self.grid.h, C.byref(rays), C.byref(self.field), C.byref(self.cfg), C.byref(smp),
+            bf["rgb"].ptr, bf["sig"].ptr, outs[0], outs[1], outs[2], self.VMB_F32, 0.0, self.n_dev.ptr + 8 * k))
+        pk.n_samples = pk.capacity
+        ups = [Ptr(u.ptr + 4 * w * b) for u, w in zip(self.ups_dev, (3, 1, 1))]
+        self.api.render_backward_device(cx, pk, bf["rgb"], bf["sig"], *ups, bf["grgb"], bf["gsig"])
+
+    def run(self, steps=1):
+        for _ in range(steps):
+            for k in range(self.K):
+                self.chunk(k)
+
+    def begin(self, slot):
+        """event `slot` on context 0; every other stream waits for it"""
+        from paper_2210_04847_b200._lib import check
+        self.dev.record(slot)
+        for cx in self.ctxs[1:]:
+            check(self.L.vmb_ctx_wait(cx.h, self.dev.h, 12))
+
+    def end(self, slot):
+        """context 0 waits for every other stream, then records `slot`"""
+        from paper_2210_04847_b200._lib import check
+        for i, cx in enumerate(self.ctxs[1:]):
+            check(self.L.vmb_ctx_wait(self.dev.h, cx.h, 13 + (i % 8)))
+        self.dev.record(slot)
+
+    def sync(self):
+        for cx in self.ctxs:
+            cx.sync()
+
+    def check(self):
+        """deferred march errors; every sub-batch fitted its sample buffers; total samples"""
+        from paper_2210_04847_b200._lib import check
+        for cx in self.ctxs:
+            check(self.L.vmb_march_check(cx.h))
+        n = self.n_dev.numpy()
+        assert int(n.max()) <= self.cap, "a sub-batch exceeded its sample capacity"
+        return int(n.sum())
 
 
 # ---------------------------------------------------------------------- e2e
@@ -482,26 +577,52 @@ def main():
         api.render_backward_device(dev, packed, rgb, sig, up_c, up_o, up_d, g_rgb, g_sig)
         rec(6)
 
+    # The timed step: the resident pipeline (sub-batches over several streams) when
+    # the forward is fused and no grid update sits inside the loop; else the
+    # single-call step above.
+    pipe = None
+    if args.fusion == "forward" and not args.grid_update_every and args.streams * args.chunks > 1:
+        pipe = ResidentPipeline(args, api, dev, grid, field, cfg, (do_, dd_), (up_c, up_o, up_d), N)
     clocks = Clocks(dist.local)
     for _ in range(max(args.warmup, 3)):
         step()
+        if pipe:
+            pipe.run()
     dev.sync()
+    if pipe:
+        pipe.sync()
     dist.barrier()
-    dev.record(0)
-    for _ in range(args.steps):
-        step()
-    dev.record(1)
-    dev.sync()
+    if pipe:
+        pipe.begin(0)
+        pipe.run(args.steps)
+        pipe.end(1)
+        pipe.sync()
+    else:
+        dev.record(0)
+        for _ in range(args.steps):
+            step()
+        dev.record(1)
+        dev.sync()
     dist.barrier()
     ms_total = dev.elapsed_ms(0, 1)
     # keep the GPU loaded ~1 s more so the clock sampler sees the steady state
     t_end = time.time() + 1.2
     while time.time() < t_end:
-        step()
+        pipe.run() if pipe else step()
     dev.sync()
+    if pipe:
+        pipe.sync()
     clk = clocks.stop()
 
     S = packed.n_samples
+    pipe_info = None
+    if pipe:  # the pipelined step's outputs == the single-call step's, bit for bit
+        s_pipe = pipe.check()
+        same = s_pipe == S and all(np.array_equal(a.numpy(), b.numpy(N * w))
+                                   for a, b, w in zip(pipe.outs, (col, op, dep), (3, 1, 1)))
+        pipe_info = {"streams": pipe.S, "sub_batches": pipe.K, "samples": s_pipe,
+                     "matches_single_call_outputs": bool(same)}
+        assert same, "pipelined step differs from the single-call step"
     ms_step = dist.max(ms_total / args.steps)
     total_rays = dist.sum(float(N))
     total_samples = dist.sum(float(S))
@@ -593,10 +714,15 @@ def main():
                            "fusion": args.fusion + " (analytic SolidSphere rgb/sigma shaded at sample midpoints)",
                            "storage": "rays/rgb/sigma/outputs f32, t f64, compute f64",
                            "l2": "inputs larger than L2 (~1 GB working set per step)",
-                           "parallelism": f"dp{dist.world} (rays sharded, grid replicated)"},
+                           "parallelism": f"dp{dist.world} (rays sharded, grid replicated)",
+                           "step_schedule": (f"{pipe.K} contiguous sub-batches over {pipe.S} streams "
+                                             "(vmb_march_render_field_async + vmb_render_backward each)"
+                                             if pipe else "single call sequence on one stream")},
+                "pipeline": pipe_info,
                 "phases_ms": phase, "grid_update_ms": grid_update_ms,
                 "roofline": roof, "e2e": e2e, "e2e_camera": e2e_cam, "cpu_baseline": cpu, "clocks": clk,
-                "gpu_launches": (KERNELS_PER_STEP - {"none": 0, "shade": 1, "forward": 2}[args.fusion]) * args.steps}
+                "gpu_launches": (KERNELS_PER_STEP - {"none": 0, "shade": 1, "forward": 2}[args.fusion])
+                * args.steps * (pipe.K if pipe else 1)}
         print(json.dumps(line), flush=True)
     if dist.world > 1:
         L.vmb_comm_destroy(dev.h)

@@ -1098,7 +1098,7 @@ void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* ray
     static int per_sm = [] {  // persistent: exactly the resident blocks
         int n = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_march_expand<RT, AT, SHADE, VOX>, 32 * kExpandWarps, 0);
-        return n < 1 ? 4 : n;
+        return env_int("VMB_EXPAND_CTAS", n < 1 ? 4 : n);
     }();
     k_march_expand<RT, AT, SHADE, VOX><<<grid_blocks(ctx, n_chunks * 32, 32 * kExpandWarps, per_sm),
                                     32 * kExpandWarps, 0, ctx->stream>>>(
@@ -1152,6 +1152,8 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, 0);
         if (per_sm < 1) per_sm = 4;
+        static const int forced = env_int("VMB_WALK_CTAS", 0);
+        if (forced > 0) per_sm = forced;
         kernel<<<ctx->num_sms * per_sm, 128, 0, ctx->stream>>>(
             P, o, d, n, out->d_counts, kept_idx, counters, n_chunks, emitted, ctx->d_err, fo);
     };

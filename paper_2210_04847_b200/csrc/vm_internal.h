@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/vmb200.h"
@@ -94,6 +95,11 @@ int cuda_fail(cudaError_t e, const char* where);
 // 3 = validation / misc. Growing synchronizes the stream before freeing.
 enum { SCRATCH_SCAN = 0, SCRATCH_MARCH = 1, SCRATCH_GRID = 2, SCRATCH_MISC = 3, SCRATCH_VOXGRAD = 4, SCRATCH_SLOTS = 5 };
 void* scratch(vmb_ctx* ctx, int slot, size_t bytes);
+// Integer tuning knob from the environment (read once per call site; dflt when unset).
+inline int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
 inline int grid_blocks(vmb_ctx* ctx, uint64_t work, int threads, int per_sm = 8) {
     uint64_t b = (work + threads - 1) / threads;
     uint64_t cap = uint64_t(ctx->num_sms) * per_sm;
