@@ -11,9 +11,13 @@
 //      the reference's operation order and in fp64 (T *= 1 - alpha; fp32 is not
 //      accurate enough);
 //   4. per-sample outputs are staged back into the tile and written coalesced.
-// render_backward groups consecutive rays whose samples fit one tile and runs
-// the reference's forward-T / reverse-suffix recurrence; only a single ray longer
-// than a tile uses two forward sweeps with suffix_k = S - P_k. Warps whose rays
+// render_backward groups consecutive rays whose samples fit one tile. Within a
+// group (k_backward_hy) only the two true recurrences run lane-serially: the
+// forward transmittance (one dependent multiply per sample) and the reverse
+// suffix sum (one dependent add per sample); everything else — alpha, v, the
+// weights, d_rgb — runs sample-parallel over the tile with every lane busy.
+// Only a single ray longer than a tile uses two forward sweeps with
+// suffix_k = S - P_k. Warps whose rays
 // are not contiguous (arbitrary user offsets) use per-lane global reads.
 // Sample positions are 32-bit: packed offsets are u32 by construction (pack()
 // rejects more than 2^32-1 samples, core_types.cpp:33-36).
@@ -336,6 +340,98 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward(
     }
 }
 
+template <typename T>
+__global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays,
+    const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
+    const T* __restrict__ sig, const T* __restrict__ dc, const T* __restrict__ dop,
+    const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig) {
+    __shared__ BwdSmem<T> smem[kWarps];
+    const int lane = threadIdx.x & 31;
+    BwdSmem<T>& sm = smem[threadIdx.x >> 5];
+    // owner lane of each staged sample: bytes of the sigma tile, which is free
+    // between the alpha phase (stage_in) and phase D (which writes d_sigma there)
+    uint8_t* own = reinterpret_cast<uint8_t*>(sm.sig);
+    const uint64_t n_warps = (n_rays + 31) / 32;
+    for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
+         w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
+        const Up u = load_up(dc, dop, ddep, rr.r, rr.valid);
+        if (!rr.contiguous) {
+            bwd_two_sweep(&sm, lane, rr.valid, false, rr.off, rr.end, 0u, 0u, u, ts, te, rgb, sig,
+                          g_rgb, g_sig);
+            continue;
+        }
+        const unsigned vmask = __ballot_sync(0xffffffffu, rr.valid);  // valid lanes: a prefix
+        int g0 = 0;
+        while (g0 < 32 && ((vmask >> g0) & 1u)) {
+            const uint32_t base = __shfl_sync(0xffffffffu, rr.off, g0);
+            const bool fits = rr.valid && lane >= g0 && rr.end - base <= uint32_t(Tile<T>::CH);
+            const unsigned fm = __ballot_sync(0xffffffffu, fits);  // monotone: ends ascend
+            if (!((fm >> g0) & 1u)) {  // ray g0 alone exceeds a tile
+                const uint32_t e0 = __shfl_sync(0xffffffffu, rr.end, g0);
+                bwd_two_sweep(&sm, lane, lane == g0, true, rr.off, rr.end, base, e0, u, ts, te, rgb,
+                              sig, g_rgb, g_sig);
+                ++g0;
+                continue;
+            }
+            const int g1 = 31 - __clz(fm);
+            const uint32_t n = __shfl_sync(0xffffffffu, rr.end, g1) - base;
+            if (n) {
+                stage_in<T, false>(sm, lane, base, n, ts, te, rgb, sig);
+                // B (lane-serial): T before each sample, rendering.cpp:89-96 — one
+                // dependent DMUL per sample; the owner map for the parallel phase
+                if (lane >= g0 && lane <= g1) {
+                    double t = 1.0;
+                    for (uint32_t i = rr.off - base; i < rr.end - base; ++i) {
+                        sm.tr[i] = t;
+                        own[i] = uint8_t(lane);
+                        t *= 1.0 - sm.al[i];
+                    }
+                }
+                __syncwarp();
+                // C (sample-parallel, every lane): w, v, d_rgb = d_color w (stored
+                // coalesced), and in place delta (ts), w v (te), T (1 - alpha) v (tr)
+                for (uint32_t r0 = 0; r0 < n; r0 += 32) {
+                    const uint32_t i = r0 + uint32_t(lane);
+                    const bool in = i < n;
+                    const int o = in ? int(own[i]) : 0;
+                    const Up uo{__shfl_sync(0xffffffffu, u.dcx, o), __shfl_sync(0xffffffffu, u.dcy, o),
+                                __shfl_sync(0xffffffffu, u.dcz, o), __shfl_sync(0xffffffffu, u.dop, o),
+                                __shfl_sync(0xffffffffu, u.ddep, o)};
+                    if (in) {
+                        const double t0 = sm.ts[i], t1 = sm.te[i], a = sm.al[i], tr = sm.tr[i];
+                        const double v = uo.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
+                                                  double(sm.rgb[3 * i + 2]), 0.5 * (t0 + t1));
+                        const double wgt = tr * a;
+                        T* gr = g_rgb + 3 * (uint64_t(base) + i);
+                        gr[0] = T(uo.dcx * wgt);
+                        gr[1] = T(uo.dcy * wgt);
+                        gr[2] = T(uo.dcz * wgt);
+                        sm.ts[i] = t1 - t0;
+                        sm.te[i] = wgt * v;
+                        sm.tr[i] = tr * (1.0 - a) * v;
+                    }
+                }
+                __syncwarp();
+                // D (lane-serial, reverse): suffix sum, rendering.cpp:99-108 — one
+                // dependent DADD per sample
+                if (lane >= g0 && lane <= g1) {
+                    double suffix = 0.0;
+                    for (uint32_t i = rr.end - base; i-- > rr.off - base;) {
+                        sm.sig[i] = T(sm.ts[i] * (sm.tr[i] - suffix));
+                        suffix += sm.te[i];
+                    }
+                }
+                __syncwarp();
+                for (uint32_t i = lane; i < n; i += 32) g_sig[uint64_t(base) + i] = sm.sig[i];
+                __syncwarp();
+            }
+            g0 = g1 + 1;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ backward, sample-parallel
 // Same greedy groups of whole rays (<= kSpCap samples), but one SAMPLE per lane:
 // a group is up to kSpRounds rounds of 32 consecutive samples, loaded straight
@@ -510,12 +606,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_backward_sp(
 
 // VMB_BACKWARD=sp selects the sample-parallel kernel (A/B measurements; the
 // shared-memory tile kernel measured faster on B200: 0.38 vs 0.52 ms at config 5).
-bool backward_tile() {
-    static int tile = [] {
+// VMB_BACKWARD=tile: the all-serial tile kernel (0.385 ms at config 5 vs 0.358 for
+// the hybrid default); VMB_BACKWARD=sp: fully sample-parallel (0.52 ms).
+int backward_impl() {
+    static int impl = [] {
         const char* v = getenv("VMB_BACKWARD");
-        return v && v[0] == 's' ? 0 : 1;
+        return v && v[0] == 's' ? 1 : v && v[0] == 't' ? 2 : 0;
     }();
-    return tile;
+    return impl;
 }
 
 // ------------------------------------------------------------------ transmittance
@@ -636,15 +734,15 @@ int vmb_render_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb,
                         int dtype) {
     if (!p->n_rays) return VMB_OK;
     int blocks = render_blocks(ctx, p->n_rays);
-    const bool tile = backward_tile();
+    const int impl = backward_impl();
     if (dtype == VMB_F32)
-        (tile ? k_backward<float> : k_backward_sp<float>)<<<blocks, kWarps * 32, 0, ctx->stream>>>(
+        (impl == 1 ? k_backward_sp<float> : impl == 2 ? k_backward<float> : k_backward_hy<float>)<<<blocks, kWarps * 32, 0, ctx->stream>>>(
             p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
             static_cast<const float*>(rgb), static_cast<const float*>(sig), static_cast<const float*>(dc),
             static_cast<const float*>(dop), static_cast<const float*>(ddep), static_cast<float*>(g_rgb),
             static_cast<float*>(g_sig));
     else
-        (tile ? k_backward<double> : k_backward_sp<double>)<<<blocks, kWarps * 32, 0, ctx->stream>>>(
+        (impl == 1 ? k_backward_sp<double> : impl == 2 ? k_backward<double> : k_backward_hy<double>)<<<blocks, kWarps * 32, 0, ctx->stream>>>(
             p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
             static_cast<const double*>(rgb), static_cast<const double*>(sig),
             static_cast<const double*>(dc), static_cast<const double*>(dop),
