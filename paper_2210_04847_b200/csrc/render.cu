@@ -90,19 +90,34 @@ template <typename T, bool kTransmittance, typename S>
 __device__ __forceinline__ void stage_in(S& sm, int lane, uint32_t cs, uint32_t n,
                                          const double* __restrict__ ts, const double* __restrict__ te,
                                          const T* __restrict__ rgb, const T* __restrict__ sig) {
-    for (uint32_t i = lane; i < n; i += 32) {
-        cp_async<8>(&sm.ts[i], ts + cs + i);
-        cp_async<8>(&sm.te[i], te + cs + i);
-        cp_async<sizeof(T)>(&sm.sig[i], sig + cs + i);
+    // fully unrolled rounds of 32 (n <= CH): per-lane base pointers + constant
+    // offsets, no loop-carried address arithmetic
+    constexpr int R = Tile<T>::CH / 32;
+    const double* pts = ts + cs + lane;
+    const double* pte = te + cs + lane;
+    const T* psg = sig + cs + lane;
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+        if (32u * k + lane < n) {
+            cp_async<8>(&sm.ts[32 * k + lane], pts + 32 * k);
+            cp_async<8>(&sm.te[32 * k + lane], pte + 32 * k);
+            cp_async<sizeof(T)>(&sm.sig[32 * k + lane], psg + 32 * k);
+        }
+    if (rgb) {
+        const T* prgb = rgb + 3 * uint64_t(cs) + lane;
+#pragma unroll
+        for (int k = 0; k < 3 * R; ++k)
+            if (32u * k + lane < 3 * n) cp_async<sizeof(T)>(&sm.rgb[32 * k + lane], prgb + 32 * k);
     }
-    if (rgb)
-        for (uint32_t i = lane; i < 3 * n; i += 32)
-            cp_async<sizeof(T)>(&sm.rgb[i], rgb + 3 * uint64_t(cs) + i);
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncwarp();
-    for (uint32_t i = lane; i < n; i += 32) {
-        double e = exp(-double(sm.sig[i]) * (sm.te[i] - sm.ts[i]));
-        sm.al[i] = kTransmittance ? e : 1.0 - e;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const uint32_t i = 32u * k + lane;
+        if (i < n) {
+            double e = exp(-double(sm.sig[i]) * (sm.te[i] - sm.ts[i]));
+            sm.al[i] = kTransmittance ? e : 1.0 - e;
+        }
     }
     __syncwarp();
 }
@@ -188,9 +203,16 @@ __device__ __forceinline__ Up load_up(const T* dc, const T* dop, const T* ddep, 
 template <typename T>
 __device__ __forceinline__ void write_out(BwdSmem<T>& sm, int lane, uint32_t cs, uint32_t n,
                                           T* __restrict__ g_rgb, T* __restrict__ g_sig) {
+    constexpr int R = Tile<T>::CH / 32;
     __syncwarp();
-    for (uint32_t i = lane; i < n; i += 32) g_sig[cs + i] = sm.sig[i];
-    for (uint32_t i = lane; i < 3 * n; i += 32) g_rgb[3 * uint64_t(cs) + i] = sm.rgb[i];
+    T* psg = g_sig + cs + lane;
+    T* prgb = g_rgb + 3 * uint64_t(cs) + lane;
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+        if (32u * k + lane < n) psg[32 * k] = sm.sig[32 * k + lane];
+#pragma unroll
+    for (int k = 0; k < 3 * R; ++k)
+        if (32u * k + lane < 3 * n) prgb[32 * k] = sm.rgb[32 * k + lane];
     __syncwarp();
 }
 
@@ -392,8 +414,10 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
                 __syncwarp();
                 // C (sample-parallel, every lane): w, v, d_rgb = d_color w (stored
                 // coalesced), and in place delta (ts), w v (te), T (1 - alpha) v (tr)
-                for (uint32_t r0 = 0; r0 < n; r0 += 32) {
-                    const uint32_t i = r0 + uint32_t(lane);
+#pragma unroll
+                for (int k = 0; k < Tile<T>::CH / 32; ++k) {
+                    const uint32_t i = 32u * k + uint32_t(lane);
+                    if (32u * k >= n) break;  // warp-uniform
                     const bool in = i < n;
                     const int o = in ? int(own[i]) : 0;
                     const Up uo{__shfl_sync(0xffffffffu, u.dcx, o), __shfl_sync(0xffffffffu, u.dcy, o),
@@ -404,7 +428,7 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
                         const double v = uo.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
                                                   double(sm.rgb[3 * i + 2]), 0.5 * (t0 + t1));
                         const double wgt = tr * a;
-                        T* gr = g_rgb + 3 * (uint64_t(base) + i);
+                        T* gr = g_rgb + 3 * uint64_t(base) + 3 * i;
                         gr[0] = T(uo.dcx * wgt);
                         gr[1] = T(uo.dcy * wgt);
                         gr[2] = T(uo.dcz * wgt);
@@ -424,7 +448,10 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
                     }
                 }
                 __syncwarp();
-                for (uint32_t i = lane; i < n; i += 32) g_sig[uint64_t(base) + i] = sm.sig[i];
+                T* psg = g_sig + base + lane;
+#pragma unroll
+                for (int k = 0; k < Tile<T>::CH / 32; ++k)
+                    if (32u * k + lane < n) psg[32 * k] = sm.sig[32 * k + lane];
                 __syncwarp();
             }
             g0 = g1 + 1;
