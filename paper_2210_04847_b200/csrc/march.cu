@@ -42,6 +42,11 @@ constexpr int kAccStride = 128;  // = the walk kernel's block size
 constexpr int VOXM = 4;
 __host__ __device__ constexpr int mbase(int m) { return m & 3; }
 __host__ __device__ constexpr bool mvox(int m) { return (m & VOXM) != 0; }
+// bit 3: k_march_walk holds the constant-density alpha table (P.atab_n entries) in
+// its dynamic shared memory, walk_dyn_smem
+constexpr int ATABM = 8;
+__host__ __device__ constexpr bool matab(int m) { return (m & ATABM) != 0; }
+extern __shared__ double walk_dyn_smem[];
 
 struct MarchParams {
     Contract k;
@@ -62,6 +67,7 @@ struct MarchParams {
     uint32_t max_cand;
     bool fast;            // fp32 DDA + filtered fp32 cell test (walk_fast)
     bool sphere_fast;     // SolidSphere field: filtered fp32 density decision
+    uint32_t atab_n;      // k_march_walk: alpha table length (n_steps, sphere_fast only) or 0
     float sph_c[3], sph_r, sph_r2, sph_cmax;
     double sph_sig32, sph_rgb32[3];  // SolidSphere sigma / rgb rounded through fp32 (fused forward)
     float step_f, m0_f, inv_step_f, near_f, far_f, Mf;
@@ -134,7 +140,7 @@ template <int MODE>
 __device__ __forceinline__ bool filter_sample(const MarchParams& P, Sink& s, uint64_t i, uint32_t ci,
                                               double t0, double t1, double sigma, DevError* err,
                                               D3 rgb = D3{0.0, 0.0, 0.0}, bool rounded = false,
-                                              double sg_r = 0.0);
+                                              double sg_r = 0.0, double alpha_pre = -1.0);
 
 // Handles one grid-passing candidate. Mirrors ray_marching.cpp:78,111-137.
 template <int MODE>
@@ -169,7 +175,7 @@ __device__ __forceinline__ bool on_candidate(const MarchParams& P, Sink& s, uint
 template <int MODE>
 __device__ __forceinline__ bool filter_sample(const MarchParams& P, Sink& s, uint64_t i, uint32_t ci,
                                               double t0, double t1, double sigma, DevError* err,
-                                              D3 rgb, bool rounded, double sg_r) {
+                                              D3 rgb, bool rounded, double sg_r, double alpha_pre) {
     if (!isfinite(sigma) || sigma < 0.0) {
         int kind = !isfinite(sigma) ? ERR_NONFINITE_SIGMA : ERR_NEGATIVE_SIGMA;
         atomicMin(&err->key, march_err_key(s.ray, ci, kind));
@@ -178,8 +184,8 @@ __device__ __forceinline__ bool filter_sample(const MarchParams& P, Sink& s, uin
     }
     // sigma == 0: alpha = 1 - exp(-0 * delta) = 0 exactly, never above a floor >= 0
     if (sigma == 0.0 && P.thr >= 0.0) return true;
-    double delta = t1 - t0;
-    double alpha = 1.0 - exp(-sigma * delta);
+    // alpha_pre: the same expression evaluated ahead (constant-density table)
+    const double alpha = alpha_pre >= 0.0 ? alpha_pre : 1.0 - exp(-sigma * (t1 - t0));
     if (alpha <= P.thr) return true;
     if (mbase(MODE) == FILL) {
         uint64_t o = s.base + s.n_kept;
@@ -482,7 +488,10 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
                                    : s.at32 ? d3(P.sph_rgb32[0], P.sph_rgb32[1], P.sph_rgb32[2])
                                             : d3(P.f.rgb[0], P.f.rgb[1], P.f.rgb[2]);
                 const double sg = !in ? 0.0 : s.at32 ? P.sph_sig32 : P.f.sigma;
-                if (!filter_sample<MODE>(P, s, uint64_t(j), ci, t0, t1, sigma, err, rgb, true, sg)) return;
+                // alpha of step j for the constant interior density (table) or computed
+                const double apre = matab(MODE) && in ? walk_dyn_smem[j] : -1.0;
+                if (!filter_sample<MODE>(P, s, uint64_t(j), ci, t0, t1, sigma, err, rgb, true, sg, apre))
+                    return;
                 ++j;
                 continue;
             }
@@ -589,7 +598,7 @@ struct FwdOut {
 
 // FAST instantiates only walk_fast (+ its exact fallback and the dense walk for
 // unsafe rays), so its register allocation is not the union of every walk.
-template <typename RT, bool FAST, typename AT, bool FWD, bool VOX>
+template <typename RT, bool FAST, typename AT, bool FWD, bool VOX, bool ATAB = false>
 __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
     MarchParams P, const RT* __restrict__ orig, const RT* __restrict__ dirs, uint64_t n_rays,
     uint32_t* __restrict__ counts, uint32_t* __restrict__ kept_idx, unsigned int* chunk_counter,
@@ -597,6 +606,15 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
     __shared__ double s_acc[FWD ? 6 : 1][kAccStride];
     const int lane = threadIdx.x & 31;
     unsigned long long emit_local = 0;
+    if (ATAB) {  // alpha per lattice step for the constant interior density (sphere)
+        for (uint32_t j = threadIdx.x; j < P.atab_n; j += blockDim.x) {
+            const double dj = double(j);
+            const double t0 = P.near_ + dj * P.step;
+            const double t1 = min_ref(P.near_ + (dj + 1.0) * P.step, P.far_);
+            walk_dyn_smem[j] = 1.0 - exp(-P.f.sigma * (t1 - t0));
+        }
+        __syncthreads();
+    }
     for (;;) {
         unsigned int chunk = 0;
         if (lane == 0) chunk = atomicAdd(chunk_counter, 1u);
@@ -616,7 +634,7 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
 #pragma unroll
                 for (int k = 1; k < 6; ++k) s.acc[k * kAccStride] = 0.0;
             }
-            constexpr int M = (FWD ? BUFFER_FWD : BUFFER) | (VOX ? VOXM : 0);
+            constexpr int M = (FWD ? BUFFER_FWD : BUFFER) | (VOX ? VOXM : 0) | (ATAB ? ATABM : 0);
             if (FAST) {
                 const D3 o = load3(orig, r), d = load3(dirs, r);
                 if (ray_safe(P, o, d))
@@ -1057,6 +1075,10 @@ void set_sphere_fast(MarchParams* P) {
     P->sph_cmax = float(cmax);
     P->sph_sig32 = double(float(f.sigma));
     for (int a = 0; a < 3; ++a) P->sph_rgb32[a] = double(float(f.rgb[a]));
+    // inside the sphere sigma is one constant, so alpha depends only on the lattice
+    // step: k_march_walk tabulates it per CTA (VMB_ATAB=0 disables)
+    static const int atab = env_int("VMB_ATAB", 1);
+    P->atab_n = P->sphere_fast && atab && P->n_steps <= 1024 ? uint32_t(P->n_steps) : 0u;
 }
 
 // VMB_MARCH_IMPL=twopass forces the count -> scan -> fill pipeline (A/B tests).
@@ -1150,18 +1172,26 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
     // persistent grid: exactly the resident capacity of the device
     auto launch_walk = [&](auto kernel, auto* o, auto* d, auto fo) {
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, 0);
+        const size_t dyn = size_t(P.atab_n) * sizeof(double);  // read only by ATAB kernels
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, dyn);
         if (per_sm < 1) per_sm = 4;
         static const int forced = env_int("VMB_WALK_CTAS", 0);
         if (forced > 0) per_sm = forced;
-        kernel<<<ctx->num_sms * per_sm, 128, 0, ctx->stream>>>(
+        kernel<<<ctx->num_sms * per_sm, 128, dyn, ctx->stream>>>(
             P, o, d, n, out->d_counts, kept_idx, counters, n_chunks, emitted, ctx->d_err, fo);
     };
     auto walk_vox = [&](auto* o, auto* d, auto VOXC) {
         using RT = std::remove_const_t<std::remove_pointer_t<decltype(o)>>;
         constexpr bool VX = decltype(VOXC)::value;
         const bool f64 = sr.dtype == VMB_F64;
-        if (P.fast) {
+        if (P.fast && P.atab_n && !VX) {  // SolidSphere: alpha table
+            if (!sr.fwd)
+                launch_walk(k_march_walk<RT, true, float, false, false, true>, o, d, FwdOut<float>{});
+            else if (f64)
+                launch_walk(k_march_walk<RT, true, double, true, false, true>, o, d, fwd_out<double>(sr));
+            else
+                launch_walk(k_march_walk<RT, true, float, true, false, true>, o, d, fwd_out<float>(sr));
+        } else if (P.fast) {
             if (!sr.fwd)
                 launch_walk(k_march_walk<RT, true, float, false, VX>, o, d, FwdOut<float>{});
             else if (f64)
