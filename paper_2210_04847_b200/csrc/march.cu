@@ -697,6 +697,7 @@ struct ShadeOut {
 // lane holds its own ray; a sample's ray is handed to its lane by shuffles. The
 // per-sample work touches registers/smem only, plus the coalesced output writes.
 constexpr int kExpandWarps = 8;
+constexpr size_t kExpandSmem = size_t(kExpandWarps) * kWalkCap * 32 * (2 * sizeof(uint32_t) + sizeof(uint16_t));
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -712,18 +713,34 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 #else
 #define VMB_EXPAND_BOUNDS __launch_bounds__(32 * kExpandWarps)
 #endif
-template <typename RT, typename AT, bool SHADE, bool VOX>
+// CONST (shading of a UniformBox / SolidSphere whose kept samples are all inside):
+// a kept sample has alpha > alpha_thre >= 0, so the march saw sigma > 0 at the
+// sample's midpoint, i.e. the constant interior density — and shading evaluates
+// the same field at the same point (time shift = identity), so rgb/sigma are the
+// field's constants: no ray, no position, no test.
+template <typename RT, typename AT, bool SHADE, bool VOX, bool CONST = false>
 __global__ void VMB_EXPAND_BOUNDS k_march_expand(
     double near_, double far_, double step, const uint32_t* __restrict__ counts,
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ kept_idx, uint64_t n_rays,
     double* __restrict__ ts, double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,
     uint32_t* __restrict__ overflow, unsigned int* n_overflow, ShadeOut<RT, AT, VOX> sh) {
-    __shared__ __align__(16) uint32_t s_idx[kExpandWarps][2][kWalkCap * 32];
+    constexpr bool RAYS = SHADE && !CONST;  // the per-sample shading needs the ray
+    // dynamic shared memory (kExpandSmem): per warp, two kept-index row buffers and
+    // the owner map of the chunk's output slots (lane | (k << 5), k = rank in the ray)
+    extern __shared__ __align__(16) uint32_t expand_smem[];
+    uint32_t(*s_idx)[2][kWalkCap * 32] = reinterpret_cast<uint32_t(*)[2][kWalkCap * 32]>(expand_smem);
+    uint16_t(*s_map)[kWalkCap * 32] =
+        reinterpret_cast<uint16_t(*)[kWalkCap * 32]>(expand_smem + kExpandWarps * 2 * kWalkCap * 32);
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const uint64_t n_chunks = (n_rays + 31) / 32;
     const uint64_t wstride = (uint64_t(gridDim.x) * blockDim.x) >> 5;
     const uint64_t c0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    AT c_rgb[3] = {AT(0), AT(0), AT(0)}, c_sig = AT(0);
+    if (CONST) {
+        c_rgb[0] = AT(sh.f.rgb[0]), c_rgb[1] = AT(sh.f.rgb[1]), c_rgb[2] = AT(sh.f.rgb[2]);
+        c_sig = AT(sh.f.sigma);
+    }
 
     // chunk-local state: count/offset of this lane's ray, its ray (RT), and the
     // number of staged rows
@@ -742,7 +759,7 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
     };
     auto load_rays = [&](uint64_t c, Stage& st) {
         const uint64_t r = c * 32 + lane;
-        if (SHADE && c < n_chunks && r < n_rays) {
+        if (RAYS && c < n_chunks && r < n_rays) {
 #pragma unroll
             for (int a = 0; a < 3; ++a) st.o[a] = sh.orig[3 * r + a], st.d[a] = sh.dirs[3 * r + a];
         }
@@ -756,6 +773,24 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
         }
         cp_async_commit();
     };
+    // one output slot p, owned by lane L (its k-th kept sample)
+    auto emit = [&](const uint32_t* sk, uint64_t chunk, uint64_t p, int L, uint32_t k, D3 o, D3 d) {
+        const uint32_t i = sk[k * 32 + L];
+        const double di = double(i);  // double(i + 1) == di + 1.0 exactly
+        const double t0 = near_ + di * step;
+        const double t1 = min_ref(near_ + (di + 1.0) * step, far_);
+        ts[p] = t0;
+        te[p] = t1;
+        idx[p] = uint32_t(chunk * 32 + L);
+        if (CONST) {
+            sh.rgb[3 * p] = c_rgb[0];
+            sh.rgb[3 * p + 1] = c_rgb[1];
+            sh.rgb[3 * p + 2] = c_rgb[2];
+            sh.sig[p] = c_sig;
+        } else if (SHADE) {
+            sh.shade_ray(o, d, p, t0, t1);
+        }
+    };
 
     Stage cur, nxt, nn;
     load_meta(c0, cur);
@@ -763,6 +798,7 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
     stage_rows(c0, cur, 0);
     load_meta(c0 + wstride, nxt);
     int buf = 0;
+    uint16_t* mp = s_map[wib];
     for (uint64_t chunk = c0; chunk < n_chunks; chunk += wstride, buf ^= 1) {
         // pipeline: rows + rays of the next chunk, counts of the one after
         stage_rows(chunk + wstride, nxt, buf ^ 1);
@@ -772,7 +808,8 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
         const uint64_t r = chunk * 32 + lane;
         const bool valid = r < n_rays;
         const uint32_t cnt = cur.cnt, off = cur.off;
-        if (cnt > uint32_t(kWalkCap)) overflow[atomicAdd(n_overflow, 1u)] = uint32_t(r);
+        const bool big = cnt > uint32_t(kWalkCap);
+        if (big) overflow[atomicAdd(n_overflow, 1u)] = uint32_t(r);
         const unsigned vmask = __ballot_sync(0xffffffffu, valid);
         const int last = 31 - __clz(vmask);
         const uint64_t base = __shfl_sync(0xffffffffu, off, 0);
@@ -780,43 +817,44 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
                              __shfl_sync(0xffffffffu, cnt, last);
         const RT ox = cur.o[0], oy = cur.o[1], oz = cur.o[2];  // shuffled in the ray's own type
         const RT dx = cur.d[0], dy = cur.d[1], dz = cur.d[2];
+        const bool mapped = !__any_sync(0xffffffffu, big);  // then end - base <= kWalkCap * 32
+        if (mapped)  // lane-serial: one 16-bit entry per kept sample
+            for (uint32_t k = 0; k < cnt; ++k) mp[off - uint32_t(base) + k] = uint16_t(lane | (k << 5));
         cp_async_wait1();  // this chunk's rows have landed
         __syncwarp();
         const uint32_t* sk = s_idx[wib][buf];
         for (uint64_t p0 = base; p0 < end; p0 += 32) {
             const uint64_t p = p0 + lane;
-            // owner = largest lane L with off_L <= p (zero-count lanes share the
-            // next lane's offset, so the largest such lane owns the slot)
+            const bool in = p < end && p < cap;
             int L = 0;
+            uint32_t k = 0;
+            if (mapped) {
+                if (in) {
+                    const uint32_t e = mp[p - base];
+                    L = int(e & 31u);
+                    k = e >> 5;
+                }
+            } else {
+                // owner = largest lane L with off_L <= p (zero-count lanes share the
+                // next lane's offset, so the largest such lane owns the slot)
 #pragma unroll
-            for (int stride = 16; stride > 0; stride >>= 1) {
-                int c = L + stride;
-                uint32_t v = __shfl_sync(0xffffffffu, off, c & 31);
-                if (c < 32 && uint64_t(v) <= p) L = c;
+                for (int stride = 16; stride > 0; stride >>= 1) {
+                    int c = L + stride;
+                    uint32_t v = __shfl_sync(0xffffffffu, off, c & 31);
+                    if (c < 32 && uint64_t(v) <= p) L = c;
+                }
+                k = uint32_t(p - __shfl_sync(0xffffffffu, off, L));
             }
-            const uint32_t loff = __shfl_sync(0xffffffffu, off, L);
-            D3 o, d;
-            if (SHADE) {
+            D3 o{}, d{};
+            if (RAYS) {
                 o = d3(double(__shfl_sync(0xffffffffu, ox, L)), double(__shfl_sync(0xffffffffu, oy, L)),
                        double(__shfl_sync(0xffffffffu, oz, L)));
                 d = d3(double(__shfl_sync(0xffffffffu, dx, L)), double(__shfl_sync(0xffffffffu, dy, L)),
                        double(__shfl_sync(0xffffffffu, dz, L)));
             }
-            if (p < end && p < cap) {
-                const uint64_t k = p - loff;
-                if (k < uint64_t(kWalkCap)) {
-                    const uint32_t i = sk[k * 32 + L];
-                    const double di = double(i);  // double(i + 1) == di + 1.0 exactly
-                    const double t0 = near_ + di * step;
-                    const double t1 = min_ref(near_ + (di + 1.0) * step, far_);
-                    ts[p] = t0;
-                    te[p] = t1;
-                    idx[p] = uint32_t(chunk * 32 + L);
-                    if (SHADE) sh.shade_ray(o, d, p, t0, t1);
-                }
-            }
+            if (in && k < uint32_t(kWalkCap)) emit(sk, chunk, p, L, k, o, d);
         }
-        __syncwarp();  // buffer `buf` is refilled two chunks from now
+        __syncwarp();  // buffer `buf` and the map are refilled from the next chunk on
         cur = nxt;
         nxt = nn;
     }
@@ -1111,21 +1149,46 @@ FwdOut<AT> fwd_out(const ShadeReq& sr) {
                       static_cast<AT*>(sr.depth), sr.time};
 }
 
+// Resident CTAs per SM of one expansion kernel (persistent grid), after opting it
+// in to kExpandSmem of dynamic shared memory — once per kernel (the kernel is the
+// template argument: instantiations share one function type).
+template <auto K>
+int expand_per_sm() {
+    static const int n = [] {
+        cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kExpandSmem));
+        int m = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, K, 32 * kExpandWarps, kExpandSmem);
+        return env_int("VMB_EXPAND_CTAS", m < 1 ? 2 : m);
+    }();
+    return n;
+}
+
 template <typename RT, typename AT, bool SHADE, bool FWD, bool VOX>
 void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
                          const uint32_t* kept_idx, uint32_t* overflow, unsigned int* n_overflow,
                          uint64_t n_chunks, const ShadeReq& sr) {
     ShadeOut<RT, AT, VOX> sh{static_cast<const RT*>(rays->d_origins), static_cast<const RT*>(rays->d_directions),
                         sr.f, sr.time, static_cast<AT*>(sr.rgb), static_cast<AT*>(sr.sig)};
-    static int per_sm = [] {  // persistent: exactly the resident blocks
-        int n = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_march_expand<RT, AT, SHADE, VOX>, 32 * kExpandWarps, 0);
-        return env_int("VMB_EXPAND_CTAS", n < 1 ? 4 : n);
-    }();
-    k_march_expand<RT, AT, SHADE, VOX><<<grid_blocks(ctx, n_chunks * 32, 32 * kExpandWarps, per_sm),
-                                    32 * kExpandWarps, 0, ctx->stream>>>(
-        P.near_, P.far_, P.step, out->d_counts, out->d_offsets, kept_idx, rays->n_rays, out->d_t_starts,
-        out->d_t_ends, out->d_ray_indices, out->capacity, overflow, n_overflow, sh);
+    auto launch = [&](auto kernel, int per_sm) {
+        kernel<<<grid_blocks(ctx, n_chunks * 32, 32 * kExpandWarps, per_sm), 32 * kExpandWarps, kExpandSmem,
+                 ctx->stream>>>(P.near_, P.far_, P.step, out->d_counts, out->d_offsets, kept_idx, rays->n_rays,
+                                out->d_t_starts, out->d_t_ends, out->d_ray_indices, out->capacity, overflow,
+                                n_overflow, sh);
+    };
+    // constant shading: every kept sample is inside a constant analytic field (see
+    // k_march_expand); needs the alpha floor, a positive density and an identity
+    // time shift
+    const vmb_field& f = sr.f;
+    bool ident = std::isfinite(sr.time) && (sr.time == 0.0 || (f.velocity[0] == 0.0 && f.velocity[1] == 0.0 &&
+                                                                f.velocity[2] == 0.0));
+    for (int a = 0; a < 3; ++a) ident = ident && std::isfinite(f.velocity[a]);
+    const bool cst = SHADE && !VOX && P.filter && P.thr >= 0.0 && ident && std::isfinite(f.sigma) &&
+                     f.sigma > 0.0 && (f.kind == VMB_FIELD_SOLID_SPHERE || f.kind == VMB_FIELD_UNIFORM_BOX) &&
+                     env_int("VMB_EXPAND_CONST", 1);
+    if (cst)
+        launch(k_march_expand<RT, AT, SHADE, VOX, true>, expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, true>>());
+    else
+        launch(k_march_expand<RT, AT, SHADE, VOX, false>, expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, false>>());
     k_march_fixup<RT, AT, SHADE, FWD, VOX><<<ctx->num_sms * 2, 128, 0, ctx->stream>>>(
         P, sh.orig, sh.dirs, out->d_offsets, out->d_t_starts, out->d_t_ends, out->d_ray_indices,
         out->capacity, overflow, n_overflow, ctx->d_err, sh, fwd_out<AT>(sr));
