@@ -405,7 +405,22 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
                 // dependent DMUL per sample; the owner map for the parallel phase
                 if (lane >= g0 && lane <= g1) {
                     double t = 1.0;
-                    for (uint32_t i = rr.off - base; i < rr.end - base; ++i) {
+                    uint32_t i = rr.off - base;
+                    const uint32_t e = rr.end - base;
+                    for (; i + 4 <= e; i += 4) {  // the 4 loads issue before the chain
+                        const double f0 = 1.0 - sm.al[i], f1 = 1.0 - sm.al[i + 1];
+                        const double f2 = 1.0 - sm.al[i + 2], f3 = 1.0 - sm.al[i + 3];
+                        sm.tr[i] = t;
+                        t *= f0;
+                        sm.tr[i + 1] = t;
+                        t *= f1;
+                        sm.tr[i + 2] = t;
+                        t *= f2;
+                        sm.tr[i + 3] = t;
+                        t *= f3;
+                        own[i] = own[i + 1] = own[i + 2] = own[i + 3] = uint8_t(lane);
+                    }
+                    for (; i < e; ++i) {
                         sm.tr[i] = t;
                         own[i] = uint8_t(lane);
                         t *= 1.0 - sm.al[i];
@@ -442,7 +457,23 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
                 // dependent DADD per sample
                 if (lane >= g0 && lane <= g1) {
                     double suffix = 0.0;
-                    for (uint32_t i = rr.end - base; i-- > rr.off - base;) {
+                    uint32_t i = rr.end - base;
+                    const uint32_t b = rr.off - base;
+                    for (; i >= b + 4; i -= 4) {  // loads first, then the chain
+                        const double d3_ = sm.ts[i - 1], a3 = sm.tr[i - 1], w3 = sm.te[i - 1];
+                        const double d2_ = sm.ts[i - 2], a2 = sm.tr[i - 2], w2 = sm.te[i - 2];
+                        const double d1_ = sm.ts[i - 3], a1 = sm.tr[i - 3], w1 = sm.te[i - 3];
+                        const double d0_ = sm.ts[i - 4], a0 = sm.tr[i - 4], w0 = sm.te[i - 4];
+                        sm.sig[i - 1] = T(d3_ * (a3 - suffix));
+                        suffix += w3;
+                        sm.sig[i - 2] = T(d2_ * (a2 - suffix));
+                        suffix += w2;
+                        sm.sig[i - 3] = T(d1_ * (a1 - suffix));
+                        suffix += w1;
+                        sm.sig[i - 4] = T(d0_ * (a0 - suffix));
+                        suffix += w0;
+                    }
+                    while (i-- > b) {
                         sm.sig[i] = T(sm.ts[i] * (sm.tr[i] - suffix));
                         suffix += sm.te[i];
                     }
