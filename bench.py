@@ -162,7 +162,7 @@ class Clocks:
 PHASE_KERNELS = {"march": ["k_march_walk", "k_scan_tiles", "k_scan_sums", "k_scan_add",
                            "k_march_expand", "k_march_fixup"],
                  "shade": ["k_shade"], "render_forward": ["k_forward"],
-                 "render_backward": ["k_backward"]}
+                 "render_backward": ["k_backward_hy"]}
 
 
 def traffic_of(phase):
