@@ -224,6 +224,10 @@ int vmb_grid_write(vmb_ctx* ctx, vmb_grid* g, const uint8_t* h_bits, const doubl
 /* The marcher's acceleration structure (not in the reference): per cell the L-inf
  * distance in cells to the nearest occupied cell, capped (*h_cap), u8 [n_cells]. */
 int vmb_grid_read_distance(vmb_ctx* ctx, const vmb_grid* g, uint8_t* h_dist, uint32_t* h_cap);
+/* The marcher's ray clip box (not in the reference): bounding box of the occupied
+ * cells in cell units, h_box = {min x, y, z, max x + 1, y + 1, z + 1}; min >= max on
+ * an axis when no cell is occupied. */
+int vmb_grid_occupied_bbox(vmb_ctx* ctx, const vmb_grid* g, uint32_t* h_box);
 const uint32_t* vmb_grid_device_bits(const vmb_grid* g);
 const double* vmb_grid_device_cache(const vmb_grid* g);
 

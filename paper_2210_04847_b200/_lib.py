@@ -192,6 +192,7 @@ SIGNATURES = {
     "vmb_grid_read": (I32, [VP, VP, VP, VP]),
     "vmb_grid_write": (I32, [VP, VP, VP, VP]),
     "vmb_grid_read_distance": (I32, [VP, VP, VP, P(C.c_uint32)]),
+    "vmb_grid_occupied_bbox": (I32, [VP, VP, VP]),
     "vmb_grid_device_bits": (VP, [VP]),
     "vmb_grid_device_cache": (VP, [VP]),
     "vmb_march_field": (I32, [VP, VP, P(Rays), P(Field), P(MarchConfig), P(Samples), P(U64),

@@ -577,6 +577,12 @@ class OccupancyGrid:
         check(self.dev.lib.vmb_grid_read_distance(self.dev.h, self.h, d.ctypes.data, C.byref(cap)))
         return d, int(cap.value)
 
+    def occupied_bbox(self) -> np.ndarray:
+        """The marcher's ray clip box: occupied cells' {min xyz, max+1 xyz} (u32[6])."""
+        b = np.zeros(6, np.uint32)
+        check(self.dev.lib.vmb_grid_occupied_bbox(self.dev.h, self.h, b.ctypes.data))
+        return b
+
     def packed_bits(self) -> np.ndarray:
         b = np.zeros((self.n_cells + 7) // 8, np.uint8)
         check(self.dev.lib.vmb_grid_read(self.dev.h, self.h, b.ctypes.data, None))

@@ -196,6 +196,45 @@ __global__ void k_coarse(const uint32_t* __restrict__ bits, uint32_t res, uint32
     }
 }
 
+// Bounding box of the occupied cells (min and max+1 per axis) by warp reductions
+// and one atomic per warp and axis; bbox is preset to {~0 x3, 0 x3}.
+__global__ void k_bbox(const uint32_t* __restrict__ bits, uint32_t res, uint64_t n_words,
+                       uint32_t* __restrict__ bbox) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    uint32_t lo[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, hi[3] = {0u, 0u, 0u};
+    for (uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < n_words; w += stride) {
+        uint32_t m = __ldg(bits + w);
+        if (m && res % 32 == 0) {  // the word is one piece of an x-row: O(1)
+            const uint64_t c0 = w * 32;
+            const uint32_t xb = uint32_t(c0 % res), y = uint32_t((c0 / res) % res), z = uint32_t(c0 / (uint64_t(res) * res));
+            lo[0] = min(lo[0], xb + uint32_t(__ffs(m) - 1)), hi[0] = max(hi[0], xb + 32u - uint32_t(__clz(m)));
+            lo[1] = min(lo[1], y), lo[2] = min(lo[2], z);
+            hi[1] = max(hi[1], y + 1), hi[2] = max(hi[2], z + 1);
+            m = 0;
+        }
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1u;
+            const uint64_t c = w * 32 + uint64_t(b);
+            const uint32_t x = uint32_t(c % res), y = uint32_t((c / res) % res), z = uint32_t(c / (uint64_t(res) * res));
+            lo[0] = min(lo[0], x), lo[1] = min(lo[1], y), lo[2] = min(lo[2], z);
+            hi[0] = max(hi[0], x + 1), hi[1] = max(hi[1], y + 1), hi[2] = max(hi[2], z + 1);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = __reduce_min_sync(0xffffffffu, lo[a]);
+        hi[a] = __reduce_max_sync(0xffffffffu, hi[a]);
+    }
+    if ((threadIdx.x & 31) == 0 && hi[0]) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            atomicMin(bbox + a, lo[a]);
+            atomicMax(bbox + 3 + a, hi[a]);
+        }
+    }
+}
+
 __global__ void k_popcount(const uint32_t* __restrict__ bits, uint64_t n_words,
                            unsigned long long* out) {
     unsigned long long local = 0;
@@ -284,6 +323,7 @@ int grid_alloc(vmb_grid* g) {
     if (e == cudaSuccess) e = cudaMalloc(&g->coarse, g->coarse_words * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMalloc(&g->dist, g->n_cells);
     if (e == cudaSuccess) e = cudaMalloc(&g->dist_tmp, g->n_cells);
+    if (e == cudaSuccess) e = cudaMalloc(&g->bbox, 6 * sizeof(uint32_t));
     return e == cudaSuccess ? VMB_OK : cuda_fail(e, "grid allocation");
 }
 
@@ -389,6 +429,9 @@ int grid_rebuild_coarse(vmb_ctx* ctx, vmb_grid* g) {
     (void)opted;
     k_dist_axis_tiled<<<tiles, 256, smem, ctx->stream>>>(g->dist, g->res, r, plane, g->dist_tmp);      // y
     k_dist_axis_tiled<<<tiles, 256, smem, ctx->stream>>>(g->dist_tmp, g->res, plane, r, g->dist);      // z
+    cudaMemsetAsync(g->bbox, 0xff, 3 * sizeof(uint32_t), ctx->stream);
+    cudaMemsetAsync(g->bbox + 3, 0, 3 * sizeof(uint32_t), ctx->stream);
+    k_bbox<<<grid_blocks(ctx, g->n_words, 256, 4), 256, 0, ctx->stream>>>(g->bits, g->res, g->n_words, g->bbox);
     return launch_check("grid coarse/dist");
 }
 
@@ -447,6 +490,7 @@ int vmb_grid_destroy(vmb_grid* g) {
     cudaFree(g->coarse);
     cudaFree(g->dist);
     cudaFree(g->dist_tmp);
+    cudaFree(g->bbox);
     cudaFree(g->probed);
     delete g;
     return VMB_OK;
@@ -470,6 +514,7 @@ int vmb_grid_clone(vmb_ctx* ctx, const vmb_grid* src, vmb_grid** out) {
     cudaMemcpyAsync(g->bits, src->bits, g->n_words * 4, cudaMemcpyDeviceToDevice, ctx->stream);
     cudaMemcpyAsync(g->coarse, src->coarse, g->coarse_words * 4, cudaMemcpyDeviceToDevice, ctx->stream);
     cudaMemcpyAsync(g->dist, src->dist, g->n_cells, cudaMemcpyDeviceToDevice, ctx->stream);
+    cudaMemcpyAsync(g->bbox, src->bbox, 6 * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream);
     rc = launch_check("grid clone");
     if (rc) {
         vmb_grid_destroy(g);
@@ -637,6 +682,12 @@ int vmb_grid_read(vmb_ctx* ctx, const vmb_grid* g, uint8_t* h_bits, double* h_ca
         cudaMemcpyAsync(h_cache, g->cache, g->n_cells * 8, cudaMemcpyDeviceToHost, ctx->stream);
     cudaError_t e = cudaStreamSynchronize(ctx->stream);
     return e == cudaSuccess ? VMB_OK : cuda_fail(e, "grid read");
+}
+
+int vmb_grid_occupied_bbox(vmb_ctx* ctx, const vmb_grid* g, uint32_t* h_box) {
+    cudaError_t e = cudaMemcpyAsync(h_box, g->bbox, 6 * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    return e == cudaSuccess ? VMB_OK : cuda_fail(e, "grid bbox");
 }
 
 int vmb_grid_read_distance(vmb_ctx* ctx, const vmb_grid* g, uint8_t* h_dist, uint32_t* h_cap) {

@@ -54,6 +54,7 @@ struct MarchParams {
     const uint32_t* bits;
     const uint32_t* coarse;
     const uint8_t* dist;  // capped L-inf distance to the nearest occupied cell
+    const uint32_t* bbox; // occupied cells' bounding box {min xyz, max+1 xyz} (vmb_grid::bbox)
     uint32_t block, res_c;
     double scale[3];      // R / size_k: world -> fine-cell units (approximate, DDA only)
     double near_, far_, step;
@@ -405,15 +406,21 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
         float e = ldexpf(3.0f * omax + 7.0f * dmax * P.Mf + 2.0f * P.sph_cmax, -24);
         sph_err = 4.0f * (ldexpf(3.0f * P.sph_r2, -24) + 3.5f * P.sph_r * e + 3.0f * e * e) + 1e-12f;
     }
-    const float EPSD = 1e-3f + 4.0f * E;  // domain guard for the fp32 clip
+    const float EPSD = 1e-3f + 4.0f * E;  // guard for the fp32 clip
+    // ray_aabb_intersect against the guarded bounding box of the occupied cells
+    // (inside the domain [0, R]^3): every lattice step outside it is an empty cell
+    // or outside the domain, so the walk covers only the clipped range (+2 steps)
     float tlo = P.near_f, thi = P.far_f;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {  // ray_aabb_intersect against the guarded domain
+    for (int a = 0; a < 3; ++a) {
+        const uint32_t b0 = __ldg(P.bbox + a), b1 = __ldg(P.bbox + 3 + a);
+        if (b0 >= b1) return;  // no occupied cell: no candidate anywhere
+        const float lo = float(b0) - EPSD, hi = fminf(float(b1), Rf) + EPSD;
         if (B[a] == 0.0f) {
-            if (A[a] < -EPSD || A[a] > Rf + EPSD) return;
+            if (A[a] < lo || A[a] > hi) return;
         } else {
             float inv = __frcp_rn(B[a]);
-            float ta = (-EPSD - A[a]) * inv, tb = (Rf + EPSD - A[a]) * inv;
+            float ta = (lo - A[a]) * inv, tb = (hi - A[a]) * inv;
             tlo = fmaxf(tlo, fminf(ta, tb));
             thi = fminf(thi, fmaxf(ta, tb));
         }
@@ -1020,6 +1027,7 @@ int march_params(const vmb_grid* g, const vmb_rays* rays, const vmb_march_config
     P->bits = g->bits;
     P->coarse = g->coarse;
     P->dist = g->dist;
+    P->bbox = g->bbox;
     P->block = g->block;
     P->res_c = g->res_c;
     P->scale[0] = double(g->res) / g->k.size.x;

@@ -81,6 +81,9 @@ struct vmb_grid {
     // cell, capped at kDistCap (0 = occupied). Lets the marcher jump D-1 cells.
     uint8_t* dist = nullptr;       // [n_cells]
     uint8_t* dist_tmp = nullptr;   // [n_cells] scratch of the separable transform
+    // Bounding box of the occupied cells, cell units: {min x, y, z, max x+1, y+1, z+1};
+    // min > max - 1 on some axis when no cell is occupied. Rebuilt with the distance map.
+    uint32_t* bbox = nullptr;      // [6]
     double* probed = nullptr;      // [n_cells] scratch for the sharded / callback update
 };
 

@@ -420,6 +420,50 @@ def test_march_skipping_random_grids(dev, orc, density):
         assert st.samples_emitted == q.samples_emitted
 
 
+@pytest.mark.parametrize("R", [48, 64])
+def test_march_bbox_clip_edges(dev, orc, R):
+    """Rays are clipped to the occupied cells' bounding box (+ guard): occupied cells on
+    the domain's faces and corners (the max face maps to cell R-1), a lone interior
+    cell and a dense sub-box, crossed by axis-aligned rays, rays through the corners
+    and rays starting on cell faces — identical samples and emitted counts."""
+    rng = np.random.default_rng(R)
+    field = Field.box((0.0, 0.0, 0.0), (1.0, 1.0, 1.0), 5.0)
+    cases = []
+    m = np.zeros((R, R, R), np.uint8)  # [z][y][x]
+    m[R - 1, R - 1, R - 1] = 1
+    m[0, 0, 0] = 1
+    cases.append(m)
+    m = np.zeros((R, R, R), np.uint8)
+    m[:, :, R - 1] = rng.uniform(size=(R, R)) < 0.3  # x = R-1 face
+    cases.append(m)
+    m = np.zeros((R, R, R), np.uint8)
+    m[R // 3, R // 2, R // 4] = 1
+    cases.append(m)
+    m = np.zeros((R, R, R), np.uint8)
+    m[10:21, 5:17, 30:41] = rng.uniform(size=(11, 12, 11)) < 0.3
+    cases.append(m)
+    o, d = _stress_rays(rng, 3000)
+    # rays aimed exactly at the corners / face centres from outside
+    tgt = np.array([[0, 0, 0], [1, 1, 1], [1, 0.5, 0.5], [0.5, 1, 0.5], [1, 1, 0]], float)
+    src = rng.uniform(-0.5, 1.5, (len(tgt) * 40, 3))
+    dd = np.repeat(tgt, 40, 0) - src
+    dd /= np.sqrt((dd * dd).sum(1))[:, None]
+    o, d = np.concatenate([o, src]), np.concatenate([d, dd])
+    for mask in cases:
+        flat = mask.ravel()
+        g = api.OccupancyGrid(R, Contraction.aabb(), dev=dev)
+        og = orc.grid(R, O.Contraction.aabb())
+        g.seed_mask(flat)
+        og.seed_mask(flat)
+        for step in (0.0041, 0.0173):
+            cfg = MarchConfig(step, 1e-4, 1e-2)
+            st = MarchStats()
+            p = api.march(api.RayBatch.create(o, d, 0.0, 3.0, dev), g, field, cfg, stats=st)
+            q = orc.march_field(o, d, 0.0, 3.0, og, ofield(field), ocfg(cfg), 4)
+            same_packed(p, q)
+            assert st.samples_emitted == q.samples_emitted
+
+
 def test_march_grazing_sphere(dev, orc):
     """Rays tangent to the sphere at distance r +- tiny: the filtered fp32 density test
     must fall back to fp64 exactly where it matters."""
@@ -476,3 +520,10 @@ def test_distance_map_is_exact_capped_chebyshev(dev, res, density):
         want = np.full(grid.shape, cap)
     want = np.minimum(want, cap).astype(np.uint8).ravel()
     assert np.array_equal(dist, want), np.argwhere(dist != want)[:5]
+    # the ray clip box: the occupied cells' bounding box, exactly
+    box = g.occupied_bbox()
+    if grid.any():
+        z, y, x = np.nonzero(grid)
+        assert list(box) == [x.min(), y.min(), z.min(), x.max() + 1, y.max() + 1, z.max() + 1]
+    else:
+        assert all(box[a] >= box[3 + a] for a in range(3))
