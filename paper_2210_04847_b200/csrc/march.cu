@@ -555,6 +555,12 @@ __device__ __forceinline__ void walk(const MarchParams& P, Sink& s, const RT* __
 //   k_march_fixup  re-walks the rare rays with more than kWalkCap kept samples.
 // ---------------------------------------------------------------------------
 constexpr int kWalkCap = 24;
+#ifndef VMB_WALK_CLAIM
+#define VMB_WALK_CLAIM 1
+#endif
+// chunks per work-stealing ticket (measured at config 5: 1 = 0.782, 2 = 0.797,
+// 4 = 0.807 ms/step; the L1 prefetch of the next claimed chunk does not pay)
+constexpr int kClaim = VMB_WALK_CLAIM;
 
 // FAST instantiates only walk_fast (+ its exact fallback and the dense walk for
 // unsafe rays), so its register allocation is not the union of every walk.
@@ -622,11 +628,23 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
         }
         __syncthreads();
     }
+    // chunks are claimed kClaim at a time; the rays of the next chunk of a claim are
+    // prefetched into L1 while the current one is walked
+    unsigned int chunk = 0, claim_end = 0;
     for (;;) {
-        unsigned int chunk = 0;
-        if (lane == 0) chunk = atomicAdd(chunk_counter, 1u);
-        chunk = __shfl_sync(0xffffffffu, chunk, 0);
+        if (chunk == claim_end) {
+            if (lane == 0) chunk = atomicAdd(chunk_counter, unsigned(kClaim));
+            chunk = __shfl_sync(0xffffffffu, chunk, 0);
+            claim_end = chunk + kClaim;
+        }
         if (chunk >= n_chunks) break;
+        if (chunk + 1 < claim_end && chunk + 1 < n_chunks) {
+            const uint64_t rn = uint64_t(chunk + 1) * 32 + lane;
+            if (rn < n_rays) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(orig + 3 * rn));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(dirs + 3 * rn));
+            }
+        }
         const uint64_t r = uint64_t(chunk) * 32 + lane;
         if (r < n_rays) {
             Sink s;
@@ -662,6 +680,7 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
             }
         }
         __syncwarp();
+        ++chunk;
     }
     if (emitted) {
         for (int o = 16; o > 0; o >>= 1) emit_local += __shfl_xor_sync(0xffffffffu, emit_local, o);
