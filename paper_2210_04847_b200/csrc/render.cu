@@ -26,7 +26,10 @@
 namespace vmb {
 namespace {
 
-constexpr int kWarps = 8;  // 256 threads per CTA
+#ifndef VMB_RENDER_WARPS
+#define VMB_RENDER_WARPS 8
+#endif
+constexpr int kWarps = VMB_RENDER_WARPS;  // threads per CTA / 32
 
 template <typename T> struct Tile;
 template <> struct Tile<float> { static constexpr int CH = 128; };
