@@ -280,7 +280,7 @@ class ResidentPipeline:
     Per-ray outputs land in full-batch arrays, so they can be compared with the
     single-call step bit for bit."""
 
-    def __init__(self, args, api, dev, grid, field, cfg, rays_dev, ups_dev, N):
+    def __init__(self, args, api, dev, grid, field, cfg, rays_dev, ups_dev, N, total_samples):
         from paper_2210_04847_b200._lib import VMB_F32
         self.api, self.dev, self.grid, self.field, self.cfg = api, dev, grid, field, cfg
         self.L = dev.lib
@@ -288,7 +288,7 @@ class ResidentPipeline:
         self.N = N
         self.bounds = [(N * i // self.K, N * (i + 1) // self.K) for i in range(self.K)]
         cmax = max(e - b for b, e in self.bounds)
-        cap = 8 * cmax
+        cap = total_samples + 1024  # no sub-batch holds more samples than the whole batch
         self.ctxs = [dev] + [api.Device(dev.index) for _ in range(self.S - 1)]
         self.rays_dev, self.ups_dev = rays_dev, ups_dev
         self.outs = [dev.empty(N * w, np.float32) for w in (3, 1, 1)]
@@ -582,7 +582,7 @@ def main():
     # single-call step above.
     pipe = None
     if args.fusion == "forward" and not args.grid_update_every and args.streams * args.chunks > 1:
-        pipe = ResidentPipeline(args, api, dev, grid, field, cfg, (do_, dd_), (up_c, up_o, up_d), N)
+        pipe = ResidentPipeline(args, api, dev, grid, field, cfg, (do_, dd_), (up_c, up_o, up_d), N, S0)
     clocks = Clocks(dist.local)
     for _ in range(max(args.warmup, 3)):
         step()

@@ -63,13 +63,18 @@ struct RayRange {
 };
 
 __device__ __forceinline__ RayRange ray_range(const uint32_t* __restrict__ offsets,
-                                              const uint32_t* __restrict__ counts, uint64_t n_rays,
+                                              const uint32_t* __restrict__ counts, uint64_t n_rays, uint64_t n_samples,
                                               uint64_t warp_id, int lane) {
     RayRange rr;
     rr.r = warp_id * 32 + lane;
     rr.valid = rr.r < n_rays;
-    rr.off = rr.valid ? __ldg(offsets + rr.r) : 0u;
-    rr.end = rr.valid ? rr.off + __ldg(counts + rr.r) : 0u;
+    // samples at or beyond n_samples (the buffers' length) are ignored: a ray range
+    // is clamped into [0, n_samples), which keeps the ranges contiguous
+    const uint64_t ns = n_samples < 0xffffffffull ? n_samples : 0xffffffffull;
+    const uint64_t o64 = rr.valid ? __ldg(offsets + rr.r) : 0u;
+    const uint64_t e64 = rr.valid ? o64 + __ldg(counts + rr.r) : 0u;
+    rr.off = uint32_t(o64 < ns ? o64 : ns);
+    rr.end = uint32_t(e64 < ns ? e64 : ns);
     const uint32_t next_off = __shfl_down_sync(0xffffffffu, rr.off, 1);
     const bool next_valid = __shfl_down_sync(0xffffffffu, int(rr.valid), 1);
     const bool ok = !(rr.valid && lane < 31 && next_valid) || rr.end == next_off;
@@ -143,7 +148,7 @@ struct Fwd {
 
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_forward(
-    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays,
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays, uint64_t n_samples,
     const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
     const T* __restrict__ sig, T* __restrict__ color, T* __restrict__ opacity, T* __restrict__ depth) {
     __shared__ FwdSmem<T> smem[kWarps];
@@ -152,7 +157,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_forward(
     const uint64_t n_warps = (n_rays + 31) / 32;
     for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
          w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-        const RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
+        const RayRange rr = ray_range(offsets, counts, n_rays, n_samples, w, lane);
         Fwd acc;
         if (rr.contiguous) {
             for (uint32_t cs = rr.s0; cs < rr.s1; cs += Tile<T>::CH) {
@@ -304,7 +309,7 @@ __device__ void bwd_two_sweep(BwdSmem<T>* smp, int lane, bool active, bool stage
 
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward(
-    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays,
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays, uint64_t n_samples,
     const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
     const T* __restrict__ sig, const T* __restrict__ dc, const T* __restrict__ dop,
     const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig) {
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward(
     const uint64_t n_warps = (n_rays + 31) / 32;
     for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
          w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-        const RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
+        const RayRange rr = ray_range(offsets, counts, n_rays, n_samples, w, lane);
         const Up u = load_up(dc, dop, ddep, rr.r, rr.valid);
         if (!rr.contiguous) {
             bwd_two_sweep(&sm, lane, rr.valid, false, rr.off, rr.end, 0u, 0u, u, ts, te, rgb, sig,
@@ -367,7 +372,7 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward(
 
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
-    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays,
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays, uint64_t n_samples,
     const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
     const T* __restrict__ sig, const T* __restrict__ dc, const T* __restrict__ dop,
     const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig) {
@@ -380,7 +385,7 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
     const uint64_t n_warps = (n_rays + 31) / 32;
     for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
          w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-        const RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
+        const RayRange rr = ray_range(offsets, counts, n_rays, n_samples, w, lane);
         const Up u = load_up(dc, dop, ddep, rr.r, rr.valid);
         if (!rr.contiguous) {
             bwd_two_sweep(&sm, lane, rr.valid, false, rr.off, rr.end, 0u, 0u, u, ts, te, rgb, sig,
@@ -519,7 +524,7 @@ __device__ __forceinline__ T shfl_idx(T v, int src) { return __shfl_sync(0xfffff
 
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32) k_backward_sp(
-    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays,
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays, uint64_t n_samples,
     const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
     const T* __restrict__ sig, const T* __restrict__ dc, const T* __restrict__ dop,
     const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig) {
@@ -528,7 +533,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_backward_sp(
     BwdSmem<T>* no_smem = nullptr;  // the two-sweep path below runs unstaged
     for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
          w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-        const RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
+        const RayRange rr = ray_range(offsets, counts, n_rays, n_samples, w, lane);
         if (!rr.contiguous) {
             const Up u = load_up(dc, dop, ddep, rr.r, rr.valid);
             bwd_two_sweep(no_smem, lane, rr.valid, false, rr.off, rr.end, 0u, 0u, u, ts, te, rgb, sig,
@@ -680,7 +685,7 @@ int backward_impl() {
 // ------------------------------------------------------------------ transmittance
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_transmittance(
-    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays,
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays, uint64_t n_samples,
     const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ sig,
     T* __restrict__ out) {
     __shared__ BwdSmem<T> smem[kWarps];
@@ -689,7 +694,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_transmittance(
     const uint64_t n_warps = (n_rays + 31) / 32;
     for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
          w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-        const RayRange rr = ray_range(offsets, counts, n_rays, w, lane);
+        const RayRange rr = ray_range(offsets, counts, n_rays, n_samples, w, lane);
         double t = 1.0;  // rendering.cpp:26-31: out = T; T *= exp(-sigma * delta)
         if (rr.contiguous) {
             for (uint32_t cs = rr.s0; cs < rr.s1; cs += Tile<T>::CH) {
@@ -717,13 +722,15 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_transmittance(
 // render_attribute (rendering.cpp:114-134): dim-D values, thread per ray.
 template <typename T>
 __global__ void k_attribute(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts,
-                            uint64_t n_rays, const double* __restrict__ ts, const double* __restrict__ te,
+                            uint64_t n_rays, uint64_t n_samples, const double* __restrict__ ts, const double* __restrict__ te,
                             const T* __restrict__ sig, const T* __restrict__ values, uint64_t dim,
                             T* __restrict__ out) {
     for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rays;
          r += uint64_t(gridDim.x) * blockDim.x) {
         for (uint64_t k = 0; k < dim; ++k) out[r * dim + k] = T(0);
         uint64_t b = offsets[r], e = b + counts[r];
+        b = b < n_samples ? b : n_samples;  // samples beyond the buffers are ignored
+        e = e < n_samples ? e : n_samples;
         double trans = 1.0;
         for (uint64_t s = b; s < e; ++s) {
             double alpha = 1.0 - exp(-double(sig[s]) * (te[s] - ts[s]));
@@ -779,12 +786,12 @@ int vmb_render_forward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, 
     int blocks = render_blocks(ctx, p->n_rays);
     if (dtype == VMB_F32)
         k_forward<float><<<blocks, kWarps * 32, 0, ctx->stream>>>(
-            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
             static_cast<const float*>(rgb), static_cast<const float*>(sig), static_cast<float*>(color),
             static_cast<float*>(opacity), static_cast<float*>(depth));
     else
         k_forward<double><<<blocks, kWarps * 32, 0, ctx->stream>>>(
-            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
             static_cast<const double*>(rgb), static_cast<const double*>(sig), static_cast<double*>(color),
             static_cast<double*>(opacity), static_cast<double*>(depth));
     return launched("render_forward");
@@ -798,13 +805,13 @@ int vmb_render_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb,
     const int impl = backward_impl();
     if (dtype == VMB_F32)
         (impl == 1 ? k_backward_sp<float> : impl == 2 ? k_backward<float> : k_backward_hy<float>)<<<blocks, kWarps * 32, 0, ctx->stream>>>(
-            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
             static_cast<const float*>(rgb), static_cast<const float*>(sig), static_cast<const float*>(dc),
             static_cast<const float*>(dop), static_cast<const float*>(ddep), static_cast<float*>(g_rgb),
             static_cast<float*>(g_sig));
     else
         (impl == 1 ? k_backward_sp<double> : impl == 2 ? k_backward<double> : k_backward_hy<double>)<<<blocks, kWarps * 32, 0, ctx->stream>>>(
-            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
             static_cast<const double*>(rgb), static_cast<const double*>(sig),
             static_cast<const double*>(dc), static_cast<const double*>(dop),
             static_cast<const double*>(ddep), static_cast<double*>(g_rgb), static_cast<double*>(g_sig));
@@ -816,11 +823,11 @@ int vmb_transmittance(vmb_ctx* ctx, const vmb_packed_view* p, const void* sig, v
     int blocks = render_blocks(ctx, p->n_rays);
     if (dtype == VMB_F32)
         k_transmittance<float><<<blocks, kWarps * 32, 0, ctx->stream>>>(
-            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
             static_cast<const float*>(sig), static_cast<float*>(out));
     else
         k_transmittance<double><<<blocks, kWarps * 32, 0, ctx->stream>>>(
-            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
             static_cast<const double*>(sig), static_cast<double*>(out));
     return launched("transmittance");
 }
@@ -832,11 +839,11 @@ int vmb_render_attribute(vmb_ctx* ctx, const vmb_packed_view* p, const void* sig
     int blocks = grid_blocks(ctx, p->n_rays, 128, 16);
     if (dtype == VMB_F32)
         k_attribute<float><<<blocks, 128, 0, ctx->stream>>>(
-            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
             static_cast<const float*>(sig), static_cast<const float*>(values), dim, static_cast<float*>(out));
     else
         k_attribute<double><<<blocks, 128, 0, ctx->stream>>>(
-            p->d_offsets, p->d_counts, p->n_rays, p->d_t_starts, p->d_t_ends,
+            p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
             static_cast<const double*>(sig), static_cast<const double*>(values), dim,
             static_cast<double*>(out));
     return launched("render_attribute");

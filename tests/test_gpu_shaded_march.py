@@ -186,3 +186,54 @@ def test_step_is_bitwise_reproducible_and_chunk_independent():
     assert np.array_equal(np.concatenate([pa.t_starts, pb.t_starts]), p1.t_starts)
     for a, b, full, w in zip(oa, ob, o1, (3, 1, 1)):
         assert np.array_equal(np.concatenate([a, b]), full)
+
+
+def test_async_capacity_overflow_is_contained():
+    """vmb_march_render_field_async with too small a sample capacity: the total on the
+    device exceeds the capacity, samples beyond it are dropped, and the render
+    kernels run on the truncated view ignore sample positions beyond n_samples
+    instead of reading/writing past the buffers; rays wholly inside the capacity
+    get the full run's gradients."""
+    import ctypes as C
+    from paper_2210_04847_b200._lib import VMB_F32 as F32, check
+    dev = api.Device(0)
+    L = dev.lib
+    field = Field.sphere(**workload.SPHERE)
+    g = api.OccupancyGrid(128, Contraction.aabb(), dev=dev)
+    for s in workload.grid_warmup_seeds(8, 5):
+        g.update_field(field, 0.95, s)
+    o, d = workload.orbit_rays(64, angle=0.9)
+    n = len(o)
+    rays, keep = _rays(dev, o, d, 0.2, 1.0, np.float32)
+    cfg = MarchConfig(5e-3, 1e-4, 1e-2)
+    full = api.march_device(dev, g, rays, field, cfg, api.DevicePacked.allocate(dev, n, 16 * n))
+    S = full.n_samples
+    cap = S // 2
+    rng = np.random.default_rng(3)
+    ups = [dev.upload(rng.uniform(-1, 1, n * w).astype(np.float32)) for w in (3, 1, 1)]
+    res = []
+    for c in (full.capacity, cap):
+        p = api.DevicePacked.allocate(dev, n, c)
+        rgb, sig = dev.empty(3 * c, np.float32), dev.empty(c, np.float32)
+        gr, gs = dev.empty(3 * c, np.float32), dev.empty(c, np.float32)
+        outs = [dev.empty(3 * n, np.float32), dev.empty(n, np.float32), dev.empty(n, np.float32)]
+        nd = dev.zeros(1, np.uint64)
+        smp = p.samples_struct()
+        check(L.vmb_march_render_field_async(dev.h, g.h, C.byref(rays), C.byref(field), C.byref(cfg), C.byref(smp),
+                                             rgb.ptr, sig.ptr, outs[0].ptr, outs[1].ptr, outs[2].ptr, F32, 0.0,
+                                             nd.ptr))
+        p.n_samples = c
+        api.render_backward_device(dev, p, rgb, sig, *ups, gr, gs)
+        dev.sync()
+        check(L.vmb_march_check(dev.h))
+        assert int(nd.numpy()[0]) == S
+        res.append((p.to_host() if c == full.capacity else None, gs.numpy(c), gr.numpy(3 * c)))
+    hp = res[0][0]
+    inside = hp.offsets.astype(np.int64) + hp.counts <= cap
+    m = np.zeros(S, bool)
+    for r in np.nonzero(inside)[0]:
+        m[hp.offsets[r]:hp.offsets[r] + hp.counts[r]] = True
+    mc = m[:cap]
+    assert mc.sum() > 0
+    assert np.array_equal(res[0][1][:cap][mc], res[1][1][mc])
+    assert np.array_equal(res[0][2].reshape(-1, 3)[:cap][mc], res[1][2].reshape(-1, 3)[mc])
