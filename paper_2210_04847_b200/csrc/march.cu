@@ -554,7 +554,7 @@ __device__ __forceinline__ void walk(const MarchParams& P, Sink& s, const RT* __
 //                  reference expressions.
 //   k_march_fixup  re-walks the rare rays with more than kWalkCap kept samples.
 // ---------------------------------------------------------------------------
-constexpr int kWalkCap = 24;
+constexpr int kWalkCap = 32;  // >= the 28 kept samples of a sphere ray at config 2 (step sqrt(3)/1024)
 #ifndef VMB_WALK_CLAIM
 #define VMB_WALK_CLAIM 1
 #endif
