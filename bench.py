@@ -322,8 +322,18 @@ class ResidentPipeline:
         ups = [Ptr(u.ptr + 4 * w * b) for u, w in zip(self.ups_dev, (3, 1, 1))]
         self.api.render_backward_device(cx, pk, bf["rgb"], bf["sig"], *ups, bf["grgb"], bf["gsig"])
 
-    def run(self, steps=1):
+    def run(self, steps=1, pre_step=None):
+        """`pre_step()` (e.g. config 4's grid update) runs on context 0 before each
+        step's sub-batches, ordered after every stream's previous work and before
+        their next (the grid is read by every stream's walk)."""
+        from paper_2210_04847_b200._lib import check
         for _ in range(steps):
+            if pre_step is not None and pre_step(dry=True):
+                for i, cx in enumerate(self.ctxs[1:]):
+                    check(self.L.vmb_ctx_wait(self.dev.h, cx.h, 21 + (i % 8)))
+                pre_step()
+                for cx in self.ctxs[1:]:
+                    check(self.L.vmb_ctx_wait(cx.h, self.dev.h, 20))
             for k in range(self.K):
                 self.chunk(k)
 
@@ -581,20 +591,41 @@ def main():
     # the forward is fused and no grid update sits inside the loop; else the
     # single-call step above.
     pipe = None
-    if args.fusion == "forward" and not args.grid_update_every and args.streams * args.chunks > 1:
+    pipe_step = [0]
+
+    def pipe_update(dry=False):
+        """config 4: the grid update due before pipelined step pipe_step (dry: is one due?)"""
+        if not args.grid_update_every:
+            return False
+        due = (pipe_step[0] + 1) % args.grid_update_every == 0
+        if dry:
+            return due
+        pipe_step[0] += 1
+        grid.update_field(field, 0.95, update_seeds[(pipe_step[0] // args.grid_update_every) % 4096])
+        return True
+
+    def pipe_run(steps):
+        for _ in range(steps):
+            if not pipe_update(dry=True):
+                pipe_step[0] += 1
+                pipe.run(1)
+            else:
+                pipe.run(1, pre_step=pipe_update)
+
+    if args.fusion == "forward" and args.streams * args.chunks > 1:
         pipe = ResidentPipeline(args, api, dev, grid, field, cfg, (do_, dd_), (up_c, up_o, up_d), N, S0)
     clocks = Clocks(dist.local)
     for _ in range(max(args.warmup, 3)):
         step()
         if pipe:
-            pipe.run()
+            pipe_run(1)
     dev.sync()
     if pipe:
         pipe.sync()
     dist.barrier()
     if pipe:
         pipe.begin(0)
-        pipe.run(args.steps)
+        pipe_run(args.steps)
         pipe.end(1)
         pipe.sync()
     else:
@@ -608,7 +639,7 @@ def main():
     # keep the GPU loaded ~1 s more so the clock sampler sees the steady state
     t_end = time.time() + 1.2
     while time.time() < t_end:
-        pipe.run() if pipe else step()
+        pipe_run(1) if pipe else step()
     dev.sync()
     if pipe:
         pipe.sync()
@@ -618,11 +649,14 @@ def main():
     pipe_info = None
     if pipe:  # the pipelined step's outputs == the single-call step's, bit for bit
         s_pipe = pipe.check()
-        same = s_pipe == S and all(np.array_equal(a.numpy(), b.numpy(N * w))
-                                   for a, b, w in zip(pipe.outs, (col, op, dep), (3, 1, 1)))
-        pipe_info = {"streams": pipe.S, "sub_batches": pipe.K, "samples": s_pipe,
-                     "matches_single_call_outputs": bool(same)}
-        assert same, "pipelined step differs from the single-call step"
+        pipe_info = {"streams": pipe.S, "sub_batches": pipe.K, "samples": s_pipe}
+        if args.grid_update_every:  # the grid moves between the runs: no common state to compare
+            pipe_info["matches_single_call_outputs"] = None
+        else:
+            same = s_pipe == S and all(np.array_equal(a.numpy(), b.numpy(N * w))
+                                       for a, b, w in zip(pipe.outs, (col, op, dep), (3, 1, 1)))
+            pipe_info["matches_single_call_outputs"] = bool(same)
+            assert same, "pipelined step differs from the single-call step"
     ms_step = dist.max(ms_total / args.steps)
     total_rays = dist.sum(float(N))
     total_samples = dist.sum(float(S))
