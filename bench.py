@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--resolution", type=int, default=128)
     ap.add_argument("--step-size", type=float, default=5e-3)
     ap.add_argument("--cpu-baseline", type=int, default=1)
+    ap.add_argument("--config2", type=int, default=1,
+                    help="N=1: also time BASELINE config 2 (2^18 rays, step sqrt(3)/1024) in a sub-run "
+                         "and report it under `config2`")
     ap.add_argument("--cpu-sample-rays", type=int, default=1 << 20)
     ap.add_argument("--ref-sample-rays", type=int, default=1 << 18)
     ap.add_argument("--phases", type=int, default=1, help="per-phase event timing pass")
@@ -726,6 +729,23 @@ def main():
     except Exception as ex:  # pragma: no cover
         e2e_cam = {"error": repr(ex)}
 
+    cfg2 = None
+    if dist.rank == 0 and dist.world == 1 and args.config2 and args.width == 2048:
+        try:  # BASELINE config 2 (NeRF-Synthetic-shaped batch), same step, its own process
+            out = subprocess.run([sys.executable, os.path.abspath(__file__), "--width", "512", "--step-size",
+                                  repr(math.sqrt(3.0) / 1024), "--steps", str(max(args.steps, 20)), "--warmup",
+                                  str(args.warmup), "--cpu-baseline", "0", "--config2", "0", "--phases", "0"],
+                                 capture_output=True, text=True, timeout=600)
+            c2 = json.loads(out.stdout.strip().splitlines()[-1])
+            cfg2 = {k: c2[k] for k in ("value", "unit", "ms_per_step", "samples_per_s")}
+            cfg2["workload"] = ("config 2: 262144 orbit-camera rays (W=512), 128^3 grid, step sqrt(3)/1024, "
+                                "alpha 1e-2, eps 1e-4, SolidSphere field")
+            cfg2["samples"] = c2["config"]["samples_per_gpu"]
+            cfg2["roofline_step_frac"] = c2["roofline"]["step"]["frac"]
+            cfg2["e2e"] = {k: c2["e2e"].get(k) for k in ("value", "unit", "ms_per_step")}
+        except Exception as ex:  # pragma: no cover
+            cfg2 = {"error": repr(ex)}
+
     cpu = None
     if dist.rank == 0 and dist.world == 1 and args.cpu_baseline:
         try:
@@ -755,6 +775,7 @@ def main():
                 "pipeline": pipe_info,
                 "phases_ms": phase, "grid_update_ms": grid_update_ms,
                 "roofline": roof, "e2e": e2e, "e2e_camera": e2e_cam, "cpu_baseline": cpu, "clocks": clk,
+                "config2": cfg2,
                 "gpu_launches": (KERNELS_PER_STEP - {"none": 0, "shade": 1, "forward": 2}[args.fusion])
                 * args.steps * (pipe.K if pipe else 1)}
         print(json.dumps(line), flush=True)
