@@ -46,6 +46,11 @@ __host__ __device__ constexpr bool mvox(int m) { return (m & VOXM) != 0; }
 // its dynamic shared memory, walk_dyn_smem
 constexpr int ATABM = 8;
 __host__ __device__ constexpr bool matab(int m) { return (m & ATABM) != 0; }
+// bit 4: walk_fast keeps the ray's fp32 constants (A, B, o, d) in the caller's
+// shared-memory slot Sink::rc, read back where used, instead of leaving the register
+// allocator to rematerialize them from the fp64 ray in every loop iteration
+constexpr int RSMM = 16;
+__host__ __device__ constexpr bool mrsm(int m) { return (m & RSMM) != 0; }
 extern __shared__ double walk_dyn_smem[];
 
 struct MarchParams {
@@ -111,6 +116,7 @@ struct Sink {
     // out of registers leaves the walk loop its 64 registers.
     bool at32 = false;
     double* acc = nullptr;
+    float* rc = nullptr;  // RSMM: 12 per-ray fp32 constants, stride kAccStride
 
     // One kept sample, with exactly k_shade + k_forward's expressions (FwdAcc):
     // sigma/rgb are rounded to the attribute dtype; alpha is reused when the
@@ -391,6 +397,17 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
         of[0] = float(o.x), of[1] = float(o.y), of[2] = float(o.z);
         df[0] = float(d.x), df[1] = float(d.y), df[2] = float(d.z);
     }
+    if (mrsm(MODE)) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            s.rc[a * kAccStride] = A[a];
+            s.rc[(3 + a) * kAccStride] = B[a];
+            s.rc[(6 + a) * kAccStride] = of[a];
+            s.rc[(9 + a) * kAccStride] = df[a];
+        }
+    }
+    // the constants where they are used: from the shared slot (RSMM) or registers
+#define VM_RC(k, reg) (mrsm(MODE) ? s.rc[(k) * kAccStride] : (reg))
     const float amax = fmaxf(fmaxf(fabsf(A[0]), fabsf(A[1])), fabsf(A[2]));
     const float bmax = fmaxf(fmaxf(fabsf(B[0]), fabsf(B[1])), fabsf(B[2]));
     const float E = ldexpf(2.0f * amax + 5.0f * bmax * P.Mf, -22) + 1e-6f;
@@ -443,7 +460,9 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
     bool alive = true;
     while (j <= jend) {
         const float m = fmaf(float(j), P.step_f, P.m0_f);
-        const float u0 = fmaf(B[0], m, A[0]), u1 = fmaf(B[1], m, A[1]), u2 = fmaf(B[2], m, A[2]);
+        const float u0 = fmaf(VM_RC(3, B[0]), m, VM_RC(0, A[0]));
+        const float u1 = fmaf(VM_RC(4, B[1]), m, VM_RC(1, A[1]));
+        const float u2 = fmaf(VM_RC(5, B[2]), m, VM_RC(2, A[2]));
         // |u| stays within a few cells of the domain here (the loop range is the
         // clipped lattice), so the float->int floor is exact and in range
         const int i0 = __float2int_rd(u0), i1 = __float2int_rd(u1), i2 = __float2int_rd(u2);
@@ -481,9 +500,9 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
         if (P.sphere_fast && s.filtering) {
             // Filtered SolidSphere test (fields.cpp:45): |p - c|^2 in fp32 with the
             // bound sph_err; decided cases skip the fp64 midpoint + sqrt.
-            float qx = fmaf(df[0], m, of[0]) - P.sph_c[0];
-            float qy = fmaf(df[1], m, of[1]) - P.sph_c[1];
-            float qz = fmaf(df[2], m, of[2]) - P.sph_c[2];
+            float qx = fmaf(VM_RC(9, df[0]), m, VM_RC(6, of[0])) - P.sph_c[0];
+            float qy = fmaf(VM_RC(10, df[1]), m, VM_RC(7, of[1])) - P.sph_c[1];
+            float qz = fmaf(VM_RC(11, df[2]), m, VM_RC(8, of[2])) - P.sph_c[2];
             float d2 = fmaf(qx, qx, fmaf(qy, qy, qz * qz));
             if (d2 > P.sph_r2 + sph_err || d2 < P.sph_r2 - sph_err) {
                 if (s.n_cand >= P.max_cand) return;  // candidate cap
@@ -508,6 +527,8 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
         ++j;
     }
 }
+
+#undef VM_RC
 
 __device__ __forceinline__ bool ray_safe(const MarchParams& P, D3 o, D3 d) {
     // Overflowing midpoints can only occur for astronomically large inputs; such
@@ -554,6 +575,9 @@ __device__ __forceinline__ void walk(const MarchParams& P, Sink& s, const RT* __
 //                  reference expressions.
 //   k_march_fixup  re-walks the rare rays with more than kWalkCap kept samples.
 // ---------------------------------------------------------------------------
+#ifndef VMB_WALK_RSM
+#define VMB_WALK_RSM 1
+#endif
 constexpr int kWalkCap = 32;  // >= the 28 kept samples of a sphere ray at config 2 (step sqrt(3)/1024)
 #ifndef VMB_WALK_CLAIM
 #define VMB_WALK_CLAIM 1
@@ -617,6 +641,7 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
     uint32_t* __restrict__ counts, uint32_t* __restrict__ kept_idx, unsigned int* chunk_counter,
     uint64_t n_chunks, unsigned long long* emitted, DevError* err, FwdOut<AT> fo) {
     __shared__ double s_acc[FWD ? 6 : 1][kAccStride];
+    __shared__ float s_rc[FAST && VMB_WALK_RSM ? 12 : 1][kAccStride];
     const int lane = threadIdx.x & 31;
     unsigned long long emit_local = 0;
     if (ATAB) {  // alpha per lattice step for the constant interior density (sphere)
@@ -659,7 +684,9 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
 #pragma unroll
                 for (int k = 1; k < 6; ++k) s.acc[k * kAccStride] = 0.0;
             }
-            constexpr int M = (FWD ? BUFFER_FWD : BUFFER) | (VOX ? VOXM : 0) | (ATAB ? ATABM : 0);
+            constexpr int M = (FWD ? BUFFER_FWD : BUFFER) | (VOX ? VOXM : 0) | (ATAB ? ATABM : 0) |
+                              (FAST && VMB_WALK_RSM ? RSMM : 0);
+            s.rc = &s_rc[0][threadIdx.x];
             if (FAST) {
                 const D3 o = load3(orig, r), d = load3(dirs, r);
                 if (ray_safe(P, o, d))
