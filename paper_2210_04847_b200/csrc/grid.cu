@@ -414,9 +414,23 @@ __global__ void k_dist_axis_tiled(const uint8_t* __restrict__ in, uint32_t res, 
 
 }  // namespace
 
-int grid_rebuild_coarse(vmb_ctx* ctx, vmb_grid* g) {
+// The dilated coarse bits serve only walk_skip (the fp64 DDA used when the fp32
+// fast walk does not apply), so they are built on that path's first use after a
+// change of the bits, synchronously (any context may then read them).
+int grid_ensure_coarse(vmb_ctx* ctx, const vmb_grid* cg) {
+    auto* g = const_cast<vmb_grid*>(cg);
+    if (g->coarse_valid) return VMB_OK;
     k_coarse<<<grid_blocks(ctx, g->coarse_words * 32, 256), 256, 0, ctx->stream>>>(
         g->bits, g->res, g->block, g->res_c, g->coarse, g->coarse_words);
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "grid coarse");
+    g->coarse_valid = true;
+    return VMB_OK;
+}
+
+int grid_rebuild_coarse(vmb_ctx* ctx, vmb_grid* g) {
+    g->coarse_valid = false;
     const int blocks = grid_blocks(ctx, g->n_cells, 256);
     k_dist_x<<<blocks, 256, 0, ctx->stream>>>(g->bits, g->res, g->n_cells, g->n_words, g->dist);
     const uint64_t r = g->res, plane = r * r;
@@ -513,6 +527,7 @@ int vmb_grid_clone(vmb_ctx* ctx, const vmb_grid* src, vmb_grid** out) {
     cudaMemcpyAsync(g->cache, src->cache, g->n_cells * 8, cudaMemcpyDeviceToDevice, ctx->stream);
     cudaMemcpyAsync(g->bits, src->bits, g->n_words * 4, cudaMemcpyDeviceToDevice, ctx->stream);
     cudaMemcpyAsync(g->coarse, src->coarse, g->coarse_words * 4, cudaMemcpyDeviceToDevice, ctx->stream);
+    g->coarse_valid = src->coarse_valid;
     cudaMemcpyAsync(g->dist, src->dist, g->n_cells, cudaMemcpyDeviceToDevice, ctx->stream);
     cudaMemcpyAsync(g->bbox, src->bbox, 6 * sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream);
     rc = launch_check("grid clone");

@@ -58,6 +58,7 @@ struct MarchParams {
     uint32_t res;
     const uint32_t* bits;
     const uint32_t* coarse;
+    const vmb_grid* grid;  // for grid_ensure_coarse (walk_skip)
     const uint8_t* dist;  // capped L-inf distance to the nearest occupied cell
     const uint32_t* bbox; // occupied cells' bounding box {min xyz, max+1 xyz} (vmb_grid::bbox)
     uint32_t block, res_c;
@@ -1075,6 +1076,7 @@ int march_params(const vmb_grid* g, const vmb_rays* rays, const vmb_march_config
     P->res = g->res;
     P->bits = g->bits;
     P->coarse = g->coarse;
+    P->grid = g;
     P->dist = g->dist;
     P->bbox = g->bbox;
     P->block = g->block;
@@ -1130,9 +1132,15 @@ void launch_march_rt(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, u
             out ? out->d_ray_indices : nullptr, out ? out->capacity : 0, emitted, ctx->d_err);
 }
 
+// walk_skip reads the grid's coarse bits: the paths that may take it build them first
+int ensure_skip_structures(vmb_ctx* ctx, const MarchParams& P) {
+    return P.skip && !P.fast ? grid_ensure_coarse(ctx, P.grid) : VMB_OK;
+}
+
 template <int MODE>
 void launch_march(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, uint32_t* counts,
                   const uint32_t* offsets, vmb_samples* out, unsigned long long* emitted) {
+    if (ensure_skip_structures(ctx, P)) return;
     if (P.f.kind == VMB_FIELD_VOXEL)
         launch_march_rt<MODE | VOXM>(ctx, P, rays, counts, offsets, out, emitted);
     else
@@ -1274,6 +1282,7 @@ void dispatch_expand(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, v
 // walk -> scan -> expand (+shade) -> fixup; the sample total lands in d_total.
 int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
                  unsigned long long* d_total, unsigned long long* emitted, const ShadeReq& sr) {
+    if (int rc = ensure_skip_structures(ctx, P)) return rc;
     const uint64_t n = rays->n_rays;
     const uint64_t n_chunks = (n + 31) / 32;
     const size_t head = 16;

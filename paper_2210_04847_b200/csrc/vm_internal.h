@@ -75,7 +75,8 @@ struct vmb_grid {
     // bit(K) = OR of fine bits over block K expanded by one fine cell per side.
     uint32_t block = 8;
     uint32_t res_c = 0;            // ceil(res / block)
-    uint32_t* coarse = nullptr;    // [ceil(res_c^3 / 32)]
+    uint32_t* coarse = nullptr;    // [ceil(res_c^3 / 32)], built on first use after a change
+    bool coarse_valid = false;     // (only the fp64 skip walk, walk_skip, reads it)
     uint64_t coarse_words = 0;
     // Chebyshev (L-inf) distance, in cells, from each cell to the nearest occupied
     // cell, capped at kDistCap (0 = occupied). Lets the marcher jump D-1 cells.
@@ -124,7 +125,8 @@ int scan_flags(vmb_ctx* ctx, const uint8_t* flags, uint64_t n, uint32_t* pos,
 
 // ---------------------------------------------------------------- grid (grid.cu)
 int grid_refresh(vmb_ctx* ctx, vmb_grid* g);      // bits + coarse from cache
-int grid_rebuild_coarse(vmb_ctx* ctx, vmb_grid* g);  // coarse bits + distance map
+int grid_rebuild_coarse(vmb_ctx* ctx, vmb_grid* g);  // distance map + bbox; invalidates coarse
+int grid_ensure_coarse(vmb_ctx* ctx, const vmb_grid* g);  // builds the coarse bits if stale (syncs)
 #ifndef VMB_DIST_CAP
 #define VMB_DIST_CAP 16
 #endif
