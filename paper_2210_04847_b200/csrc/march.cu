@@ -831,8 +831,7 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
         cp_async_commit();
     };
     // one output slot p, owned by lane L (its k-th kept sample)
-    auto emit = [&](const uint32_t* sk, uint64_t chunk, uint64_t p, int L, uint32_t k, D3 o, D3 d) {
-        const uint32_t i = sk[k * 32 + L];
+    auto emit = [&](uint64_t chunk, uint64_t p, int L, uint32_t i, D3 o, D3 d) {
         const double di = double(i);  // double(i + 1) == di + 1.0 exactly
         const double t0 = near_ + di * step;
         const double t1 = min_ref(near_ + (di + 1.0) * step, far_);
@@ -880,6 +879,17 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
         cp_async_wait1();  // this chunk's rows have landed
         __syncwarp();
         const uint32_t* sk = s_idx[wib][buf];
+        if (CONST && mapped) {  // no ray needed: two independent 32-slot rounds per iteration
+            for (uint64_t p0 = base; p0 < end; p0 += 64) {
+                const uint64_t pa = p0 + lane, pb = pa + 32;
+                const bool ina = pa < end && pa < cap, inb = pb < end && pb < cap;
+                const uint32_t ea = ina ? mp[pa - base] : 0u, eb = inb ? mp[pb - base] : 0u;
+                const uint32_t ia = ina ? sk[(ea >> 5) * 32 + (ea & 31u)] : 0u;
+                const uint32_t ib = inb ? sk[(eb >> 5) * 32 + (eb & 31u)] : 0u;
+                if (ina) emit(chunk, pa, int(ea & 31u), ia, D3{}, D3{});
+                if (inb) emit(chunk, pb, int(eb & 31u), ib, D3{}, D3{});
+            }
+        } else
         for (uint64_t p0 = base; p0 < end; p0 += 32) {
             const uint64_t p = p0 + lane;
             const bool in = p < end && p < cap;
@@ -909,7 +919,7 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
                 d = d3(double(__shfl_sync(0xffffffffu, dx, L)), double(__shfl_sync(0xffffffffu, dy, L)),
                        double(__shfl_sync(0xffffffffu, dz, L)));
             }
-            if (in && k < uint32_t(kWalkCap)) emit(sk, chunk, p, L, k, o, d);
+            if (in && k < uint32_t(kWalkCap)) emit(chunk, p, L, sk[k * 32 + L], o, d);
         }
         __syncwarp();  // buffer `buf` and the map are refilled from the next chunk on
         cur = nxt;
