@@ -754,6 +754,10 @@ struct ShadeOut {
 #define VMB_EXPAND_WARPS 16  // one 122 KB CTA per SM: 0.769 ms/step vs 0.780 (8), 0.820 (4), 0.774 (20)
 #endif
 constexpr int kExpandWarps = VMB_EXPAND_WARPS;
+#ifndef VMB_EXPAND_UNROLL
+#define VMB_EXPAND_UNROLL 4
+#endif
+constexpr int kExpandUnroll = VMB_EXPAND_UNROLL;  // rounds per iteration of the constant-shading path
 constexpr size_t kExpandSmem = size_t(kExpandWarps) * kWalkCap * 32 * (2 * sizeof(uint32_t) + sizeof(uint16_t));
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -879,15 +883,20 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
         cp_async_wait1();  // this chunk's rows have landed
         __syncwarp();
         const uint32_t* sk = s_idx[wib][buf];
-        if (CONST && mapped) {  // no ray needed: two independent 32-slot rounds per iteration
-            for (uint64_t p0 = base; p0 < end; p0 += 64) {
-                const uint64_t pa = p0 + lane, pb = pa + 32;
-                const bool ina = pa < end && pa < cap, inb = pb < end && pb < cap;
-                const uint32_t ea = ina ? mp[pa - base] : 0u, eb = inb ? mp[pb - base] : 0u;
-                const uint32_t ia = ina ? sk[(ea >> 5) * 32 + (ea & 31u)] : 0u;
-                const uint32_t ib = inb ? sk[(eb >> 5) * 32 + (eb & 31u)] : 0u;
-                if (ina) emit(chunk, pa, int(ea & 31u), ia, D3{}, D3{});
-                if (inb) emit(chunk, pb, int(eb & 31u), ib, D3{}, D3{});
+        if (CONST && mapped) {  // no ray needed: kExpandUnroll independent 32-slot rounds per iteration
+            for (uint64_t p0 = base; p0 < end; p0 += 32 * kExpandUnroll) {
+                uint32_t e[kExpandUnroll], ii[kExpandUnroll];
+#pragma unroll
+                for (int q = 0; q < kExpandUnroll; ++q) {
+                    const uint64_t pq = p0 + 32 * q + lane;
+                    e[q] = pq < end && pq < cap ? mp[pq - base] | 0x80000000u : 0u;
+                }
+#pragma unroll
+                for (int q = 0; q < kExpandUnroll; ++q)
+                    ii[q] = e[q] ? sk[((e[q] >> 5) & 31u) * 32 + (e[q] & 31u)] : 0u;
+#pragma unroll
+                for (int q = 0; q < kExpandUnroll; ++q)
+                    if (e[q]) emit(chunk, p0 + 32 * q + lane, int(e[q] & 31u), ii[q], D3{}, D3{});
             }
         } else
         for (uint64_t p0 = base; p0 < end; p0 += 32) {
