@@ -640,7 +640,8 @@ template <typename RT, bool FAST, typename AT, bool FWD, bool VOX, bool ATAB = f
 __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
     MarchParams P, const RT* __restrict__ orig, const RT* __restrict__ dirs, uint64_t n_rays,
     uint32_t* __restrict__ counts, uint32_t* __restrict__ kept_idx, unsigned int* chunk_counter,
-    uint64_t n_chunks, unsigned long long* emitted, DevError* err, FwdOut<AT> fo) {
+    uint64_t n_chunks, unsigned long long* emitted, DevError* err, FwdOut<AT> fo,
+    uint32_t* __restrict__ chunk_tot) {
     __shared__ double s_acc[FWD ? 6 : 1][kAccStride];
     __shared__ float s_rc[FAST && VMB_WALK_RSM ? 12 : 1][kAccStride];
     const int lane = threadIdx.x & 31;
@@ -672,6 +673,7 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
             }
         }
         const uint64_t r = uint64_t(chunk) * 32 + lane;
+        uint32_t kept = 0;
         if (r < n_rays) {
             Sink s;
             s.ray = r;
@@ -698,6 +700,7 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
                 walk<M>(P, s, orig, dirs, r, err);
             }
             counts[r] = s.n_kept;
+            kept = s.n_kept;
             emit_local += s.n_cand;
             if (FWD) {  // every kept sample was composited (rays over kWalkCap too)
                 fo.color[3 * r] = AT(s.acc[1 * kAccStride]);
@@ -707,7 +710,9 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
                 fo.depth[r] = AT(s.acc[5 * kAccStride]);
             }
         }
-        __syncwarp();
+        // the chunk's sample total: the packing scans these (32x fewer than rays)
+        const uint32_t tot = __reduce_add_sync(0xffffffffu, kept);
+        if (lane == 0) chunk_tot[chunk] = tot;
         ++chunk;
     }
     if (emitted) {
@@ -782,7 +787,8 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 template <typename RT, typename AT, bool SHADE, bool VOX, bool CONST = false>
 __global__ void VMB_EXPAND_BOUNDS k_march_expand(
     double near_, double far_, double step, const uint32_t* __restrict__ counts,
-    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ kept_idx, uint64_t n_rays,
+    const uint32_t* __restrict__ chunk_off, uint32_t* __restrict__ offsets,
+    const uint32_t* __restrict__ kept_idx, uint64_t n_rays,
     double* __restrict__ ts, double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,
     uint32_t* __restrict__ overflow, unsigned int* n_overflow, ShadeOut<RT, AT, VOX> sh) {
     constexpr bool RAYS = SHADE && !CONST;  // the per-sample shading needs the ray
@@ -805,18 +811,18 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
 
     // chunk-local state: count/offset of this lane's ray, its ray (RT), and the
     // number of staged rows
+    // (off: the chunk's first packed position, chunk_off[c]; a ray's own offset is
+    // that plus the exclusive warp scan of the counts, written to offsets[])
     struct Stage {
-        uint32_t cnt = 0u, off = 0xffffffffu;
+        uint32_t cnt = 0u, off = 0u;
         RT o[3] = {}, d[3] = {};
     };
     auto load_meta = [&](uint64_t c, Stage& st) {
         const uint64_t r = c * 32 + lane;
         st.cnt = 0u;
-        st.off = 0xffffffffu;
-        if (c < n_chunks && r < n_rays) {
-            st.cnt = counts[r];
-            st.off = offsets[r];
-        }
+        st.off = 0u;
+        if (c < n_chunks) st.off = chunk_off[c];
+        if (c < n_chunks && r < n_rays) st.cnt = counts[r];
     };
     auto load_rays = [&](uint64_t c, Stage& st) {
         const uint64_t r = c * 32 + lane;
@@ -867,7 +873,15 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
 
         const uint64_t r = chunk * 32 + lane;
         const bool valid = r < n_rays;
-        const uint32_t cnt = cur.cnt, off = cur.off;
+        const uint32_t cnt = cur.cnt;
+        uint32_t incl = cnt;  // inclusive warp scan of the counts
+#pragma unroll
+        for (int dd = 1; dd < 32; dd <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, dd);
+            if (lane >= dd) incl += v;
+        }
+        const uint32_t off = valid ? cur.off + incl - cnt : 0xffffffffu;
+        if (valid) offsets[r] = off;
         const bool big = cnt > uint32_t(kWalkCap);
         if (big) overflow[atomicAdd(n_overflow, 1u)] = uint32_t(r);
         const unsigned vmask = __ballot_sync(0xffffffffu, valid);
@@ -1250,12 +1264,12 @@ int expand_per_sm() {
 template <typename RT, typename AT, bool SHADE, bool FWD, bool VOX>
 void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
                          const uint32_t* kept_idx, uint32_t* overflow, unsigned int* n_overflow,
-                         uint64_t n_chunks, const ShadeReq& sr) {
+                         uint64_t n_chunks, const ShadeReq& sr, const uint32_t* chunk_off) {
     ShadeOut<RT, AT, VOX> sh{static_cast<const RT*>(rays->d_origins), static_cast<const RT*>(rays->d_directions),
                         sr.f, sr.time, static_cast<AT*>(sr.rgb), static_cast<AT*>(sr.sig)};
     auto launch = [&](auto kernel, int per_sm) {
         kernel<<<grid_blocks(ctx, n_chunks * 32, 32 * kExpandWarps, per_sm), 32 * kExpandWarps, kExpandSmem,
-                 ctx->stream>>>(P.near_, P.far_, P.step, out->d_counts, out->d_offsets, kept_idx, rays->n_rays,
+                 ctx->stream>>>(P.near_, P.far_, P.step, out->d_counts, chunk_off, out->d_offsets, kept_idx, rays->n_rays,
                                 out->d_t_starts, out->d_t_ends, out->d_ray_indices, out->capacity, overflow,
                                 n_overflow, sh);
     };
@@ -1281,9 +1295,10 @@ void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* ray
 template <typename RT>
 void dispatch_expand(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
                      const uint32_t* kept_idx, uint32_t* overflow, unsigned int* n_overflow,
-                     uint64_t n_chunks, const ShadeReq& sr) {
+                     uint64_t n_chunks, const ShadeReq& sr, const uint32_t* chunk_off) {
 #define VMB_EXPAND(AT, SH, FW, VX) \
-    launch_expand_fixup<RT, AT, SH, FW, VX>(ctx, P, rays, out, kept_idx, overflow, n_overflow, n_chunks, sr)
+    launch_expand_fixup<RT, AT, SH, FW, VX>(ctx, P, rays, out, kept_idx, overflow, n_overflow, n_chunks, sr, \
+                                            chunk_off)
     const bool vox = P.f.kind == VMB_FIELD_VOXEL;
     if (!sr.on)
         vox ? VMB_EXPAND(float, false, false, true) : VMB_EXPAND(float, false, false, false);
@@ -1306,11 +1321,13 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
     const uint64_t n_chunks = (n + 31) / 32;
     const size_t head = 16;
     const size_t idx_bytes = n_chunks * kWalkCap * 32 * sizeof(uint32_t);
-    char* base = static_cast<char*>(scratch(ctx, SCRATCH_MARCH, head + idx_bytes + n * 4 + 64));
+    char* base = static_cast<char*>(scratch(ctx, SCRATCH_MARCH, head + idx_bytes + n * 4 + 8 * n_chunks + 64));
     if (!base) return VMB_CUDA;
     auto* counters = reinterpret_cast<unsigned int*>(base);  // [chunk, overflow]
     auto* kept_idx = reinterpret_cast<uint32_t*>(base + head);
     auto* overflow = reinterpret_cast<uint32_t*>(base + head + idx_bytes);
+    auto* chunk_tot = reinterpret_cast<uint32_t*>(base + head + idx_bytes + n * 4);  // per-chunk totals
+    auto* chunk_off = chunk_tot + n_chunks;                                         // and their scan
     cudaMemsetAsync(base, 0, head, ctx->stream);
     if (n == 0) {
         cudaMemsetAsync(d_total, 0, 8, ctx->stream);
@@ -1326,7 +1343,7 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
         static const int forced = env_int("VMB_WALK_CTAS", 0);
         if (forced > 0) per_sm = forced;
         kernel<<<ctx->num_sms * per_sm, 128, dyn, ctx->stream>>>(
-            P, o, d, n, out->d_counts, kept_idx, counters, n_chunks, emitted, ctx->d_err, fo);
+            P, o, d, n, out->d_counts, kept_idx, counters, n_chunks, emitted, ctx->d_err, fo, chunk_tot);
     };
     auto walk_vox = [&](auto* o, auto* d, auto VOXC) {
         using RT = std::remove_const_t<std::remove_pointer_t<decltype(o)>>;
@@ -1365,12 +1382,14 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
         walk_rt(static_cast<const float*>(rays->d_origins), static_cast<const float*>(rays->d_directions));
     else
         walk_rt(static_cast<const double*>(rays->d_origins), static_cast<const double*>(rays->d_directions));
-    int rc = scan_counts(ctx, out->d_counts, n, out->d_offsets, d_total);
+    // offsets: the scan of the walk's per-chunk totals, then within each chunk the
+    // expansion's warp scan (it writes out->d_offsets)
+    int rc = scan_counts(ctx, chunk_tot, n_chunks, chunk_off, d_total);
     if (rc) return rc;
     if (rays->dtype == VMB_F32)
-        dispatch_expand<float>(ctx, P, rays, out, kept_idx, overflow, counters + 1, n_chunks, sr);
+        dispatch_expand<float>(ctx, P, rays, out, kept_idx, overflow, counters + 1, n_chunks, sr, chunk_off);
     else
-        dispatch_expand<double>(ctx, P, rays, out, kept_idx, overflow, counters + 1, n_chunks, sr);
+        dispatch_expand<double>(ctx, P, rays, out, kept_idx, overflow, counters + 1, n_chunks, sr, chunk_off);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? VMB_OK : cuda_fail(e, "march");
 }
