@@ -583,8 +583,8 @@ constexpr int kWalkCap = 32;  // >= the 28 kept samples of a sphere ray at confi
 #ifndef VMB_WALK_CLAIM
 #define VMB_WALK_CLAIM 1
 #endif
-// chunks per work-stealing ticket (measured at config 5: 1 = 0.782, 2 = 0.797,
-// 4 = 0.807 ms/step; the L1 prefetch of the next claimed chunk does not pay)
+// chunks per work-stealing ticket (measured at config 5: 1 = 0.756, 2 = 0.757,
+// 4 = 0.769 ms/step; an L1 prefetch of the next claimed chunk did not pay either)
 constexpr int kClaim = VMB_WALK_CLAIM;
 
 // FAST instantiates only walk_fast (+ its exact fallback and the dense walk for
@@ -655,8 +655,7 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
         }
         __syncthreads();
     }
-    // chunks are claimed kClaim at a time; the rays of the next chunk of a claim are
-    // prefetched into L1 while the current one is walked
+    // chunks are claimed kClaim at a time (one atomic per claim)
     unsigned int chunk = 0, claim_end = 0;
     for (;;) {
         if (chunk == claim_end) {
@@ -665,13 +664,6 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
             claim_end = chunk + kClaim;
         }
         if (chunk >= n_chunks) break;
-        if (chunk + 1 < claim_end && chunk + 1 < n_chunks) {
-            const uint64_t rn = uint64_t(chunk + 1) * 32 + lane;
-            if (rn < n_rays) {
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(orig + 3 * rn));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(dirs + 3 * rn));
-            }
-        }
         const uint64_t r = uint64_t(chunk) * 32 + lane;
         uint32_t kept = 0;
         if (r < n_rays) {
