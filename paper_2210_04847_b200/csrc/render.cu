@@ -300,6 +300,89 @@ __device__ void bwd_two_sweep(BwdSmem<T>* smp, int lane, bool active, bool stage
     }
 }
 
+// One ray longer than a tile, by the whole warp: the two sweeps of bwd_two_sweep
+// (S = sum_k w_k v_k, then suffix_k = S - P_k) with every lane on one sample per
+// 32-sample round — T by a product scan over the lanes (carried across rounds and
+// tiles), S and P by sum scans. Same expressions per sample as the reference
+// (rendering.cpp:85-108) up to the association order of the products/sums.
+template <typename T>
+__device__ void bwd_long_ray(BwdSmem<T>& sm, int lane, uint32_t s0, uint32_t s1, const Up& u,
+                             const double* __restrict__ ts, const double* __restrict__ te,
+                             const T* __restrict__ rgb, const T* __restrict__ sig,
+                             T* __restrict__ g_rgb, T* __restrict__ g_sig) {
+    double S = 0.0;
+    for (int sweep = 0; sweep < 2; ++sweep) {
+        double carryT = 1.0, carryP = 0.0;
+        for (uint32_t cs = s0; cs < s1; cs += Tile<T>::CH) {
+            const uint32_t n = min(uint32_t(Tile<T>::CH), s1 - cs);
+            stage_in<T, false>(sm, lane, cs, n, ts, te, rgb, sig);
+            for (uint32_t r0 = 0; r0 < n; r0 += 32) {
+                const uint32_t i = r0 + uint32_t(lane);
+                const bool in = i < n;
+                const double a = in ? sm.al[i] : 0.0;
+                double x = in ? 1.0 - a : 1.0;  // inclusive product of (1 - alpha)
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const double y = __shfl_up_sync(0xffffffffu, x, d);
+                    if (lane >= d) x *= y;
+                }
+                double tr = __shfl_up_sync(0xffffffffu, x, 1);
+                tr = (lane == 0 ? 1.0 : tr) * carryT;  // T before sample i
+                carryT *= __shfl_sync(0xffffffffu, x, 31);
+                double t0 = 0.0, t1 = 0.0, v = 0.0;
+                if (in) {
+                    t0 = sm.ts[i], t1 = sm.te[i];
+                    v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]), double(sm.rgb[3 * i + 2]),
+                                0.5 * (t0 + t1));
+                }
+                const double wgt = tr * a;
+                double wv = wgt * v;  // inclusive sum scan of w v
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const double y = __shfl_up_sync(0xffffffffu, wv, d);
+                    if (lane >= d) wv += y;
+                }
+                const double P = carryP + wv;
+                carryP += __shfl_sync(0xffffffffu, wv, 31);
+                if (sweep == 1 && in) {
+                    sm.rgb[3 * i] = T(u.dcx * wgt);
+                    sm.rgb[3 * i + 1] = T(u.dcy * wgt);
+                    sm.rgb[3 * i + 2] = T(u.dcz * wgt);
+                    sm.sig[i] = T((t1 - t0) * (tr * (1.0 - a) * v - (S - P)));
+                }
+            }
+            if (sweep == 1)
+                write_out(sm, lane, cs, n, g_rgb, g_sig);
+            else
+                __syncwarp();
+        }
+        S = carryP;
+    }
+}
+
+// The rays k_backward_hy set aside (longer than a tile), one warp each.
+template <typename T>
+__global__ void __launch_bounds__(kWarps * 32) k_backward_long(
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_samples,
+    const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
+    const T* __restrict__ sig, const T* __restrict__ dc, const T* __restrict__ dop,
+    const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig,
+    const uint32_t* __restrict__ long_rays, const unsigned int* __restrict__ n_long) {
+    __shared__ BwdSmem<T> smem[kWarps];
+    const int lane = threadIdx.x & 31;
+    BwdSmem<T>& sm = smem[threadIdx.x >> 5];
+    const unsigned int n = *n_long;
+    for (uint64_t k = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; k < n;
+         k += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const uint64_t r = long_rays[k];
+        const uint64_t ns = n_samples < 0xffffffffull ? n_samples : 0xffffffffull;
+        const uint64_t o = offsets[r], e = o + counts[r];
+        const Up u = load_up(dc, dop, ddep, r, true);
+        bwd_long_ray(sm, lane, uint32_t(o < ns ? o : ns), uint32_t(e < ns ? e : ns), u, ts, te, rgb, sig,
+                     g_rgb, g_sig);
+    }
+}
+
 // render_backward: greedy groups of consecutive rays whose samples fit one tile;
 // each group is staged once and every lane runs the reference's exact forward-T /
 // reverse-suffix recurrence (rendering.cpp:85-108) from shared memory.
@@ -375,7 +458,8 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays, uint64_t n_samples,
     const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
     const T* __restrict__ sig, const T* __restrict__ dc, const T* __restrict__ dop,
-    const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig) {
+    const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig,
+    uint32_t* __restrict__ long_rays, unsigned int* __restrict__ n_long) {
     __shared__ BwdSmem<T> smem[kWarps];
     const int lane = threadIdx.x & 31;
     BwdSmem<T>& sm = smem[threadIdx.x >> 5];
@@ -398,10 +482,8 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
             const uint32_t base = __shfl_sync(0xffffffffu, rr.off, g0);
             const bool fits = rr.valid && lane >= g0 && rr.end - base <= uint32_t(Tile<T>::CH);
             const unsigned fm = __ballot_sync(0xffffffffu, fits);  // monotone: ends ascend
-            if (!((fm >> g0) & 1u)) {  // ray g0 alone exceeds a tile
-                const uint32_t e0 = __shfl_sync(0xffffffffu, rr.end, g0);
-                bwd_two_sweep(&sm, lane, lane == g0, true, rr.off, rr.end, base, e0, u, ts, te, rgb,
-                              sig, g_rgb, g_sig);
+            if (!((fm >> g0) & 1u)) {  // ray g0 alone exceeds a tile: k_backward_long's
+                if (lane == 0) long_rays[atomicAdd(n_long, 1u)] = uint32_t(w * 32 + g0);
                 ++g0;
                 continue;
             }
@@ -773,6 +855,43 @@ int render_blocks(vmb_ctx* ctx, uint64_t n_rays) {
     return grid_blocks(ctx, (n_rays + 31) / 32 * 32, kWarps * 32, per_sm);
 }
 
+// render_backward: k_backward_hy, then the rays it set aside (longer than a tile)
+// by k_backward_long; VMB_BACKWARD=sp|tile select the alternative kernels.
+template <typename T>
+int launch_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, const void* sig, const void* dc,
+                    const void* dop, const void* ddep, void* g_rgb, void* g_sig) {
+    const int blocks = render_blocks(ctx, p->n_rays);
+    const int impl = backward_impl();
+    auto args = [&](auto kernel) {
+        kernel<<<blocks, kWarps * 32, 0, ctx->stream>>>(
+            p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
+            static_cast<const T*>(rgb), static_cast<const T*>(sig), static_cast<const T*>(dc),
+            static_cast<const T*>(dop), static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig));
+    };
+    if (impl == 1) {
+        args(k_backward_sp<T>);
+        return launched("render_backward");
+    }
+    if (impl == 2) {
+        args(k_backward<T>);
+        return launched("render_backward");
+    }
+    auto* list = static_cast<uint32_t*>(scratch(ctx, SCRATCH_RENDER, 16 + 4 * p->n_rays));
+    if (!list) return VMB_CUDA;
+    auto* n_long = reinterpret_cast<unsigned int*>(list);
+    cudaMemsetAsync(n_long, 0, 4, ctx->stream);
+    k_backward_hy<T><<<blocks, kWarps * 32, 0, ctx->stream>>>(
+        p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
+        static_cast<const T*>(rgb), static_cast<const T*>(sig), static_cast<const T*>(dc),
+        static_cast<const T*>(dop), static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig),
+        list + 4, n_long);
+    k_backward_long<T><<<ctx->num_sms * 4, kWarps * 32, 0, ctx->stream>>>(
+        p->d_offsets, p->d_counts, p->n_samples, p->d_t_starts, p->d_t_ends, static_cast<const T*>(rgb),
+        static_cast<const T*>(sig), static_cast<const T*>(dc), static_cast<const T*>(dop),
+        static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig), list + 4, n_long);
+    return launched("render_backward");
+}
+
 }  // namespace
 }  // namespace vmb
 
@@ -801,21 +920,9 @@ int vmb_render_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb,
                         const void* dc, const void* dop, const void* ddep, void* g_rgb, void* g_sig,
                         int dtype) {
     if (!p->n_rays) return VMB_OK;
-    int blocks = render_blocks(ctx, p->n_rays);
-    const int impl = backward_impl();
-    if (dtype == VMB_F32)
-        (impl == 1 ? k_backward_sp<float> : impl == 2 ? k_backward<float> : k_backward_hy<float>)<<<blocks, kWarps * 32, 0, ctx->stream>>>(
-            p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
-            static_cast<const float*>(rgb), static_cast<const float*>(sig), static_cast<const float*>(dc),
-            static_cast<const float*>(dop), static_cast<const float*>(ddep), static_cast<float*>(g_rgb),
-            static_cast<float*>(g_sig));
-    else
-        (impl == 1 ? k_backward_sp<double> : impl == 2 ? k_backward<double> : k_backward_hy<double>)<<<blocks, kWarps * 32, 0, ctx->stream>>>(
-            p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
-            static_cast<const double*>(rgb), static_cast<const double*>(sig),
-            static_cast<const double*>(dc), static_cast<const double*>(dop),
-            static_cast<const double*>(ddep), static_cast<double*>(g_rgb), static_cast<double*>(g_sig));
-    return launched("render_backward");
+    return dtype == VMB_F32
+               ? launch_backward<float>(ctx, p, rgb, sig, dc, dop, ddep, g_rgb, g_sig)
+               : launch_backward<double>(ctx, p, rgb, sig, dc, dop, ddep, g_rgb, g_sig);
 }
 
 int vmb_transmittance(vmb_ctx* ctx, const vmb_packed_view* p, const void* sig, void* out, int dtype) {

@@ -51,8 +51,8 @@ struct vmb_ctx {
     vmb::DevError* h_err = nullptr;     // pinned mirror
     unsigned long long* d_u64 = nullptr;  // 8 device scalars (totals, counters)
     unsigned long long* h_u64 = nullptr;  // pinned mirror
-    void* scratch[5] = {};          // per-purpose growable device scratch (see scratch())
-    size_t scratch_bytes[5] = {};
+    void* scratch[6] = {};          // per-purpose growable device scratch (see scratch(), SCRATCH_SLOTS)
+    size_t scratch_bytes[6] = {};
     cudaEvent_t events[32] = {};
     // NCCL (dlopen'ed lazily; see comm.cpp)
     void* nccl_comm = nullptr;
@@ -97,7 +97,8 @@ int cuda_fail(cudaError_t e, const char* where);
 // Growable device scratch, one buffer per slot so nested users never alias:
 // slot 0 = scan tile sums, 1 = march / candidates temporaries, 2 = grid update,
 // 3 = validation / misc. Growing synchronizes the stream before freeing.
-enum { SCRATCH_SCAN = 0, SCRATCH_MARCH = 1, SCRATCH_GRID = 2, SCRATCH_MISC = 3, SCRATCH_VOXGRAD = 4, SCRATCH_SLOTS = 5 };
+enum { SCRATCH_SCAN = 0, SCRATCH_MARCH = 1, SCRATCH_GRID = 2, SCRATCH_MISC = 3, SCRATCH_VOXGRAD = 4, SCRATCH_RENDER = 5, SCRATCH_SLOTS = 6 };
+static_assert(sizeof(vmb_ctx::scratch) / sizeof(void*) == SCRATCH_SLOTS, "one scratch buffer per slot");
 void* scratch(vmb_ctx* ctx, int slot, size_t bytes);
 // Integer tuning knob from the environment (read once per call site; dflt when unset).
 inline int env_int(const char* name, int dflt) {
