@@ -41,8 +41,8 @@ sys.path.insert(0, ROOT)
 BASELINE_METRIC = "rays/sec & samples/sec (march+render fwd+bwd) at 1/2/4/8 B200; % HBM roofline"
 SCENE = dict(center=(0.5, 0.5, 0.5), radius=0.2, sigma=200.0, rgb=(0.8, 0.25, 0.25))
 # march = k_march_walk + k_scan_tiles + k_scan_sums + k_scan_add + k_march_expand + k_march_fixup;
-# then k_shade, k_forward, k_backward
-KERNELS_PER_STEP = 9
+# then k_shade, k_forward, k_backward_hy + k_backward_long
+KERNELS_PER_STEP = 10
 
 
 def parse():
@@ -165,7 +165,7 @@ class Clocks:
 PHASE_KERNELS = {"march": ["k_march_walk", "k_scan_tiles", "k_scan_sums", "k_scan_add",
                            "k_march_expand", "k_march_fixup"],
                  "shade": ["k_shade"], "render_forward": ["k_forward"],
-                 "render_backward": ["k_backward_hy"]}
+                 "render_backward": ["k_backward_hy", "k_backward_long"]}
 
 
 def traffic_of(phase):
