@@ -94,6 +94,8 @@ __device__ __forceinline__ bool fine_bit(const uint32_t* bits, int64_t c) {
 
 // Per-ray consumer of candidate intervals: alpha floor + transmittance cut and
 // output (count or fill). Returns false when the ray is finished.
+constexpr int kStgStride = 128;  // k_march's block size
+
 struct Sink {
     uint64_t ray;
     uint32_t n_cand = 0;   // candidates seen (emitted)
@@ -106,6 +108,59 @@ struct Sink {
     uint32_t* idx = nullptr;
     uint64_t base = 0;
     uint64_t cap = 0;
+    // FILL staging (k_march): a lane's samples are collected per aligned group of 4
+    // output slots in shared memory (stg[k * kStgStride], k = slot & 3: t0 at +0,
+    // t1 at +4 * kStgStride) and a complete group goes out as 16-byte vector stores;
+    // per-sample scalar stores from 32 lanes at 32 unrelated addresses were the
+    // two-pass fill's bound (partial-sector writes: 1.6x the algorithmic DRAM bytes).
+    double* stg = nullptr;
+    bool vec = false;  // ts/te/idx 16-byte aligned
+
+    __device__ __forceinline__ void put(double t0, double t1) {
+        const uint64_t o = base + n_kept;
+        if (o >= cap) return;
+        if (!stg) {
+            ts[o] = t0;
+            te[o] = t1;
+            idx[o] = uint32_t(ray);
+            return;
+        }
+        const int k = int(o & 3);
+        stg[k * kStgStride] = t0;
+        stg[(4 + k) * kStgStride] = t1;
+        if (k == 3) flush_group(o - 3 >= base ? o - 3 : base, o + 1);
+    }
+    // slots [lo, hi) of one aligned group of 4, all < cap
+    __device__ __forceinline__ void flush_group(uint64_t lo, uint64_t hi) {
+        if (vec && hi - lo == 4) {
+            const double2 a0 = make_double2(stg[0], stg[kStgStride]);
+            const double2 a1 = make_double2(stg[2 * kStgStride], stg[3 * kStgStride]);
+            const double2 b0 = make_double2(stg[4 * kStgStride], stg[5 * kStgStride]);
+            const double2 b1 = make_double2(stg[6 * kStgStride], stg[7 * kStgStride]);
+            reinterpret_cast<double2*>(ts + lo)[0] = a0;
+            reinterpret_cast<double2*>(ts + lo)[1] = a1;
+            reinterpret_cast<double2*>(te + lo)[0] = b0;
+            reinterpret_cast<double2*>(te + lo)[1] = b1;
+            const uint32_t r = uint32_t(ray);
+            *reinterpret_cast<uint4*>(idx + lo) = make_uint4(r, r, r, r);
+            return;
+        }
+        for (uint64_t q = lo; q < hi; ++q) {
+            const int k = int(q & 3);
+            ts[q] = stg[k * kStgStride];
+            te[q] = stg[(4 + k) * kStgStride];
+            idx[q] = uint32_t(ray);
+        }
+    }
+    // after the walk: the incomplete last group
+    __device__ __forceinline__ void flush_tail() {
+        if (!stg) return;
+        uint64_t e = base + n_kept;
+        if (e > cap) e = cap;
+        if (e <= base || (e & 3) == 0) return;
+        const uint64_t g = e & ~uint64_t(3);
+        flush_group(g > base ? g : base, e);
+    }
     // BUFFER (fused single-pass kernel): kept lattice indices go to shared memory
     uint32_t* buf = nullptr;
     uint32_t buf_stride = 0;
@@ -158,12 +213,7 @@ __device__ __forceinline__ bool on_candidate(const MarchParams& P, Sink& s, uint
     uint32_t ci = s.n_cand++;
     if (!P.filter) {  // candidate mode: keep every grid-passing interval
         if (mbase(MODE) == FILL) {
-            uint64_t o = s.base + s.n_kept;
-            if (o < s.cap) {
-                s.ts[o] = t0;
-                s.te[o] = t1;
-                s.idx[o] = uint32_t(s.ray);
-            }
+            s.put(t0, t1);
         }
         if (mbase(MODE) >= BUFFER && s.n_kept < s.buf_cap) s.buf[s.n_kept * s.buf_stride] = uint32_t(i);
         s.n_kept++;
@@ -196,12 +246,7 @@ __device__ __forceinline__ bool filter_sample(const MarchParams& P, Sink& s, uin
     const double alpha = alpha_pre >= 0.0 ? alpha_pre : 1.0 - exp(-sigma * (t1 - t0));
     if (alpha <= P.thr) return true;
     if (mbase(MODE) == FILL) {
-        uint64_t o = s.base + s.n_kept;
-        if (o < s.cap) {
-            s.ts[o] = t0;
-            s.te[o] = t1;
-            s.idx[o] = uint32_t(s.ray);
-        }
+        s.put(t0, t1);
     }
     if (mbase(MODE) >= BUFFER && s.n_kept < s.buf_cap) s.buf[s.n_kept * s.buf_stride] = uint32_t(i);
     if (mbase(MODE) == BUFFER_FWD) {
@@ -981,6 +1026,9 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, const RT* __restri
                                                uint32_t* __restrict__ idx, uint64_t cap,
                                                unsigned long long* emitted, DevError* err) {
     unsigned long long emit_local = 0;
+    __shared__ double stg[mbase(MODE) == FILL ? 8 * kStgStride : 1];
+    const bool vec = ((reinterpret_cast<uintptr_t>(ts) | reinterpret_cast<uintptr_t>(te) |
+                       reinterpret_cast<uintptr_t>(idx)) & 15) == 0;
     for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rays;
          r += uint64_t(gridDim.x) * blockDim.x) {
         Sink s;
@@ -991,8 +1039,11 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, const RT* __restri
             s.idx = idx;
             s.base = offsets[r];
             s.cap = cap;
+            s.stg = stg + threadIdx.x;
+            s.vec = vec;
         }
         walk<MODE>(P, s, orig, dirs, r, err);
+        if (mbase(MODE) == FILL) s.flush_tail();
         if (mbase(MODE) == COUNT) counts[r] = s.n_kept;
         emit_local += s.n_cand;
     }

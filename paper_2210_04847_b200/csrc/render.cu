@@ -146,6 +146,11 @@ struct Fwd {
     }
 };
 
+#ifndef VMB_FWD_LANE_AVG
+#define VMB_FWD_LANE_AVG 16
+#endif
+constexpr uint32_t kFwdLaneAvg = VMB_FWD_LANE_AVG;
+
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_forward(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays, uint64_t n_samples,
@@ -159,7 +164,11 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_forward(
          w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
         const RayRange rr = ray_range(offsets, counts, n_rays, n_samples, w, lane);
         Fwd acc;
-        if (rr.contiguous) {
+        // Long rays (more than kFwdLaneAvg samples per ray on average, e.g. growth
+        // lattices): one tile then holds the samples of one or two rays, so the
+        // tile loop would run on one lane in 32; each lane streams its own ray
+        // from global memory instead (same expressions, same order).
+        if (rr.contiguous && rr.s1 - rr.s0 <= 32u * kFwdLaneAvg) {
             for (uint32_t cs = rr.s0; cs < rr.s1; cs += Tile<T>::CH) {
                 const uint32_t n = min(uint32_t(Tile<T>::CH), rr.s1 - cs);
                 stage_in<T, false>(sm, lane, cs, n, ts, te, rgb, sig);
@@ -172,6 +181,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_forward(
                 __syncwarp();
             }
         } else {
+#pragma unroll 4
             for (uint32_t s = rr.off; s < rr.end; ++s)
                 acc.add(ts[s], te[s], double(rgb[3 * uint64_t(s)]), double(rgb[3 * uint64_t(s) + 1]),
                         double(rgb[3 * uint64_t(s) + 2]), 1.0 - exp(-double(sig[s]) * (te[s] - ts[s])));
@@ -182,6 +192,82 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_forward(
             color[3 * rr.r + 2] = T(acc.cb);
             opacity[rr.r] = T(acc.op);
             depth[rr.r] = T(acc.dep);
+        }
+    }
+}
+
+// render_forward for long rays (render_forward picks it when the batch averages
+// more than kFwdLaneAvg samples per ray, e.g. growth lattices): one lane per ray,
+// every lane active, and the samples reach shared memory coalesced: the warp
+// stages a window of the next W samples of each of its 32 rays (32 / W rays per
+// load instruction, W = 16 consecutive samples each for f32 attributes, 8 for f64) into a [sample][ray] tile, then
+// each lane composites its own ray's window from it (rendering.cpp:47-58, the
+// tile kernel's expressions in the same order: bit-identical).
+constexpr int kWinWarps = 2, kWinPad = 33;
+template <typename T> struct Win { static constexpr int W = sizeof(T) == 4 ? 16 : 8; };
+
+template <typename T>
+struct WinSmem {
+    static constexpr int kWinW = Win<T>::W;
+    double ts[kWinW][kWinPad];
+    double te[kWinW][kWinPad];
+    T r[kWinW][kWinPad], g[kWinW][kWinPad], b[kWinW][kWinPad], sig[kWinW][kWinPad];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kWinWarps * 32) k_forward_win(
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays, uint64_t n_samples,
+    const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
+    const T* __restrict__ sig, T* __restrict__ color, T* __restrict__ opacity, T* __restrict__ depth) {
+    __shared__ WinSmem<T> smem[kWinWarps];
+    const int lane = threadIdx.x & 31;
+    constexpr int kWinW = Win<T>::W, kRq = 32 / kWinW;  // rays per load instruction
+    const int half = lane / kWinW, j = lane % kWinW;
+    WinSmem<T>& sm = smem[threadIdx.x >> 5];
+    const uint64_t ns = n_samples < 0xffffffffull ? n_samples : 0xffffffffull;
+    const uint64_t n_warps = (n_rays + 31) / 32;
+    for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
+         w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const uint64_t r = w * 32 + lane;
+        const bool valid = r < n_rays;
+        const uint64_t o64 = valid ? __ldg(offsets + r) : 0u;
+        const uint64_t e64 = valid ? o64 + __ldg(counts + r) : 0u;
+        uint32_t pos = uint32_t(o64 < ns ? o64 : ns);
+        const uint32_t end = uint32_t(e64 < ns ? e64 : ns);
+        Fwd acc;
+        while (__any_sync(0xffffffffu, pos < end)) {
+#pragma unroll 4
+            for (int q0 = 0; q0 < 32; q0 += kRq) {
+                const int q = q0 + half;
+                const uint32_t p = __shfl_sync(0xffffffffu, pos, q);
+                const uint32_t e = __shfl_sync(0xffffffffu, end, q);
+                if (p + uint32_t(j) < e) {
+                    const uint64_t x = uint64_t(p) + j;
+                    cp_async<8>(&sm.ts[j][q], ts + x);
+                    cp_async<8>(&sm.te[j][q], te + x);
+                    cp_async<sizeof(T)>(&sm.sig[j][q], sig + x);
+                    cp_async<sizeof(T)>(&sm.r[j][q], rgb + 3 * x);
+                    cp_async<sizeof(T)>(&sm.g[j][q], rgb + 3 * x + 1);
+                    cp_async<sizeof(T)>(&sm.b[j][q], rgb + 3 * x + 2);
+                }
+            }
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+            __syncwarp();
+            const uint32_t n = pos < end ? min(uint32_t(kWinW), end - pos) : 0u;
+            for (uint32_t i = 0; i < n; ++i) {
+                const double t0 = sm.ts[i][lane], t1 = sm.te[i][lane];
+                const double e = exp(-double(sm.sig[i][lane]) * (t1 - t0));
+                acc.add(t0, t1, double(sm.r[i][lane]), double(sm.g[i][lane]), double(sm.b[i][lane]), 1.0 - e);
+            }
+            pos += n;
+            __syncwarp();
+        }
+        if (valid) {
+            color[3 * r] = T(acc.cr);
+            color[3 * r + 1] = T(acc.cg);
+            color[3 * r + 2] = T(acc.cb);
+            opacity[r] = T(acc.op);
+            depth[r] = T(acc.dep);
         }
     }
 }
@@ -902,6 +988,21 @@ extern "C" {
 int vmb_render_forward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, const void* sig,
                        void* color, void* opacity, void* depth, int dtype) {
     if (!p->n_rays) return VMB_OK;
+    if (p->n_samples > uint64_t(kFwdLaneAvg) * p->n_rays) {
+        static const int per_sm = env_int("VMB_FWD_WIN_CTAS", 6);
+        const int wb = grid_blocks(ctx, (p->n_rays + 31) / 32 * 32, kWinWarps * 32, per_sm);
+        if (dtype == VMB_F32)
+            k_forward_win<float><<<wb, kWinWarps * 32, 0, ctx->stream>>>(
+                p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
+                static_cast<const float*>(rgb), static_cast<const float*>(sig), static_cast<float*>(color),
+                static_cast<float*>(opacity), static_cast<float*>(depth));
+        else
+            k_forward_win<double><<<wb, kWinWarps * 32, 0, ctx->stream>>>(
+                p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
+                static_cast<const double*>(rgb), static_cast<const double*>(sig),
+                static_cast<double*>(color), static_cast<double*>(opacity), static_cast<double*>(depth));
+        return launched("render_forward");
+    }
     int blocks = render_blocks(ctx, p->n_rays);
     if (dtype == VMB_F32)
         k_forward<float><<<blocks, kWarps * 32, 0, ctx->stream>>>(

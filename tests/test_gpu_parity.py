@@ -372,6 +372,31 @@ def test_render_paths_vs_oracle(dev, orc, n_rays, max_per_ray, contiguous):
     close(api.transmittance(ap, sig, dev), orc.transmittance(p, sig))
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_render_forward_long_ray_kernel_bit_identical(dev, orc, dtype):
+    """Batches averaging > 16 samples per ray take k_forward_win (staged windows,
+    lane per ray); the same rays padded with empty rays (average below 16) take
+    the tile kernel: the outputs must agree bit for bit (same expressions, same
+    order, rendering.cpp:47-58)."""
+    rng = np.random.default_rng(7)
+    p, rgb, sig = _instance(rng, 300, 200, True)
+    n, s = p.n_rays, len(p.t_starts)
+    assert s > 16 * n
+    r32 = rgb.astype(dtype).astype(np.float64)
+    s32 = sig.astype(dtype).astype(np.float64)
+    pad = 40 * n
+    off = np.concatenate([p.offsets, np.full(pad, s, np.uint32)]).astype(np.uint32)
+    cnt = np.concatenate([p.counts, np.zeros(pad, np.uint32)]).astype(np.uint32)
+    a = api.PackedSamples(p.offsets, p.counts, p.t_starts, p.t_ends, p.ray_indices)
+    b = api.PackedSamples(off, cnt, p.t_starts, p.t_ends, p.ray_indices)
+    fa = api.render_forward(a, r32, s32, dev=dev, dtype=dtype)
+    fb = api.render_forward(b, r32, s32, dev=dev, dtype=dtype)
+    for x, y in zip(fa, fb):
+        assert np.array_equal(np.asarray(x), np.asarray(y)[:n])
+    for x, y in zip(fa, orc.render_forward(p, r32, s32)):
+        close(x, y)
+
+
 def test_render_closed_forms(dev):
     p = api.PackedSamples(np.array([0], np.uint32), np.array([2], np.uint32), np.array([0.0, 1.0]),
                           np.array([1.0, 2.0]), np.array([0, 0], np.uint32))
