@@ -845,7 +845,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_backward_sp(
 int backward_impl() {
     static int impl = [] {
         const char* v = getenv("VMB_BACKWARD");
-        return v && v[0] == 's' ? 1 : v && v[0] == 't' ? 2 : 0;
+        return v && v[0] == 's' ? 1 : v && v[0] == 't' ? 2 : v && v[0] == 'w' ? 3 : 0;
     }();
     return impl;
 }
@@ -941,8 +941,100 @@ int render_blocks(vmb_ctx* ctx, uint64_t n_rays) {
     return grid_blocks(ctx, (n_rays + 31) / 32 * 32, kWarps * 32, per_sm);
 }
 
+// The rays k_backward_hy set aside, with VMB_BACKWARD=win: one lane per ray, in the
+// reference's sequential order (bwd_two_sweep's two sweeps, rendering.cpp:85-108:
+// bit-identical to the one-lane tile path), with k_forward_win's coalesced
+// [sample][ray] windows; the second sweep writes its gradients back into the
+// window and stores them coalesced per ray.
+template <typename T>
+__global__ void __launch_bounds__(kWinWarps * 32) k_backward_win(
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_samples,
+    const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
+    const T* __restrict__ sig, const T* __restrict__ dc, const T* __restrict__ dop,
+    const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig,
+    const uint32_t* __restrict__ long_rays, const unsigned int* __restrict__ n_long) {
+    __shared__ WinSmem<T> smem[kWinWarps];
+    const int lane = threadIdx.x & 31;
+    constexpr int kWinW = Win<T>::W, kRq = 32 / kWinW;
+    const int half = lane / kWinW, j = lane % kWinW;
+    WinSmem<T>& sm = smem[threadIdx.x >> 5];
+    const uint64_t ns = n_samples < 0xffffffffull ? n_samples : 0xffffffffull;
+    const uint64_t n = *n_long;
+    for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w * 32 < n;
+         w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const uint64_t k = w * 32 + lane;
+        const bool valid = k < n;
+        const uint64_t r = valid ? long_rays[k] : 0;
+        const uint64_t o64 = valid ? __ldg(offsets + r) : 0u;
+        const uint64_t e64 = valid ? o64 + __ldg(counts + r) : 0u;
+        const uint32_t off = uint32_t(o64 < ns ? o64 : ns), end = uint32_t(e64 < ns ? e64 : ns);
+        const Up u = load_up(dc, dop, ddep, r, valid);
+        double S = 0.0;
+        for (int sweep = 0; sweep < 2; ++sweep) {
+            uint32_t pos = off;
+            double t = 1.0, P = 0.0;
+            while (__any_sync(0xffffffffu, pos < end)) {
+#pragma unroll 4
+                for (int q0 = 0; q0 < 32; q0 += kRq) {
+                    const int q = q0 + half;
+                    const uint32_t p = __shfl_sync(0xffffffffu, pos, q);
+                    const uint32_t e = __shfl_sync(0xffffffffu, end, q);
+                    if (p + uint32_t(j) < e) {
+                        const uint64_t x = uint64_t(p) + j;
+                        cp_async<8>(&sm.ts[j][q], ts + x);
+                        cp_async<8>(&sm.te[j][q], te + x);
+                        cp_async<sizeof(T)>(&sm.sig[j][q], sig + x);
+                        cp_async<sizeof(T)>(&sm.r[j][q], rgb + 3 * x);
+                        cp_async<sizeof(T)>(&sm.g[j][q], rgb + 3 * x + 1);
+                        cp_async<sizeof(T)>(&sm.b[j][q], rgb + 3 * x + 2);
+                    }
+                }
+                asm volatile("cp.async.wait_all;\n" ::: "memory");
+                __syncwarp();
+                const uint32_t m = pos < end ? min(uint32_t(kWinW), end - pos) : 0u;
+                for (uint32_t i = 0; i < m; ++i) {
+                    const double t0 = sm.ts[i][lane], t1 = sm.te[i][lane];
+                    const double a = 1.0 - exp(-double(sm.sig[i][lane]) * (t1 - t0));
+                    const double v = u.value(double(sm.r[i][lane]), double(sm.g[i][lane]),
+                                             double(sm.b[i][lane]), 0.5 * (t0 + t1));
+                    if (sweep == 0) {
+                        S += t * a * v;
+                    } else {
+                        const double delta = t1 - t0;
+                        const double wgt = t * a;
+                        P += wgt * v;
+                        sm.r[i][lane] = T(u.dcx * wgt);
+                        sm.g[i][lane] = T(u.dcy * wgt);
+                        sm.b[i][lane] = T(u.dcz * wgt);
+                        sm.sig[i][lane] = T(delta * (t * (1.0 - a) * v - (S - P)));
+                    }
+                    t *= 1.0 - a;
+                }
+                __syncwarp();
+                if (sweep == 1) {
+#pragma unroll 4
+                    for (int q0 = 0; q0 < 32; q0 += kRq) {
+                        const int q = q0 + half;
+                        const uint32_t p = __shfl_sync(0xffffffffu, pos, q);
+                        const uint32_t e = __shfl_sync(0xffffffffu, end, q);
+                        if (p + uint32_t(j) < e) {
+                            const uint64_t x = uint64_t(p) + j;
+                            g_sig[x] = sm.sig[j][q];
+                            g_rgb[3 * x] = sm.r[j][q];
+                            g_rgb[3 * x + 1] = sm.g[j][q];
+                            g_rgb[3 * x + 2] = sm.b[j][q];
+                        }
+                    }
+                    __syncwarp();
+                }
+                pos += m;
+            }
+        }
+    }
+}
+
 // render_backward: k_backward_hy, then the rays it set aside (longer than a tile)
-// by k_backward_long; VMB_BACKWARD=sp|tile select the alternative kernels.
+// by k_backward_long (VMB_BACKWARD=win: k_backward_win, the reference's order); VMB_BACKWARD=sp|tile select the alternative kernels.
 template <typename T>
 int launch_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, const void* sig, const void* dc,
                     const void* dop, const void* ddep, void* g_rgb, void* g_sig) {
@@ -971,6 +1063,14 @@ int launch_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, con
         static_cast<const T*>(rgb), static_cast<const T*>(sig), static_cast<const T*>(dc),
         static_cast<const T*>(dop), static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig),
         list + 4, n_long);
+    if (impl == 3) {  // measured at the config 3 stand-in: 4.56 vs 3.48 ms (two DRAM sweeps)
+        static const int per_sm = env_int("VMB_BWD_WIN_CTAS", 6);
+        k_backward_win<T><<<ctx->num_sms * per_sm, kWinWarps * 32, 0, ctx->stream>>>(
+            p->d_offsets, p->d_counts, p->n_samples, p->d_t_starts, p->d_t_ends, static_cast<const T*>(rgb),
+            static_cast<const T*>(sig), static_cast<const T*>(dc), static_cast<const T*>(dop),
+            static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig), list + 4, n_long);
+        return launched("render_backward");
+    }
     k_backward_long<T><<<ctx->num_sms * 4, kWarps * 32, 0, ctx->stream>>>(
         p->d_offsets, p->d_counts, p->n_samples, p->d_t_starts, p->d_t_ends, static_cast<const T*>(rgb),
         static_cast<const T*>(sig), static_cast<const T*>(dc), static_cast<const T*>(dop),
