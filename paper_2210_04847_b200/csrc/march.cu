@@ -1480,6 +1480,13 @@ int march_packed(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
     if (total) launch_march<FILL>(ctx, P, rays, out->d_counts, out->d_offsets, out, nullptr);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "march fill");
+    if (sr.on && sr.fwd && total) {  // long-ray batches: one shade + composite pass
+        vmb_packed_view v{out->d_offsets, out->d_counts, rays->n_rays, out->d_t_starts,
+                          out->d_t_ends, total};
+        rc = shade_forward_long(ctx, rays, &sr.f, sr.time, &v, sr.rgb, sr.sig, sr.color, sr.opacity,
+                                sr.depth, sr.dtype);
+        if (rc != 1) return rc;
+    }
     if (sr.on && total) {
         rc = vmb_shade_field(ctx, rays, &sr.f, sr.time, out->d_ray_indices, out->d_t_starts,
                              out->d_t_ends, total, sr.rgb, sr.sig, sr.dtype);

@@ -272,6 +272,93 @@ __global__ void __launch_bounds__(kWinWarps * 32) k_forward_win(
     }
 }
 
+// march_render for long-ray batches on the two-pass march path (growth lattices):
+// k_shade and k_forward_win in one pass. Each lane keeps its ray's origin and
+// direction, stages windows of t0/t1 coalesced, shades every sample of its ray
+// at the midpoint (k_shade's expressions: voxmarch.cpp:243-244), composites it
+// (rendering.cpp:47-58) and the window's rgb/sigma go out coalesced per ray.
+// Bit-identical to k_shade -> render_forward; t0/t1/ray_indices are read once
+// instead of twice and rgb/sigma are never re-read.
+template <typename RT, typename T, bool VOX>
+__global__ void __launch_bounds__(kWinWarps * 32) k_shade_forward_win(
+    const RT* __restrict__ orig, const RT* __restrict__ dirs, vmb_field f, double time,
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays, uint64_t n_samples,
+    const double* __restrict__ ts, const double* __restrict__ te, T* __restrict__ rgb, T* __restrict__ sig,
+    T* __restrict__ color, T* __restrict__ opacity, T* __restrict__ depth) {
+    __shared__ WinSmem<T> smem[kWinWarps];
+    const int lane = threadIdx.x & 31;
+    constexpr int kWinW = Win<T>::W, kRq = 32 / kWinW;
+    const int half = lane / kWinW, j = lane % kWinW;
+    WinSmem<T>& sm = smem[threadIdx.x >> 5];
+    const uint64_t ns = n_samples < 0xffffffffull ? n_samples : 0xffffffffull;
+    const uint64_t n_warps = (n_rays + 31) / 32;
+    for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
+         w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const uint64_t r = w * 32 + lane;
+        const bool valid = r < n_rays;
+        const uint64_t o64 = valid ? __ldg(offsets + r) : 0u;
+        const uint64_t e64 = valid ? o64 + __ldg(counts + r) : 0u;
+        uint32_t pos = uint32_t(o64 < ns ? o64 : ns);
+        const uint32_t end = uint32_t(e64 < ns ? e64 : ns);
+        const uint64_t rr = valid ? r : 0;
+        const D3 o = d3(double(orig[3 * rr]), double(orig[3 * rr + 1]), double(orig[3 * rr + 2]));
+        const D3 d = d3(double(dirs[3 * rr]), double(dirs[3 * rr + 1]), double(dirs[3 * rr + 2]));
+        Fwd acc;
+        while (__any_sync(0xffffffffu, pos < end)) {
+#pragma unroll 4
+            for (int q0 = 0; q0 < 32; q0 += kRq) {
+                const int q = q0 + half;
+                const uint32_t p = __shfl_sync(0xffffffffu, pos, q);
+                const uint32_t e = __shfl_sync(0xffffffffu, end, q);
+                if (p + uint32_t(j) < e) {
+                    const uint64_t x = uint64_t(p) + j;
+                    cp_async<8>(&sm.ts[j][q], ts + x);
+                    cp_async<8>(&sm.te[j][q], te + x);
+                }
+            }
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+            __syncwarp();
+            const uint32_t m = pos < end ? min(uint32_t(kWinW), end - pos) : 0u;
+            for (uint32_t i = 0; i < m; ++i) {
+                const double t0 = sm.ts[i][lane], t1 = sm.te[i][lane];
+                const D3 x = o + d * (0.5 * (t0 + t1));
+                D3 c;
+                const double sigma = field_rgb_sigma_t<VOX>(f, time_shift(f, x, time), &c);
+                const T cr = T(c.x), cg = T(c.y), cb = T(c.z), sg = T(sigma);
+                sm.r[i][lane] = cr;
+                sm.g[i][lane] = cg;
+                sm.b[i][lane] = cb;
+                sm.sig[i][lane] = sg;
+                const double ex = exp(-double(sg) * (t1 - t0));
+                acc.add(t0, t1, double(cr), double(cg), double(cb), 1.0 - ex);
+            }
+            __syncwarp();
+#pragma unroll 4
+            for (int q0 = 0; q0 < 32; q0 += kRq) {
+                const int q = q0 + half;
+                const uint32_t p = __shfl_sync(0xffffffffu, pos, q);
+                const uint32_t e = __shfl_sync(0xffffffffu, end, q);
+                if (p + uint32_t(j) < e) {
+                    const uint64_t x = uint64_t(p) + j;
+                    sig[x] = sm.sig[j][q];
+                    rgb[3 * x] = sm.r[j][q];
+                    rgb[3 * x + 1] = sm.g[j][q];
+                    rgb[3 * x + 2] = sm.b[j][q];
+                }
+            }
+            __syncwarp();
+            pos += m;
+        }
+        if (valid) {
+            color[3 * r] = T(acc.cr);
+            color[3 * r + 1] = T(acc.cg);
+            color[3 * r + 2] = T(acc.cb);
+            opacity[r] = T(acc.op);
+            depth[r] = T(acc.dep);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ backward
 struct Up {
     double dcx, dcy, dcz, dop, ddep;
@@ -1078,7 +1165,41 @@ int launch_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, con
     return launched("render_backward");
 }
 
+template <typename RT, typename T>
+void launch_shade_forward(vmb_ctx* ctx, const vmb_rays* rays, const vmb_field* f, double time,
+                          const vmb_packed_view* p, void* rgb, void* sig, void* color, void* opacity,
+                          void* depth) {
+    static const int per_sm = env_int("VMB_FWD_WIN_CTAS", 6);
+    const int wb = grid_blocks(ctx, (p->n_rays + 31) / 32 * 32, kWinWarps * 32, per_sm);
+    (f->kind == VMB_FIELD_VOXEL ? k_shade_forward_win<RT, T, true> : k_shade_forward_win<RT, T, false>)
+        <<<wb, kWinWarps * 32, 0, ctx->stream>>>(
+            static_cast<const RT*>(rays->d_origins), static_cast<const RT*>(rays->d_directions), *f, time,
+            p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
+            static_cast<T*>(rgb), static_cast<T*>(sig), static_cast<T*>(color), static_cast<T*>(opacity),
+            static_cast<T*>(depth));
+}
+
 }  // namespace
+}  // namespace vmb
+
+namespace vmb {
+// shade + render_forward in one pass for long-ray batches; returns 1 when the
+// batch is not long-ray dominated (the caller runs k_shade -> render_forward).
+int shade_forward_long(vmb_ctx* ctx, const vmb_rays* rays, const vmb_field* f, double time,
+                       const vmb_packed_view* p, void* rgb, void* sig, void* color, void* opacity,
+                       void* depth, int dtype) {
+    if (!p->n_rays || p->n_samples <= uint64_t(kFwdLaneAvg) * p->n_rays) return 1;
+    if (int frc = check_field(f)) return frc;
+    if (rays->dtype == VMB_F32 && dtype == VMB_F32)
+        launch_shade_forward<float, float>(ctx, rays, f, time, p, rgb, sig, color, opacity, depth);
+    else if (rays->dtype == VMB_F32)
+        launch_shade_forward<float, double>(ctx, rays, f, time, p, rgb, sig, color, opacity, depth);
+    else if (dtype == VMB_F32)
+        launch_shade_forward<double, float>(ctx, rays, f, time, p, rgb, sig, color, opacity, depth);
+    else
+        launch_shade_forward<double, double>(ctx, rays, f, time, p, rgb, sig, color, opacity, depth);
+    return launched("shade_forward");
+}
 }  // namespace vmb
 
 using namespace vmb;

@@ -113,6 +113,9 @@ inline int grid_blocks(vmb_ctx* ctx, uint64_t work, int threads, int per_sm = 8)
 // Host-side field descriptor checks (Aabb ctor math.hpp:50 for box/voxel boxes,
 // TrilinearVoxelField ctor fields.cpp:95-101).
 int check_field(const vmb_field* f);
+int shade_forward_long(vmb_ctx* ctx, const vmb_rays* rays, const vmb_field* f, double time,
+                       const vmb_packed_view* p, void* rgb, void* sig, void* color, void* opacity,
+                       void* depth, int dtype);  // render.cu; 1 = not applicable
 int reset_error(vmb_ctx* ctx);
 int read_error(vmb_ctx* ctx, DevError* out);  // synchronizes
 

@@ -237,3 +237,25 @@ def test_async_capacity_overflow_is_contained():
     assert mc.sum() > 0
     assert np.array_equal(res[0][1][:cap][mc], res[1][1][mc])
     assert np.array_equal(res[0][2].reshape(-1, 3)[:cap][mc], res[1][2].reshape(-1, 3)[mc])
+
+
+@pytest.mark.parametrize("ray_dtype,attr_dtype", [(np.float32, np.float32), (np.float64, np.float64),
+                                                  (np.float32, np.float64)])
+def test_march_render_long_ray_growth(ray_dtype, attr_dtype):
+    """Growth lattices with > 16 kept samples per ray take k_shade_forward_win
+    (shade + composite in one pass): bit for bit march_shaded -> render_forward."""
+    dev = api.Device(0)
+    con = Contraction.sphere((0.5, 0.5, 0.5), 0.5)
+    field = Field.sphere(radius=0.3, sigma=40.0)
+    g = api.OccupancyGrid(64, con, dev=dev)
+    for s in (1, 2, 3):
+        g.update_field(field, 0.95, s)
+    rng = np.random.default_rng(5)
+    d = rng.normal(size=(700, 3))
+    d /= np.sqrt((d * d).sum(1))[:, None]
+    o = np.tile([[0.5, 0.5, 0.55]], (700, 1))
+    rays, keep = _rays(dev, o, d, 0.01, 100.0, ray_dtype)
+    cfg = MarchConfig(1.6914558667664816e-3, 1e-4, 1e-2, 2048, 1.01)
+    a = api.march_device(dev, g, rays, field, cfg, api.DevicePacked.allocate(dev, 700, 64 * 700))
+    assert a.n_samples > 16 * 700
+    _render_both(dev, g, rays, field, cfg, 700, attr_dtype)
