@@ -70,6 +70,12 @@ struct MarchParams {
     double growth;
     D3 ball_c;
     double ball_r;
+    // filtered growth test: |q|^2 outside [r2_lo, r2_hi] decides norm(q) > r
+    // without the sqrt (r^2 (1 -+ 2^-40): far beyond the roundings of r^2 and
+    // of the correctly rounded sqrt); ball_filter = false when r^2 is not a
+    // well-scaled normal number
+    bool ball_filter;
+    double ball_r2_lo, ball_r2_hi;
     double eps, thr;
     uint32_t max_cand;
     bool fast;            // fp32 DDA + filtered fp32 cell test (walk_fast)
@@ -403,7 +409,12 @@ __device__ void walk_growth(const MarchParams& P, Sink& s, D3 o, D3 d, DevError*
         if (c >= 0 && fine_bit(P.bits, c))
             if (!on_candidate<MODE>(P, s, s.n_cand, t, t1, mid, err)) return;
         t += dt;
-        if (norm(mid - P.ball_c) > P.ball_r)
+        const D3 q = mid - P.ball_c;
+        const double q2 = dot(q, q);  // norm() = sqrt(dot(q, q)), math.hpp:31
+        const bool outside = P.ball_filter && q2 > P.ball_r2_hi   ? true
+                             : P.ball_filter && q2 < P.ball_r2_lo ? false
+                                                                  : sqrt(q2) > P.ball_r;
+        if (outside)
             dt *= P.growth;
         else
             dt = P.step;
@@ -1167,6 +1178,12 @@ int march_params(const vmb_grid* g, const vmb_rays* rays, const vmb_march_config
     P->growth = cfg->unbounded_step_growth;
     P->ball_c = g->k.center;
     P->ball_r = g->k.radius;
+    {
+        const double r = P->ball_r;
+        P->ball_filter = r > 1e-100 && r < 1e100;
+        P->ball_r2_lo = P->ball_filter ? r * r * (1.0 - 0x1p-40) : 0.0;
+        P->ball_r2_hi = P->ball_filter ? r * r * (1.0 + 0x1p-40) : 0.0;
+    }
     P->eps = cfg->early_stop_eps;
     P->thr = cfg->alpha_thre;
     P->max_cand = cfg->max_samples_per_ray;

@@ -52,6 +52,8 @@ struct Contract {
     int pow2[3];        // size_k == 2^e exactly -> x/size == x*inv_size bit for bit
     D3 center;          // SphereContract
     double radius;
+    int rpow2;          // radius == 2^e exactly -> x/radius == x*inv_radius bit for bit
+    double inv_radius;
 };
 
 inline Contract make_contract(const vmb_contraction& c) {
@@ -71,6 +73,12 @@ inline Contract make_contract(const vmb_contraction& c) {
     k.inv_size = d3(inv[0], inv[1], inv[2]);
     k.center = d3(c.center[0], c.center[1], c.center[2]);
     k.radius = c.radius;
+    {
+        int e = 0;
+        const double m = frexp(c.radius, &e);
+        k.rpow2 = (m == 0.5) && c.radius > 0.0 && e > -1000 && e < 1000;
+        k.inv_radius = k.rpow2 ? ldexp(1.0, 1 - e) : 0.0;
+    }
     return k;
 }
 
@@ -88,8 +96,12 @@ VM_HD D3 contract(const Contract& c, D3 x) {
         return d3(aabb_axis(x.x, c.lo.x, c.size.x, c.inv_size.x, c.pow2[0]),
                   aabb_axis(x.y, c.lo.y, c.size.y, c.inv_size.y, c.pow2[1]),
                   aabb_axis(x.z, c.lo.z, c.size.z, c.inv_size.z, c.pow2[2]));
-    D3 u = d3((x.x - c.center.x) / c.radius, (x.y - c.center.y) / c.radius,
-              (x.z - c.center.z) / c.radius);
+    // (x - center) / radius (contraction.cpp:19); a power-of-two radius divides
+    // by multiplying with its exact reciprocal (same real number, same rounding)
+    D3 u = c.rpow2 ? d3((x.x - c.center.x) * c.inv_radius, (x.y - c.center.y) * c.inv_radius,
+                        (x.z - c.center.z) * c.inv_radius)
+                   : d3((x.x - c.center.x) / c.radius, (x.y - c.center.y) / c.radius,
+                        (x.z - c.center.z) / c.radius);
     double r = norm(u);
     if (!(r <= 1.0)) u = u * ((2.0 - 1.0 / r) / r);  // contract_to_ball (:18-22)
     return d3((u.x + 2.0) / 4.0, (u.y + 2.0) / 4.0, (u.z + 2.0) / 4.0);
