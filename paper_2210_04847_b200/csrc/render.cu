@@ -204,7 +204,10 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_forward(
 // each lane composites its own ray's window from it (rendering.cpp:47-58, the
 // tile kernel's expressions in the same order: bit-identical).
 constexpr int kWinWarps = 2, kWinPad = 33;
-template <typename T> struct Win { static constexpr int W = sizeof(T) == 4 ? 16 : 8; };
+#ifndef VMB_WIN_W32
+#define VMB_WIN_W32 16
+#endif
+template <typename T> struct Win { static constexpr int W = sizeof(T) == 4 ? VMB_WIN_W32 : 8; };
 
 template <typename T>
 struct WinSmem {
