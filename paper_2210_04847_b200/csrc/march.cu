@@ -1028,8 +1028,15 @@ __global__ void k_march_fixup(MarchParams P, const RT* __restrict__ orig, const 
     }
 }
 
+// two-pass walk kernel (count / fill): capped at 80 registers (6 CTAs/SM); the
+// uncapped build took 120 (count) / 96 (fill) registers. Config 3 stand-in step
+// 10.27 -> 9.86 ms (8 CTAs / 64 registers: 10.10 ms).
+#ifndef VMB_MARCH_MINB
+#define VMB_MARCH_MINB 6
+#endif
+#define VMB_MARCH_LB __launch_bounds__(128, VMB_MARCH_MINB)
 template <typename RT, int MODE>
-__global__ void __launch_bounds__(128) k_march(MarchParams P, const RT* __restrict__ orig,
+__global__ void VMB_MARCH_LB k_march(MarchParams P, const RT* __restrict__ orig,
                                                const RT* __restrict__ dirs, uint64_t n_rays,
                                                uint32_t* __restrict__ counts,
                                                const uint32_t* __restrict__ offsets,
