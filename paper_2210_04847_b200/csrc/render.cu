@@ -653,13 +653,22 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
             continue;
         }
         const unsigned vmask = __ballot_sync(0xffffffffu, rr.valid);  // valid lanes: a prefix
+        {  // rays longer than a tile go to k_backward_long: one list append per warp
+            const unsigned lm = __ballot_sync(0xffffffffu, rr.valid && rr.end - rr.off > uint32_t(Tile<T>::CH));
+            if (lm) {
+                unsigned at = 0;
+                if (lane == 0) at = atomicAdd(n_long, unsigned(__popc(lm)));
+                at = __shfl_sync(0xffffffffu, at, 0);
+                if ((lm >> lane) & 1u)
+                    long_rays[at + __popc(lm & ((1u << lane) - 1u))] = uint32_t(rr.r);
+            }
+        }
         int g0 = 0;
         while (g0 < 32 && ((vmask >> g0) & 1u)) {
             const uint32_t base = __shfl_sync(0xffffffffu, rr.off, g0);
             const bool fits = rr.valid && lane >= g0 && rr.end - base <= uint32_t(Tile<T>::CH);
             const unsigned fm = __ballot_sync(0xffffffffu, fits);  // monotone: ends ascend
-            if (!((fm >> g0) & 1u)) {  // ray g0 alone exceeds a tile: k_backward_long's
-                if (lane == 0) long_rays[atomicAdd(n_long, 1u)] = uint32_t(w * 32 + g0);
+            if (!((fm >> g0) & 1u)) {  // ray g0 alone exceeds a tile: listed above
                 ++g0;
                 continue;
             }
