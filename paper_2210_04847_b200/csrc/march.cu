@@ -1030,7 +1030,8 @@ __global__ void k_march_fixup(MarchParams P, const RT* __restrict__ orig, const 
 
 // two-pass walk kernel (count / fill): capped at 80 registers (6 CTAs/SM); the
 // uncapped build took 120 (count) / 96 (fill) registers. Config 3 stand-in step
-// 10.27 -> 9.86 ms (8 CTAs / 64 registers: 10.10 ms).
+// 10.27 -> 9.86 ms (8 CTAs / 64 registers: 10.10 ms; later A/B at 9.30 ms: 5 CTAs
+// 9.71, 7 CTAs 9.40).
 #ifndef VMB_MARCH_MINB
 #define VMB_MARCH_MINB 6
 #endif
