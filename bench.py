@@ -38,6 +38,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_2210_04847_b200.pipeline import ResidentPipeline  # noqa: E402
+
 BASELINE_METRIC = "rays/sec & samples/sec (march+render fwd+bwd) at 1/2/4/8 B200; % HBM roofline"
 SCENE = dict(center=(0.5, 0.5, 0.5), radius=0.2, sigma=200.0, rgb=(0.8, 0.25, 0.25))
 # march = k_march_walk + k_scan_tiles + k_scan_sums + k_scan_add + k_march_expand + k_march_fixup;
@@ -271,101 +273,6 @@ def run_reference(args):
                              "sample": f"every {stride}th ray per step, {threads} threads, {cpu_model()}"},
             "e2e": {"value": v, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-
-
-# ---------------------------------------------------------------------- resident pipeline
-class ResidentPipeline:
-    """The resident step (rays, upstream gradients, outputs in HBM) as `--chunks`
-    contiguous ray sub-batches served round-robin by `--streams` contexts, each
-    sub-batch one vmb_march_render_field_async + vmb_render_backward pair on its
-    context's stream. Sub-batches of different streams overlap on the device (one
-    sub-batch's expansion/backward fills the SMs the other's walk tail leaves idle).
-    Per-ray outputs land in full-batch arrays, so they can be compared with the
-    single-call step bit for bit."""
-
-    def __init__(self, args, api, dev, grid, field, cfg, rays_dev, ups_dev, N, total_samples):
-        from paper_2210_04847_b200._lib import VMB_F32
-        self.api, self.dev, self.grid, self.field, self.cfg = api, dev, grid, field, cfg
-        self.L = dev.lib
-        self.S, self.K = max(1, args.streams), max(1, args.chunks)
-        self.N = N
-        self.bounds = [(N * i // self.K, N * (i + 1) // self.K) for i in range(self.K)]
-        cmax = max(e - b for b, e in self.bounds)
-        cap = total_samples + 1024  # no sub-batch holds more samples than the whole batch
-        self.ctxs = [dev] + [api.Device(dev.index) for _ in range(self.S - 1)]
-        self.rays_dev, self.ups_dev = rays_dev, ups_dev
-        self.outs = [dev.empty(N * w, np.float32) for w in (3, 1, 1)]
-        self.n_dev = dev.zeros(self.K, np.uint64)
-        self.bufs = [dict(packed=api.DevicePacked.allocate(cx, cmax, cap),
-                          rgb=cx.empty(cap * 3, np.float32), sig=cx.empty(cap, np.float32),
-                          grgb=cx.empty(cap * 3, np.float32), gsig=cx.empty(cap, np.float32))
-                     for cx in self.ctxs]
-        self.cap = cap
-        self.VMB_F32 = VMB_F32
-
-    def chunk(self, k):
-        from paper_2210_04847_b200._lib import Rays, check
-
-        class Ptr:  # a device pointer with the DeviceArray interface the api needs
-            def __init__(self, ptr):
-                self.ptr = ptr
-
-        ci = k % self.S
-        cx, bf = self.ctxs[ci], self.bufs[ci]
-        b, e = self.bounds[k]
-        o, d = self.rays_dev
-        rays = Rays(o.ptr + 12 * b, d.ptr + 12 * b, self.VMB_F32, 0, e - b, 0.2, 1.0)
-        pk = bf["packed"]
-        smp = pk.samples_struct()
-        outs = [a.ptr + 4 * w * b for a, w in zip(self.outs, (3, 1, 1))]
-        check(self.L.vmb_march_render_field_async(
-            cx.h, self.grid.h, C.byref(rays), C.byref(self.field), C.byref(self.cfg), C.byref(smp),
-            bf["rgb"].ptr, bf["sig"].ptr, outs[0], outs[1], outs[2], self.VMB_F32, 0.0, self.n_dev.ptr + 8 * k))
-        pk.n_samples = pk.capacity
-        ups = [Ptr(u.ptr + 4 * w * b) for u, w in zip(self.ups_dev, (3, 1, 1))]
-        self.api.render_backward_device(cx, pk, bf["rgb"], bf["sig"], *ups, bf["grgb"], bf["gsig"])
-
-    def run(self, steps=1, pre_step=None):
-        """`pre_step()` (e.g. config 4's grid update) runs on context 0 before each
-        step's sub-batches, ordered after every stream's previous work and before
-        their next (the grid is read by every stream's walk)."""
-        from paper_2210_04847_b200._lib import check
-        for _ in range(steps):
-            if pre_step is not None and pre_step(dry=True):
-                for i, cx in enumerate(self.ctxs[1:]):
-                    check(self.L.vmb_ctx_wait(self.dev.h, cx.h, 21 + (i % 8)))
-                pre_step()
-                for cx in self.ctxs[1:]:
-                    check(self.L.vmb_ctx_wait(cx.h, self.dev.h, 20))
-            for k in range(self.K):
-                self.chunk(k)
-
-    def begin(self, slot):
-        """event `slot` on context 0; every other stream waits for it"""
-        from paper_2210_04847_b200._lib import check
-        self.dev.record(slot)
-        for cx in self.ctxs[1:]:
-            check(self.L.vmb_ctx_wait(cx.h, self.dev.h, 12))
-
-    def end(self, slot):
-        """context 0 waits for every other stream, then records `slot`"""
-        from paper_2210_04847_b200._lib import check
-        for i, cx in enumerate(self.ctxs[1:]):
-            check(self.L.vmb_ctx_wait(self.dev.h, cx.h, 13 + (i % 8)))
-        self.dev.record(slot)
-
-    def sync(self):
-        for cx in self.ctxs:
-            cx.sync()
-
-    def check(self):
-        """deferred march errors; every sub-batch fitted its sample buffers; total samples"""
-        from paper_2210_04847_b200._lib import check
-        for cx in self.ctxs:
-            check(self.L.vmb_march_check(cx.h))
-        n = self.n_dev.numpy()
-        assert int(n.max()) <= self.cap, "a sub-batch exceeded its sample capacity"
-        return int(n.sum())
 
 
 # ---------------------------------------------------------------------- e2e
@@ -616,7 +523,7 @@ def main():
                 pipe.run(1, pre_step=pipe_update)
 
     if args.fusion == "forward" and args.streams * args.chunks > 1:
-        pipe = ResidentPipeline(args, api, dev, grid, field, cfg, (do_, dd_), (up_c, up_o, up_d), N, S0)
+        pipe = ResidentPipeline(args.streams, args.chunks, api, dev, grid, field, cfg, (do_, dd_), (up_c, up_o, up_d), N, S0)
     clocks = Clocks(dist.local)
     for _ in range(max(args.warmup, 3)):
         step()

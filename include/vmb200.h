@@ -303,6 +303,11 @@ int vmb_shade_field(vmb_ctx* ctx, const vmb_rays* rays, const vmb_field* f, doub
                     int dtype);
 
 /* ------------------------------------------------------------------ rendering */
+/* Per-sample outputs (transmittance, render_backward) are written only at samples
+ * inside some ray's [offset, offset + count): the buffers are caller-owned, so a
+ * pack whose rays do not cover [0, n_samples) leaves the other positions as they
+ * were. The reference returns zero-initialised vectors (rendering.cpp:22, 78-79);
+ * the C++ facade and the Python binding zero the buffers first to match it. */
 /* transmittance (rendering.cpp:19-33): exclusive per-ray T, out [n_samples]. */
 int vmb_transmittance(vmb_ctx* ctx, const vmb_packed_view* p, const void* d_sigmas,
                       void* d_out, int dtype);

@@ -829,7 +829,7 @@ def transmittance(p: PackedSamples, sigmas, dev: Optional[Device] = None) -> np.
     dev = dev or default_device()
     d = p.to_device(dev)
     ds = dev.upload(_f64(sigmas) if p.n_samples else np.zeros(1))
-    out = dev.empty(max(p.n_samples, 1), np.float64)
+    out = dev.zeros(max(p.n_samples, 1), np.float64)  # rendering.cpp:22: zero where no ray covers
     v = d.view()
     check(dev.lib.vmb_transmittance(dev.h, C.byref(v), ds.ptr, out.ptr, VMB_F64))
     return out.numpy(p.n_samples)
@@ -862,7 +862,7 @@ def render_backward(p: PackedSamples, rgbs, sigmas, d_color, d_opacity, d_depth,
     up = lambda a, k=1: dev.upload(np.asarray(a, dtype).reshape(-1) if len(a) else np.zeros(k, dtype))  # noqa: E731
     dr, ds = up(rgbs, 3), up(sigmas)
     dc, do, dd = up(d_color, 3), up(d_opacity), up(d_depth)
-    gr, gs = dev.empty(max(s, 1) * 3, dtype), dev.empty(max(s, 1), dtype)
+    gr, gs = dev.zeros(max(s, 1) * 3, dtype), dev.zeros(max(s, 1), dtype)  # rendering.cpp:78-79
     v = d.view()
     check(dev.lib.vmb_render_backward(dev.h, C.byref(v), dr.ptr, ds.ptr, dc.ptr, do.ptr, dd.ptr,
                                       gr.ptr, gs.ptr, _dt(dtype)))

@@ -659,6 +659,9 @@ std::vector<double> transmittance(const PackedSamples& packed, std::span<const d
     std::lock_guard<std::recursive_mutex> lock(g_mu);
     DevView dv(packed);
     Dev ds = upload(sigmas.data(), sigmas.size()), out(packed.n_samples() * 8);
+    // the reference returns a zero-initialised vector (rendering.cpp:22); the kernel
+    // writes only samples inside some ray's range
+    check(vmb_memset(ctx(), out.p, 0, packed.n_samples() * 8));
     check(vmb_transmittance(ctx(), &dv.v, ds.p, out.p, VMB_F64));
     return download<double>(out, packed.n_samples());
 }
@@ -695,6 +698,9 @@ RenderGradients render_backward(const PackedSamples& packed, const SampleAttribu
     Dev dc = upload(reinterpret_cast<const double*>(d_color.data()), 3 * d_color.size());
     Dev dop = upload(d_opacity.data(), d_opacity.size()), ddep = upload(d_depth.data(), d_depth.size());
     Dev g_rgb(s * 24), g_sig(s * 8);
+    // rendering.cpp:78-79 zero-fills; samples outside every ray stay 0
+    check(vmb_memset(ctx(), g_rgb.p, 0, s * 24));
+    check(vmb_memset(ctx(), g_sig.p, 0, s * 8));
     check(vmb_render_backward(ctx(), &dv.v, rgb.p, sig.p, dc.p, dop.p, ddep.p, g_rgb.p, g_sig.p,
                               VMB_F64));
     RenderGradients g;

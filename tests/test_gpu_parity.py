@@ -372,6 +372,39 @@ def test_render_paths_vs_oracle(dev, orc, n_rays, max_per_ray, contiguous):
     close(api.transmittance(ap, sig, dev), orc.transmittance(p, sig))
 
 
+def test_render_pack_with_gaps_zero_fills(dev, orc):
+    """Rays covering only part of [0, n_samples): gaps between rays and a trailing
+    gap. The reference zero-initialises the per-sample outputs (rendering.cpp:22,
+    78-79), so the uncovered samples must come back 0, not stale memory."""
+    rng = np.random.default_rng(11)
+    p, rgb, sig = _instance(rng, 400, 20, True)
+    n, s = p.n_rays, len(p.t_starts)
+    gap = rng.integers(0, 3, n).astype(np.uint32)  # holes before each ray
+    new_off = (p.offsets + np.cumsum(gap)).astype(np.uint32)
+    tot = int(new_off[-1] + p.counts[-1]) + 7  # + a trailing gap
+    ts, te = np.zeros(tot), np.zeros(tot)
+    for r in range(n):
+        b, c, nb = p.offsets[r], p.counts[r], new_off[r]
+        ts[nb:nb + c], te[nb:nb + c] = p.t_starts[b:b + c], p.t_ends[b:b + c]
+    covered = np.zeros(tot, bool)
+    for r in range(n):
+        covered[new_off[r]:new_off[r] + p.counts[r]] = True
+    te[~covered] = ts[~covered] + 0.05
+    rgb2, sig2 = rng.uniform(0, 1, (tot, 3)), rng.uniform(0, 8, tot)
+    q = O.Packed(new_off, p.counts, ts, te, np.zeros(tot, np.uint32))
+    aq = api.PackedSamples(new_off, p.counts, ts, te, np.zeros(tot, np.uint32))
+    dc, do, dd = rng.uniform(-1, 1, (n, 3)), rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    for _ in range(2):  # the second call reuses freed device memory holding the first's outputs
+        got = api.render_backward(aq, rgb2, sig2, dc, do, dd, dev=dev)
+        ref = orc.render_backward(q, rgb2, sig2, dc, do, dd)
+        for a, b in zip(got, ref):
+            close(a, b)
+        assert not np.asarray(got[1])[~covered].any() and not np.asarray(got[0])[~covered].any()
+        tr = api.transmittance(aq, sig2, dev)
+        close(tr, orc.transmittance(q, sig2))
+        assert not np.asarray(tr)[~covered].any()
+
+
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 def test_render_forward_long_ray_kernel_bit_identical(dev, orc, dtype):
     """Batches averaging > 16 samples per ray take k_forward_win (staged windows,
