@@ -324,6 +324,51 @@ int vmb_render_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* d_rg
 int vmb_render_attribute(vmb_ctx* ctx, const vmb_packed_view* p, const void* d_sigmas,
                          const void* d_values, uint64_t dim, void* d_out, int dtype);
 
+/* ------------------------------------------------------------------ NerfAcc operators
+ * Standalone forms of the compositing the reference performs inside render_forward /
+ * render_backward (rendering.cpp:47-58, 67-112) — the north_star's
+ * render_weight_from_density / render_transmittance_from_alpha (+ backward),
+ * accumulate_along_rays and ray_aabb_intersect. Per-sample arrays are [n_samples]
+ * (values [n_samples][dim]) in dtype; every output and every upstream-gradient
+ * pointer may be NULL (not written / taken as 0). Results agree with the
+ * reference's sequential order within rtol 1e-5 (warp-shuffle segmented scans
+ * reassociate the products and sums; in practice a few ulps). */
+/* alpha = 1 - exp(-sigma (t_end - t_start)), trans = exclusive prod (1 - alpha),
+ * weights = trans * alpha (rendering.cpp:47-58 order of operations per sample). */
+int vmb_render_weight_from_density(vmb_ctx* ctx, const vmb_packed_view* p, const void* d_sigmas,
+                                   void* d_weights, void* d_trans, void* d_alphas, int dtype);
+/* d_grad_sigmas from dL/dweights, dL/dtrans, dL/dalphas; with only dL/dweights = v it
+ * is render_backward's d_sigma (rendering.cpp:99-108). */
+int vmb_render_weight_from_density_backward(vmb_ctx* ctx, const vmb_packed_view* p,
+                                            const void* d_sigmas, const void* d_grad_weights,
+                                            const void* d_grad_trans, const void* d_grad_alphas,
+                                            void* d_grad_sigmas, int dtype);
+/* trans = exclusive prod (1 - alpha), weights = trans * alpha (t's unused). */
+int vmb_render_weight_from_alpha(vmb_ctx* ctx, const vmb_packed_view* p, const void* d_alphas,
+                                 void* d_weights, void* d_trans, int dtype);
+int vmb_render_weight_from_alpha_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* d_alphas,
+                                          const void* d_grad_weights, const void* d_grad_trans,
+                                          void* d_grad_alphas, int dtype);
+int vmb_render_transmittance_from_alpha(vmb_ctx* ctx, const vmb_packed_view* p, const void* d_alphas,
+                                        void* d_trans, int dtype);
+int vmb_render_transmittance_from_alpha_backward(vmb_ctx* ctx, const vmb_packed_view* p,
+                                                 const void* d_alphas, const void* d_grad_trans,
+                                                 void* d_grad_alphas, int dtype);
+/* out [n_rays][dim] = per-ray sum of weights * values (values NULL: sum of weights);
+ * render_attribute (rendering.cpp:114-134) with the weights given. */
+int vmb_accumulate_along_rays(vmb_ctx* ctx, const vmb_packed_view* p, const void* d_weights,
+                              const void* d_values, uint64_t dim, void* d_out, int dtype);
+int vmb_accumulate_along_rays_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* d_weights,
+                                       const void* d_values, uint64_t dim, const void* d_grad_out,
+                                       void* d_grad_weights, void* d_grad_values, int dtype);
+/* Slab test of every ray against every box [n_aabbs][6] = {min xyz, max xyz}, fp64:
+ * t_min = max(near, max_a min(t1, t2)), t_max = min(far, min_a max(t1, t2)) with
+ * t = (box - o) / d; hit = t_max > t_min, misses store miss_value. Outputs
+ * [n_rays][n_aabbs]; d_hit may be NULL. Nearest reference behaviour: the domain
+ * reject of OccupancyGrid::query (occupancy_grid.cpp:69, contraction.cpp:27). */
+int vmb_ray_aabb_intersect(vmb_ctx* ctx, const vmb_rays* rays, const double* d_aabbs, uint64_t n_aabbs,
+                           double miss_value, double* d_t_min, double* d_t_max, uint8_t* d_hit);
+
 /* ------------------------------------------------------------------ multi-GPU (NCCL) */
 /* NCCL is loaded at run time (dlopen "libnccl.so.2") only when these are used. */
 int vmb_comm_unique_id(void* h_id128);

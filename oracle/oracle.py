@@ -518,3 +518,86 @@ class OracleGrid:
 
     def save(self, path):
         self.o._check(self.o._f("grid_save")(self.h, path.encode()))
+
+
+class NerfaccOracle:
+    """The port's sequential restatement of NerfAcc's standalone operators
+    (vm_oracle.h: vmo_weight_from_density ... vmo_ray_aabb_intersect). The
+    reference has no such functions; tests pin these against its render_forward /
+    render_backward / transmittance by decomposition and by finite differences."""
+
+    def __init__(self):
+        self.lib = C.CDLL(LIBS["port"])
+        for name in ("weight_from_density", "weight_from_density_backward", "weight_from_alpha",
+                     "weight_from_alpha_backward", "accumulate_along_rays",
+                     "accumulate_along_rays_backward", "ray_aabb_intersect"):
+            getattr(self.lib, "vmo_" + name).restype = C.c_int
+
+    def _pk(self, packed):
+        off, cnt = _u32(packed.offsets), _u32(packed.counts)
+        self._keep = (off, cnt)
+        return [_p(off, C.c_uint32), _p(cnt, C.c_uint32), C.c_uint64(len(cnt))]
+
+    @staticmethod
+    def _opt(a, shape=None):
+        return None if a is None else _f64(a, shape)
+
+    def weight_from_density(self, packed, sigmas):
+        s = packed.n_samples
+        ts, te, sig = _f64(packed.t_starts), _f64(packed.t_ends), _f64(sigmas)
+        w, t, a = np.zeros(s), np.zeros(s), np.zeros(s)
+        assert self.lib.vmo_weight_from_density(*self._pk(packed), _p(ts, C.c_double), _p(te, C.c_double),
+                                                _p(sig, C.c_double), _p(w, C.c_double), _p(t, C.c_double),
+                                                _p(a, C.c_double)) == 0
+        return w, t, a
+
+    def weight_from_density_backward(self, packed, sigmas, g_weights, g_trans=None, g_alphas=None):
+        s = packed.n_samples
+        ts, te, sig = _f64(packed.t_starts), _f64(packed.t_ends), _f64(sigmas)
+        gw, gt, ga = self._opt(g_weights), self._opt(g_trans), self._opt(g_alphas)
+        out = np.zeros(s)
+        assert self.lib.vmo_weight_from_density_backward(
+            *self._pk(packed), _p(ts, C.c_double), _p(te, C.c_double), _p(sig, C.c_double), _p(gw, C.c_double),
+            _p(gt, C.c_double), _p(ga, C.c_double), _p(out, C.c_double)) == 0
+        return out
+
+    def weight_from_alpha(self, packed, alphas):
+        s = packed.n_samples
+        al = _f64(alphas)
+        w, t = np.zeros(s), np.zeros(s)
+        assert self.lib.vmo_weight_from_alpha(*self._pk(packed), _p(al, C.c_double), _p(w, C.c_double),
+                                              _p(t, C.c_double)) == 0
+        return w, t
+
+    def weight_from_alpha_backward(self, packed, alphas, g_weights=None, g_trans=None):
+        al, gw, gt = _f64(alphas), self._opt(g_weights), self._opt(g_trans)
+        out = np.zeros(packed.n_samples)
+        assert self.lib.vmo_weight_from_alpha_backward(*self._pk(packed), _p(al, C.c_double), _p(gw, C.c_double),
+                                                       _p(gt, C.c_double), _p(out, C.c_double)) == 0
+        return out
+
+    def accumulate_along_rays(self, packed, weights, values=None, dim=1):
+        w, v = _f64(weights), self._opt(values)
+        out = np.zeros(packed.n_rays * dim)
+        assert self.lib.vmo_accumulate_along_rays(*self._pk(packed), _p(w, C.c_double), _p(v, C.c_double),
+                                                  C.c_uint64(dim), _p(out, C.c_double)) == 0
+        return out.reshape(packed.n_rays, dim)
+
+    def accumulate_along_rays_backward(self, packed, weights, values, dim, g_out):
+        w, v, g = _f64(weights), self._opt(values), _f64(g_out)
+        s = packed.n_samples
+        gw, gv = np.zeros(s), np.zeros(s * dim)
+        assert self.lib.vmo_accumulate_along_rays_backward(
+            *self._pk(packed), _p(w, C.c_double), _p(v, C.c_double), C.c_uint64(dim), _p(g, C.c_double),
+            _p(gw, C.c_double), _p(gv, C.c_double)) == 0
+        return gw, gv.reshape(s, dim)
+
+    def ray_aabb_intersect(self, origins, dirs, aabbs, near=-np.inf, far=np.inf, miss=np.inf):
+        o, d, b = _f64(origins, (-1, 3)), _f64(dirs, (-1, 3)), _f64(aabbs, (-1, 6))
+        n, m = len(o), len(b)
+        tmin, tmax, hit = np.zeros(n * m), np.zeros(n * m), np.zeros(n * m, np.uint8)
+        assert self.lib.vmo_ray_aabb_intersect(_p(o, C.c_double), _p(d, C.c_double), C.c_uint64(n),
+                                               _p(b, C.c_double), C.c_uint64(m), C.c_double(near), C.c_double(far),
+                                               C.c_double(miss), _p(tmin, C.c_double), _p(tmax, C.c_double),
+                                               _p(hit, C.c_uint8)) == 0
+        return tmin.reshape(n, m), tmax.reshape(n, m), hit.reshape(n, m).astype(bool)

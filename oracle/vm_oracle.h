@@ -138,6 +138,32 @@ int vmo_grid_probe_range(const vmo_grid* g, const vmb_field* f, const double* ti
                          uint64_t c1, double* probed);
 int vmo_grid_apply(vmo_grid* g, const double* probed, double ema_decay);
 
+/* NerfAcc operators (port only; the reference performs them only inside
+ * render_forward / render_backward, rendering.cpp:47-58, 67-112). Sequential per
+ * ray in the reference's order; NULL outputs are skipped, NULL upstream gradients
+ * count as 0. The density backward keeps rendering.cpp:99-108's suffix form, so
+ * with only grad_weights = value it is render_backward's d_sigma bit for bit. */
+int vmo_weight_from_density(const uint32_t* offsets, const uint32_t* counts, uint64_t n_rays,
+                            const double* t_starts, const double* t_ends, const double* sigmas,
+                            double* weights, double* trans, double* alphas);
+int vmo_weight_from_density_backward(const uint32_t* offsets, const uint32_t* counts, uint64_t n_rays,
+                                     const double* t_starts, const double* t_ends, const double* sigmas,
+                                     const double* g_weights, const double* g_trans,
+                                     const double* g_alphas, double* g_sigmas);
+int vmo_weight_from_alpha(const uint32_t* offsets, const uint32_t* counts, uint64_t n_rays,
+                          const double* alphas, double* weights, double* trans);
+int vmo_weight_from_alpha_backward(const uint32_t* offsets, const uint32_t* counts, uint64_t n_rays,
+                                   const double* alphas, const double* g_weights, const double* g_trans,
+                                   double* g_alphas);
+int vmo_accumulate_along_rays(const uint32_t* offsets, const uint32_t* counts, uint64_t n_rays,
+                              const double* weights, const double* values, uint64_t dim, double* out);
+int vmo_accumulate_along_rays_backward(const uint32_t* offsets, const uint32_t* counts, uint64_t n_rays,
+                                       const double* weights, const double* values, uint64_t dim,
+                                       const double* g_out, double* g_weights, double* g_values);
+int vmo_ray_aabb_intersect(const double* origins, const double* dirs, uint64_t n_rays,
+                           const double* aabbs, uint64_t n_aabbs, double near_, double far_,
+                           double miss_value, double* t_min, double* t_max, uint8_t* hit);
+
 #ifdef __cplusplus
 }
 #endif

@@ -173,6 +173,15 @@ SIGNATURES = {
     "vmb_generate_rays": (I32, [VP, P(Camera), C.c_double, C.c_double, I32, VP, VP, P(Rays)]),
     "vmb_generate_rays_range": (I32, [VP, P(Camera), C.c_double, C.c_double, I32, U64, U64, VP, VP, P(Rays)]),
     "vmb_uniform_step_count": (U64, [D, D, D]),
+    "vmb_render_weight_from_density": (I32, [VP, P(PackedView), VP, VP, VP, VP, I32]),
+    "vmb_render_weight_from_density_backward": (I32, [VP, P(PackedView), VP, VP, VP, VP, VP, I32]),
+    "vmb_render_weight_from_alpha": (I32, [VP, P(PackedView), VP, VP, VP, I32]),
+    "vmb_render_weight_from_alpha_backward": (I32, [VP, P(PackedView), VP, VP, VP, VP, I32]),
+    "vmb_render_transmittance_from_alpha": (I32, [VP, P(PackedView), VP, VP, I32]),
+    "vmb_render_transmittance_from_alpha_backward": (I32, [VP, P(PackedView), VP, VP, VP, I32]),
+    "vmb_accumulate_along_rays": (I32, [VP, P(PackedView), VP, VP, U64, VP, I32]),
+    "vmb_accumulate_along_rays_backward": (I32, [VP, P(PackedView), VP, VP, U64, VP, VP, VP, I32]),
+    "vmb_ray_aabb_intersect": (I32, [VP, P(Rays), VP, U64, D, VP, VP, VP]),
     "vmb_pack": (I32, [VP, VP, U64, VP, VP, U64, P(U64)]),
     "vmb_validate": (I32, [VP, P(PackedView), VP, U64, U64, U64, P(I32)]),
     "vmb_contract": (I32, [VP, P(Contraction), VP, U64, VP]),

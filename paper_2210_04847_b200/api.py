@@ -884,3 +884,149 @@ def render_attribute(p: PackedSamples, sigmas, values, dim: int, dev: Optional[D
     v = d.view()
     check(dev.lib.vmb_render_attribute(dev.h, C.byref(v), ds.ptr, dv.ptr, dim, out.ptr, VMB_F64))
     return out.numpy(p.n_rays * dim)
+
+
+# ---------------------------------------------------------------------- NerfAcc operators
+# Host mirrors of nerfacc.volrend's standalone functions over packed samples
+# (include/vmb200.h "NerfAcc operators"); arrays come back as numpy. Gradients
+# take the upstream gradient of each output (None = 0) and return the input's.
+def _opt_upload(dev, a, dtype, n):
+    if a is None:
+        return None
+    a = np.asarray(a, dtype).reshape(-1)
+    if len(a) != n:
+        raise ValueError("rendering: upstream gradient length mismatch")
+    return dev.upload(a if len(a) else np.zeros(1, dtype))
+
+
+def _ptr(a):
+    return a.ptr if a is not None else None
+
+
+def _per_sample(dev, p: PackedSamples, x, dtype, what="sigma"):
+    x = np.asarray(x, dtype).reshape(-1)
+    if len(x) != p.n_samples:
+        raise ValueError(f"rendering: {what} length mismatch")
+    return dev.upload(x if len(x) else np.zeros(1, dtype))
+
+
+def render_weight_from_density(p: PackedSamples, sigmas, dev: Optional[Device] = None, dtype=np.float64):
+    """-> (weights, transmittance, alphas) per sample; rendering.cpp:47-58 per sample."""
+    dev = dev or default_device()
+    d, s = p.to_device(dev), p.n_samples
+    ds = _per_sample(dev, p, sigmas, dtype)
+    w, t, a = (dev.empty(max(s, 1), dtype) for _ in range(3))
+    v = d.view()
+    check(dev.lib.vmb_render_weight_from_density(dev.h, C.byref(v), ds.ptr, w.ptr, t.ptr, a.ptr, _dt(dtype)))
+    return w.numpy(s), t.numpy(s), a.numpy(s)
+
+
+def render_weight_from_density_backward(p: PackedSamples, sigmas, g_weights=None, g_trans=None, g_alphas=None,
+                                        dev: Optional[Device] = None, dtype=np.float64):
+    """-> dL/dsigmas."""
+    dev = dev or default_device()
+    d, s = p.to_device(dev), p.n_samples
+    ds = _per_sample(dev, p, sigmas, dtype)
+    gw, gt, ga = (_opt_upload(dev, g, dtype, s) for g in (g_weights, g_trans, g_alphas))
+    out = dev.zeros(max(s, 1), dtype)
+    v = d.view()
+    check(dev.lib.vmb_render_weight_from_density_backward(dev.h, C.byref(v), ds.ptr, _ptr(gw), _ptr(gt), _ptr(ga),
+                                                          out.ptr, _dt(dtype)))
+    return out.numpy(s)
+
+
+def render_weight_from_alpha(p: PackedSamples, alphas, dev: Optional[Device] = None, dtype=np.float64):
+    """-> (weights, transmittance)."""
+    dev = dev or default_device()
+    d, s = p.to_device(dev), p.n_samples
+    da = _per_sample(dev, p, alphas, dtype, "alpha")
+    w, t = dev.empty(max(s, 1), dtype), dev.empty(max(s, 1), dtype)
+    v = d.view()
+    check(dev.lib.vmb_render_weight_from_alpha(dev.h, C.byref(v), da.ptr, w.ptr, t.ptr, _dt(dtype)))
+    return w.numpy(s), t.numpy(s)
+
+
+def render_weight_from_alpha_backward(p: PackedSamples, alphas, g_weights=None, g_trans=None,
+                                      dev: Optional[Device] = None, dtype=np.float64):
+    """-> dL/dalphas."""
+    dev = dev or default_device()
+    d, s = p.to_device(dev), p.n_samples
+    da = _per_sample(dev, p, alphas, dtype, "alpha")
+    gw, gt = (_opt_upload(dev, g, dtype, s) for g in (g_weights, g_trans))
+    out = dev.zeros(max(s, 1), dtype)
+    v = d.view()
+    check(dev.lib.vmb_render_weight_from_alpha_backward(dev.h, C.byref(v), da.ptr, _ptr(gw), _ptr(gt), out.ptr,
+                                                        _dt(dtype)))
+    return out.numpy(s)
+
+
+def render_transmittance_from_alpha(p: PackedSamples, alphas, dev: Optional[Device] = None, dtype=np.float64):
+    """-> transmittance (exclusive product of 1 - alpha along each ray)."""
+    dev = dev or default_device()
+    d, s = p.to_device(dev), p.n_samples
+    da = _per_sample(dev, p, alphas, dtype, "alpha")
+    t = dev.empty(max(s, 1), dtype)
+    v = d.view()
+    check(dev.lib.vmb_render_transmittance_from_alpha(dev.h, C.byref(v), da.ptr, t.ptr, _dt(dtype)))
+    return t.numpy(s)
+
+
+def render_transmittance_from_alpha_backward(p: PackedSamples, alphas, g_trans, dev: Optional[Device] = None,
+                                             dtype=np.float64):
+    """-> dL/dalphas."""
+    return render_weight_from_alpha_backward(p, alphas, None, g_trans, dev=dev, dtype=dtype)
+
+
+def accumulate_along_rays(p: PackedSamples, weights, values=None, dim: int = 1, dev: Optional[Device] = None,
+                          dtype=np.float64):
+    """-> out[n_rays, dim] = per-ray sum of weights * values (values None: sum of weights)."""
+    if dim == 0:
+        raise ValueError("rendering: value length mismatch")
+    dev = dev or default_device()
+    d, s, n = p.to_device(dev), p.n_samples, p.n_rays
+    dw = _per_sample(dev, p, weights, dtype, "weight")
+    dv = None
+    if values is not None:
+        values = np.asarray(values, dtype).reshape(-1)
+        if len(values) != s * dim:
+            raise ValueError("rendering: value length mismatch")
+        dv = dev.upload(values if len(values) else np.zeros(1, dtype))
+    out = dev.empty(max(n * dim, 1), dtype)
+    v = d.view()
+    check(dev.lib.vmb_accumulate_along_rays(dev.h, C.byref(v), dw.ptr, _ptr(dv), dim, out.ptr, _dt(dtype)))
+    return out.numpy(n * dim).reshape(n, dim)
+
+
+def accumulate_along_rays_backward(p: PackedSamples, weights, values, dim: int, g_out,
+                                   dev: Optional[Device] = None, dtype=np.float64):
+    """-> (dL/dweights, dL/dvalues or None)."""
+    dev = dev or default_device()
+    d, s, n = p.to_device(dev), p.n_samples, p.n_rays
+    dw = _per_sample(dev, p, weights, dtype, "weight")
+    dv = None if values is None else dev.upload(np.asarray(values, dtype).reshape(-1) if s else np.zeros(1, dtype))
+    g = dev.upload(np.asarray(g_out, dtype).reshape(-1) if n else np.zeros(1, dtype))
+    gw = dev.zeros(max(s, 1), dtype)
+    gv = dev.zeros(max(s * dim, 1), dtype) if values is not None else None
+    v = d.view()
+    check(dev.lib.vmb_accumulate_along_rays_backward(dev.h, C.byref(v), dw.ptr, _ptr(dv), dim, g.ptr, gw.ptr,
+                                                     _ptr(gv), _dt(dtype)))
+    return gw.numpy(s), (gv.numpy(s * dim).reshape(s, dim) if gv is not None else None)
+
+
+def ray_aabb_intersect(origins, dirs, aabbs, near_plane=-np.inf, far_plane=np.inf, miss_value=np.inf,
+                       dev: Optional[Device] = None):
+    """-> (t_min, t_max, hit), each [n_rays, n_aabbs]; aabbs [n_aabbs, 6] = min xyz, max xyz."""
+    dev = dev or default_device()
+    o = np.ascontiguousarray(origins, np.float64).reshape(-1, 3)
+    d = np.ascontiguousarray(dirs, np.float64).reshape(-1, 3)
+    b = np.ascontiguousarray(aabbs, np.float64).reshape(-1, 6)
+    n, m = len(o), len(b)
+    do_, dd_ = dev.upload(o if n else np.zeros((1, 3))), dev.upload(d if n else np.zeros((1, 3)))
+    db = dev.upload(b if m else np.zeros((1, 6)))
+    rays = Rays(do_.ptr, dd_.ptr, VMB_F64, 0, n, float(near_plane), float(far_plane))
+    tmin, tmax = dev.empty(max(n * m, 1), np.float64), dev.empty(max(n * m, 1), np.float64)
+    hit = dev.empty(max(n * m, 1), np.uint8)
+    check(dev.lib.vmb_ray_aabb_intersect(dev.h, C.byref(rays), db.ptr, m, float(miss_value), tmin.ptr, tmax.ptr,
+                                         hit.ptr))
+    return (tmin.numpy(n * m).reshape(n, m), tmax.numpy(n * m).reshape(n, m),
+            hit.numpy(n * m).reshape(n, m).astype(bool))
