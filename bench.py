@@ -60,6 +60,11 @@ def parse():
     ap.add_argument("--config2", type=int, default=1,
                     help="N=1: also time BASELINE config 2 (2^18 rays, step sqrt(3)/1024) in a sub-run "
                          "and report it under `config2`")
+    ap.add_argument("--config3", type=int, default=1,
+                    help="N=1: also time BASELINE config 3 (4-level cascaded grid, cone stepping, 2^20 rays) "
+                         "in a sub-run and report it under `config3`")
+    ap.add_argument("--workload", default="config5", choices=["config5", "config3"],
+                    help="config3: the multi-level grid + cone-step workload alone (one JSON line)")
     ap.add_argument("--cpu-sample-rays", type=int, default=1 << 20)
     ap.add_argument("--ref-sample-rays", type=int, default=1 << 18)
     ap.add_argument("--phases", type=int, default=1, help="per-phase event timing pass")
@@ -418,11 +423,127 @@ def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev
                     f"{n_chunk} chunks pipelined over {n_ctx} streams"}
 
 
+
+# ---------------------------------------------------------------------- config 3
+def run_config3(args):
+    """BASELINE config 3 (Mip-NeRF-360-shaped, unbounded): a 4-level cascaded
+    occupancy grid (128^3 per level, level l = the unit box scaled by 2^l about its
+    center, up to [-3.5, 4.5]^3) and NerfAcc cone stepping (cone_angle 1/256), 2^20
+    rays of the orbit camera from inside level 1 (near 0.01, far 100), SolidSphere
+    r=0.3 sigma=40: central rays end in the sphere (T cut), the others cross every
+    level until they leave the outermost box. Step = vmb_march_render_cascade (walk
+    count -> scan -> fill, shading + forward) -> vmb_render_backward."""
+    from paper_2210_04847_b200 import api, workload
+    from paper_2210_04847_b200._lib import VMB_F32, Contraction, Field, MarchConfig, MarchStats, Rays, check
+    dev = api.Device(0)
+    L = dev.lib
+    field = Field.sphere(radius=0.3, sigma=40.0)
+    cfg = MarchConfig(math.sqrt(3.0) / 1024, 1e-4, 1e-2, 4096, 1.0)
+    cone = 1.0 / 256
+    R, levels, W = 128, 4, 1024
+    cas = api.Cascade(R, Contraction.aabb((0, 0, 0), (1, 1, 1)), levels, dev=dev)
+    dev.record(10)
+    for s in workload.grid_warmup_seeds(16, 5):
+        cas.update_field(field, 0.95, s)
+    dev.record(11)
+    upd_ms = dev.elapsed_ms(10, 11) / 16
+    o64, d64 = workload.orbit_rays(W, near=0.01, far=100.0)
+    N = len(o64)
+    o32, d32 = o64.astype(np.float32), d64.astype(np.float32)
+    dc, do, dd = (x.astype(np.float32) for x in workload.upstream_grads(N, 31))
+    do_, dd_ = dev.upload(o32), dev.upload(d32)
+    rays = Rays(do_.ptr, dd_.ptr, VMB_F32, 0, N, 0.01, 100.0)
+    st = MarchStats()
+    packed = api.march_cascade_device(dev, cas, rays, field, cfg, api.DevicePacked.allocate(dev, N, 64 * N), cone,
+                                      1e10, st)
+    S, cap = packed.n_samples, packed.capacity
+    rgb, sig = dev.empty(3 * cap, np.float32), dev.empty(cap, np.float32)
+    gr, gs = dev.empty(3 * cap, np.float32), dev.empty(cap, np.float32)
+    outs = [dev.empty(3 * N, np.float32), dev.empty(N, np.float32), dev.empty(N, np.float32)]
+    ups = [dev.upload(x) for x in (dc, do, dd)]
+
+    def step():
+        api.march_render_cascade_device(dev, cas, rays, field, cfg, packed, rgb, sig, *outs, cone_angle=cone)
+        api.render_backward_device(dev, packed, rgb, sig, *ups, gr, gs)
+
+    clocks = Clocks(0)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    dev.sync()
+    dev.record(0)
+    for _ in range(args.steps):
+        step()
+    dev.record(1)
+    dev.sync()
+    ms = dev.elapsed_ms(0, 1) / args.steps
+    t_end = time.time() + 1.0
+    while time.time() < t_end:
+        step()
+    dev.sync()
+    clk = clocks.stop()
+    assert packed.n_samples == S
+    # e2e through the C ABI: pinned host rays + upstream grads in, outputs out
+    host = [o32, d32, dc, do, dd]
+    pins = []
+    for a in host:
+        pp = C.c_void_p()
+        check(L.vmb_host_alloc(a.nbytes, C.byref(pp)))
+        C.memmove(pp.value, a.ctypes.data, a.nbytes)
+        pins.append(pp)
+    outp = []
+    for w in (3, 1, 1):
+        pp = C.c_void_p()
+        check(L.vmb_host_alloc(4 * w * N, C.byref(pp)))
+        outp.append(pp)
+    dst = [do_, dd_] + ups
+
+    def e2e_step():
+        for pp, a, dv in zip(pins, host, dst):
+            check(L.vmb_memcpy_h2d(dev.h, dv.ptr, pp.value, a.nbytes))
+        step()
+        for pp, o, w in zip(outp, outs, (3, 1, 1)):
+            check(L.vmb_memcpy_d2h(dev.h, pp.value, o.ptr, 4 * w * N))
+
+    e2e_step()
+    dev.sync()
+    dev.record(2)
+    for _ in range(args.steps):
+        e2e_step()
+    dev.record(3)
+    dev.sync()
+    e2e_ms = dev.elapsed_ms(2, 3) / args.steps
+    for pp in pins + outp:
+        L.vmb_host_free(pp)
+    pk = peaks()
+    peak = pk.get("hbm_gbs", 6650.0)
+    # fused march + shade + forward, then backward: 80 N + 84 S + the levels' bits
+    step_bytes = 80 * N + 84 * S + levels * R ** 3 / 8
+    line = {"metric": BASELINE_METRIC, "value": N / (ms * 1e-3), "unit": "rays/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "samples_per_s": S / (ms * 1e-3), "samples": S, "samples_emitted": st.samples_emitted,
+            "grid_update_ms": upd_ms,
+            "config": {"workload": f"config 3: {N} orbit-camera rays from inside level 1 (W={W}, near 0.01, far 100), "
+                                   f"{levels}-level cascaded {R}^3 grid over [0,1]^3 (to [-3.5,4.5]^3), cone "
+                                   f"stepping cone_angle 1/256, step sqrt(3)/1024, SolidSphere r=0.3 sigma=40",
+                       "l2": "inputs larger than L2 (~0.4 GB working set per step)"},
+            "roofline": {"bound": "hbm", "kernel": "step (vmb_march_render_cascade + vmb_render_backward)",
+                         "algorithmic_bytes": step_bytes, "achieved": step_bytes / (ms * 1e-3) / 1e9,
+                         "peak": peak, "unit": "GB/s", "frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
+                         "traffic": None},
+            "e2e": {"value": N / (e2e_ms * 1e-3), "unit": "rays/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": int(sum(a.nbytes for a in host)), "d2h_bytes_per_step": 20 * N},
+            "clocks": clk}
+    print(json.dumps(line), flush=True)
+
+
 # ---------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "config3":
+        return run_config3(args)
     from paper_2210_04847_b200 import api, workload
     from paper_2210_04847_b200._lib import VMB_F32, Contraction, Field, MarchConfig, Rays, check
 
@@ -653,6 +774,20 @@ def main():
         except Exception as ex:  # pragma: no cover
             cfg2 = {"error": repr(ex)}
 
+    cfg3 = None
+    if dist.rank == 0 and dist.world == 1 and args.config3 and args.width == 2048:
+        try:  # BASELINE config 3 (cascaded grid + cone stepping), its own process
+            out = subprocess.run([sys.executable, os.path.abspath(__file__), "--workload", "config3", "--steps",
+                                  str(max(min(args.steps, 20), 5)), "--warmup", str(args.warmup)],
+                                 capture_output=True, text=True, timeout=900)
+            c3 = json.loads(out.stdout.strip().splitlines()[-1])
+            cfg3 = {k: c3[k] for k in ("value", "unit", "ms_per_step", "samples_per_s", "samples", "e2e",
+                                       "clocks", "grid_update_ms")}
+            cfg3["workload"] = c3["config"]["workload"]
+            cfg3["roofline_step_frac"] = c3["roofline"]["frac"]
+        except Exception as ex:  # pragma: no cover
+            cfg3 = {"error": repr(ex)}
+
     cpu = None
     if dist.rank == 0 and dist.world == 1 and args.cpu_baseline:
         try:
@@ -682,7 +817,7 @@ def main():
                 "pipeline": pipe_info,
                 "phases_ms": phase, "grid_update_ms": grid_update_ms,
                 "roofline": roof, "e2e": e2e, "e2e_camera": e2e_cam, "cpu_baseline": cpu, "clocks": clk,
-                "config2": cfg2,
+                "config2": cfg2, "config3": cfg3,
                 "gpu_launches": (KERNELS_PER_STEP - {"none": 0, "shade": 1, "forward": 2}[args.fusion])
                 * args.steps * (pipe.K if pipe else 1)}
         print(json.dumps(line), flush=True)

@@ -294,6 +294,38 @@ int vmb_march_filter(vmb_ctx* ctx, const vmb_packed_view* candidates, const doub
 int vmb_march_uniform(vmb_ctx* ctx, const vmb_rays* rays, const vmb_march_config* cfg,
                       vmb_samples* out, uint64_t* h_n);
 
+/* ------------------------------------------------------------------ multi-level grid + cone stepping
+ * NerfAcc's cascaded occupancy grid and cone-step sampling (reference non-goals,
+ * SPEC.md:215,276). Level 0 is the call's grid (any contraction);
+ * levels[0..n_levels) are AABB grids, each strictly containing the one below
+ * (vmb_cascade_level_box: level 0's box scaled by 2^l about its center). A point is
+ * decided by the FINEST level whose domain contains it, with that level's own
+ * OccupancyGrid::query (occupancy_grid.cpp:67-76); each level is updated with the
+ * grid API. With n_levels = 0 and cone = 0 the marcher is march() (A13/A14)
+ * exactly. cone != 0: the interval starting at t has width
+ * dt = min(max(t * cone_angle, step_size), max_step) and t accumulates (t += dt,
+ * the growth walk's arithmetic, ray_marching.cpp:88-106); growth > 1 and cone are
+ * exclusive. Stacked levels / cone take the accumulated-t walk (count -> scan ->
+ * fill), which ends a ray once its midpoint has left the outermost AABB level. */
+typedef struct vmb_march_ext {
+    const vmb_grid* const* levels; /* levels above level 0, finest first */
+    uint32_t n_levels;             /* <= 7 */
+    int32_t cone;                  /* 1: cone stepping */
+    double cone_angle;
+    double max_step;               /* >= step_size */
+} vmb_march_ext;
+int vmb_cascade_level_box(const vmb_contraction* base, uint32_t level, vmb_contraction* out);
+int vmb_cascade_query(vmb_ctx* ctx, const vmb_grid* level0, const vmb_march_ext* ext, const double* d_points,
+                      uint64_t n, uint8_t* d_occupied);
+int vmb_march_cascade(vmb_ctx* ctx, const vmb_grid* level0, const vmb_march_ext* ext, const vmb_rays* rays,
+                      const vmb_field* f, const vmb_march_config* cfg, vmb_samples* out, uint64_t* h_n,
+                      vmb_march_stats* stats);
+/* + analytic shading and render_forward (the vmb_march_render_field outputs). */
+int vmb_march_render_cascade(vmb_ctx* ctx, const vmb_grid* level0, const vmb_march_ext* ext,
+                             const vmb_rays* rays, const vmb_field* f, const vmb_march_config* cfg,
+                             vmb_samples* out, void* d_rgbs, void* d_sigmas, void* d_color, void* d_opacity,
+                             void* d_depth, int dtype, double time, uint64_t* h_n, vmb_march_stats* stats);
+
 /* ------------------------------------------------------------------ shading (harness) */
 /* shade_samples (voxmarch.cpp:235-251) for an analytic field (+time shift):
  * rgb and sigma at each sample midpoint, written as dtype. */

@@ -289,6 +289,31 @@ class Oracle:
                                            C.byref(cfg), C.c_int(n_threads), C.byref(pp)))
         return self._take_packed(pp)
 
+    def march_cascade(self, origins, dirs, near, far, grid, levels, field, cfg, cone_angle=None, max_step=1e10):
+        """port only: vmo_march_cascade (levels = OracleGrids above `grid`, finest first)"""
+        assert self.kind == "port"
+        o, d = _f64(origins, (-1, 3)), _f64(dirs, (-1, 3))
+        arr = (C.c_void_p * max(len(levels), 1))(*[g.h.value for g in levels])
+        pp = C.POINTER(_Packed)()
+        f = self.lib.vmo_march_cascade
+        f.restype = C.c_int
+        self._check(f(_p(o, C.c_double), _p(d, C.c_double), C.c_uint64(len(o)), C.c_double(near), C.c_double(far),
+                      grid.h, arr, C.c_uint32(len(levels)), C.c_int(cone_angle is not None),
+                      C.c_double(cone_angle or 0.0), C.c_double(max_step), C.byref(field), C.byref(cfg),
+                      C.byref(pp)))
+        return self._take_packed(pp)
+
+    def cascade_query(self, grid, levels, points):
+        assert self.kind == "port"
+        x = _f64(points, (-1, 3))
+        out = np.zeros(len(x), np.uint8)
+        arr = (C.c_void_p * max(len(levels), 1))(*[g.h.value for g in levels])
+        f = self.lib.vmo_cascade_query
+        f.restype = C.c_int
+        self._check(f(grid.h, arr, C.c_uint32(len(levels)), _p(x, C.c_double), C.c_uint64(len(x)),
+                      _p(out, C.c_uint8)))
+        return out.astype(bool)
+
     def march_callback(self, origins, dirs, near, far, grid, sigma_fn, cfg, n_threads=1):
         """sigma_fn(ts, te, idx) -> array of sigmas (any length; mismatch is an error)."""
         o, d = _f64(origins, (-1, 3)), _f64(dirs, (-1, 3))

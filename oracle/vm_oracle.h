@@ -138,6 +138,16 @@ int vmo_grid_probe_range(const vmo_grid* g, const vmb_field* f, const double* ti
                          uint64_t c1, double* probed);
 int vmo_grid_apply(vmo_grid* g, const double* probed, double ema_decay);
 
+/* Multi-level grid + cone stepping (port only; vmb_march_ext semantics, include/vmb200.h):
+ * levels above level 0 (finest first), the finest level containing a point decides;
+ * cone: dt = min(max(t cone_angle, step), max_step), t accumulated. Walks to `far`. */
+int vmo_march_cascade(const double* origins, const double* dirs, uint64_t n_rays, double near_, double far_,
+                      const vmo_grid* level0, const vmo_grid* const* levels, uint32_t n_levels, int cone,
+                      double cone_angle, double max_step, const vmb_field* f, const vmb_march_config* cfg,
+                      vmo_packed** out);
+int vmo_cascade_query(const vmo_grid* level0, const vmo_grid* const* levels, uint32_t n_levels,
+                      const double* points, uint64_t n, uint8_t* out);
+
 /* NerfAcc operators (port only; the reference performs them only inside
  * render_forward / render_backward, rendering.cpp:47-58, 67-112). Sequential per
  * ray in the reference's order; NULL outputs are skipped, NULL upstream gradients

@@ -132,6 +132,12 @@ class PackedView(C.Structure):
                 ("d_t_starts", C.c_void_p), ("d_t_ends", C.c_void_p), ("n_samples", C.c_uint64)]
 
 
+class MarchExt(C.Structure):
+    """vmb_march_ext: stacked grid levels (NerfAcc cascades) and cone stepping."""
+    _fields_ = [("levels", C.c_void_p), ("n_levels", C.c_uint32), ("cone", C.c_int32),
+                ("cone_angle", C.c_double), ("max_step", C.c_double)]
+
+
 P = C.POINTER
 VP, U64, I32, D = C.c_void_p, C.c_uint64, C.c_int, C.c_double
 
@@ -173,6 +179,12 @@ SIGNATURES = {
     "vmb_generate_rays": (I32, [VP, P(Camera), C.c_double, C.c_double, I32, VP, VP, P(Rays)]),
     "vmb_generate_rays_range": (I32, [VP, P(Camera), C.c_double, C.c_double, I32, U64, U64, VP, VP, P(Rays)]),
     "vmb_uniform_step_count": (U64, [D, D, D]),
+    "vmb_cascade_level_box": (I32, [P(Contraction), C.c_uint32, P(Contraction)]),
+    "vmb_cascade_query": (I32, [VP, VP, P(MarchExt), VP, U64, VP]),
+    "vmb_march_cascade": (I32, [VP, VP, P(MarchExt), P(Rays), P(Field), P(MarchConfig), P(Samples), P(U64),
+                                P(MarchStats)]),
+    "vmb_march_render_cascade": (I32, [VP, VP, P(MarchExt), P(Rays), P(Field), P(MarchConfig), P(Samples), VP, VP,
+                                       VP, VP, VP, I32, D, P(U64), P(MarchStats)]),
     "vmb_render_weight_from_density": (I32, [VP, P(PackedView), VP, VP, VP, VP, I32]),
     "vmb_render_weight_from_density_backward": (I32, [VP, P(PackedView), VP, VP, VP, VP, VP, I32]),
     "vmb_render_weight_from_alpha": (I32, [VP, P(PackedView), VP, VP, VP, I32]),

@@ -20,7 +20,7 @@ from typing import Callable, Optional
 
 import numpy as np
 
-from ._lib import (VMB_CAPACITY, VMB_F32, VMB_F64, Camera, Contraction, Field, MarchConfig,
+from ._lib import (VMB_CAPACITY, VMB_F32, VMB_F64, Camera, Contraction, Field, MarchConfig, MarchExt,
                    MarchStats, PackedView, Rays, Samples, VmbError, check, lib)
 
 __all__ = ["Device", "DeviceArray", "default_device", "Contraction", "Field", "MarchConfig",
@@ -1030,3 +1030,80 @@ def ray_aabb_intersect(origins, dirs, aabbs, near_plane=-np.inf, far_plane=np.in
                                          hit.ptr))
     return (tmin.numpy(n * m).reshape(n, m), tmax.numpy(n * m).reshape(n, m),
             hit.numpy(n * m).reshape(n, m).astype(bool))
+
+
+# ---------------------------------------------------------------------- multi-level grid
+class Cascade:
+    """NerfAcc's multi-level occupancy grid (vmb_march_ext): level 0
+    is an AABB OccupancyGrid over `base`, level l its box scaled by 2^l about the
+    center (vmb_cascade_level_box). Each level is a full OccupancyGrid (update /
+    query / bits / OGRD) with the reference's semantics; a point is decided by the
+    finest level containing it. levels=1 is a plain OccupancyGrid."""
+
+    def __init__(self, resolution: int, base: Contraction, levels: int = 4, alpha_threshold: float = 1e-2,
+                 reference_step: float = 0.0, initial_density: float = 0.0, dev: Optional[Device] = None):
+        self.dev = dev or default_device()
+        self.grids = []
+        for level in range(levels):
+            con = Contraction()
+            check(self.dev.lib.vmb_cascade_level_box(C.byref(base), level, C.byref(con)))
+            self.grids.append(OccupancyGrid(resolution, con, alpha_threshold, reference_step, initial_density,
+                                            dev=self.dev))
+        self._arr = (C.c_void_p * max(levels - 1, 1))(*[g.h.value for g in self.grids[1:]])
+
+    @property
+    def levels(self):
+        return len(self.grids)
+
+    def update_field(self, field: Field, decay: float, seed=None, timestamps=(0.0,)):
+        for g in self.grids:
+            g.update_field(field, decay, seed, timestamps)
+
+    def ext(self, cone_angle: Optional[float] = None, max_step: float = 1e10) -> MarchExt:
+        return MarchExt(C.cast(self._arr, C.c_void_p), len(self.grids) - 1, int(cone_angle is not None),
+                        float(cone_angle or 0.0), float(max_step))
+
+    def query(self, points) -> np.ndarray:
+        x = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        dx = self.dev.upload(x if len(x) else np.zeros((1, 3)))
+        out = self.dev.empty(max(len(x), 1), np.uint8)
+        e = self.ext()
+        check(self.dev.lib.vmb_cascade_query(self.dev.h, self.grids[0].h, C.byref(e), dx.ptr, len(x), out.ptr))
+        return out.numpy(len(x)).astype(bool)
+
+
+def march_cascade_device(dev: Device, cascade: Cascade, rays: Rays, field: Field, cfg: MarchConfig,
+                         out: DevicePacked, cone_angle: Optional[float] = None, max_step: float = 1e10,
+                         stats: Optional[MarchStats] = None) -> DevicePacked:
+    """vmb_march_cascade into caller buffers; grows them once on VMB_CAPACITY."""
+    e = cascade.ext(cone_angle, max_step)
+    n = C.c_uint64()
+    for attempt in range(2):
+        smp = out.samples_struct()
+        rc = dev.lib.vmb_march_cascade(dev.h, cascade.grids[0].h, C.byref(e), C.byref(rays), C.byref(field),
+                                       C.byref(cfg), C.byref(smp), C.byref(n),
+                                       C.byref(stats) if stats is not None else None)
+        if rc != VMB_CAPACITY or attempt:
+            break
+        grown = DevicePacked.allocate(dev, out.n_rays, int(n.value * 1.25) + 1024)
+        out.t_starts, out.t_ends, out.ray_indices = grown.t_starts, grown.t_ends, grown.ray_indices
+    check(rc)
+    out.n_samples = int(n.value)
+    return out
+
+
+def march_render_cascade_device(dev: Device, cascade: Cascade, rays: Rays, field: Field, cfg: MarchConfig,
+                                out: DevicePacked, rgbs: DeviceArray, sigmas: DeviceArray, color: DeviceArray,
+                                opacity: DeviceArray, depth: DeviceArray, cone_angle: Optional[float] = None,
+                                max_step: float = 1e10, time: float = 0.0,
+                                stats: Optional[MarchStats] = None) -> DevicePacked:
+    """vmb_march_render_cascade: cascade march + analytic shading + render_forward."""
+    e = cascade.ext(cone_angle, max_step)
+    n = C.c_uint64()
+    smp = out.samples_struct()
+    check(dev.lib.vmb_march_render_cascade(dev.h, cascade.grids[0].h, C.byref(e), C.byref(rays), C.byref(field),
+                                           C.byref(cfg), C.byref(smp), rgbs.ptr, sigmas.ptr, color.ptr, opacity.ptr,
+                                           depth.ptr, _dt(rgbs.dtype), time, C.byref(n),
+                                           C.byref(stats) if stats is not None else None))
+    out.n_samples = int(n.value)
+    return out

@@ -51,7 +51,13 @@ __host__ __device__ constexpr bool matab(int m) { return (m & ATABM) != 0; }
 // allocator to rematerialize them from the fp64 ray in every loop iteration
 constexpr int RSMM = 16;
 __host__ __device__ constexpr bool mrsm(int m) { return (m & RSMM) != 0; }
+// bit 5: vmb_march_cascade's accumulated-t walk (stacked levels / cone stepping),
+// in its own k_march instantiations so the other walks keep their register budget
+constexpr int EXTM = 32;
+__host__ __device__ constexpr bool mext(int m) { return (m & EXTM) != 0; }
 extern __shared__ double walk_dyn_smem[];
+
+constexpr int kMaxLevels = 8;  // vmb_march_ext: level 0 + up to 7 nested levels
 
 struct MarchParams {
     Contract k;
@@ -87,6 +93,22 @@ struct MarchParams {
     bool full;            // walk to the end (stats / candidate mode), ignore the T cut
     bool filter;          // apply inline density + alpha floor + T cut
     vmb_field f;
+    // Multi-level grid (NerfAcc cascades, vmb_march_cascade): levels 1..n_lv are AABB
+    // grids nested around level 0 (k / res / bits above); a point is decided by the
+    // FINEST level whose domain contains it (level 0 first: with n_lv = 0 this is
+    // OccupancyGrid::query exactly, occupancy_grid.cpp:67-76).
+    uint32_t n_lv;
+    Contract lv_k[kMaxLevels - 1];
+    uint32_t lv_res[kMaxLevels - 1];
+    const uint32_t* lv_bits[kMaxLevels - 1];
+    // accumulated-t walk (walk_growth) for cascades / cone stepping, not only growth
+    bool accum;
+    // cone stepping: dt = min(max(t cone_angle, step), max_step) at each interval's t
+    bool cone;
+    double cone_angle, max_step;
+    // the outermost level is an AABB: a midpoint outside it on an axis the ray does
+    // not come back along ends the walk (every later midpoint is outside every level)
+    bool exit_box;
 };
 
 template <typename T>
@@ -393,6 +415,29 @@ __device__ void walk_dense(const MarchParams& P, Sink& s, D3 o, D3 d, DevError* 
         if (!eval_step<MODE>(P, s, o, d, i, err, &alive)) return;
 }
 
+// Cascade query of one midpoint: 1 occupied, 0 empty / outside every level, -1
+// outside the outermost (AABB) level on an axis the ray does not come back along.
+// The computed midpoint o + d m is monotone in m per axis (both roundings are),
+// and so is the AABB contraction (x - lo) / size, so once the outermost level
+// rejects it that way it rejects every later midpoint; the inner levels are
+// nested inside it with a margin of whole cells (checked on the host).
+__device__ __forceinline__ int cascade_query(const MarchParams& P, D3 p, D3 d) {
+    int64_t c = cell_of_point(P.k, P.res, p);
+    if (c >= 0) return fine_bit(P.bits, c);
+    for (uint32_t l = 0; l < P.n_lv; ++l) {
+        c = cell_of_point(P.lv_k[l], P.lv_res[l], p);
+        if (c >= 0) return fine_bit(P.lv_bits[l], c);
+    }
+    if (P.exit_box) {
+        const Contract& k = P.n_lv ? P.lv_k[P.n_lv - 1] : P.k;
+        const D3 g = contract(k, p);
+        if ((g.x > 1.0 && d.x >= 0.0) || (g.x < 0.0 && d.x <= 0.0) || (g.y > 1.0 && d.y >= 0.0) ||
+            (g.y < 0.0 && d.y <= 0.0) || (g.z > 1.0 && d.z >= 0.0) || (g.z < 0.0 && d.z <= 0.0))
+            return -1;
+    }
+    return 0;
+}
+
 // Geometric step growth outside the unit ball (ray_marching.cpp:88-106).
 template <int MODE>
 __device__ void walk_growth(const MarchParams& P, Sink& s, D3 o, D3 d, DevError* err) {
@@ -414,6 +459,39 @@ __device__ void walk_growth(const MarchParams& P, Sink& s, D3 o, D3 d, DevError*
         const bool outside = P.ball_filter && q2 > P.ball_r2_hi   ? true
                              : P.ball_filter && q2 < P.ball_r2_lo ? false
                                                                   : sqrt(q2) > P.ball_r;
+        if (outside)
+            dt *= P.growth;
+        else
+            dt = P.step;
+    }
+}
+
+// The accumulated-t walk of vmb_march_cascade (k_march instantiations with EXTM):
+// the growth walk's arithmetic (t += dt, t1 = min(t + dt, far)) with NerfAcc's cone
+// rule dt = min(max(t cone_angle, step), max_step) at each interval's t, or the
+// growth rule (sphere level 0), over a cascade of nested levels.
+template <int MODE>
+__device__ void walk_ext(const MarchParams& P, Sink& s, D3 o, D3 d, DevError* err) {
+    double t = P.near_, dt = P.step;
+    while (t < P.far_ && s.n_cand < P.max_cand) {
+        if (P.cone) dt = fmin(fmax(t * P.cone_angle, P.step), P.max_step);
+        double t1 = min_ref(t + dt, P.far_);
+        if (!(t1 > t)) break;
+        D3 mid = o + d * (0.5 * (t + t1));
+        if (!finite3(mid)) {
+            atomicMin(&err->key, march_err_key(s.ray, 0, ERR_NONFINITE_COORD));
+            return;
+        }
+        const int q = cascade_query(P, mid, d);
+        if (q < 0) return;
+        if (q && !on_candidate<MODE>(P, s, s.n_cand, t, t1, mid, err)) return;
+        t += dt;
+        if (!P.grows) continue;
+        const D3 b = mid - P.ball_c;
+        const double b2 = dot(b, b);
+        const bool outside = P.ball_filter && b2 > P.ball_r2_hi   ? true
+                             : P.ball_filter && b2 < P.ball_r2_lo ? false
+                                                                  : sqrt(b2) > P.ball_r;
         if (outside)
             dt *= P.growth;
         else
@@ -602,6 +680,10 @@ __device__ __forceinline__ void walk(const MarchParams& P, Sink& s, const RT* __
     {
         const D3 o = load3(orig, r), d = load3(dirs, r);
         safe = ray_safe(P, o, d);
+        if (mext(MODE)) {
+            walk_ext<MODE>(P, s, o, d, err);
+            return;
+        }
         if (P.grows) {
             walk_growth<MODE>(P, s, o, d, err);
             return;
@@ -1242,7 +1324,11 @@ template <int MODE>
 void launch_march(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, uint32_t* counts,
                   const uint32_t* offsets, vmb_samples* out, unsigned long long* emitted) {
     if (ensure_skip_structures(ctx, P)) return;
-    if (P.f.kind == VMB_FIELD_VOXEL)
+    if (P.accum && P.f.kind == VMB_FIELD_VOXEL)
+        launch_march_rt<MODE | VOXM | EXTM>(ctx, P, rays, counts, offsets, out, emitted);
+    else if (P.accum)
+        launch_march_rt<MODE | EXTM>(ctx, P, rays, counts, offsets, out, emitted);
+    else if (P.f.kind == VMB_FIELD_VOXEL)
         launch_march_rt<MODE | VOXM>(ctx, P, rays, counts, offsets, out, emitted);
     else
         launch_march_rt<MODE>(ctx, P, rays, counts, offsets, out, emitted);
@@ -1285,13 +1371,71 @@ void set_sphere_fast(MarchParams* P) {
     P->atab_n = P->sphere_fast && atab && P->n_steps <= 1024 ? uint32_t(P->n_steps) : 0u;
 }
 
+
+// vmb_march_ext -> MarchParams: stacked levels and the cone rule (vmb_march_cascade).
+int apply_ext(const vmb_grid* g, const vmb_march_ext* x, const vmb_march_config* cfg, MarchParams* P) {
+    if (!x) return VMB_OK;
+    if (x->n_levels > uint32_t(kMaxLevels - 1))
+        return fail(VMB_INVALID_ARGUMENT, "cascade: at most 7 levels above level 0");
+    if (x->n_levels && !x->levels) return fail(VMB_INVALID_ARGUMENT, "cascade: levels required");
+    if (x->cone) {
+        if (!(x->cone_angle >= 0.0) || !std::isfinite(x->cone_angle))
+            return fail(VMB_INVALID_ARGUMENT, "cascade: cone_angle must be finite and >= 0");
+        if (!(x->max_step >= cfg->step_size))
+            return fail(VMB_INVALID_ARGUMENT, "cascade: max_step must be >= step_size");
+        if (P->grows)
+            return fail(VMB_INVALID_ARGUMENT, "cascade: cone stepping and unbounded_step_growth > 1 are exclusive");
+    }
+    const vmb_grid* prev = g;
+    for (uint32_t l = 0; l < x->n_levels; ++l) {
+        const vmb_grid* L = x->levels[l];
+        if (!L) return fail(VMB_INVALID_ARGUMENT, "cascade: levels required");
+        if (prev->con.kind != VMB_CONTRACT_AABB || L->con.kind != VMB_CONTRACT_AABB)
+            return fail(VMB_INVALID_ARGUMENT, "cascade: stacked levels must be AABB grids");
+        // strictly nested with a margin far above the contraction's rounding
+        for (int a = 0; a < 3; ++a) {
+            const double m = 1e-9 * (1.0 + fmax(fmax(fabs(L->con.box_min[a]), fabs(L->con.box_max[a])),
+                                                fmax(fabs(prev->con.box_min[a]), fabs(prev->con.box_max[a]))));
+            if (!(L->con.box_min[a] < prev->con.box_min[a] - m && L->con.box_max[a] > prev->con.box_max[a] + m))
+                return fail(VMB_INVALID_ARGUMENT, "cascade: each level must strictly contain the level below");
+        }
+        P->lv_k[l] = L->k;
+        P->lv_res[l] = L->res;
+        P->lv_bits[l] = L->bits;
+        prev = L;
+    }
+    P->n_lv = x->n_levels;
+    P->cone = x->cone != 0;
+    P->cone_angle = x->cone_angle;
+    P->max_step = x->max_step;
+    P->accum = P->n_lv > 0 || P->cone || P->grows;
+    P->exit_box = P->accum && prev->con.kind == VMB_CONTRACT_AABB;
+    if (P->accum) P->skip = P->fast = false;
+    return VMB_OK;
+}
+
+// Points -> occupancy under the cascade rule (the finest level containing each).
+__global__ void k_cascade_query(MarchParams P, const double* __restrict__ pts, uint64_t n,
+                                uint8_t* __restrict__ out, DevError* err) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        D3 p = d3(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+        if (!finite3(p)) {
+            atomicMin(&err->key, (unsigned long long)i);
+            out[i] = 0;
+            continue;
+        }
+        out[i] = uint8_t(cascade_query(P, p, d3(0.0, 0.0, 0.0)) > 0);
+    }
+}
+
 // VMB_MARCH_IMPL=twopass forces the count -> scan -> fill pipeline (A/B tests).
 bool use_fused(const MarchParams& P) {
     static int forced = [] {
         const char* v = getenv("VMB_MARCH_IMPL");
         return v && std::string(v) == "twopass" ? 1 : 0;
     }();
-    return !P.grows && !forced;
+    return !P.grows && !P.accum && !forced;
 }
 
 // Optional analytic-field shading fused into the packing (vmb_march_field_shaded).
@@ -1663,6 +1807,83 @@ int vmb_march_render_field_async(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays
     sr.opacity = d_opacity;
     sr.depth = d_depth;
     return launch_fused(ctx, P, rays, out, reinterpret_cast<unsigned long long*>(d_n), nullptr, sr);
+}
+
+int vmb_cascade_level_box(const vmb_contraction* base, uint32_t level, vmb_contraction* out) {
+    if (!base || !out || base->kind != VMB_CONTRACT_AABB)
+        return fail(VMB_INVALID_ARGUMENT, "cascade: level 0 must be an AABB contraction");
+    if (level >= uint32_t(kMaxLevels)) return fail(VMB_INVALID_ARGUMENT, "cascade: at most 7 levels above level 0");
+    *out = *base;
+    const double s = ldexp(1.0, int(level));
+    for (int a = 0; a < 3; ++a) {
+        const double c = 0.5 * (base->box_min[a] + base->box_max[a]);
+        const double h = 0.5 * (base->box_max[a] - base->box_min[a]);
+        out->box_min[a] = c - h * s;
+        out->box_max[a] = c + h * s;
+    }
+    return VMB_OK;
+}
+
+int vmb_cascade_query(vmb_ctx* ctx, const vmb_grid* g, const vmb_march_ext* ext, const double* d_points,
+                      uint64_t n, uint8_t* d_out) {
+    MarchParams P{};
+    P.k = g->k;
+    P.res = g->res;
+    P.bits = g->bits;
+    vmb_march_config cfg{1.0, 1e-4, 1e-2, 1, 0, 1.0};
+    if (int rc = apply_ext(g, ext, &cfg, &P)) return rc;
+    P.exit_box = false;
+    if (!n) return VMB_OK;
+    int rc = reset_error(ctx);
+    if (rc) return rc;
+    k_cascade_query<<<grid_blocks(ctx, n, 256), 256, 0, ctx->stream>>>(P, d_points, n, d_out, ctx->d_err);
+    DevError err;
+    rc = read_error(ctx, &err);
+    if (rc) return rc;
+    if (err.key != ~0ull) return fail(VMB_INVALID_ARGUMENT, "non-finite coordinate");
+    return VMB_OK;
+}
+
+int vmb_march_cascade(vmb_ctx* ctx, const vmb_grid* g, const vmb_march_ext* ext, const vmb_rays* rays,
+                      const vmb_field* f, const vmb_march_config* cfg, vmb_samples* out, uint64_t* h_n,
+                      vmb_march_stats* stats) {
+    MarchParams P;
+    int rc = march_params(g, rays, cfg, &P);
+    if (rc) return rc;
+    if ((rc = apply_ext(g, ext, cfg, &P))) return rc;
+    if (int frc = check_field(f)) return frc;
+    P.f = *f;
+    P.filter = true;
+    P.full = stats != nullptr;
+    set_sphere_fast(&P);
+    return march_packed(ctx, P, rays, out, h_n, stats);
+}
+
+int vmb_march_render_cascade(vmb_ctx* ctx, const vmb_grid* g, const vmb_march_ext* ext, const vmb_rays* rays,
+                             const vmb_field* f, const vmb_march_config* cfg, vmb_samples* out, void* d_rgbs,
+                             void* d_sigmas, void* d_color, void* d_opacity, void* d_depth, int dtype, double time,
+                             uint64_t* h_n, vmb_march_stats* stats) {
+    MarchParams P;
+    int rc = march_params(g, rays, cfg, &P);
+    if (rc) return rc;
+    if ((rc = apply_ext(g, ext, cfg, &P))) return rc;
+    if (int frc = check_field(f)) return frc;
+    P.f = *f;
+    P.filter = true;
+    P.full = stats != nullptr;
+    set_sphere_fast(&P);
+    ShadeReq sr;
+    sr.on = true;
+    sr.f = *f;
+    sr.time = time;
+    sr.rgb = d_rgbs;
+    sr.sig = d_sigmas;
+    sr.dtype = dtype;
+    sr.fwd = true;
+    sr.color = d_color;
+    sr.opacity = d_opacity;
+    sr.depth = d_depth;
+    return march_packed(ctx, P, rays, out, h_n, stats, sr);
 }
 
 int vmb_march_check(vmb_ctx* ctx) {  // reports the recorded error once, then clears the record

@@ -189,3 +189,66 @@ def test_config3_standin_full_size_matches_reference(dev, orc):
     ref = reference_step(orc, og, field, o32.astype(np.float64), d32.astype(np.float64), 0.01, 100.0, cfg,
                          [x.astype(np.float64) for x in ups32])
     _compare(got, *ref)
+
+
+def test_config3_cascade_full_size_matches_port(dev):
+    """bench.py --workload config3 at full size (2^20 rays, 4 cascaded 128^3 levels,
+    cone 1/256): the device's whole batch, checked on every 16th ray against the
+    port's sequential cascade march (oracle/vm_oracle.c vmo_march_cascade; the
+    reference has no cascade), bit-exact, plus shading and the
+    forward/backward of those rays against the port's render functions."""
+    import math
+    from paper_2210_04847_b200._lib import MarchStats
+    port = Oracle("port")
+    field = Field.sphere(radius=0.3, sigma=40.0)
+    cfg = MarchConfig(math.sqrt(3.0) / 1024, 1e-4, 1e-2, 4096, 1.0)
+    cas = api.Cascade(128, Contraction.aabb((0, 0, 0), (1, 1, 1)), 4, dev=dev)
+    pg = []
+    for level in range(4):
+        con = Contraction()
+        import ctypes as C
+        dev.lib.vmb_cascade_level_box(C.byref(Contraction.aabb((0, 0, 0), (1, 1, 1))), level, C.byref(con))
+        pg.append(port.grid(128, O.Contraction.aabb(tuple(con.box_min), tuple(con.box_max))))
+    for s in workload.grid_warmup_seeds(16, 5):
+        cas.update_field(field, 0.95, s)
+        for g in pg:
+            g.update_field(ofield(field), 0.95, s)
+    for g, q in zip(cas.grids, pg):
+        assert np.array_equal(g.bits(), q.bits())
+    o, d = workload.orbit_rays(1024, near=0.01, far=100.0)
+    N = len(o)
+    o32, d32 = o.astype(np.float32), d.astype(np.float32)
+    do_, dd_ = dev.upload(o32), dev.upload(d32)
+    rays = Rays(do_.ptr, dd_.ptr, VMB_F32, 0, N, 0.01, 100.0)
+    st = MarchStats()
+    p = api.march_cascade_device(dev, cas, rays, field, cfg, api.DevicePacked.allocate(dev, N, 64 * N), 1 / 256,
+                                 1e10, st)
+    cap = p.capacity
+    rgb, sig = dev.empty(3 * cap, np.float32), dev.empty(cap, np.float32)
+    outs = [dev.empty(3 * N, np.float32), dev.empty(N, np.float32), dev.empty(N, np.float32)]
+    api.march_render_cascade_device(dev, cas, rays, field, cfg, p, rgb, sig, *outs, cone_angle=1 / 256)
+    ups32 = [x.astype(np.float32) for x in workload.upstream_grads(N, 31)]
+    ups = [dev.upload(x) for x in ups32]
+    gr, gs = dev.empty(3 * cap, np.float32), dev.empty(cap, np.float32)
+    api.render_backward_device(dev, p, rgb, sig, *ups, gr, gs)
+    h = p.to_host()
+    S = h.n_samples
+    sel = np.arange(0, N, 16)
+    ref = port.march_cascade(o32[sel].astype(np.float64), d32[sel].astype(np.float64), 0.01, 100.0, pg[0], pg[1:],
+                             ofield(field), O.MarchConfig(cfg.step_size, 1e-4, 1e-2, 4096, 1.0), 1 / 256, 1e10)
+    assert np.array_equal(h.counts[sel], ref.counts)
+    idx = np.concatenate([np.arange(h.offsets[r], h.offsets[r] + h.counts[r]) for r in sel])
+    assert np.array_equal(h.t_starts[idx], ref.t_starts) and np.array_equal(h.t_ends[idx], ref.t_ends)
+    assert np.array_equal(h.ray_indices[idx], sel[ref.ray_indices])
+    prgb, psig = port.shade(o32[sel].astype(np.float64), d32[sel].astype(np.float64), ref, ofield(field))
+    r32 = prgb.astype(np.float32).astype(np.float64)
+    s32 = psig.astype(np.float32).astype(np.float64)
+    assert np.array_equal(rgb.numpy(3 * S).reshape(-1, 3)[idx].astype(np.float64), r32)
+    assert np.array_equal(sig.numpy(S)[idx].astype(np.float64), s32)
+    fwd = port.render_forward(ref, r32, s32)
+    for a, b, what in zip(outs, fwd, ("color", "opacity", "depth")):
+        got = a.numpy().reshape(N, -1)[sel].reshape(np.shape(b))
+        close(got, b, what)
+    bwd = port.render_backward(ref, r32, s32, *[u[sel].astype(np.float64) for u in ups32])
+    close(gr.numpy(3 * S).reshape(-1, 3)[idx], bwd[0], "d_rgb")
+    close(gs.numpy(S)[idx], bwd[1], "d_sigma")
