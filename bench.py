@@ -63,8 +63,11 @@ def parse():
     ap.add_argument("--config3", type=int, default=1,
                     help="N=1: also time BASELINE config 3 (4-level cascaded grid, cone stepping, 2^20 rays) "
                          "in a sub-run and report it under `config3`")
-    ap.add_argument("--workload", default="config5", choices=["config5", "config3"],
-                    help="config3: the multi-level grid + cone-step workload alone (one JSON line)")
+    ap.add_argument("--workload", default="config5", choices=["config5", "config3", "config1"],
+                    help="config3: the multi-level grid + cone-step workload alone; config1: the 4096-ray "
+                         "batch as a CUDA graph (one JSON line each)")
+    ap.add_argument("--config1", type=int, default=1,
+                    help="N=1: also time BASELINE config 1 (4096 rays, CUDA graph) in a sub-run -> `config1`")
     ap.add_argument("--cpu-sample-rays", type=int, default=1 << 20)
     ap.add_argument("--ref-sample-rays", type=int, default=1 << 18)
     ap.add_argument("--phases", type=int, default=1, help="per-phase event timing pass")
@@ -424,6 +427,98 @@ def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev
 
 
 
+# ---------------------------------------------------------------------- config 1
+def run_config1(args):
+    """BASELINE config 1: the reference CLI's bench batch, 4096 orbit-camera rays
+    (W=64), 128^3 grid, step 5e-3 — launch-bound. The step (async march + shading +
+    forward, then backward: ~10 kernel/memset nodes) is captured once as a CUDA
+    graph (vmb_graph_begin/end) and replayed; the same step launched call by call
+    is timed beside it."""
+    from paper_2210_04847_b200 import api, workload
+    from paper_2210_04847_b200._lib import VMB_F32, Contraction, Field, MarchConfig, Rays, check
+    dev = api.Device(0)
+    L = dev.lib
+    field = Field.sphere(**SCENE)
+    cfg = MarchConfig(5e-3, 1e-4, 1e-2)
+    R, W = 128, 64
+    grid = api.OccupancyGrid(R, Contraction.aabb(), dev=dev)
+    for s in workload.grid_warmup_seeds(16, 5):
+        grid.update_field(field, 0.95, s)
+    o64, d64 = workload.orbit_rays(W)
+    N = len(o64)
+    o32, d32 = o64.astype(np.float32), d64.astype(np.float32)
+    dc, do, dd = (x.astype(np.float32) for x in workload.upstream_grads(N, 113))
+    do_, dd_ = dev.upload(o32), dev.upload(d32)
+    rays = Rays(do_.ptr, dd_.ptr, VMB_F32, 0, N, 0.2, 1.0)
+    packed = api.march_device(dev, grid, rays, field, cfg, api.DevicePacked.allocate(dev, N, 16 * N))
+    S = packed.n_samples
+    cap = packed.capacity
+    rgb, sig = dev.empty(3 * cap, np.float32), dev.empty(cap, np.float32)
+    gr, gs = dev.empty(3 * cap, np.float32), dev.empty(cap, np.float32)
+    outs = [dev.empty(3 * N, np.float32), dev.empty(N, np.float32), dev.empty(N, np.float32)]
+    ups = [dev.upload(x) for x in (dc, do, dd)]
+    n_dev = dev.zeros(1, np.uint64)
+    smp = packed.samples_struct()
+    packed.n_samples = cap  # the backward reads the exact ranges from offsets/counts
+
+    def step():
+        check(L.vmb_march_render_field_async(dev.h, grid.h, C.byref(rays), C.byref(field), C.byref(cfg),
+                                             C.byref(smp), rgb.ptr, sig.ptr, outs[0].ptr, outs[1].ptr, outs[2].ptr,
+                                             VMB_F32, 0.0, n_dev.ptr))
+        api.render_backward_device(dev, packed, rgb, sig, *ups, gr, gs)
+
+    def timed(fn, k):
+        dev.sync()
+        dev.record(0)
+        for _ in range(k):
+            fn()
+        dev.record(1)
+        dev.sync()
+        return dev.elapsed_ms(0, 1) / k
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    dev.sync()
+    check(L.vmb_march_check(dev.h))
+    assert int(n_dev.numpy()[0]) == S
+    graph = C.c_void_p()
+    check(L.vmb_graph_begin(dev.h))
+    step()
+    check(L.vmb_graph_end(dev.h, C.byref(graph)))
+    launch = lambda: check(L.vmb_graph_launch(dev.h, graph))  # noqa: E731
+    steps = max(args.steps, 200)
+    clocks = Clocks(0)
+    for _ in range(max(args.warmup, 3)):
+        launch()
+    ms_graph = timed(launch, steps)
+    ms_calls = timed(step, steps)
+    t_end = time.time() + 1.0
+    while time.time() < t_end:
+        for _ in range(50):
+            launch()
+        dev.sync()
+    clk = clocks.stop()
+    check(L.vmb_march_check(dev.h))
+    assert int(n_dev.numpy()[0]) == S
+    check(L.vmb_graph_destroy(graph))
+    pk = peaks()
+    peak = pk.get("hbm_gbs", 6650.0)
+    step_bytes = 80 * N + 84 * S + R ** 3 / 8
+    line = {"metric": BASELINE_METRIC, "value": N / (ms_graph * 1e-3), "unit": "rays/s", "n_gpus": 1,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": ms_graph, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "samples_per_s": S / (ms_graph * 1e-3), "samples": S,
+            "calls_ms_per_step": ms_calls, "graph": "one CUDA graph per step (vmb_graph_begin/end/launch)",
+            "config": {"workload": f"config 1: {N} orbit-camera rays (W={W}), {R}^3 grid, SolidSphere r=0.2 "
+                                   "sigma=200, step 5e-3 (launch-bound)",
+                       "l2": "working set ~1 MB (L2-resident; the batch is launch-bound, not HBM-bound)"},
+            "roofline": {"bound": "hbm", "kernel": "step", "algorithmic_bytes": step_bytes,
+                         "achieved": step_bytes / (ms_graph * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": step_bytes / (ms_graph * 1e-3) / 1e9 / peak, "traffic": None},
+            "clocks": clk}
+    print(json.dumps(line), flush=True)
+
+
 # ---------------------------------------------------------------------- config 3
 def run_config3(args):
     """BASELINE config 3 (Mip-NeRF-360-shaped, unbounded): a 4-level cascaded
@@ -544,6 +639,8 @@ def main():
         return run_reference(args)
     if args.workload == "config3":
         return run_config3(args)
+    if args.workload == "config1":
+        return run_config1(args)
     from paper_2210_04847_b200 import api, workload
     from paper_2210_04847_b200._lib import VMB_F32, Contraction, Field, MarchConfig, Rays, check
 
@@ -774,6 +871,18 @@ def main():
         except Exception as ex:  # pragma: no cover
             cfg2 = {"error": repr(ex)}
 
+    cfg1 = None
+    if dist.rank == 0 and dist.world == 1 and args.config1 and args.width == 2048:
+        try:  # BASELINE config 1 (4096 rays, launch-bound): CUDA graph, its own process
+            out = subprocess.run([sys.executable, os.path.abspath(__file__), "--workload", "config1", "--steps",
+                                  "200", "--warmup", str(args.warmup)], capture_output=True, text=True, timeout=600)
+            c1 = json.loads(out.stdout.strip().splitlines()[-1])
+            cfg1 = {k: c1[k] for k in ("value", "unit", "ms_per_step", "calls_ms_per_step", "samples_per_s",
+                                       "samples", "clocks")}
+            cfg1["workload"] = c1["config"]["workload"]
+        except Exception as ex:  # pragma: no cover
+            cfg1 = {"error": repr(ex)}
+
     cfg3 = None
     if dist.rank == 0 and dist.world == 1 and args.config3 and args.width == 2048:
         try:  # BASELINE config 3 (cascaded grid + cone stepping), its own process
@@ -817,7 +926,7 @@ def main():
                 "pipeline": pipe_info,
                 "phases_ms": phase, "grid_update_ms": grid_update_ms,
                 "roofline": roof, "e2e": e2e, "e2e_camera": e2e_cam, "cpu_baseline": cpu, "clocks": clk,
-                "config2": cfg2, "config3": cfg3,
+                "config1": cfg1, "config2": cfg2, "config3": cfg3,
                 "gpu_launches": (KERNELS_PER_STEP - {"none": 0, "shade": 1, "forward": 2}[args.fusion])
                 * args.steps * (pipe.K if pipe else 1)}
         print(json.dumps(line), flush=True)

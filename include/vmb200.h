@@ -95,6 +95,14 @@ int vmb_event_elapsed_ms(vmb_ctx* ctx, int slot_begin, int slot_end, float* h_ms
  * on's event `slot`). Lets several contexts on one device pipeline host<->device
  * copies against compute, each context being one CUDA stream. */
 int vmb_ctx_wait(vmb_ctx* waiter, vmb_ctx* on, int slot);
+/* CUDA graph capture of the context's stream: the calls between begin and end
+ * must be asynchronous (the *_async march entry points, render_*, memcpy_*_async)
+ * and their scratch already grown by one uncaptured call; end instantiates the
+ * graph (an opaque handle), launch replays it on the stream. */
+int vmb_graph_begin(vmb_ctx* ctx);
+int vmb_graph_end(vmb_ctx* ctx, void** h_graph);
+int vmb_graph_launch(vmb_ctx* ctx, void* graph);
+int vmb_graph_destroy(void* graph);
 /* Host-only helper (no device work): the contiguous shard of n units owned by
  * rank — the static split of parallel_for (parallel.hpp:28-35). */
 int vmb_shard_range(uint64_t n, int nranks, int rank, uint64_t* h_begin, uint64_t* h_end);

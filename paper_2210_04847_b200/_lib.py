@@ -162,6 +162,10 @@ SIGNATURES = {
     "vmb_memset": (I32, [VP, VP, I32, U64]),
     "vmb_event_record": (I32, [VP, I32]),
     "vmb_ctx_wait": (I32, [VP, VP, I32]),
+    "vmb_graph_begin": (I32, [VP]),
+    "vmb_graph_end": (I32, [VP, P(VP)]),
+    "vmb_graph_launch": (I32, [VP, VP]),
+    "vmb_graph_destroy": (I32, [VP]),
     "vmb_event_elapsed_ms": (I32, [VP, I32, I32, P(C.c_float)]),
     "vmb_shard_range": (I32, [U64, I32, I32, P(U64), P(U64)]),
     "vmb_rays_validate": (I32, [VP, P(Rays)]),

@@ -343,6 +343,35 @@ int vmb_ctx_wait(vmb_ctx* waiter, vmb_ctx* on, int slot) {
     return VMB_OK;
 }
 
+// CUDA graphs of a context's stream: everything enqueued between begin and end
+// (kernels, memsets, copies of the async entry points) becomes one graph that
+// replays with a single launch — the launch-bound small batches (config 1).
+int vmb_graph_begin(vmb_ctx* ctx) {
+    VMB_CUDA_TRY(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    return VMB_OK;
+}
+
+int vmb_graph_end(vmb_ctx* ctx, void** h_graph) {
+    cudaGraph_t g = nullptr;
+    VMB_CUDA_TRY(cudaStreamEndCapture(ctx->stream, &g), "cudaStreamEndCapture");
+    cudaGraphExec_t x = nullptr;
+    cudaError_t e = cudaGraphInstantiate(&x, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    *h_graph = x;
+    return VMB_OK;
+}
+
+int vmb_graph_launch(vmb_ctx* ctx, void* graph) {
+    VMB_CUDA_TRY(cudaGraphLaunch(static_cast<cudaGraphExec_t>(graph), ctx->stream), "cudaGraphLaunch");
+    return VMB_OK;
+}
+
+int vmb_graph_destroy(void* graph) {
+    if (graph) VMB_CUDA_TRY(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph)), "cudaGraphExecDestroy");
+    return VMB_OK;
+}
+
 int vmb_event_elapsed_ms(vmb_ctx* ctx, int a, int b, float* ms) {
     if (a < 0 || a >= 32 || b < 0 || b >= 32) return fail(VMB_INVALID_ARGUMENT, "event slot out of range");
     VMB_CUDA_TRY(cudaEventSynchronize(ctx->events[b]), "cudaEventSynchronize");
