@@ -68,6 +68,12 @@ def parse():
                          "batch as a CUDA graph (one JSON line each)")
     ap.add_argument("--config1", type=int, default=1,
                     help="N=1: also time BASELINE config 1 (4096 rays, CUDA graph) in a sub-run -> `config1`")
+    ap.add_argument("--field", default="sphere", choices=["sphere", "checker", "voxel"],
+                    help="density field of the config 5 step: the SolidSphere scene (default), a Checker "
+                         "(per-sample colour, dense everywhere) or a 128^3 TrilinearVoxelField holding the "
+                         "sphere (stored density: trilinear + softplus/sigmoid per sample)")
+    ap.add_argument("--fields", type=int, default=1,
+                    help="N=1, sphere: also time the checker and voxel fields in sub-runs -> `fields`")
     ap.add_argument("--cpu-sample-rays", type=int, default=1 << 20)
     ap.add_argument("--ref-sample-rays", type=int, default=1 << 18)
     ap.add_argument("--phases", type=int, default=1, help="per-phase event timing pass")
@@ -632,6 +638,25 @@ def run_config3(args):
     print(json.dumps(line), flush=True)
 
 
+def make_field(kind, api, dev):
+    """(field descriptor, keep-alive, label) of the config 5 step's density field."""
+    from paper_2210_04847_b200._lib import Field
+    if kind == "checker":
+        f = Field.checker(period=0.125, sigma=200.0, rgb_a=(0.8, 0.25, 0.25), rgb_b=(0.2, 0.3, 0.9))
+        return f, None, "Checker period 0.125 sigma=200 (dense everywhere, two colours)"
+    if kind == "voxel":
+        res = 128
+        vf = api.VoxelField(res, (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), dev=dev)
+        g = (np.arange(res) + 0.0) / (res - 1)
+        x, y, z = np.meshgrid(g, g, g, indexing="ij")
+        inside = ((x - 0.5) ** 2 + (y - 0.5) ** 2 + (z - 0.5) ** 2) <= 0.2 ** 2
+        dens = np.where(inside, 200.0, -30.0).transpose(2, 1, 0).ravel()  # x fastest
+        col = np.tile(np.log(np.array([0.8, 0.25, 0.25]) / (1 - np.array([0.8, 0.25, 0.25]))), (res ** 3, 1))
+        vf.set_params(dens, col)
+        return vf.field, vf, "TrilinearVoxelField 128^3 over [0,1]^3 holding the sphere (raw density 200 / -30)"
+    return Field.sphere(**SCENE), None, "SolidSphere r=0.2 sigma=200"
+
+
 # ---------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -655,7 +680,7 @@ def main():
         uid = (C.c_char * 128).from_buffer_copy(raw)
         check(L.vmb_comm_init(dev.h, uid, dist.world, dist.rank))
 
-    field = Field.sphere(**SCENE)
+    field, field_keep, field_label = make_field(args.field, api, dev)
     cfg = MarchConfig(args.step_size, 1e-4, 1e-2)
     R = args.resolution
     grid = api.OccupancyGrid(R, Contraction.aabb(), dev=dev)
@@ -871,6 +896,25 @@ def main():
         except Exception as ex:  # pragma: no cover
             cfg2 = {"error": repr(ex)}
 
+    fields = None
+    if dist.rank == 0 and dist.world == 1 and args.fields and args.field == "sphere" and args.width == 2048:
+        fields = {}
+        for kind in ("checker", "voxel"):
+            try:  # the same step with a general field: no constant-density shortcuts
+                out = subprocess.run([sys.executable, os.path.abspath(__file__), "--field", kind, "--steps",
+                                      str(args.steps), "--warmup", str(args.warmup), "--cpu-baseline", "0",
+                                      "--config1", "0", "--config2", "0", "--config3", "0", "--fields", "0"],
+                                     capture_output=True, text=True, timeout=900)
+                fl = json.loads(out.stdout.strip().splitlines()[-1])
+                fields[kind] = {k: fl[k] for k in ("value", "unit", "ms_per_step", "samples_per_s", "phases_ms",
+                                                   "clocks")}
+                fields[kind]["workload"] = fl["config"]["workload"]
+                fields[kind]["samples"] = fl["config"]["samples_per_gpu"]
+                fields[kind]["roofline_step_frac"] = fl["roofline"]["step"]["frac"]
+                fields[kind]["roofline_march_frac"] = fl["roofline"]["frac"]
+            except Exception as ex:  # pragma: no cover
+                fields[kind] = {"error": repr(ex)}
+
     cfg1 = None
     if dist.rank == 0 and dist.world == 1 and args.config1 and args.width == 2048:
         try:  # BASELINE config 1 (4096 rays, launch-bound): CUDA graph, its own process
@@ -913,10 +957,10 @@ def main():
                 "config": {"workload": (f"config 4: grid update every {args.grid_update_every} steps, "
                                         if args.grid_update_every else "config 5: ") +
                                        f"{N} orbit-camera rays/GPU (W={args.width}), "
-                                       f"{R}^3 grid (16 jittered warm-up updates), SolidSphere r=0.2 "
-                                       f"sigma=200, step {args.step_size}, alpha 1e-2, eps 1e-4",
+                                       f"{R}^3 grid (16 jittered warm-up updates), {field_label}, "
+                                       f"step {args.step_size}, alpha 1e-2, eps 1e-4",
                            "rays_per_gpu": N, "samples_per_gpu": S, "resolution": R,
-                           "fusion": args.fusion + " (analytic SolidSphere rgb/sigma shaded at sample midpoints)",
+                           "fusion": args.fusion + " (the field's rgb/sigma shaded at sample midpoints)",
                            "storage": "rays/rgb/sigma/outputs f32, t f64, compute f64",
                            "l2": "inputs larger than L2 (~1 GB working set per step)",
                            "parallelism": f"dp{dist.world} (rays sharded, grid replicated)",
@@ -926,7 +970,7 @@ def main():
                 "pipeline": pipe_info,
                 "phases_ms": phase, "grid_update_ms": grid_update_ms,
                 "roofline": roof, "e2e": e2e, "e2e_camera": e2e_cam, "cpu_baseline": cpu, "clocks": clk,
-                "config1": cfg1, "config2": cfg2, "config3": cfg3,
+                "config1": cfg1, "config2": cfg2, "config3": cfg3, "fields": fields,
                 "gpu_launches": (KERNELS_PER_STEP - {"none": 0, "shade": 1, "forward": 2}[args.fusion])
                 * args.steps * (pipe.K if pipe else 1)}
         print(json.dumps(line), flush=True)

@@ -718,6 +718,17 @@ __device__ __forceinline__ void walk(const MarchParams& P, Sink& s, const RT* __
 #define VMB_WALK_RSM 1
 #endif
 constexpr int kWalkCap = 32;  // >= the 28 kept samples of a sphere ray at config 2 (step sqrt(3)/1024)
+// A/B build switches (make variant DEFS=...): the constant-density alpha table, the
+// expansion's constant shading, and the two-pass march for every lattice
+#ifndef VMB_ATAB
+#define VMB_ATAB 1
+#endif
+#ifndef VMB_EXPAND_CONST
+#define VMB_EXPAND_CONST 1
+#endif
+#ifndef VMB_MARCH_TWOPASS
+#define VMB_MARCH_TWOPASS 0
+#endif
 #ifndef VMB_WALK_CLAIM
 #define VMB_WALK_CLAIM 1
 #endif
@@ -1366,9 +1377,8 @@ void set_sphere_fast(MarchParams* P) {
     P->sph_sig32 = double(float(f.sigma));
     for (int a = 0; a < 3; ++a) P->sph_rgb32[a] = double(float(f.rgb[a]));
     // inside the sphere sigma is one constant, so alpha depends only on the lattice
-    // step: k_march_walk tabulates it per CTA (VMB_ATAB=0 disables)
-    static const int atab = env_int("VMB_ATAB", 1);
-    P->atab_n = P->sphere_fast && atab && P->n_steps <= 1024 ? uint32_t(P->n_steps) : 0u;
+    // step: k_march_walk tabulates it per CTA (built with -DVMB_ATAB=0: off)
+    P->atab_n = P->sphere_fast && VMB_ATAB && P->n_steps <= 1024 ? uint32_t(P->n_steps) : 0u;
 }
 
 
@@ -1429,14 +1439,8 @@ __global__ void k_cascade_query(MarchParams P, const double* __restrict__ pts, u
     }
 }
 
-// VMB_MARCH_IMPL=twopass forces the count -> scan -> fill pipeline (A/B tests).
-bool use_fused(const MarchParams& P) {
-    static int forced = [] {
-        const char* v = getenv("VMB_MARCH_IMPL");
-        return v && std::string(v) == "twopass" ? 1 : 0;
-    }();
-    return !P.grows && !P.accum && !forced;
-}
+// A build with -DVMB_MARCH_TWOPASS=1 forces the count -> scan -> fill pipeline (A/B).
+bool use_fused(const MarchParams& P) { return !P.grows && !P.accum && !VMB_MARCH_TWOPASS; }
 
 // Optional analytic-field shading fused into the packing (vmb_march_field_shaded).
 struct ShadeReq {
@@ -1468,7 +1472,7 @@ int expand_per_sm() {
         cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kExpandSmem));
         int m = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, K, 32 * kExpandWarps, kExpandSmem);
-        return env_int("VMB_EXPAND_CTAS", m < 1 ? 2 : m);
+        return m < 1 ? 2 : m;
     }();
     return n;
 }
@@ -1494,7 +1498,7 @@ void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* ray
     for (int a = 0; a < 3; ++a) ident = ident && std::isfinite(f.velocity[a]);
     const bool cst = SHADE && !VOX && P.filter && P.thr >= 0.0 && ident && std::isfinite(f.sigma) &&
                      f.sigma > 0.0 && (f.kind == VMB_FIELD_SOLID_SPHERE || f.kind == VMB_FIELD_UNIFORM_BOX) &&
-                     env_int("VMB_EXPAND_CONST", 1);
+                     VMB_EXPAND_CONST;
     if (cst)
         launch(k_march_expand<RT, AT, SHADE, VOX, true>, expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, true>>());
     else
@@ -1552,8 +1556,6 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
         const size_t dyn = size_t(P.atab_n) * sizeof(double);  // read only by ATAB kernels
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, dyn);
         if (per_sm < 1) per_sm = 4;
-        static const int forced = env_int("VMB_WALK_CTAS", 0);
-        if (forced > 0) per_sm = forced;
         kernel<<<ctx->num_sms * per_sm, 128, dyn, ctx->stream>>>(
             P, o, d, n, out->d_counts, kept_idx, counters, n_chunks, emitted, ctx->d_err, fo, chunk_tot);
     };

@@ -400,139 +400,92 @@ __device__ __forceinline__ void write_out(BwdSmem<T>& sm, int lane, uint32_t cs,
     __syncwarp();
 }
 
-// Two forward sweeps for one ray range (a single ray longer than a tile, or with
-// per-lane global reads when the warp's rays are not contiguous):
-// sweep 1 computes S = sum_k w_k v_k, sweep 2 emits suffix_k = S - P_k.
-template <typename T>
-__device__ void bwd_two_sweep(BwdSmem<T>* smp, int lane, bool active, bool staged, uint32_t off,
-                              uint32_t end, uint32_t s0, uint32_t s1, const Up& u,
-                              const double* __restrict__ ts, const double* __restrict__ te,
-                              const T* __restrict__ rgb, const T* __restrict__ sig,
-                              T* __restrict__ g_rgb, T* __restrict__ g_sig) {
-    double S = 0.0, t = 1.0;
-    if (staged) {
-        for (uint32_t cs = s0; cs < s1; cs += Tile<T>::CH) {
-            const uint32_t n = min(uint32_t(Tile<T>::CH), s1 - cs);
-            BwdSmem<T>& sm = *smp;
-            stage_in<T, false>(sm, lane, cs, n, ts, te, rgb, sig);
-            if (active)
-                for (uint32_t s = max(off, cs); s < min(end, cs + n); ++s) {
-                    const uint32_t i = s - cs;
-                    const double a = sm.al[i];
-                    const double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
-                                             double(sm.rgb[3 * i + 2]), 0.5 * (sm.ts[i] + sm.te[i]));
-                    S += t * a * v;
-                    t *= 1.0 - a;
-                }
-            __syncwarp();
-        }
-    } else if (active) {
-        for (uint32_t s = off; s < end; ++s) {
-            const double a = 1.0 - exp(-double(sig[s]) * (te[s] - ts[s]));
-            const double v = u.value(double(rgb[3 * uint64_t(s)]), double(rgb[3 * uint64_t(s) + 1]),
-                                     double(rgb[3 * uint64_t(s) + 2]), 0.5 * (ts[s] + te[s]));
-            S += t * a * v;
-            t *= 1.0 - a;
-        }
-    }
-    t = 1.0;
-    double P = 0.0;
-    if (staged) {
-        for (uint32_t cs = s0; cs < s1; cs += Tile<T>::CH) {
-            const uint32_t n = min(uint32_t(Tile<T>::CH), s1 - cs);
-            BwdSmem<T>& sm = *smp;
-            stage_in<T, false>(sm, lane, cs, n, ts, te, rgb, sig);
-            if (active)
-                for (uint32_t s = max(off, cs); s < min(end, cs + n); ++s) {
-                    const uint32_t i = s - cs;
-                    const double delta = sm.te[i] - sm.ts[i];
-                    const double a = sm.al[i];
-                    const double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
-                                             double(sm.rgb[3 * i + 2]), 0.5 * (sm.ts[i] + sm.te[i]));
-                    const double wgt = t * a;
-                    P += wgt * v;
-                    sm.rgb[3 * i] = T(u.dcx * wgt);
-                    sm.rgb[3 * i + 1] = T(u.dcy * wgt);
-                    sm.rgb[3 * i + 2] = T(u.dcz * wgt);
-                    sm.sig[i] = T(delta * (t * (1.0 - a) * v - (S - P)));
-                    t *= 1.0 - a;
-                }
-            write_out(*smp, lane, cs, n, g_rgb, g_sig);
-        }
-    } else if (active) {
-        for (uint32_t s = off; s < end; ++s) {
-            const double delta = te[s] - ts[s];
-            const double a = 1.0 - exp(-double(sig[s]) * delta);
-            const double v = u.value(double(rgb[3 * uint64_t(s)]), double(rgb[3 * uint64_t(s) + 1]),
-                                     double(rgb[3 * uint64_t(s) + 2]), 0.5 * (ts[s] + te[s]));
-            const double wgt = t * a;
-            P += wgt * v;
-            g_rgb[3 * uint64_t(s)] = T(u.dcx * wgt);
-            g_rgb[3 * uint64_t(s) + 1] = T(u.dcy * wgt);
-            g_rgb[3 * uint64_t(s) + 2] = T(u.dcz * wgt);
-            g_sig[s] = T(delta * (t * (1.0 - a) * v - (S - P)));
-            t *= 1.0 - a;
-        }
-    }
-}
+// One ray [s0, s1) by the whole warp (a ray longer than a tile, or a ray of a warp
+// whose rays are not stored contiguously), rendering.cpp:85-108 with the
+// reference's directions: T by a product scan over the lanes carried forward
+// across rounds and tiles, and the suffix of w v accumulated from the ray's END —
+// a reverse sum scan carried backwards across rounds and tiles — so the tail
+// gradients never come from a difference of two large sums. A forward sweep over
+// the tiles stores the transmittance carried into each tile (kCarryTiles per
+// super-block; longer rays repeat it per super-block), then the tiles are
+// processed last to first. Per sample the same expressions as the reference, up
+// to the association order of the scans' products and sums.
+constexpr int kCarryTiles = 32;  // one per lane: lane k holds the T carried into tile sb_start + k
 
-// One ray longer than a tile, by the whole warp: the two sweeps of bwd_two_sweep
-// (S = sum_k w_k v_k, then suffix_k = S - P_k) with every lane on one sample per
-// 32-sample round — T by a product scan over the lanes (carried across rounds and
-// tiles), S and P by sum scans. Same expressions per sample as the reference
-// (rendering.cpp:85-108) up to the association order of the products/sums.
 template <typename T>
 __device__ void bwd_long_ray(BwdSmem<T>& sm, int lane, uint32_t s0, uint32_t s1, const Up& u,
                              const double* __restrict__ ts, const double* __restrict__ te,
                              const T* __restrict__ rgb, const T* __restrict__ sig,
                              T* __restrict__ g_rgb, T* __restrict__ g_sig) {
-    double S = 0.0;
-    for (int sweep = 0; sweep < 2; ++sweep) {
-        double carryT = 1.0, carryP = 0.0;
-        for (uint32_t cs = s0; cs < s1; cs += Tile<T>::CH) {
-            const uint32_t n = min(uint32_t(Tile<T>::CH), s1 - cs);
-            stage_in<T, false>(sm, lane, cs, n, ts, te, rgb, sig);
+    constexpr uint32_t CH = Tile<T>::CH;
+    const uint32_t nt = (s1 - s0 + CH - 1) / CH;
+    double carryS = 0.0;  // sum of w v over the samples after the current round
+    for (uint32_t sb_end = nt; sb_end > 0;) {
+        const uint32_t sb_start = sb_end > uint32_t(kCarryTiles) ? sb_end - kCarryTiles : 0u;
+        double carryT = 1.0, my_carry = 1.0;  // forward sweep: T carried into every tile
+        for (uint32_t t = 0; t < sb_end; ++t) {
+            if (t >= sb_start && uint32_t(lane) == t - sb_start) my_carry = carryT;
+            const uint32_t cs = s0 + t * CH, n = min(CH, s1 - cs);
+            stage_in<T, false>(sm, lane, cs, n, ts, te, static_cast<const T*>(nullptr), sig);
             for (uint32_t r0 = 0; r0 < n; r0 += 32) {
+                double x = r0 + lane < n ? 1.0 - sm.al[r0 + lane] : 1.0;
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) x *= __shfl_xor_sync(0xffffffffu, x, d);
+                carryT *= x;
+            }
+            __syncwarp();
+        }
+        __syncwarp();
+        for (uint32_t t = sb_end; t-- > sb_start;) {
+            const uint32_t cs = s0 + t * CH, n = min(CH, s1 - cs);
+            stage_in<T, false>(sm, lane, cs, n, ts, te, rgb, sig);
+            double cT = __shfl_sync(0xffffffffu, my_carry, int(t - sb_start));
+            for (uint32_t r0 = 0; r0 < n; r0 += 32) {  // T before each sample of the tile
                 const uint32_t i = r0 + uint32_t(lane);
-                const bool in = i < n;
-                const double a = in ? sm.al[i] : 0.0;
-                double x = in ? 1.0 - a : 1.0;  // inclusive product of (1 - alpha)
+                double x = i < n ? 1.0 - sm.al[i] : 1.0;  // inclusive product of (1 - alpha)
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {
                     const double y = __shfl_up_sync(0xffffffffu, x, d);
                     if (lane >= d) x *= y;
                 }
                 double tr = __shfl_up_sync(0xffffffffu, x, 1);
-                tr = (lane == 0 ? 1.0 : tr) * carryT;  // T before sample i
-                carryT *= __shfl_sync(0xffffffffu, x, 31);
-                double t0 = 0.0, t1 = 0.0, v = 0.0;
+                tr = (lane == 0 ? 1.0 : tr) * cT;
+                cT *= __shfl_sync(0xffffffffu, x, 31);
+                if (i < n) sm.tr[i] = tr;
+            }
+            __syncwarp();
+            for (uint32_t r0 = (n - 1) / 32 * 32 + 32; r0 > 0;) {  // rounds last to first
+                r0 -= 32;
+                const uint32_t i = r0 + uint32_t(lane);
+                const bool in = i < n;
+                double t0 = 0.0, t1 = 0.0, a = 0.0, tr = 0.0, v = 0.0;
                 if (in) {
-                    t0 = sm.ts[i], t1 = sm.te[i];
+                    t0 = sm.ts[i], t1 = sm.te[i], a = sm.al[i], tr = sm.tr[i];
                     v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]), double(sm.rgb[3 * i + 2]),
                                 0.5 * (t0 + t1));
                 }
                 const double wgt = tr * a;
-                double wv = wgt * v;  // inclusive sum scan of w v
+                const double x = in ? wgt * v : 0.0;
+                double incl = x;  // sum of x over this lane and the later ones
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {
-                    const double y = __shfl_up_sync(0xffffffffu, wv, d);
-                    if (lane >= d) wv += y;
+                    const double y = __shfl_down_sync(0xffffffffu, incl, d);
+                    if (lane + d < 32) incl += y;
                 }
-                const double P = carryP + wv;
-                carryP += __shfl_sync(0xffffffffu, wv, 31);
-                if (sweep == 1 && in) {
+                double later = __shfl_down_sync(0xffffffffu, incl, 1);
+                if (lane == 31) later = 0.0;
+                const double suffix = later + carryS;
+                carryS += __shfl_sync(0xffffffffu, incl, 0);
+                if (in) {
                     sm.rgb[3 * i] = T(u.dcx * wgt);
                     sm.rgb[3 * i + 1] = T(u.dcy * wgt);
                     sm.rgb[3 * i + 2] = T(u.dcz * wgt);
-                    sm.sig[i] = T((t1 - t0) * (tr * (1.0 - a) * v - (S - P)));
+                    sm.sig[i] = T((t1 - t0) * (tr * (1.0 - a) * v - suffix));
                 }
             }
-            if (sweep == 1)
-                write_out(sm, lane, cs, n, g_rgb, g_sig);
-            else
-                __syncwarp();
+            write_out(sm, lane, cs, n, g_rgb, g_sig);
         }
-        S = carryP;
+        sb_end = sb_start;
     }
 }
 
@@ -554,8 +507,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_backward_long(
         const uint64_t ns = n_samples < 0xffffffffull ? n_samples : 0xffffffffull;
         const uint64_t o = offsets[r], e = o + counts[r];
         const Up u = load_up(dc, dop, ddep, r, true);
-        bwd_long_ray(sm, lane, uint32_t(o < ns ? o : ns), uint32_t(e < ns ? e : ns), u, ts, te, rgb, sig,
-                     g_rgb, g_sig);
+        bwd_long_ray(sm, lane, uint32_t(o < ns ? o : ns), uint32_t(e < ns ? e : ns), u,
+                     ts, te, rgb, sig, g_rgb, g_sig);
     }
 }
 
@@ -565,69 +518,6 @@ __global__ void __launch_bounds__(kWarps * 32) k_backward_long(
 #ifndef VMB_BWD_MINB
 #define VMB_BWD_MINB 4
 #endif
-
-template <typename T>
-__global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward(
-    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays, uint64_t n_samples,
-    const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
-    const T* __restrict__ sig, const T* __restrict__ dc, const T* __restrict__ dop,
-    const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig) {
-    __shared__ BwdSmem<T> smem[kWarps];
-    const int lane = threadIdx.x & 31;
-    BwdSmem<T>& sm = smem[threadIdx.x >> 5];
-    const uint64_t n_warps = (n_rays + 31) / 32;
-    for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
-         w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-        const RayRange rr = ray_range(offsets, counts, n_rays, n_samples, w, lane);
-        const Up u = load_up(dc, dop, ddep, rr.r, rr.valid);
-        if (!rr.contiguous) {
-            bwd_two_sweep(&sm, lane, rr.valid, false, rr.off, rr.end, 0u, 0u, u, ts, te, rgb, sig,
-                          g_rgb, g_sig);
-            continue;
-        }
-        const unsigned vmask = __ballot_sync(0xffffffffu, rr.valid);  // valid lanes: a prefix
-        int g0 = 0;
-        while (g0 < 32 && ((vmask >> g0) & 1u)) {
-            const uint32_t base = __shfl_sync(0xffffffffu, rr.off, g0);
-            const bool fits = rr.valid && lane >= g0 && rr.end - base <= uint32_t(Tile<T>::CH);
-            const unsigned fm = __ballot_sync(0xffffffffu, fits);  // monotone: ends ascend
-            if (!((fm >> g0) & 1u)) {  // ray g0 alone exceeds a tile
-                const uint32_t e0 = __shfl_sync(0xffffffffu, rr.end, g0);
-                bwd_two_sweep(&sm, lane, lane == g0, true, rr.off, rr.end, base, e0, u, ts, te, rgb,
-                              sig, g_rgb, g_sig);
-                ++g0;
-                continue;
-            }
-            const int g1 = 31 - __clz(fm);
-            const uint32_t n = __shfl_sync(0xffffffffu, rr.end, g1) - base;
-            if (n) {
-                stage_in<T, false>(sm, lane, base, n, ts, te, rgb, sig);
-                if (lane >= g0 && lane <= g1) {
-                    double t = 1.0;
-                    for (uint32_t i = rr.off - base; i < rr.end - base; ++i) {  // rendering.cpp:89-96
-                        sm.tr[i] = t;
-                        t *= 1.0 - sm.al[i];
-                    }
-                    double suffix = 0.0;
-                    for (uint32_t i = rr.end - base; i-- > rr.off - base;) {  // rendering.cpp:99-108
-                        const double delta = sm.te[i] - sm.ts[i];
-                        const double mid = 0.5 * (sm.ts[i] + sm.te[i]);
-                        const double v = u.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
-                                                 double(sm.rgb[3 * i + 2]), mid);
-                        const double wgt = sm.tr[i] * sm.al[i];
-                        sm.rgb[3 * i] = T(u.dcx * wgt);
-                        sm.rgb[3 * i + 1] = T(u.dcy * wgt);
-                        sm.rgb[3 * i + 2] = T(u.dcz * wgt);
-                        sm.sig[i] = T(delta * (sm.tr[i] * (1.0 - sm.al[i]) * v - suffix));
-                        suffix += wgt * v;
-                    }
-                }
-                write_out(sm, lane, base, n, g_rgb, g_sig);
-            }
-            g0 = g1 + 1;
-        }
-    }
-}
 
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
@@ -647,9 +537,15 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
          w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
         const RayRange rr = ray_range(offsets, counts, n_rays, n_samples, w, lane);
         const Up u = load_up(dc, dop, ddep, rr.r, rr.valid);
-        if (!rr.contiguous) {
-            bwd_two_sweep(&sm, lane, rr.valid, false, rr.off, rr.end, 0u, 0u, u, ts, te, rgb, sig,
-                          g_rgb, g_sig);
+        if (!rr.contiguous) {  // rays not stored one after the other: each by the whole warp
+            for (int q = 0; q < 32; ++q) {
+                const uint32_t a = __shfl_sync(0xffffffffu, rr.off, q), b = __shfl_sync(0xffffffffu, rr.end, q);
+                const Up uq{__shfl_sync(0xffffffffu, u.dcx, q), __shfl_sync(0xffffffffu, u.dcy, q),
+                            __shfl_sync(0xffffffffu, u.dcz, q), __shfl_sync(0xffffffffu, u.dop, q),
+                            __shfl_sync(0xffffffffu, u.ddep, q)};
+                if (__shfl_sync(0xffffffffu, int(rr.valid), q) && a < b)
+                    bwd_long_ray(sm, lane, a, b, uq, ts, te, rgb, sig, g_rgb, g_sig);
+            }
             continue;
         }
         const unsigned vmask = __ballot_sync(0xffffffffu, rr.valid);  // valid lanes: a prefix
@@ -765,190 +661,6 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
     }
 }
 
-// ------------------------------------------------------------------ backward, sample-parallel
-// Same greedy groups of whole rays (<= kSpCap samples), but one SAMPLE per lane:
-// a group is up to kSpRounds rounds of 32 consecutive samples, loaded straight
-// into registers with coalesced loads (no shared memory, no per-lane serial
-// loops, no idle lanes on short rays). Per round:
-//   * owner ray of each sample: shuffle binary search over the 32 ray offsets;
-//     its segment [st, en] in lane units and its upstream gradients by shuffles;
-//   * alpha = 1 - exp(-sigma * delta) (rendering.cpp:91-92), T = exclusive
-//     segmented product of (1 - alpha) (Hillis-Steele over shuffles, carried
-//     across rounds) — the reference's T *= 1 - alpha up to the association
-//     order of the product;
-//   * w = T alpha, d_rgb = d_color w stored at once; T (1 - alpha) v and w v kept;
-// then rounds in reverse: suffix = exclusive segmented suffix sum of w v (carried
-// backwards across rounds), d_sigma = delta (T (1 - alpha) v - suffix)
-// (rendering.cpp:99-108). Rounding differs from the sequential reference only in
-// the association order of the products/sums (~1e-16 relative; the contract is
-// rel 1e-5). Rays longer than kSpCap and non-contiguous warps
-// use the per-lane two-sweep path.
-constexpr int kSpRounds = 4;
-constexpr int kSpCap = 32 * kSpRounds;
-
-template <typename T>
-__device__ __forceinline__ T shfl_idx(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
-
-template <typename T>
-__global__ void __launch_bounds__(kWarps * 32) k_backward_sp(
-    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays, uint64_t n_samples,
-    const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
-    const T* __restrict__ sig, const T* __restrict__ dc, const T* __restrict__ dop,
-    const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t n_warps = (n_rays + 31) / 32;
-    BwdSmem<T>* no_smem = nullptr;  // the two-sweep path below runs unstaged
-    for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
-         w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-        const RayRange rr = ray_range(offsets, counts, n_rays, n_samples, w, lane);
-        if (!rr.contiguous) {
-            const Up u = load_up(dc, dop, ddep, rr.r, rr.valid);
-            bwd_two_sweep(no_smem, lane, rr.valid, false, rr.off, rr.end, 0u, 0u, u, ts, te, rgb, sig,
-                          g_rgb, g_sig);
-            continue;
-        }
-        if (rr.s0 == rr.s1) continue;  // no samples in these 32 rays
-        // upstream gradients stay in the attribute dtype until a sample needs them
-        T ucx = T(0), ucy = T(0), ucz = T(0), uop = T(0), udp = T(0);
-        if (rr.valid) {
-            ucx = dc[3 * rr.r], ucy = dc[3 * rr.r + 1], ucz = dc[3 * rr.r + 2];
-            uop = dop[rr.r], udp = ddep[rr.r];
-        }
-        const uint32_t soff = rr.valid ? rr.off : 0xffffffffu;  // search key (invalid lanes last)
-        const uint32_t scnt = rr.end - rr.off;
-        const unsigned vmask = __ballot_sync(0xffffffffu, rr.valid);  // valid lanes: a prefix
-        int g0 = 0;
-        while (g0 < 32 && ((vmask >> g0) & 1u)) {
-            const uint32_t base = __shfl_sync(0xffffffffu, rr.off, g0);
-            const bool fits = rr.valid && lane >= g0 && rr.end - base <= uint32_t(kSpCap);
-            const unsigned fm = __ballot_sync(0xffffffffu, fits);  // monotone: ends ascend
-            if (!((fm >> g0) & 1u)) {  // ray g0 alone exceeds kSpCap samples
-                const Up u{double(shfl_idx(ucx, g0)), double(shfl_idx(ucy, g0)), double(shfl_idx(ucz, g0)),
-                           double(shfl_idx(uop, g0)), double(shfl_idx(udp, g0))};
-                const uint32_t e0 = __shfl_sync(0xffffffffu, rr.end, g0);
-                bwd_two_sweep(no_smem, lane, lane == g0, false, base, e0, 0u, 0u, u, ts, te, rgb, sig,
-                              g_rgb, g_sig);
-                ++g0;
-                continue;
-            }
-            const int g1 = 31 - __clz(fm);
-            const uint32_t n = __shfl_sync(0xffffffffu, rr.end, g1) - base;
-            g0 = g1 + 1;
-            if (!n) continue;
-            const int nr = int((n + 31) >> 5);
-            // ---- loads of every round first (all in flight together)
-            double t0[kSpRounds], t1[kSpRounds];
-            T sg[kSpRounds], cr[kSpRounds], cg[kSpRounds], cb[kSpRounds];
-#pragma unroll
-            for (int k = 0; k < kSpRounds; ++k) {
-                const uint32_t q = 32u * k + lane;
-                t0[k] = t1[k] = 0.0;
-                sg[k] = cr[k] = cg[k] = cb[k] = T(0);
-                if (k < nr && q < n) {
-                    const uint64_t p = uint64_t(base) + q;
-                    t0[k] = ts[p];
-                    t1[k] = te[p];
-                    sg[k] = sig[p];
-                    cr[k] = rgb[3 * p];
-                    cg[k] = rgb[3 * p + 1];
-                    cb[k] = rgb[3 * p + 2];
-                }
-            }
-            // ---- forward rounds: T scan, d_rgb
-            double keep_wv[kSpRounds], keep_a[kSpRounds], keep_d[kSpRounds];
-            int keep_en[kSpRounds];
-            double carryT = 1.0;
-#pragma unroll
-            for (int k = 0; k < kSpRounds; ++k) {
-                keep_wv[k] = keep_a[k] = keep_d[k] = 0.0;
-                keep_en[k] = lane;
-                if (k >= nr) continue;  // warp-uniform
-                const uint32_t q = 32u * k + lane;
-                const bool in = q < n;
-                const uint32_t p = base + q;
-                // owner = largest lane L with off_L <= p (zero-count lanes share the next
-                // lane's offset; invalid lanes have the largest key)
-                int L = 0;
-#pragma unroll
-                for (int stride = 16; stride > 0; stride >>= 1) {
-                    const uint32_t v = __shfl_sync(0xffffffffu, soff, L + stride);
-                    if (v <= p) L += stride;
-                }
-                const int o_l = int(__shfl_sync(0xffffffffu, rr.off, L) - base) - 32 * k;
-                const int c_l = int(__shfl_sync(0xffffffffu, scnt, L));
-                const int st = in ? o_l : lane;           // segment start (may be < 0: carried in)
-                const int en = in ? o_l + c_l - 1 : lane;  // segment end (may be > 31: continues)
-                const double dcx = double(shfl_idx(ucx, L)), dcy = double(shfl_idx(ucy, L));
-                const double dcz = double(shfl_idx(ucz, L)), dopv = double(shfl_idx(uop, L));
-                const double ddv = double(shfl_idx(udp, L));
-                const double delta = t1[k] - t0[k];
-                const double alpha = 1.0 - exp(-double(sg[k]) * delta);
-                const double f = 1.0 - alpha;
-                double x = f;  // inclusive segmented product
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const double y = __shfl_up_sync(0xffffffffu, x, d);
-                    if (lane - d >= st && lane >= d) x *= y;
-                }
-                double tr = __shfl_up_sync(0xffffffffu, x, 1);
-                if (!(lane >= 1 && lane - 1 >= st)) tr = 1.0;
-                if (st < 0) {
-                    tr *= carryT;
-                    x *= carryT;
-                }
-                carryT = __shfl_sync(0xffffffffu, x, 31);
-                const double wgt = tr * alpha;
-                const double v = (dcx * double(cr[k]) + dcy * double(cg[k]) + dcz * double(cb[k])) + dopv +
-                                 ddv * (0.5 * (t0[k] + t1[k]));
-                if (in) {
-                    const uint64_t pp = uint64_t(p);
-                    g_rgb[3 * pp] = T(dcx * wgt);
-                    g_rgb[3 * pp + 1] = T(dcy * wgt);
-                    g_rgb[3 * pp + 2] = T(dcz * wgt);
-                    keep_wv[k] = wgt * v;
-                    keep_a[k] = tr * (1.0 - alpha) * v;
-                    keep_d[k] = delta;
-                    keep_en[k] = en;
-                }
-            }
-            // ---- reverse rounds: suffix sums, d_sigma
-            double carryS = 0.0;
-#pragma unroll
-            for (int k = kSpRounds - 1; k >= 0; --k) {
-                if (k >= nr) continue;
-                const int en = keep_en[k];
-                double y = keep_wv[k];  // inclusive segmented suffix sum
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const double z = __shfl_down_sync(0xffffffffu, y, d);
-                    if (lane + d <= en && lane + d < 32) y += z;
-                }
-                double suf = __shfl_down_sync(0xffffffffu, y, 1);
-                if (!(lane + 1 <= en && lane < 31)) suf = 0.0;
-                if (en > 31) {
-                    suf += carryS;
-                    y += carryS;
-                }
-                carryS = __shfl_sync(0xffffffffu, y, 0);
-                const uint32_t q = 32u * k + lane;
-                if (q < n) g_sig[uint64_t(base) + q] = T(keep_d[k] * (keep_a[k] - suf));
-            }
-        }
-    }
-}
-
-// VMB_BACKWARD=sp selects the sample-parallel kernel (A/B measurements; the
-// shared-memory tile kernel measured faster on B200: 0.38 vs 0.52 ms at config 5).
-// VMB_BACKWARD=tile: the all-serial tile kernel (0.385 ms at config 5 vs 0.358 for
-// the hybrid default); VMB_BACKWARD=sp: fully sample-parallel (0.52 ms).
-int backward_impl() {
-    static int impl = [] {
-        const char* v = getenv("VMB_BACKWARD");
-        return v && v[0] == 's' ? 1 : v && v[0] == 't' ? 2 : v && v[0] == 'w' ? 3 : 0;
-    }();
-    return impl;
-}
-
 // ------------------------------------------------------------------ transmittance
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_transmittance(
@@ -1035,124 +747,23 @@ int launched(const char* where) {
     return e == cudaSuccess ? VMB_OK : cuda_fail(e, where);
 }
 
+#ifndef VMB_RENDER_CTAS
+#define VMB_RENDER_CTAS 16
+#endif
+#ifndef VMB_FWD_WIN_CTAS
+#define VMB_FWD_WIN_CTAS 6  // windowed forward CTAs per SM (r1 sweep: 6 best)
+#endif
 int render_blocks(vmb_ctx* ctx, uint64_t n_rays) {
-    static const int per_sm = env_int("VMB_RENDER_CTAS", 16);
-    return grid_blocks(ctx, (n_rays + 31) / 32 * 32, kWarps * 32, per_sm);
+    return grid_blocks(ctx, (n_rays + 31) / 32 * 32, kWarps * 32, VMB_RENDER_CTAS);
 }
 
-// The rays k_backward_hy set aside, with VMB_BACKWARD=win: one lane per ray, in the
-// reference's sequential order (bwd_two_sweep's two sweeps, rendering.cpp:85-108:
-// bit-identical to the one-lane tile path), with k_forward_win's coalesced
-// [sample][ray] windows; the second sweep writes its gradients back into the
-// window and stores them coalesced per ray.
-template <typename T>
-__global__ void __launch_bounds__(kWinWarps * 32) k_backward_win(
-    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_samples,
-    const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
-    const T* __restrict__ sig, const T* __restrict__ dc, const T* __restrict__ dop,
-    const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig,
-    const uint32_t* __restrict__ long_rays, const unsigned int* __restrict__ n_long) {
-    __shared__ WinSmem<T> smem[kWinWarps];
-    const int lane = threadIdx.x & 31;
-    constexpr int kWinW = Win<T>::W, kRq = 32 / kWinW;
-    const int half = lane / kWinW, j = lane % kWinW;
-    WinSmem<T>& sm = smem[threadIdx.x >> 5];
-    const uint64_t ns = n_samples < 0xffffffffull ? n_samples : 0xffffffffull;
-    const uint64_t n = *n_long;
-    for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w * 32 < n;
-         w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-        const uint64_t k = w * 32 + lane;
-        const bool valid = k < n;
-        const uint64_t r = valid ? long_rays[k] : 0;
-        const uint64_t o64 = valid ? __ldg(offsets + r) : 0u;
-        const uint64_t e64 = valid ? o64 + __ldg(counts + r) : 0u;
-        const uint32_t off = uint32_t(o64 < ns ? o64 : ns), end = uint32_t(e64 < ns ? e64 : ns);
-        const Up u = load_up(dc, dop, ddep, r, valid);
-        double S = 0.0;
-        for (int sweep = 0; sweep < 2; ++sweep) {
-            uint32_t pos = off;
-            double t = 1.0, P = 0.0;
-            while (__any_sync(0xffffffffu, pos < end)) {
-#pragma unroll 4
-                for (int q0 = 0; q0 < 32; q0 += kRq) {
-                    const int q = q0 + half;
-                    const uint32_t p = __shfl_sync(0xffffffffu, pos, q);
-                    const uint32_t e = __shfl_sync(0xffffffffu, end, q);
-                    if (p + uint32_t(j) < e) {
-                        const uint64_t x = uint64_t(p) + j;
-                        cp_async<8>(&sm.ts[j][q], ts + x);
-                        cp_async<8>(&sm.te[j][q], te + x);
-                        cp_async<sizeof(T)>(&sm.sig[j][q], sig + x);
-                        cp_async<sizeof(T)>(&sm.r[j][q], rgb + 3 * x);
-                        cp_async<sizeof(T)>(&sm.g[j][q], rgb + 3 * x + 1);
-                        cp_async<sizeof(T)>(&sm.b[j][q], rgb + 3 * x + 2);
-                    }
-                }
-                asm volatile("cp.async.wait_all;\n" ::: "memory");
-                __syncwarp();
-                const uint32_t m = pos < end ? min(uint32_t(kWinW), end - pos) : 0u;
-                for (uint32_t i = 0; i < m; ++i) {
-                    const double t0 = sm.ts[i][lane], t1 = sm.te[i][lane];
-                    const double a = 1.0 - exp(-double(sm.sig[i][lane]) * (t1 - t0));
-                    const double v = u.value(double(sm.r[i][lane]), double(sm.g[i][lane]),
-                                             double(sm.b[i][lane]), 0.5 * (t0 + t1));
-                    if (sweep == 0) {
-                        S += t * a * v;
-                    } else {
-                        const double delta = t1 - t0;
-                        const double wgt = t * a;
-                        P += wgt * v;
-                        sm.r[i][lane] = T(u.dcx * wgt);
-                        sm.g[i][lane] = T(u.dcy * wgt);
-                        sm.b[i][lane] = T(u.dcz * wgt);
-                        sm.sig[i][lane] = T(delta * (t * (1.0 - a) * v - (S - P)));
-                    }
-                    t *= 1.0 - a;
-                }
-                __syncwarp();
-                if (sweep == 1) {
-#pragma unroll 4
-                    for (int q0 = 0; q0 < 32; q0 += kRq) {
-                        const int q = q0 + half;
-                        const uint32_t p = __shfl_sync(0xffffffffu, pos, q);
-                        const uint32_t e = __shfl_sync(0xffffffffu, end, q);
-                        if (p + uint32_t(j) < e) {
-                            const uint64_t x = uint64_t(p) + j;
-                            g_sig[x] = sm.sig[j][q];
-                            g_rgb[3 * x] = sm.r[j][q];
-                            g_rgb[3 * x + 1] = sm.g[j][q];
-                            g_rgb[3 * x + 2] = sm.b[j][q];
-                        }
-                    }
-                    __syncwarp();
-                }
-                pos += m;
-            }
-        }
-    }
-}
-
-// render_backward: k_backward_hy, then the rays it set aside (longer than a tile)
-// by k_backward_long (VMB_BACKWARD=win: k_backward_win, the reference's order); VMB_BACKWARD=sp|tile select the alternative kernels.
+// render_backward: k_backward_hy (groups of whole rays per tile, the reference's
+// sequential recurrences), then the rays it set aside (longer than a tile) by
+// k_backward_long (one warp per ray, scans, suffix accumulated from the end).
 template <typename T>
 int launch_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, const void* sig, const void* dc,
                     const void* dop, const void* ddep, void* g_rgb, void* g_sig) {
     const int blocks = render_blocks(ctx, p->n_rays);
-    const int impl = backward_impl();
-    auto args = [&](auto kernel) {
-        kernel<<<blocks, kWarps * 32, 0, ctx->stream>>>(
-            p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
-            static_cast<const T*>(rgb), static_cast<const T*>(sig), static_cast<const T*>(dc),
-            static_cast<const T*>(dop), static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig));
-    };
-    if (impl == 1) {
-        args(k_backward_sp<T>);
-        return launched("render_backward");
-    }
-    if (impl == 2) {
-        args(k_backward<T>);
-        return launched("render_backward");
-    }
     auto* list = static_cast<uint32_t*>(scratch(ctx, SCRATCH_RENDER, 16 + 4 * p->n_rays));
     if (!list) return VMB_CUDA;
     auto* n_long = reinterpret_cast<unsigned int*>(list);
@@ -1162,14 +773,6 @@ int launch_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, con
         static_cast<const T*>(rgb), static_cast<const T*>(sig), static_cast<const T*>(dc),
         static_cast<const T*>(dop), static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig),
         list + 4, n_long);
-    if (impl == 3) {  // measured at the config 3 stand-in: 4.56 vs 3.48 ms (two DRAM sweeps)
-        static const int per_sm = env_int("VMB_BWD_WIN_CTAS", 6);
-        k_backward_win<T><<<ctx->num_sms * per_sm, kWinWarps * 32, 0, ctx->stream>>>(
-            p->d_offsets, p->d_counts, p->n_samples, p->d_t_starts, p->d_t_ends, static_cast<const T*>(rgb),
-            static_cast<const T*>(sig), static_cast<const T*>(dc), static_cast<const T*>(dop),
-            static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig), list + 4, n_long);
-        return launched("render_backward");
-    }
     k_backward_long<T><<<ctx->num_sms * 4, kWarps * 32, 0, ctx->stream>>>(
         p->d_offsets, p->d_counts, p->n_samples, p->d_t_starts, p->d_t_ends, static_cast<const T*>(rgb),
         static_cast<const T*>(sig), static_cast<const T*>(dc), static_cast<const T*>(dop),
@@ -1181,8 +784,7 @@ template <typename RT, typename T>
 void launch_shade_forward(vmb_ctx* ctx, const vmb_rays* rays, const vmb_field* f, double time,
                           const vmb_packed_view* p, void* rgb, void* sig, void* color, void* opacity,
                           void* depth) {
-    static const int per_sm = env_int("VMB_FWD_WIN_CTAS", 6);
-    const int wb = grid_blocks(ctx, (p->n_rays + 31) / 32 * 32, kWinWarps * 32, per_sm);
+    const int wb = grid_blocks(ctx, (p->n_rays + 31) / 32 * 32, kWinWarps * 32, VMB_FWD_WIN_CTAS);
     (f->kind == VMB_FIELD_VOXEL ? k_shade_forward_win<RT, T, true> : k_shade_forward_win<RT, T, false>)
         <<<wb, kWinWarps * 32, 0, ctx->stream>>>(
             static_cast<const RT*>(rays->d_origins), static_cast<const RT*>(rays->d_directions), *f, time,
@@ -1222,8 +824,7 @@ int vmb_render_forward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, 
                        void* color, void* opacity, void* depth, int dtype) {
     if (!p->n_rays) return VMB_OK;
     if (p->n_samples > uint64_t(kFwdLaneAvg) * p->n_rays) {
-        static const int per_sm = env_int("VMB_FWD_WIN_CTAS", 6);
-        const int wb = grid_blocks(ctx, (p->n_rays + 31) / 32 * 32, kWinWarps * 32, per_sm);
+        const int wb = grid_blocks(ctx, (p->n_rays + 31) / 32 * 32, kWinWarps * 32, VMB_FWD_WIN_CTAS);
         if (dtype == VMB_F32)
             k_forward_win<float><<<wb, kWinWarps * 32, 0, ctx->stream>>>(
                 p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,

@@ -12,6 +12,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 
 #include "../../include/vmb200_types.h"
 
@@ -154,6 +155,26 @@ VM_HD double vox_sigmoid(double x) {
     return e / (1.0 + e);
 }
 
+// 1/x when x is a normal power of two (exact: x / y == x * (1/y) bit for bit), else 0
+VM_HD double pow2_recip(double x) {
+#ifdef __CUDA_ARCH__
+    const unsigned long long b = __double_as_longlong(x);
+#else
+    unsigned long long b;
+    memcpy(&b, &x, 8);
+#endif
+    const unsigned long long e = (b >> 52) & 0x7ffull;
+    if ((b & 0x800fffffffffffffull) != 0 || e == 0 || e >= 2046) return 0.0;
+    const unsigned long long r = (2046ull - e) << 52;
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double(r);
+#else
+    double y;
+    memcpy(&y, &r, 8);
+    return y;
+#endif
+}
+
 // stencil_at: cell (lower corner vertex) and fractional offsets; false outside
 // the box (Aabb::contains, inclusive).
 VM_HD bool vox_stencil(const vmb_field& f, D3 p, uint32_t c[3], double fr[3]) {
@@ -162,8 +183,12 @@ VM_HD bool vox_stencil(const vmb_field& f, D3 p, uint32_t c[3], double fr[3]) {
     const uint32_t last_cell = f.vox_resolution - 2;
     const double pk[3] = {p.x, p.y, p.z};
     for (int a = 0; a < 3; ++a) {
-        // Vec3 rel = (p - min) / box.size() * double(R - 1)
-        const double rel = ((pk[a] - f.box_min[a]) / (f.box_max[a] - f.box_min[a])) * r1;
+        // Vec3 rel = (p - min) / box.size() * double(R - 1); a power-of-two size
+        // divides exactly by multiplying with its (exact) reciprocal
+        const double size = f.box_max[a] - f.box_min[a];
+        const double inv = pow2_recip(size);
+        const double q = inv != 0.0 ? (pk[a] - f.box_min[a]) * inv : (pk[a] - f.box_min[a]) / size;
+        const double rel = q * r1;
         const double fl = floor(rel);
         uint32_t ca = 0;
         if (!(fl < 0.0)) {

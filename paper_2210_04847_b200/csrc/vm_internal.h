@@ -100,11 +100,6 @@ int cuda_fail(cudaError_t e, const char* where);
 enum { SCRATCH_SCAN = 0, SCRATCH_MARCH = 1, SCRATCH_GRID = 2, SCRATCH_MISC = 3, SCRATCH_VOXGRAD = 4, SCRATCH_RENDER = 5, SCRATCH_SLOTS = 6 };
 static_assert(sizeof(vmb_ctx::scratch) / sizeof(void*) == SCRATCH_SLOTS, "one scratch buffer per slot");
 void* scratch(vmb_ctx* ctx, int slot, size_t bytes);
-// Integer tuning knob from the environment (read once per call site; dflt when unset).
-inline int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
-}
 inline int grid_blocks(vmb_ctx* ctx, uint64_t work, int threads, int per_sm = 8) {
     uint64_t b = (work + threads - 1) / threads;
     uint64_t cap = uint64_t(ctx->num_sms) * per_sm;
