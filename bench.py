@@ -74,6 +74,9 @@ def parse():
                          "sphere (stored density: trilinear + softplus/sigmoid per sample)")
     ap.add_argument("--fields", type=int, default=1,
                     help="N=1, sphere: also time the checker and voxel fields in sub-runs -> `fields`")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank marches its own 2^22-ray batch (its own camera angle); strong: the "
+                         "ranks split ONE 2^22-ray batch by vmb_shard_range (BASELINE config 5's sweep)")
     ap.add_argument("--cpu-sample-rays", type=int, default=1 << 20)
     ap.add_argument("--ref-sample-rays", type=int, default=1 << 18)
     ap.add_argument("--phases", type=int, default=1, help="per-phase event timing pass")
@@ -290,7 +293,8 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------- e2e
-def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev_out, total_rays, cam=None):
+def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev_out, total_rays, cam=None,
+                 pixel0=0):
     """The same step through the C ABI from HOST memory: every step copies its rays and
     upstream gradients host->device and reads the rendered color/opacity/depth back.
 
@@ -345,7 +349,7 @@ def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev
             check(L.vmb_memcpy_h2d(cx.h, arr.ptr, p.value + b * w * 4, n * w * 4))
         rays = Rays(bf["ins"][0].ptr, bf["ins"][1].ptr, VMB_F32, 0, n, 0.2, 1.0)
         if cam is not None:
-            check(L.vmb_generate_rays_range(cx.h, C.byref(cam), 0.2, 1.0, VMB_F32, b, n, bf["ins"][0].ptr,
+            check(L.vmb_generate_rays_range(cx.h, C.byref(cam), 0.2, 1.0, VMB_F32, pixel0 + b, n, bf["ins"][0].ptr,
                                             bf["ins"][1].ptr, C.byref(rays)))
         pk = bf["packed"]
         if args.e2e_async:  # no host round trip: the sample total stays on the device
@@ -691,11 +695,21 @@ def main():
     dev.record(11)
     grid_update_ms = dev.elapsed_ms(10, 11) / len(seeds)
 
-    angle = 2.0 * math.pi * dist.rank / max(dist.world, 1)
+    strong = args.scaling == "strong"
+    angle = 0.0 if strong else 2.0 * math.pi * dist.rank / max(dist.world, 1)
     o64, d64 = workload.orbit_rays(args.width, angle=angle)
+    shard = (0, len(o64))
+    if strong:  # this rank's contiguous slice of the one batch (parallel_for's static split)
+        b_, e_ = C.c_uint64(), C.c_uint64()
+        check(L.vmb_shard_range(len(o64), dist.world, dist.rank, C.byref(b_), C.byref(e_)))
+        shard = (b_.value, e_.value)
+        o64, d64 = o64[shard[0]:shard[1]], d64[shard[0]:shard[1]]
     N = len(o64)
     o32, d32 = o64.astype(np.float32), d64.astype(np.float32)
-    dc, do, dd = workload.upstream_grads(N, 113 + dist.rank)
+    if strong:
+        dc, do, dd = (x[shard[0]:shard[1]] for x in workload.upstream_grads(args.width ** 2, 113))
+    else:
+        dc, do, dd = workload.upstream_grads(N, 113 + dist.rank)
     do_, dd_ = dev.upload(o32), dev.upload(d32)
     rays = Rays(do_.ptr, dd_.ptr, VMB_F32, 0, N, 0.2, 1.0)
     check(L.vmb_rays_validate(dev.h, C.byref(rays)))
@@ -869,13 +883,14 @@ def main():
     except Exception as ex:  # pragma: no cover
         e2e = {"error": repr(ex)}
     try:  # the same step with the benchmark camera's rays generated on the device
-        ang = 2.0 * math.pi * dist.rank / max(dist.world, 1)
+        ang = 0.0 if strong else 2.0 * math.pi * dist.rank / max(dist.world, 1)
         rad = 0.6 * math.sqrt(3.0) / math.sqrt(3.0)  # orbit_camera's radius, as workload.orbit_rays
         eye = [0.5 + rad * math.cos(ang) * math.cos(0.4), 0.5 + rad * math.sin(ang) * math.cos(0.4),
                0.5 + rad * math.sin(0.4)]
         cam = api.look_at(eye, (0.5, 0.5, 0.5), (0, 0, 1), 1.1 * args.width, args.width, args.width)
         e2e_cam = e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32,
-                               [x.astype(np.float32) for x in (dc, do, dd)], cap, (col, op, dep), total_rays, cam)
+                               [x.astype(np.float32) for x in (dc, do, dd)], cap, (col, op, dep), total_rays, cam,
+                               shard[0])
     except Exception as ex:  # pragma: no cover
         e2e_cam = {"error": repr(ex)}
 
@@ -951,7 +966,7 @@ def main():
     if dist.rank == 0:
         line = {"metric": BASELINE_METRIC, "value": value, "unit": "rays/s", "n_gpus": dist.world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
                 "samples_per_s": total_samples / (ms_step * 1e-3),
                 "config": {"workload": (f"config 4: grid update every {args.grid_update_every} steps, "
@@ -964,6 +979,9 @@ def main():
                            "storage": "rays/rgb/sigma/outputs f32, t f64, compute f64",
                            "l2": "inputs larger than L2 (~1 GB working set per step)",
                            "parallelism": f"dp{dist.world} (rays sharded, grid replicated)",
+                           "sharding": ("one batch of " + str(args.width ** 2) + " rays split by vmb_shard_range "
+                                        f"(rank 0: rays [{shard[0]}, {shard[1]}))" if strong else
+                                        "each rank its own batch (camera angle 2 pi rank / N)"),
                            "step_schedule": (f"{pipe.K} contiguous sub-batches over {pipe.S} streams "
                                              "(vmb_march_render_field_async + vmb_render_backward each)"
                                              if pipe else "single call sequence on one stream")},

@@ -418,6 +418,9 @@ int vmb_comm_destroy(vmb_ctx* ctx);
 int vmb_comm_allreduce_max_f64(vmb_ctx* ctx, double* d_buf, uint64_t n);
 /* In-place sum all-reduce of n f64 (data-parallel parameter gradients). */
 int vmb_comm_allreduce_sum_f64(vmb_ctx* ctx, double* d_buf, uint64_t n);
+/* In-place all-gather: rank k's block is d_buf[k n, (k + 1) n); the grid update's
+ * collective (each rank probes one equal block of cells). */
+int vmb_comm_allgather_f64(vmb_ctx* ctx, double* d_buf, uint64_t n_per_rank);
 
 /* ------------------------------------------------------------------ training step helpers
  * (tools/voxmarch.cpp cmd_train, :460-498 — the reference's trainer, outside its

@@ -1,6 +1,9 @@
-// comm.cpp — the collectives of the path: ncclAllReduce(max) of the grid's probe
-// densities at each occupancy-grid update, and ncclAllReduce(sum)
-// of the voxel-field parameter gradients in data-parallel training (§8f rank 4).
+// comm.cpp — the collectives of the path: the in-place ncclAllGather of the
+// grid's probe densities at each occupancy-grid update (every rank probes one
+// equal block of cells; SURVEY §8e's all-reduce(max) of disjoint shards moves
+// twice the bytes for the same result), ncclAllReduce(max) for callers combining
+// overlapping probes, and ncclAllReduce(sum) of the voxel-field parameter
+// gradients in data-parallel training (§8f rank 4).
 //
 // NCCL is resolved at run time with dlopen("libnccl.so.2") so the library loads
 // (and the single-GPU path runs) on machines without NCCL. The all-reduce runs on
@@ -23,6 +26,7 @@ struct Nccl {
     ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                                cudaStream_t) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*destroy)(ncclComm_t) = nullptr;
     const char* (*error_string)(ncclResult_t) = nullptr;
     std::string load_error;
@@ -40,9 +44,10 @@ Nccl& nccl() {
         n.get_unique_id = reinterpret_cast<decltype(n.get_unique_id)>(dlsym(n.h, "ncclGetUniqueId"));
         n.init_rank = reinterpret_cast<decltype(n.init_rank)>(dlsym(n.h, "ncclCommInitRank"));
         n.all_reduce = reinterpret_cast<decltype(n.all_reduce)>(dlsym(n.h, "ncclAllReduce"));
+        n.all_gather = reinterpret_cast<decltype(n.all_gather)>(dlsym(n.h, "ncclAllGather"));
         n.destroy = reinterpret_cast<decltype(n.destroy)>(dlsym(n.h, "ncclCommDestroy"));
         n.error_string = reinterpret_cast<decltype(n.error_string)>(dlsym(n.h, "ncclGetErrorString"));
-        if (!n.get_unique_id || !n.init_rank || !n.all_reduce || !n.destroy)
+        if (!n.get_unique_id || !n.init_rank || !n.all_reduce || !n.all_gather || !n.destroy)
             n.load_error = "NCCL symbols missing";
     });
     return n;
@@ -105,6 +110,16 @@ int vmb_comm_allreduce_max_f64(vmb_ctx* ctx, double* buf, uint64_t count) {
     ncclResult_t r = n.all_reduce(buf, buf, count, ncclUint64, ncclMax,
                                   static_cast<ncclComm_t>(ctx->nccl_comm), ctx->stream);
     if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
+    return VMB_OK;
+}
+
+int vmb_comm_allgather_f64(vmb_ctx* ctx, double* buf, uint64_t count_per_rank) {
+    if (!ctx->nccl_comm) return VMB_OK;
+    Nccl& n = nccl();
+    // in place: rank k's block is buf[k * count, (k + 1) * count)
+    ncclResult_t r = n.all_gather(buf + uint64_t(ctx->rank) * count_per_rank, buf, count_per_rank, ncclFloat64,
+                                  static_cast<ncclComm_t>(ctx->nccl_comm), ctx->stream);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
     return VMB_OK;
 }
 

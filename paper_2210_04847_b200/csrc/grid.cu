@@ -12,6 +12,8 @@
 #include <cstring>
 #include <string>
 
+#include <algorithm>
+
 #include "vm_internal.h"
 
 namespace vmb {
@@ -110,6 +112,17 @@ __global__ void k_probe_range(GridDev g, vmb_field f, Timestamps ts, bool has_se
             v = probe_cell<VOX>(g, f, ts, cell, has_seed, seed, &bad);
         }
         probed[cell] = v;
+    }
+}
+
+// The cells [c0, c1) only, each at its own index (the block of an all-gather).
+template <bool VOX>
+__global__ void k_probe_block(GridDev g, vmb_field f, Timestamps ts, bool has_seed, uint64_t seed, uint64_t c0,
+                              uint64_t c1, double* __restrict__ probed) {
+    for (uint64_t cell = c0 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; cell < c1;
+         cell += uint64_t(gridDim.x) * blockDim.x) {
+        int bad;
+        probed[cell] = probe_cell<VOX>(g, f, ts, cell, has_seed, seed, &bad);
     }
 }
 
@@ -571,18 +584,24 @@ int vmb_grid_update_field(vmb_ctx* ctx, vmb_grid* g, const vmb_field* f, const d
         if (rc) return rc;
         if (err.key != ~0ull) return fail(VMB_RUNTIME, cell_name(g, err.key & ((1ull << 40) - 1)));
     }
-    if (ctx->nccl_comm) {  // a communicator attached (any size): sharded probe + all-reduce
-        if (!g->probed) {
-            cudaError_t e = cudaMalloc(&g->probed, g->n_cells * sizeof(double));
+    if (ctx->nccl_comm) {  // a communicator attached (any size): block probe + all-gather
+        // rank k probes cells [k B, (k + 1) B), B = ceil(n / nranks), into their own
+        // positions; the in-place all-gather gives every rank every block
+        const uint64_t B = (g->n_cells + ctx->nranks - 1) / ctx->nranks;
+        if (!g->probed || g->probed_words < B * ctx->nranks) {
+            if (g->probed) cudaFree(g->probed);
+            g->probed = nullptr;
+            cudaError_t e = cudaMalloc(&g->probed, B * ctx->nranks * sizeof(double));
             if (e != cudaSuccess) return cuda_fail(e, "probe buffer");
+            g->probed_words = B * ctx->nranks;
         }
-        uint64_t c0, c1;
-        vmb_shard_range(g->n_cells, ctx->nranks, ctx->rank, &c0, &c1);
-        (f->kind == VMB_FIELD_VOXEL ? k_probe_range<true> : k_probe_range<false>)<<<grid_blocks(ctx, g->n_cells, 256), 256, 0, ctx->stream>>>(
-            gd, *f, ts, has_seed != 0, seed, c0, c1, g->probed);
+        const uint64_t c0 = B * ctx->rank, c1 = std::min(g->n_cells, c0 + B);
+        if (c1 > c0)
+            (f->kind == VMB_FIELD_VOXEL ? k_probe_block<true> : k_probe_block<false>)<<<grid_blocks(ctx, c1 - c0, 256), 256, 0, ctx->stream>>>(
+                gd, *f, ts, has_seed != 0, seed, c0, c1, g->probed);
         rc = launch_check("grid probe");
         if (rc) return rc;
-        rc = vmb_comm_allreduce_max_f64(ctx, g->probed, g->n_cells);
+        rc = vmb_comm_allgather_f64(ctx, g->probed, B);
         if (rc) return rc;
         k_apply<<<grid_blocks(ctx, g->n_words * 32, 256), 256, 0, ctx->stream>>>(
             gd, g->probed, decay, g->cache, g->bits, g->n_words);

@@ -85,7 +85,8 @@ struct vmb_grid {
     // Bounding box of the occupied cells, cell units: {min x, y, z, max x+1, y+1, z+1};
     // min > max - 1 on some axis when no cell is occupied. Rebuilt with the distance map.
     uint32_t* bbox = nullptr;      // [6]
-    double* probed = nullptr;      // [n_cells] scratch for the sharded / callback update
+    double* probed = nullptr;      // scratch of the sharded / callback update (probed_words doubles)
+    uint64_t probed_words = 0;
 };
 
 namespace vmb {
@@ -121,6 +122,11 @@ int scan_counts(vmb_ctx* ctx, const uint32_t* counts, uint64_t n, uint32_t* offs
 // Exclusive scan of u8 flags into u32 positions (compaction), device total at d_total.
 int scan_flags(vmb_ctx* ctx, const uint8_t* flags, uint64_t n, uint32_t* pos,
                unsigned long long* d_total);
+
+// Stable LSD radix sort of (u32 key, u32 value) pairs by the low end_bit key bits
+// (sort.cu); sorted pairs end in one of the two buffers (*k_res / *v_res).
+int radix_sort_pairs(vmb_ctx* ctx, uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, uint64_t m,
+                     int end_bit, uint32_t** k_res, uint32_t** v_res);
 
 // ---------------------------------------------------------------- grid (grid.cu)
 int grid_refresh(vmb_ctx* ctx, vmb_grid* g);      // bits + coarse from cache

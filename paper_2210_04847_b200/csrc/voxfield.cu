@@ -11,13 +11,11 @@
 // bitwise reproducible (fields.hpp:76-81). Two device modes:
 //   VMB_GRAD_DETERMINISTIC — the same folds, bit for bit: every inside sample
 //     emits 8 (vertex, record) pairs, record = 8 i + k; a stable LSD radix sort
-//     by vertex (CUB) orders each vertex's records by sample; one thread per
+//     by vertex (in-tree, sort.cu) orders each vertex's records by sample; one thread per
 //     vertex segment then folds accum[v] + c_1 + c_2 + ... in that order.
 //   VMB_GRAD_ATOMIC — fp64 atomicAdd per (sample, vertex); the fold order is
 //     the hardware's, so sums differ from the reference in the last bits
 //     (relative error ~ n_contributions * 2^-53; tests use rtol 1e-12).
-#include <cub/device/device_radix_sort.cuh>
-
 #include "vm_internal.h"
 
 namespace vmb {
@@ -205,11 +203,7 @@ int vox_backward(vmb_ctx* ctx, const vmb_field& f, const Positions& pos, uint64_
     while (end_bit < 32 && (1ull << end_bit) <= n_vert) ++end_bit;  // keys < 2^end_bit except the sentinel
     // the sentinel must sort last: give it the top key within end_bit bits
     const uint32_t sent = end_bit >= 32 ? sentinel : uint32_t((1ull << end_bit) - 1);
-    size_t temp = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, temp, static_cast<uint32_t*>(nullptr),
-                                    static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
-                                    static_cast<uint32_t*>(nullptr), int64_t(m), 0, end_bit, ctx->stream);
-    const size_t bytes = m * 16 + n * 64 + temp + 256;
+    const size_t bytes = m * 16 + n * 64 + 256;
     char* base = static_cast<char*>(scratch(ctx, SCRATCH_VOXGRAD, bytes));
     if (!base) return VMB_CUDA;
     auto* k_in = reinterpret_cast<uint32_t*>(base);
@@ -218,15 +212,12 @@ int vox_backward(vmb_ctx* ctx, const vmb_field& f, const Positions& pos, uint64_
     auto* v_out = v_in + m;
     auto* sg = reinterpret_cast<double4*>(base + ((m * 16 + 31) & ~size_t(31)));
     auto* sfr = sg + n;
-    void* tmp = reinterpret_cast<char*>(sfr + n);
     k_vox_grad_records<GT><<<grid_blocks(ctx, n, 256, 8), 256, 0, ctx->stream>>>(f, pos, n, d_rgbs, d_sigmas, sg,
                                                                                  sfr, k_in, v_in, sent);
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, temp, k_in, k_out, v_in, v_out, int64_t(m), 0, end_bit,
-                                                    ctx->stream);
-    if (e != cudaSuccess) return cuda_fail(e, "voxel field backward sort");
-    k_vox_grad_fold<<<grid_blocks(ctx, m, 256, 8), 256, 0, ctx->stream>>>(k_out, v_out, m, sent, sg, sfr, acc_d,
-                                                                          acc_c);
-    e = cudaGetLastError();
+    uint32_t *ks = nullptr, *vs = nullptr;
+    if (int rc = radix_sort_pairs(ctx, k_in, v_in, k_out, v_out, m, end_bit, &ks, &vs)) return rc;
+    k_vox_grad_fold<<<grid_blocks(ctx, m, 256, 8), 256, 0, ctx->stream>>>(ks, vs, m, sent, sg, sfr, acc_d, acc_c);
+    cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? VMB_OK : cuda_fail(e, "voxel field backward");
 }
 

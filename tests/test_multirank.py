@@ -1,9 +1,10 @@
 """Multi-rank decomposition of the path, on CPU with torch.distributed (gloo,
 world size 2): exactly the host logic the multi-GPU run uses.
 
-* grid update: each rank probes its contiguous cell shard (vmb_shard_range, the
-  parallel_for split) -> all_reduce(MAX) -> EMA/binarise; the grid must be
-  bit-identical to a single-process update and to the reference;
+* grid update: each rank probes one equal block of cells (B = ceil(n / world),
+  as vmb_grid_update_field does under NCCL) -> in-place all_gather of the blocks
+  -> EMA/binarise; the grid must be bit-identical to a single-process update and
+  to the reference;
 * marching: each rank marches its contiguous ray shard; the global packing is
   the concatenation with offsets shifted by the exclusive scan of the per-rank
   sample totals (all_gather) and must equal the single-process packing.
@@ -44,12 +45,15 @@ def _worker(rank, world, port, q):
     R = 32
     g = port_o.grid(R, O.Contraction.aabb())
     seeds = workload.grid_warmup_seeds(4, 5)
+    n = R ** 3
+    B = (n + world - 1) // world
     for s in seeds:
-        b, e = C.c_uint64(), C.c_uint64()
-        assert lib.vmb_shard_range(R ** 3, world, rank, C.byref(b), C.byref(e)) == 0
-        probed = torch.from_numpy(g.probe_range(field, b.value, e.value, seed=s))
-        dist.all_reduce(probed, op=dist.ReduceOp.MAX)
-        g.apply(probed.numpy(), 0.95)
+        c0, c1 = B * rank, min(n, B * (rank + 1))
+        mine = np.zeros(B)
+        mine[:c1 - c0] = g.probe_range(field, c0, c1, seed=s)[c0:c1]
+        blocks = [torch.zeros(B, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(blocks, torch.from_numpy(mine))
+        g.apply(torch.cat(blocks).numpy()[:n], 0.95)
     bits, cache = g.bits(), g.cache()
     # ray sharding + global packing
     o, d = workload.orbit_rays(24)
