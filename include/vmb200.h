@@ -286,6 +286,19 @@ int vmb_march_render_field_async(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays
                                  const vmb_march_config* cfg, vmb_samples* out, void* d_rgbs, void* d_sigmas,
                                  void* d_color, void* d_opacity, void* d_depth, int dtype, double time,
                                  uint64_t* d_n_samples);
+/* The training step in one call: vmb_march_render_field_async's outputs plus
+ * render_backward (rendering.cpp:67-112) of them for the upstream gradients
+ * d_grad_color [n_rays][3] / d_grad_opacity / d_grad_depth -> d_grad_rgbs
+ * [capacity][3] / d_grad_sigmas, computed by the expansion from the samples it has
+ * just produced (no re-read). Gradients agree with vmb_render_backward on the same
+ * outputs within the rendering tolerance (scans reassociate the T products and
+ * suffix sums); packing, shading and the forward are identical. */
+int vmb_march_render_backward_field_async(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,
+                                          const vmb_field* f, const vmb_march_config* cfg, vmb_samples* out,
+                                          void* d_rgbs, void* d_sigmas, void* d_color, void* d_opacity,
+                                          void* d_depth, const void* d_grad_color, const void* d_grad_opacity,
+                                          const void* d_grad_depth, void* d_grad_rgbs, void* d_grad_sigmas,
+                                          int dtype, double time, uint64_t* d_n);
 int vmb_march_check(vmb_ctx* ctx);
 /* Generic host-SigmaFn path, step 1: the grid-passing candidate intervals of every
  * ray, capped at max_samples_per_ray (ray_marching.cpp:75-106). Same two-call

@@ -230,6 +230,8 @@ SIGNATURES = {
     "vmb_march_render_field_async": (I32, [VP, VP, P(Rays), P(Field), P(MarchConfig), P(Samples), VP, VP, VP, VP,
                                            VP, I32, D, VP]),
     "vmb_march_check": (I32, [VP]),
+    "vmb_march_render_backward_field_async": (I32, [VP, VP, P(Rays), P(Field), P(MarchConfig), P(Samples), VP, VP,
+                                                    VP, VP, VP, VP, VP, VP, VP, VP, I32, D, VP]),
     "vmb_march_candidates": (I32, [VP, VP, P(Rays), P(MarchConfig), P(Samples), P(U64)]),
     "vmb_march_filter": (I32, [VP, P(PackedView), VP, P(MarchConfig), P(Samples), P(U64)]),
     "vmb_march_uniform": (I32, [VP, P(Rays), P(MarchConfig), P(Samples), P(U64)]),

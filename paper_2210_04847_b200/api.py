@@ -221,6 +221,24 @@ def march_render_device(dev: Device, grid: "OccupancyGrid", rays: Rays, field: F
     return out
 
 
+def march_render_backward_device(dev: Device, grid: "OccupancyGrid", rays: Rays, field: Field,
+                                 cfg: MarchConfig, out: DevicePacked, rgbs: DeviceArray, sigmas: DeviceArray,
+                                 color: DeviceArray, opacity: DeviceArray, depth: DeviceArray, d_color, d_opacity,
+                                 d_depth, g_rgbs: DeviceArray, g_sigmas: DeviceArray, n_dev: DeviceArray,
+                                 time: float = 0.0):
+    """vmb_march_render_backward_field_async: the whole training step (march + shading
+    + render_forward + render_backward) on the context's stream; the sample total
+    stays on the device (n_dev, u64); errors are deferred to vmb_march_check. The
+    upstream gradients are device arrays (or objects with .ptr) in rgbs' dtype."""
+    smp = out.samples_struct()
+    check(dev.lib.vmb_march_render_backward_field_async(
+        dev.h, grid.h, C.byref(rays), C.byref(field), C.byref(cfg), C.byref(smp), rgbs.ptr, sigmas.ptr, color.ptr,
+        opacity.ptr, depth.ptr, d_color.ptr, d_opacity.ptr, d_depth.ptr, g_rgbs.ptr, g_sigmas.ptr, _dt(rgbs.dtype),
+        time, n_dev.ptr))
+    out.n_samples = out.capacity
+    return out
+
+
 def shade_device(dev: Device, rays: Rays, field: Field, packed: DevicePacked, rgbs: DeviceArray,
                  sigmas: DeviceArray, time: float = 0.0):
     check(dev.lib.vmb_shade_field(dev.h, C.byref(rays), C.byref(field), time,

@@ -27,6 +27,7 @@
 #include <type_traits>
 
 #include "vm_internal.h"
+#include "vm_scan.cuh"
 
 namespace vmb {
 
@@ -905,6 +906,7 @@ constexpr int kExpandWarps = VMB_EXPAND_WARPS;
 #endif
 constexpr int kExpandUnroll = VMB_EXPAND_UNROLL;  // rounds per iteration of the constant-shading path
 constexpr size_t kExpandSmem = size_t(kExpandWarps) * kWalkCap * 32 * (2 * sizeof(uint32_t) + sizeof(uint16_t));
+constexpr uint32_t kMaxAlphaTable = 1024;  // the fused backward's constant-density alpha table
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -920,18 +922,43 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 #else
 #define VMB_EXPAND_BOUNDS __launch_bounds__(32 * kExpandWarps)
 #endif
+// Fused training step (vmb_march_render_backward_field_async): the expansion also
+// runs render_backward (rendering.cpp:67-112) on the samples it has just written —
+// t0/t1 from the lattice index, rgb/sigma from the shading — so nothing is read
+// back. Per chunk (mapped: no ray above kWalkCap kept samples) two sweeps over its
+// 32-slot rounds, one sample per lane: the forward sweep carries T (segmented
+// product scan of 1 - alpha, the carry into round q kept by lane q), the reverse
+// sweep recomputes T, takes the owner ray's upstream gradients by shuffles and
+// accumulates the suffix of w v from the ray's end (segmented reverse sum scan),
+// then writes every output of the slot. alpha = 1 - exp(-sigma delta) with sigma
+// in the attribute dtype, as render_backward recomputes it from the stored sigma
+// (for a constant field: a per-CTA table over the lattice). Chunks with a longer
+// ray list their rays for k_backward_long after the fixup re-walk.
+template <typename AT>
+struct BwdOut {
+    const AT* dc;
+    const AT* dop;
+    const AT* ddep;
+    AT* g_rgb;
+    AT* g_sig;
+    uint32_t* list;         // rays of unmapped chunks (backward after the fixup)
+    unsigned int* n_list;
+    uint32_t atab_n;        // CONST: alpha table entries (lattice steps), 0 = compute
+    double sig_at;          // CONST: the field's sigma in the attribute dtype
+};
+
 // CONST (shading of a UniformBox / SolidSphere whose kept samples are all inside):
 // a kept sample has alpha > alpha_thre >= 0, so the march saw sigma > 0 at the
 // sample's midpoint, i.e. the constant interior density — and shading evaluates
 // the same field at the same point (time shift = identity), so rgb/sigma are the
 // field's constants: no ray, no position, no test.
-template <typename RT, typename AT, bool SHADE, bool VOX, bool CONST = false>
+template <typename RT, typename AT, bool SHADE, bool VOX, bool CONST = false, bool BWD = false>
 __global__ void VMB_EXPAND_BOUNDS k_march_expand(
     double near_, double far_, double step, const uint32_t* __restrict__ counts,
     const uint32_t* __restrict__ chunk_off, uint32_t* __restrict__ offsets,
     const uint32_t* __restrict__ kept_idx, uint64_t n_rays,
     double* __restrict__ ts, double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,
-    uint32_t* __restrict__ overflow, unsigned int* n_overflow, ShadeOut<RT, AT, VOX> sh) {
+    uint32_t* __restrict__ overflow, unsigned int* n_overflow, ShadeOut<RT, AT, VOX> sh, BwdOut<AT> bo) {
     constexpr bool RAYS = SHADE && !CONST;  // the per-sample shading needs the ray
     // dynamic shared memory (kExpandSmem): per warp, two kept-index row buffers and
     // the owner map of the chunk's output slots (lane | (k << 5), k = rank in the ray)
@@ -948,6 +975,17 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
     if (CONST) {
         c_rgb[0] = AT(sh.f.rgb[0]), c_rgb[1] = AT(sh.f.rgb[1]), c_rgb[2] = AT(sh.f.rgb[2]);
         c_sig = AT(sh.f.sigma);
+    }
+    // BWD && CONST: alpha per lattice step, after the per-warp buffers
+    double* atab = reinterpret_cast<double*>(expand_smem + kExpandWarps * (2 * kWalkCap * 32 + kWalkCap * 16));
+    if (BWD && CONST) {
+        for (uint32_t j = threadIdx.x; j < bo.atab_n; j += blockDim.x) {
+            const double dj = double(j);
+            const double t0 = near_ + dj * step;
+            const double t1 = min_ref(near_ + (dj + 1.0) * step, far_);
+            atab[j] = 1.0 - exp(-bo.sig_at * (t1 - t0));
+        }
+        __syncthreads();
     }
 
     // chunk-local state: count/offset of this lane's ray, its ray (RT), and the
@@ -1038,7 +1076,109 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
         cp_async_wait1();  // this chunk's rows have landed
         __syncwarp();
         const uint32_t* sk = s_idx[wib][buf];
-        if (CONST && mapped) {  // no ray needed: kExpandUnroll independent 32-slot rounds per iteration
+        if (BWD && !mapped) {  // a ray above kWalkCap: the chunk's rays go to k_backward_long
+            const unsigned lm = __ballot_sync(0xffffffffu, valid && cnt > 0u);
+            unsigned at = 0;
+            if (lane == 0) at = atomicAdd(bo.n_list, unsigned(__popc(lm)));
+            at = __shfl_sync(0xffffffffu, at, 0);
+            if ((lm >> lane) & 1u) bo.list[at + __popc(lm & ((1u << lane) - 1u))] = uint32_t(r);
+        }
+        if (BWD && mapped) {
+            // upstream gradients of this lane's ray (rendering.cpp:101-102)
+            double u_dcx = 0.0, u_dcy = 0.0, u_dcz = 0.0, u_dop = 0.0, u_ddep = 0.0;
+            if (valid) {
+                u_dcx = double(bo.dc[3 * r]), u_dcy = double(bo.dc[3 * r + 1]), u_dcz = double(bo.dc[3 * r + 2]);
+                u_dop = double(bo.dop[r]), u_ddep = double(bo.ddep[r]);
+            }
+            const uint32_t n_rounds = uint32_t(end - base + 31) / 32;  // <= 32: mapped
+            // one slot's sample: owner lane, rank, interval, alpha, rgb (rgb only when `col`)
+            auto sample = [&](uint64_t p, bool in, int* L, uint32_t* k, double* t0, double* t1, double* a,
+                              double c[3], bool col) {
+                *L = 0, *k = 0;
+                *t0 = 0.0, *t1 = 0.0, *a = 0.0;
+                c[0] = c[1] = c[2] = 0.0;
+                if (in) {
+                    const uint32_t e = mp[p - base];
+                    *L = int(e & 31u);
+                    *k = e >> 5;
+                }
+                D3 o{}, d{};
+                if (RAYS) {
+                    o = d3(double(__shfl_sync(0xffffffffu, ox, *L)), double(__shfl_sync(0xffffffffu, oy, *L)),
+                           double(__shfl_sync(0xffffffffu, oz, *L)));
+                    d = d3(double(__shfl_sync(0xffffffffu, dx, *L)), double(__shfl_sync(0xffffffffu, dy, *L)),
+                           double(__shfl_sync(0xffffffffu, dz, *L)));
+                }
+                if (!in) return;
+                const uint32_t i = sk[*k * 32 + *L];
+                const double di = double(i);
+                *t0 = near_ + di * step;
+                *t1 = min_ref(near_ + (di + 1.0) * step, far_);
+                if (CONST) {
+                    *a = i < bo.atab_n ? atab[i] : 1.0 - exp(-bo.sig_at * (*t1 - *t0));
+                    if (col) c[0] = double(c_rgb[0]), c[1] = double(c_rgb[1]), c[2] = double(c_rgb[2]);
+                } else if (!col) {  // forward sweep: shade (k_shade's expressions), keep rgb/sigma
+                    const D3 x = o + d * (0.5 * (*t0 + *t1));
+                    D3 cc;
+                    const double sg = field_rgb_sigma_t<VOX>(sh.f, time_shift(sh.f, x, sh.time), &cc);
+                    const AT sga = AT(sg);
+                    if (p < cap) {
+                        sh.rgb[3 * p] = AT(cc.x);
+                        sh.rgb[3 * p + 1] = AT(cc.y);
+                        sh.rgb[3 * p + 2] = AT(cc.z);
+                        sh.sig[p] = sga;
+                    }
+                    *a = 1.0 - exp(-double(sga) * (*t1 - *t0));
+                } else if (p < cap) {  // reverse sweep: the attributes just written
+                    c[0] = double(sh.rgb[3 * p]), c[1] = double(sh.rgb[3 * p + 1]), c[2] = double(sh.rgb[3 * p + 2]);
+                    *a = 1.0 - exp(-double(sh.sig[p]) * (*t1 - *t0));
+                }
+            };
+            double cin = 1.0, carry = 1.0;  // lane q: T carried into round q
+            for (uint32_t q = 0; q < n_rounds; ++q) {
+                if (uint32_t(lane) == q) cin = carry;
+                const uint64_t p = base + 32 * q + lane;
+                const bool in = p < end;
+                int L;
+                uint32_t k;
+                double t0, t1, a, c[3];
+                sample(p, in, &L, &k, &t0, &t1, &a, c, false);
+                seg_excl_prod(in ? 1.0 - a : 1.0, !in || k == 0, carry);
+            }
+            double carryS = 0.0;  // suffix of w v beyond the current round
+            for (uint32_t q = n_rounds; q-- > 0;) {
+                double cT = __shfl_sync(0xffffffffu, cin, int(q));
+                const uint64_t p = base + 32 * q + lane;
+                const bool in = p < end;
+                int L;
+                uint32_t k;
+                double t0, t1, a, c[3];
+                sample(p, in, &L, &k, &t0, &t1, &a, c, true);
+                const double tr = seg_excl_prod(in ? 1.0 - a : 1.0, !in || k == 0, cT);
+                const double dcx = __shfl_sync(0xffffffffu, u_dcx, L), dcy = __shfl_sync(0xffffffffu, u_dcy, L);
+                const double dcz = __shfl_sync(0xffffffffu, u_dcz, L), dop = __shfl_sync(0xffffffffu, u_dop, L);
+                const double ddep = __shfl_sync(0xffffffffu, u_ddep, L);
+                const uint32_t cntL = __shfl_sync(0xffffffffu, cnt, L);
+                const double v = (dcx * c[0] + dcy * c[1] + dcz * c[2]) + dop + ddep * (0.5 * (t0 + t1));
+                const double wgt = tr * a;
+                const double later = seg_excl_sum_rev(in ? wgt * v : 0.0, !in || k + 1 == cntL, carryS);
+                if (in && p < cap) {
+                    ts[p] = t0;
+                    te[p] = t1;
+                    idx[p] = uint32_t(chunk * 32 + L);
+                    if (CONST) {
+                        sh.rgb[3 * p] = c_rgb[0];
+                        sh.rgb[3 * p + 1] = c_rgb[1];
+                        sh.rgb[3 * p + 2] = c_rgb[2];
+                        sh.sig[p] = c_sig;
+                    }
+                    bo.g_rgb[3 * p] = AT(dcx * wgt);
+                    bo.g_rgb[3 * p + 1] = AT(dcy * wgt);
+                    bo.g_rgb[3 * p + 2] = AT(dcz * wgt);
+                    bo.g_sig[p] = AT((t1 - t0) * (tr * (1.0 - a) * v - later));
+                }
+            }
+        } else if (CONST && mapped) {  // no ray needed: kExpandUnroll independent 32-slot rounds per iteration
             for (uint64_t p0 = base; p0 < end; p0 += 32 * kExpandUnroll) {
                 uint32_t e[kExpandUnroll], ii[kExpandUnroll];
 #pragma unroll
@@ -1455,6 +1595,13 @@ struct ShadeReq {
     void* color = nullptr;
     void* opacity = nullptr;
     void* depth = nullptr;
+    // fused render_backward (requires fwd): upstream gradients in, gradients out
+    bool bwd = false;
+    const void* dc = nullptr;
+    const void* dop = nullptr;
+    const void* ddep = nullptr;
+    void* g_rgb = nullptr;
+    void* g_sig = nullptr;
 };
 
 template <typename AT>
@@ -1466,12 +1613,14 @@ FwdOut<AT> fwd_out(const ShadeReq& sr) {
 // Resident CTAs per SM of one expansion kernel (persistent grid), after opting it
 // in to kExpandSmem of dynamic shared memory — once per kernel (the kernel is the
 // template argument: instantiations share one function type).
-template <auto K>
+constexpr size_t kExpandSmemBwd = kExpandSmem + kMaxAlphaTable * sizeof(double);  // + alpha table
+
+template <auto K, size_t SMEM = kExpandSmem>
 int expand_per_sm() {
     static const int n = [] {
-        cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kExpandSmem));
+        cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM));
         int m = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, K, 32 * kExpandWarps, kExpandSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, K, 32 * kExpandWarps, SMEM);
         return m < 1 ? 2 : m;
     }();
     return n;
@@ -1480,14 +1629,21 @@ int expand_per_sm() {
 template <typename RT, typename AT, bool SHADE, bool FWD, bool VOX>
 void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
                          const uint32_t* kept_idx, uint32_t* overflow, unsigned int* n_overflow,
-                         uint64_t n_chunks, const ShadeReq& sr, const uint32_t* chunk_off) {
+                         uint64_t n_chunks, const ShadeReq& sr, const uint32_t* chunk_off, uint32_t* bwd_list) {
     ShadeOut<RT, AT, VOX> sh{static_cast<const RT*>(rays->d_origins), static_cast<const RT*>(rays->d_directions),
                         sr.f, sr.time, static_cast<AT*>(sr.rgb), static_cast<AT*>(sr.sig)};
-    auto launch = [&](auto kernel, int per_sm) {
-        kernel<<<grid_blocks(ctx, n_chunks * 32, 32 * kExpandWarps, per_sm), 32 * kExpandWarps, kExpandSmem,
+    BwdOut<AT> bo{};
+    if (sr.bwd) {
+        bo = BwdOut<AT>{static_cast<const AT*>(sr.dc), static_cast<const AT*>(sr.dop), static_cast<const AT*>(sr.ddep),
+                        static_cast<AT*>(sr.g_rgb), static_cast<AT*>(sr.g_sig), bwd_list + 4,
+                        reinterpret_cast<unsigned int*>(bwd_list), 0u, double(AT(sr.f.sigma))};
+        bo.atab_n = P.n_steps <= kMaxAlphaTable ? uint32_t(P.n_steps) : 0u;
+    }
+    auto launch = [&](auto kernel, int per_sm, size_t smem) {
+        kernel<<<grid_blocks(ctx, n_chunks * 32, 32 * kExpandWarps, per_sm), 32 * kExpandWarps, smem,
                  ctx->stream>>>(P.near_, P.far_, P.step, out->d_counts, chunk_off, out->d_offsets, kept_idx, rays->n_rays,
                                 out->d_t_starts, out->d_t_ends, out->d_ray_indices, out->capacity, overflow,
-                                n_overflow, sh);
+                                n_overflow, sh, bo);
     };
     // constant shading: every kept sample is inside a constant analytic field (see
     // k_march_expand); needs the alpha floor, a positive density and an identity
@@ -1499,22 +1655,42 @@ void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* ray
     const bool cst = SHADE && !VOX && P.filter && P.thr >= 0.0 && ident && std::isfinite(f.sigma) &&
                      f.sigma > 0.0 && (f.kind == VMB_FIELD_SOLID_SPHERE || f.kind == VMB_FIELD_UNIFORM_BOX) &&
                      VMB_EXPAND_CONST;
-    if (cst)
-        launch(k_march_expand<RT, AT, SHADE, VOX, true>, expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, true>>());
-    else
-        launch(k_march_expand<RT, AT, SHADE, VOX, false>, expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, false>>());
+    bool plain = true;
+    if constexpr (FWD && SHADE) {
+        if (sr.bwd) {
+            plain = false;
+            cudaMemsetAsync(bwd_list, 0, 4, ctx->stream);
+            if (cst)
+                launch(k_march_expand<RT, AT, SHADE, VOX, true, true>,
+                       expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, true, true>, kExpandSmemBwd>(), kExpandSmemBwd);
+            else
+                launch(k_march_expand<RT, AT, SHADE, VOX, false, true>,
+                       expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, false, true>>(), kExpandSmem);
+        }
+    }
+    if (plain && cst)
+        launch(k_march_expand<RT, AT, SHADE, VOX, true>, expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, true>>(),
+               kExpandSmem);
+    else if (plain)
+        launch(k_march_expand<RT, AT, SHADE, VOX, false>, expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, false>>(),
+               kExpandSmem);
     k_march_fixup<RT, AT, SHADE, FWD, VOX><<<ctx->num_sms * 2, 128, 0, ctx->stream>>>(
         P, sh.orig, sh.dirs, out->d_offsets, out->d_t_starts, out->d_t_ends, out->d_ray_indices,
         out->capacity, overflow, n_overflow, ctx->d_err, sh, fwd_out<AT>(sr));
+    if (!plain) {  // the rays of chunks with a ray above kWalkCap samples, after the fixup
+        vmb_packed_view v{out->d_offsets, out->d_counts, rays->n_rays, out->d_t_starts, out->d_t_ends, out->capacity};
+        backward_listed(ctx, &v, sr.rgb, sr.sig, sr.dc, sr.dop, sr.ddep, sr.g_rgb, sr.g_sig, bwd_list + 4,
+                        reinterpret_cast<const unsigned int*>(bwd_list), sr.dtype);
+    }
 }
 
 template <typename RT>
 void dispatch_expand(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out,
                      const uint32_t* kept_idx, uint32_t* overflow, unsigned int* n_overflow,
-                     uint64_t n_chunks, const ShadeReq& sr, const uint32_t* chunk_off) {
+                     uint64_t n_chunks, const ShadeReq& sr, const uint32_t* chunk_off, uint32_t* bwd_list) {
 #define VMB_EXPAND(AT, SH, FW, VX) \
     launch_expand_fixup<RT, AT, SH, FW, VX>(ctx, P, rays, out, kept_idx, overflow, n_overflow, n_chunks, sr, \
-                                            chunk_off)
+                                            chunk_off, bwd_list)
     const bool vox = P.f.kind == VMB_FIELD_VOXEL;
     if (!sr.on)
         vox ? VMB_EXPAND(float, false, false, true) : VMB_EXPAND(float, false, false, false);
@@ -1537,13 +1713,15 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
     const uint64_t n_chunks = (n + 31) / 32;
     const size_t head = 16;
     const size_t idx_bytes = n_chunks * kWalkCap * 32 * sizeof(uint32_t);
-    char* base = static_cast<char*>(scratch(ctx, SCRATCH_MARCH, head + idx_bytes + n * 4 + 8 * n_chunks + 64));
+    char* base = static_cast<char*>(
+        scratch(ctx, SCRATCH_MARCH, head + idx_bytes + n * 4 + 8 * n_chunks + (sr.bwd ? 16 + 4 * n : 0) + 64));
     if (!base) return VMB_CUDA;
     auto* counters = reinterpret_cast<unsigned int*>(base);  // [chunk, overflow]
     auto* kept_idx = reinterpret_cast<uint32_t*>(base + head);
     auto* overflow = reinterpret_cast<uint32_t*>(base + head + idx_bytes);
     auto* chunk_tot = reinterpret_cast<uint32_t*>(base + head + idx_bytes + n * 4);  // per-chunk totals
     auto* chunk_off = chunk_tot + n_chunks;                                         // and their scan
+    auto* bwd_list = chunk_off + n_chunks;  // fused backward: [count, pad x3, rays...]
     cudaMemsetAsync(base, 0, head, ctx->stream);
     if (n == 0) {
         cudaMemsetAsync(d_total, 0, 8, ctx->stream);
@@ -1601,9 +1779,10 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
     int rc = scan_counts(ctx, chunk_tot, n_chunks, chunk_off, d_total);
     if (rc) return rc;
     if (rays->dtype == VMB_F32)
-        dispatch_expand<float>(ctx, P, rays, out, kept_idx, overflow, counters + 1, n_chunks, sr, chunk_off);
+        dispatch_expand<float>(ctx, P, rays, out, kept_idx, overflow, counters + 1, n_chunks, sr, chunk_off, bwd_list);
     else
-        dispatch_expand<double>(ctx, P, rays, out, kept_idx, overflow, counters + 1, n_chunks, sr, chunk_off);
+        dispatch_expand<double>(ctx, P, rays, out, kept_idx, overflow, counters + 1, n_chunks, sr, chunk_off,
+                                bwd_list);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? VMB_OK : cuda_fail(e, "march");
 }
@@ -1886,6 +2065,56 @@ int vmb_march_render_cascade(vmb_ctx* ctx, const vmb_grid* g, const vmb_march_ex
     sr.opacity = d_opacity;
     sr.depth = d_depth;
     return march_packed(ctx, P, rays, out, h_n, stats, sr);
+}
+
+int vmb_march_render_backward_field_async(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,
+                                          const vmb_field* f, const vmb_march_config* cfg, vmb_samples* out,
+                                          void* d_rgbs, void* d_sigmas, void* d_color, void* d_opacity, void* d_depth,
+                                          const void* d_grad_color, const void* d_grad_opacity,
+                                          const void* d_grad_depth, void* d_grad_rgbs, void* d_grad_sigmas,
+                                          int dtype, double time, uint64_t* d_n) {
+    MarchParams P;
+    int rc = march_params(g, rays, cfg, &P);
+    if (rc) return rc;
+    if (int frc = check_field(f)) return frc;
+    P.f = *f;
+    P.filter = true;
+    P.full = false;
+    set_sphere_fast(&P);
+    bool ident = std::isfinite(time) && (time == 0.0 || (f->velocity[0] == 0.0 &&
+                                                          f->velocity[1] == 0.0 && f->velocity[2] == 0.0));
+    for (int a = 0; a < 3; ++a) ident = ident && std::isfinite(f->velocity[a]);
+    if (!ident || !use_fused(P)) {  // march + render_forward, then render_backward on the result
+        rc = vmb_march_render_field_async(ctx, g, rays, f, cfg, out, d_rgbs, d_sigmas, d_color, d_opacity, d_depth,
+                                          dtype, time, d_n);
+        if (rc) return rc;
+        uint64_t n = 0;
+        cudaError_t e = cudaMemcpyAsync(&n, d_n, 8, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "march");
+        vmb_packed_view v{out->d_offsets, out->d_counts, rays->n_rays, out->d_t_starts, out->d_t_ends,
+                          n < out->capacity ? n : out->capacity};
+        return vmb_render_backward(ctx, &v, d_rgbs, d_sigmas, d_grad_color, d_grad_opacity, d_grad_depth,
+                                   d_grad_rgbs, d_grad_sigmas, dtype);
+    }
+    ShadeReq sr;
+    sr.on = true;
+    sr.f = *f;
+    sr.time = time;
+    sr.rgb = d_rgbs;
+    sr.sig = d_sigmas;
+    sr.dtype = dtype;
+    sr.fwd = true;
+    sr.color = d_color;
+    sr.opacity = d_opacity;
+    sr.depth = d_depth;
+    sr.bwd = true;
+    sr.dc = d_grad_color;
+    sr.dop = d_grad_opacity;
+    sr.ddep = d_grad_depth;
+    sr.g_rgb = d_grad_rgbs;
+    sr.g_sig = d_grad_sigmas;
+    return launch_fused(ctx, P, rays, out, reinterpret_cast<unsigned long long*>(d_n), nullptr, sr);
 }
 
 int vmb_march_check(vmb_ctx* ctx) {  // reports the recorded error once, then clears the record

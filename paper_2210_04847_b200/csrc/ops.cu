@@ -34,6 +34,7 @@
 // reference's sequential order to a few ulps (the contract is rel 1e-5).
 // Warps whose rays are not contiguous run the same scans one ray at a time.
 #include "vm_internal.h"
+#include "vm_scan.cuh"
 
 namespace vmb {
 namespace {
@@ -110,58 +111,6 @@ __device__ __forceinline__ double alpha_at(const T* __restrict__ x, const double
                                            const double* __restrict__ te, uint32_t p) {
     if (DENS) return 1.0 - exp(-double(x[p]) * (te[p] - ts[p]));  // rendering.cpp:47-49
     return double(x[p]);
-}
-
-// Exclusive segmented product of m over the warp's 32 lanes, continuing `carry`
-// (the running product of the ray that is open at lane 0) — returns T before
-// this lane's sample and updates carry for the next round.
-__device__ __forceinline__ double seg_excl_prod(double m, bool head, double& carry) {
-    double x = m;
-    int f = head;
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const double y = __shfl_up_sync(0xffffffffu, x, d);
-        const int g = __shfl_up_sync(0xffffffffu, f, d);
-        if (lane >= d) {
-            if (!f) x = y * x;
-            f |= g;
-        }
-    }
-    if (!f) x = carry * x;  // the segment open at lane 0 continues the previous round
-    double t = __shfl_up_sync(0xffffffffu, x, 1);
-    if (lane == 0) t = carry;
-    if (head) t = 1.0;
-    carry = __shfl_sync(0xffffffffu, x, 31);
-    return t;
-}
-
-// Reverse segmented scan of affine maps (c, m): inclusive V_i = c_i + m_i V_{i+1}
-// within a ray (tail flag at its last sample), continuing `carry` (V at lane 0 of
-// the next round, for the ray still open at lane 31). Returns the EXCLUSIVE value
-// W_i = V_{i+1} (0 at a tail) and updates carry for the previous round.
-__device__ __forceinline__ double seg_excl_affine_rev(double c, double m, bool tail, double& carry) {
-    int f = tail;
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const double c2 = __shfl_down_sync(0xffffffffu, c, d);
-        const double m2 = __shfl_down_sync(0xffffffffu, m, d);
-        const int g = __shfl_down_sync(0xffffffffu, f, d);
-        if (lane + d < 32) {
-            if (!f) {
-                c = c + m * c2;
-                m = m * m2;
-            }
-            f |= g;
-        }
-    }
-    const double v = f ? c : c + m * carry;  // inclusive V_i
-    double w = __shfl_down_sync(0xffffffffu, v, 1);
-    if (lane == 31) w = carry;
-    if (tail) w = 0.0;
-    carry = __shfl_sync(0xffffffffu, v, 0);
-    return w;
 }
 
 // ------------------------------------------------------------------ forward

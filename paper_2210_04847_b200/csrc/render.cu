@@ -797,6 +797,25 @@ void launch_shade_forward(vmb_ctx* ctx, const vmb_rays* rays, const vmb_field* f
 }  // namespace vmb
 
 namespace vmb {
+// render_backward of the listed rays only (one warp per ray): the fused training
+// step's rays that its expansion could not differentiate (vm_internal.h).
+int backward_listed(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, const void* sig, const void* dc,
+                    const void* dop, const void* ddep, void* g_rgb, void* g_sig, const uint32_t* list,
+                    const unsigned int* n_list, int dtype) {
+    auto go = [&](auto* t) {
+        using T = std::remove_pointer_t<decltype(t)>;
+        k_backward_long<T><<<ctx->num_sms * 4, kWarps * 32, 0, ctx->stream>>>(
+            p->d_offsets, p->d_counts, p->n_samples, p->d_t_starts, p->d_t_ends, static_cast<const T*>(rgb),
+            static_cast<const T*>(sig), static_cast<const T*>(dc), static_cast<const T*>(dop),
+            static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig), list, n_list);
+    };
+    if (dtype == VMB_F32)
+        go(static_cast<float*>(nullptr));
+    else
+        go(static_cast<double*>(nullptr));
+    return launched("render_backward");
+}
+
 // shade + render_forward in one pass for long-ray batches; returns 1 when the
 // batch is not long-ray dominated (the caller runs k_shade -> render_forward).
 int shade_forward_long(vmb_ctx* ctx, const vmb_rays* rays, const vmb_field* f, double time,

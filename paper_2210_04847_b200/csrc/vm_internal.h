@@ -112,6 +112,9 @@ int check_field(const vmb_field* f);
 int shade_forward_long(vmb_ctx* ctx, const vmb_rays* rays, const vmb_field* f, double time,
                        const vmb_packed_view* p, void* rgb, void* sig, void* color, void* opacity,
                        void* depth, int dtype);  // render.cu; 1 = not applicable
+int backward_listed(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, const void* sig, const void* dc,
+                    const void* dop, const void* ddep, void* g_rgb, void* g_sig, const uint32_t* list,
+                    const unsigned int* n_list, int dtype);  // render.cu: k_backward_long over a ray list
 int reset_error(vmb_ctx* ctx);
 int read_error(vmb_ctx* ctx, DevError* out);  // synchronizes
 

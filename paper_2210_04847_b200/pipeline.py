@@ -20,11 +20,13 @@ class ResidentPipeline:
     Per-ray outputs land in full-batch arrays, so they can be compared with the
     single-call step bit for bit."""
 
-    def __init__(self, streams, chunks, api, dev, grid, field, cfg, rays_dev, ups_dev, N, total_samples):
+    def __init__(self, streams, chunks, api, dev, grid, field, cfg, rays_dev, ups_dev, N, total_samples,
+                 train=False):
         from paper_2210_04847_b200._lib import VMB_F32
         self.api, self.dev, self.grid, self.field, self.cfg = api, dev, grid, field, cfg
         self.L = dev.lib
         self.S, self.K = max(1, streams), max(1, chunks)
+        self.train = train  # one vmb_march_render_backward_field_async per sub-batch
         self.N = N
         self.bounds = [(N * i // self.K, N * (i + 1) // self.K) for i in range(self.K)]
         cmax = max(e - b for b, e in self.bounds)
@@ -55,11 +57,18 @@ class ResidentPipeline:
         pk = bf["packed"]
         smp = pk.samples_struct()
         outs = [a.ptr + 4 * w * b for a, w in zip(self.outs, (3, 1, 1))]
+        ups = [Ptr(u.ptr + 4 * w * b) for u, w in zip(self.ups_dev, (3, 1, 1))]
+        if self.train:
+            check(self.L.vmb_march_render_backward_field_async(
+                cx.h, self.grid.h, C.byref(rays), C.byref(self.field), C.byref(self.cfg), C.byref(smp),
+                bf["rgb"].ptr, bf["sig"].ptr, outs[0], outs[1], outs[2], ups[0].ptr, ups[1].ptr, ups[2].ptr,
+                bf["grgb"].ptr, bf["gsig"].ptr, self.VMB_F32, 0.0, self.n_dev.ptr + 8 * k))
+            pk.n_samples = pk.capacity
+            return
         check(self.L.vmb_march_render_field_async(
             cx.h, self.grid.h, C.byref(rays), C.byref(self.field), C.byref(self.cfg), C.byref(smp),
             bf["rgb"].ptr, bf["sig"].ptr, outs[0], outs[1], outs[2], self.VMB_F32, 0.0, self.n_dev.ptr + 8 * k))
         pk.n_samples = pk.capacity
-        ups = [Ptr(u.ptr + 4 * w * b) for u, w in zip(self.ups_dev, (3, 1, 1))]
         self.api.render_backward_device(cx, pk, bf["rgb"], bf["sig"], *ups, bf["grgb"], bf["gsig"])
 
     def run(self, steps=1, pre_step=None):
