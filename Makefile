@@ -17,7 +17,7 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC \
             -Xcompiler -ffp-contract=off -Xptxas -v -Iinclude
 CU_SRCS  := $(SRC)/runtime.cu $(SRC)/scan.cu $(SRC)/grid.cu $(SRC)/march.cu $(SRC)/render.cu $(SRC)/camera.cu $(SRC)/voxfield.cu $(SRC)/train.cu $(SRC)/ops.cu $(SRC)/sort.cu
 CU_OBJS  := $(patsubst $(SRC)/%.cu,build/obj/%.o,$(CU_SRCS))
-HDRS     := $(SRC)/vm_internal.h $(SRC)/vm_exact.cuh $(SRC)/vm_scan.cuh include/vmb200.h include/vmb200_types.h
+HDRS     := $(SRC)/vm_internal.h $(SRC)/vm_exact.cuh $(SRC)/vm_scan.cuh $(SRC)/vm_bulk.cuh include/vmb200.h include/vmb200_types.h
 
 CXXFLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Wextra -Iinclude -I$(SRC)
 

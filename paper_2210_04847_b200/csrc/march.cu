@@ -28,6 +28,7 @@
 
 #include "vm_internal.h"
 #include "vm_scan.cuh"
+#include "vm_bulk.cuh"
 
 namespace vmb {
 
@@ -920,7 +921,9 @@ constexpr int kExpandWarps = VMB_EXPAND_WARPS;
 #define VMB_EXPAND_UNROLL 4
 #endif
 constexpr int kExpandUnroll = VMB_EXPAND_UNROLL;  // rounds per iteration of the constant-shading path
-constexpr size_t kExpandSmem = size_t(kExpandWarps) * kWalkCap * 32 * (2 * sizeof(uint32_t) + sizeof(uint16_t));
+// per warp: two kept-index row buffers, the owner map, and the rows' two mbarriers
+constexpr size_t kExpandSmem =
+    size_t(kExpandWarps) * (kWalkCap * 32 * (2 * sizeof(uint32_t) + sizeof(uint16_t)) + 2 * sizeof(uint64_t));
 constexpr uint32_t kMaxAlphaTable = 1024;  // the fused backward's constant-density alpha table
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -996,8 +999,10 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
         c_rgb[0] = AT(sh.f.rgb[0]), c_rgb[1] = AT(sh.f.rgb[1]), c_rgb[2] = AT(sh.f.rgb[2]);
         c_sig = AT(sh.f.sigma);
     }
-    // BWD && CONST: alpha per lattice step, after the per-warp buffers
-    double* atab = reinterpret_cast<double*>(expand_smem + kExpandWarps * (2 * kWalkCap * 32 + kWalkCap * 16));
+    // the row buffers' mbarriers, then (BWD && CONST) alpha per lattice step
+    unsigned long long* rbar = reinterpret_cast<unsigned long long*>(
+        expand_smem + kExpandWarps * (2 * kWalkCap * 32 + kWalkCap * 16)) + 2 * wib;
+    double* atab = reinterpret_cast<double*>(expand_smem + kExpandWarps * (2 * kWalkCap * 32 + kWalkCap * 16 + 4));
     if (BWD && CONST) {
         for (uint32_t j = threadIdx.x; j < bo.atab_n; j += blockDim.x) {
             const double dj = double(j);
@@ -1030,14 +1035,22 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
             for (int a = 0; a < 3; ++a) st.o[a] = sh.orig[3 * r + a], st.d[a] = sh.dirs[3 * r + a];
         }
     };
+    // the chunk's used kept-index rows (rows x 128 B, contiguous, 16 B aligned): one
+    // bulk copy issued by lane 0, completed on the buffer's mbarrier
+    if (lane == 0) {
+        mbar_init(&rbar[0]);
+        mbar_init(&rbar[1]);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    uint32_t rphase = 0u;  // bit b: parity of buffer b's next completion
     auto stage_rows = [&](uint64_t c, const Stage& st, int buf) {
-        if (c < n_chunks) {
-            const uint32_t rows = min(__reduce_max_sync(0xffffffffu, st.cnt), uint32_t(kWalkCap));
-            const uint32_t* src = kept_idx + c * (kWalkCap * 32);
-            uint32_t* dst = s_idx[wib][buf];
-            for (uint32_t q = lane; q < rows * 8; q += 32) cp_async16(dst + 4 * q, src + 4 * q);
+        const uint32_t rows = c < n_chunks ? min(__reduce_max_sync(0xffffffffu, st.cnt), uint32_t(kWalkCap)) : 0u;
+        if (lane == 0) {
+            fence_proxy_async();  // the buffer's earlier reads happen before the copy
+            mbar_expect(&rbar[buf], rows * 128u);
+            if (rows) bulk_g2s(s_idx[wib][buf], kept_idx + c * (kWalkCap * 32), rows * 128u, &rbar[buf]);
         }
-        cp_async_commit();
     };
     // one output slot p, owned by lane L (its k-th kept sample)
     auto emit = [&](uint64_t chunk, uint64_t p, int L, uint32_t i, D3 o, D3 d, uint32_t k = 0) {
@@ -1099,7 +1112,8 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
         const bool mapped = !__any_sync(0xffffffffu, big);  // then end - base <= kWalkCap * 32
         if (mapped)  // lane-serial: one 16-bit entry per kept sample
             for (uint32_t k = 0; k < cnt; ++k) mp[off - uint32_t(base) + k] = uint16_t(lane | (k << 5));
-        cp_async_wait1();  // this chunk's rows have landed
+        mbar_wait(&rbar[buf], (rphase >> buf) & 1u);  // this chunk's rows have landed
+        rphase ^= 1u << buf;
         __syncwarp();
         const uint32_t* sk = s_idx[wib][buf];
         if (BWD && !mapped) {  // a ray above kWalkCap: the chunk's rays go to k_backward_long
@@ -1261,7 +1275,8 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
         cur = nxt;
         nxt = nn;
     }
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    // the last prefetch (a chunk past the end: rows = 0) completes at once
+    mbar_wait(&rbar[buf], (rphase >> buf) & 1u);
 }
 
 // Re-walks the (rare) rays whose kept samples overflowed the shared buffer.
@@ -1645,7 +1660,7 @@ FwdOut<AT> fwd_out(const ShadeReq& sr) {
 // Resident CTAs per SM of one expansion kernel (persistent grid), after opting it
 // in to kExpandSmem of dynamic shared memory — once per kernel (the kernel is the
 // template argument: instantiations share one function type).
-constexpr size_t kExpandSmemBwd = kExpandSmem + kMaxAlphaTable * sizeof(double);  // + alpha table
+constexpr size_t kExpandSmemBwd = kExpandSmem + kMaxAlphaTable * sizeof(double);  // + alpha table (8 B aligned)
 
 template <auto K, size_t SMEM = kExpandSmem>
 int expand_per_sm() {

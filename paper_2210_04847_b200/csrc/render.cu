@@ -519,6 +519,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_backward_long(
 #define VMB_BWD_MINB 4
 #endif
 
+
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays, uint64_t n_samples,
