@@ -93,7 +93,8 @@ struct MarchParams {
     uint32_t max_cand;
     bool fast;            // fp32 DDA + filtered fp32 cell test (walk_fast)
     bool sphere_fast;     // SolidSphere field: filtered fp32 density decision
-    uint32_t atab_n;      // k_march_walk: alpha table length (n_steps, sphere_fast only) or 0
+    uint32_t atab_n;      // k_march_walk: alpha + midpoint table length (n_steps, sphere_fast only) or 0
+    bool tab_same32;      // the SolidSphere sigma is exact in fp32 (attribute dtype f32: same alpha, same T)
     float sph_c[3], sph_r, sph_r2, sph_cmax;
     double sph_sig32, sph_rgb32[3];  // SolidSphere sigma / rgb rounded through fp32 (fused forward)
     float step_f, m0_f, inv_step_f, near_f, far_f, Mf;
@@ -645,8 +646,6 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
         }
         // occupied cell: a candidate, with the reference's exact interval
         const double dj = double(j);  // double(j + 1) == dj + 1.0 exactly (j < 2^20): one I2F
-        double t0 = P.near_ + dj * P.step;
-        double t1 = min_ref(P.near_ + (dj + 1.0) * P.step, P.far_);
         if (P.sphere_fast && s.filtering) {
             // Filtered SolidSphere test (fields.cpp:45): |p - c|^2 in fp32 with the
             // bound sph_err; decided cases skip the fp64 midpoint + sqrt.
@@ -658,6 +657,46 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
                 if (s.n_cand >= P.max_cand) return;  // candidate cap
                 uint32_t ci = s.n_cand++;
                 const bool in = d2 < P.sph_r2;
+                if (matab(MODE) && (s.at32 ? P.tab_same32 : true)) {
+                    // The constant interior density from the table: alpha and the
+                    // midpoint 0.5 (t0 + t1) of step j. sigma = 0 outside is never kept
+                    // (alpha_thre >= 0); inside, the attribute-dtype sigma equals the
+                    // march sigma, so the compositing T is the march's T (acc[0]
+                    // follows it for the general path) and alpha is the same value.
+                    if (!in) {
+                        ++j;
+                        continue;
+                    }
+                    const double a = walk_dyn_smem[2 * j];
+                    if (a <= P.thr) {
+                        ++j;
+                        continue;
+                    }
+                    if (s.n_kept < s.buf_cap) s.buf[s.n_kept * s.buf_stride] = uint32_t(j);
+                    if (mbase(MODE) == BUFFER_FWD) {  // rendering.cpp:50-58, in its operation order
+                        const double w = s.T * a;
+                        const double mid = walk_dyn_smem[2 * j + 1];  // (w 0.5)(t0 + t1) == w (0.5 (t0 + t1))
+                        const double cr = s.at32 ? P.sph_rgb32[0] : P.f.rgb[0];
+                        const double cg = s.at32 ? P.sph_rgb32[1] : P.f.rgb[1];
+                        const double cb = s.at32 ? P.sph_rgb32[2] : P.f.rgb[2];
+                        s.acc[1 * kAccStride] = s.acc[1 * kAccStride] + cr * w;
+                        s.acc[2 * kAccStride] = s.acc[2 * kAccStride] + cg * w;
+                        s.acc[3 * kAccStride] = s.acc[3 * kAccStride] + cb * w;
+                        s.acc[4 * kAccStride] += w;
+                        s.acc[5 * kAccStride] += w * mid;
+                    }
+                    s.n_kept++;
+                    s.T *= 1.0 - a;
+                    if (mbase(MODE) == BUFFER_FWD) s.acc[0] = s.T;
+                    if (s.T < P.eps) {
+                        s.filtering = false;
+                        if (!P.full) return;
+                    }
+                    ++j;
+                    continue;
+                }
+                const double t0 = P.near_ + dj * P.step;
+                const double t1 = min_ref(P.near_ + (dj + 1.0) * P.step, P.far_);
                 const double sigma = in ? P.f.sigma : 0.0;
                 // attribute-dtype roundings precomputed on the host (k_shade's AT(rgb), AT(sigma))
                 const D3 rgb = !in ? d3(0.0, 0.0, 0.0)
@@ -665,13 +704,15 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
                                             : d3(P.f.rgb[0], P.f.rgb[1], P.f.rgb[2]);
                 const double sg = !in ? 0.0 : s.at32 ? P.sph_sig32 : P.f.sigma;
                 // alpha of step j for the constant interior density (table) or computed
-                const double apre = matab(MODE) && in ? walk_dyn_smem[j] : -1.0;
+                const double apre = matab(MODE) && in ? walk_dyn_smem[2 * j] : -1.0;
                 if (!filter_sample<MODE>(P, s, uint64_t(j), ci, t0, t1, sigma, err, rgb, true, sg, apre))
                     return;
                 ++j;
                 continue;
             }
         }
+        const double t0 = P.near_ + dj * P.step;
+        const double t1 = min_ref(P.near_ + (dj + 1.0) * P.step, P.far_);
         D3 p = load3(orig, r) + load3(dirs, r) * (0.5 * (t0 + t1));
         if (!on_candidate<MODE>(P, s, uint64_t(j), t0, t1, p, err)) return;
         ++j;
@@ -815,7 +856,8 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
             const double dj = double(j);
             const double t0 = P.near_ + dj * P.step;
             const double t1 = min_ref(P.near_ + (dj + 1.0) * P.step, P.far_);
-            walk_dyn_smem[j] = 1.0 - exp(-P.f.sigma * (t1 - t0));
+            walk_dyn_smem[2 * j] = 1.0 - exp(-P.f.sigma * (t1 - t0));
+            walk_dyn_smem[2 * j + 1] = 0.5 * (t0 + t1);
         }
         __syncthreads();
     }
@@ -1566,6 +1608,7 @@ void set_sphere_fast(MarchParams* P) {
     // inside the sphere sigma is one constant, so alpha depends only on the lattice
     // step: k_march_walk tabulates it per CTA (built with -DVMB_ATAB=0: off)
     P->atab_n = P->sphere_fast && VMB_ATAB && P->n_steps <= 1024 ? uint32_t(P->n_steps) : 0u;
+    P->tab_same32 = double(float(f.sigma)) == f.sigma;
 }
 
 
@@ -1798,7 +1841,7 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
     // persistent grid: exactly the resident capacity of the device
     auto launch_walk = [&](auto kernel, auto* o, auto* d, auto fo) {
         int per_sm = 0;
-        const size_t dyn = size_t(P.atab_n) * sizeof(double);  // read only by ATAB kernels
+        const size_t dyn = size_t(P.atab_n) * 2 * sizeof(double);  // read only by ATAB kernels: alpha, midpoint
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, dyn);
         if (per_sm < 1) per_sm = 4;
         kernel<<<ctx->num_sms * per_sm, 128, dyn, ctx->stream>>>(
