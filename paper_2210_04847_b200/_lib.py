@@ -244,6 +244,7 @@ SIGNATURES = {
     "vmb_comm_init": (I32, [VP, VP, I32, I32]),
     "vmb_comm_destroy": (I32, [VP]),
     "vmb_comm_allreduce_max_f64": (I32, [VP, VP, U64]),
+    "vmb_comm_allgather_f64": (I32, [VP, VP, U64]),
 }
 
 _LIB = None
