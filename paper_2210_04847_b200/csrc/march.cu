@@ -40,6 +40,14 @@ namespace {
 // in filter_sample as the sample is kept (vmb_march_render_field).
 enum Mode { COUNT = 0, FILL = 1, BUFFER = 2, BUFFER_FWD = 3 };
 constexpr int kAccStride = 128;  // = the walk kernel's block size
+// k_march_walk's per-thread shared-memory slots, at namespace scope so every access
+// is indexed by threadIdx.x (two generic pointers held in the Sink cost registers and
+// spills under the 64-register cap): the six fused-forward accumulators (k = Tf, r,
+// g, b, opacity, depth) and the ray's twelve fp32 constants (A, B, o, d; RSMM).
+__shared__ double walk_acc[6][kAccStride];
+__shared__ float walk_rc[12][kAccStride];
+#define WACC(k) walk_acc[k][threadIdx.x]
+#define WRC(k) walk_rc[k][threadIdx.x]
 // bit 2 of a mode: the kernel evaluates a stored voxel field (field_density_t<true>)
 constexpr int VOXM = 4;
 __host__ __device__ constexpr int mbase(int m) { return m & 3; }
@@ -92,6 +100,7 @@ struct MarchParams {
     double eps, thr;
     uint32_t max_cand;
     bool fast;            // fp32 DDA + filtered fp32 cell test (walk_fast)
+    bool f32_safe;        // max(|near|, |far|) < 1e250: every f32 ray passes ray_safe
     bool sphere_fast;     // SolidSphere field: filtered fp32 density decision
     uint32_t atab_n;      // k_march_walk: alpha + midpoint table length (n_steps, sphere_fast only) or 0
     bool tab_same32;      // the SolidSphere sigma is exact in fp32 (attribute dtype f32: same alpha, same T)
@@ -208,8 +217,6 @@ struct Sink {
     // out of registers leaves the walk loop its 64 registers.
     bool at32 = false;
     void* attr = nullptr;  // ATTRM: float4 / double4 rows beside buf (same stride)
-    double* acc = nullptr;
-    float* rc = nullptr;  // RSMM: 12 per-ray fp32 constants, stride kAccStride
 
     // One kept sample, with exactly k_shade + k_forward's expressions (FwdAcc):
     // sigma/rgb are rounded to the attribute dtype; alpha is reused when the
@@ -225,14 +232,14 @@ struct Sink {
     __device__ __forceinline__ void composite_rounded(double sigma, double sg, D3 c, double t0, double t1,
                                                       double alpha) {
         const double a = sg == sigma ? alpha : 1.0 - exp(-sg * (t1 - t0));
-        const double Tf = acc[0];
+        const double Tf = WACC(0);
         const double w = Tf * a;
-        acc[1 * kAccStride] = acc[1 * kAccStride] + c.x * w;
-        acc[2 * kAccStride] = acc[2 * kAccStride] + c.y * w;
-        acc[3 * kAccStride] = acc[3 * kAccStride] + c.z * w;
-        acc[4 * kAccStride] += w;
-        acc[5 * kAccStride] += w * 0.5 * (t0 + t1);
-        acc[0] = Tf * (1.0 - a);
+        WACC(1) = WACC(1) + c.x * w;
+        WACC(2) = WACC(2) + c.y * w;
+        WACC(3) = WACC(3) + c.z * w;
+        WACC(4) += w;
+        WACC(5) += w * 0.5 * (t0 + t1);
+        WACC(0) = Tf * (1.0 - a);
     }
 };
 
@@ -551,17 +558,18 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
     if (mrsm(MODE)) {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            s.rc[a * kAccStride] = A[a];
-            s.rc[(3 + a) * kAccStride] = B[a];
-            s.rc[(6 + a) * kAccStride] = of[a];
-            s.rc[(9 + a) * kAccStride] = df[a];
+            WRC(a) = A[a];
+            WRC(3 + a) = B[a];
+            WRC(6 + a) = of[a];
+            WRC(9 + a) = df[a];
         }
     }
     // the constants where they are used: from the shared slot (RSMM) or registers
-#define VM_RC(k, reg) (mrsm(MODE) ? s.rc[(k) * kAccStride] : (reg))
+#define VM_RC(k, reg) (mrsm(MODE) ? WRC(k) : (reg))
     const float amax = fmaxf(fmaxf(fabsf(A[0]), fabsf(A[1])), fabsf(A[2]));
     const float bmax = fmaxf(fmaxf(fabsf(B[0]), fabsf(B[1])), fabsf(B[2]));
-    const float E = ldexpf(2.0f * amax + 5.0f * bmax * P.Mf, -22) + 1e-6f;
+    // (scalings by powers of two are exact: x * 2^-22 == ldexpf(x, -22))
+    const float E = (2.0f * amax + 5.0f * bmax * P.Mf) * 0x1p-22f + 1e-6f;
     const bool fast_ok = E < 0.05f;
     // Error bound of the fp32 |p - c|^2 (see the filtered sphere test below):
     // per-axis position error e <= 2^-24 (3|o| + 7|d| M + 2|c|) (rounding of o, d, c,
@@ -571,8 +579,8 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
     if (P.sphere_fast) {
         float omax = fmaxf(fmaxf(fabsf(of[0]), fabsf(of[1])), fabsf(of[2]));
         float dmax = fmaxf(fmaxf(fabsf(df[0]), fabsf(df[1])), fabsf(df[2]));
-        float e = ldexpf(3.0f * omax + 7.0f * dmax * P.Mf + 2.0f * P.sph_cmax, -24);
-        sph_err = 4.0f * (ldexpf(3.0f * P.sph_r2, -24) + 3.5f * P.sph_r * e + 3.0f * e * e) + 1e-12f;
+        float e = (3.0f * omax + 7.0f * dmax * P.Mf + 2.0f * P.sph_cmax) * 0x1p-24f;
+        sph_err = 4.0f * ((3.0f * P.sph_r2) * 0x1p-24f + 3.5f * P.sph_r * e + 3.0f * e * e) + 1e-12f;
     }
     const float EPSD = 1e-3f + 4.0f * E;  // guard for the fp32 clip
     // ray_aabb_intersect against the guarded bounding box of the occupied cells
@@ -587,7 +595,11 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
         if (B[a] == 0.0f) {
             if (A[a] < lo || A[a] > hi) return;
         } else {
-            float inv = __frcp_rn(B[a]);
+            // approximate reciprocal (rel. error < 2^-22): the clipped range carries
+            // EPSD cells and two lattice steps of slack on each side, against a t error
+            // of ~1e-7 t (n_steps < 2^20 on this path: < 0.2 steps)
+            float inv;
+            asm("rcp.approx.f32 %0, %1;" : "=f"(inv) : "f"(B[a]));
             float ta = (lo - A[a]) * inv, tb = (hi - A[a]) * inv;
             tlo = fmaxf(tlo, fminf(ta, tb));
             thi = fminf(thi, fmaxf(ta, tb));
@@ -601,7 +613,8 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
     // the next floor(L / (bmax * step)) lattice steps are skipped unevaluated
     // (bmax * step = largest per-step move along any axis, in cells).
     const int last = int(P.n_steps) - 1;
-    const float inv_bms = 1.0f / fmaxf(bmax * P.step_f, 1e-30f);
+    float inv_bms;  // approximate: jumps are cut by the 0.99999 factor below (1e-5 >> 2^-22)
+    asm("rcp.approx.f32 %0, %1;" : "=f"(inv_bms) : "f"(fmaxf(bmax * P.step_f, 1e-30f)));
     const float jump_margin = 1.0f + 2.0f * E + 0.01f;
     const int Ri = int(P.res);
     int j = int(floorf((tlo - P.near_f) * P.inv_step_f)) - 2;
@@ -679,15 +692,15 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
                         const double cr = s.at32 ? P.sph_rgb32[0] : P.f.rgb[0];
                         const double cg = s.at32 ? P.sph_rgb32[1] : P.f.rgb[1];
                         const double cb = s.at32 ? P.sph_rgb32[2] : P.f.rgb[2];
-                        s.acc[1 * kAccStride] = s.acc[1 * kAccStride] + cr * w;
-                        s.acc[2 * kAccStride] = s.acc[2 * kAccStride] + cg * w;
-                        s.acc[3 * kAccStride] = s.acc[3 * kAccStride] + cb * w;
-                        s.acc[4 * kAccStride] += w;
-                        s.acc[5 * kAccStride] += w * mid;
+                        WACC(1) = WACC(1) + cr * w;
+                        WACC(2) = WACC(2) + cg * w;
+                        WACC(3) = WACC(3) + cb * w;
+                        WACC(4) += w;
+                        WACC(5) += w * mid;
                     }
                     s.n_kept++;
                     s.T *= 1.0 - a;
-                    if (mbase(MODE) == BUFFER_FWD) s.acc[0] = s.T;
+                    if (mbase(MODE) == BUFFER_FWD) WACC(0) = s.T;
                     if (s.T < P.eps) {
                         s.filtering = false;
                         if (!P.full) return;
@@ -847,8 +860,6 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
     uint32_t* __restrict__ counts, uint32_t* __restrict__ kept_idx, unsigned int* chunk_counter,
     uint64_t n_chunks, unsigned long long* emitted, DevError* err, FwdOut<AT> fo,
     uint32_t* __restrict__ chunk_tot, void* __restrict__ kept_attr) {
-    __shared__ double s_acc[FWD ? 6 : 1][kAccStride];
-    __shared__ float s_rc[FAST && VMB_WALK_RSM ? 12 : 1][kAccStride];
     const int lane = threadIdx.x & 31;
     unsigned long long emit_local = 0;
     if (ATAB) {  // alpha per lattice step for the constant interior density (sphere)
@@ -882,17 +893,17 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
             if (ATTR)
                 s.attr = static_cast<char*>(kept_attr) + (uint64_t(chunk) * (kWalkCap * 32) + lane) * 4 * sizeof(AT);
             if (FWD) {
-                s.acc = &s_acc[0][threadIdx.x];
-                s.acc[0] = 1.0;
+                WACC(0) = 1.0;
 #pragma unroll
-                for (int k = 1; k < 6; ++k) s.acc[k * kAccStride] = 0.0;
+                for (int k = 1; k < 6; ++k) WACC(k) = 0.0;
             }
             constexpr int M = (FWD ? BUFFER_FWD : BUFFER) | (VOX ? VOXM : 0) | (ATAB ? ATABM : 0) |
                               (FAST && VMB_WALK_RSM ? RSMM : 0) | (FWD && ATTR ? ATTRM : 0);
-            s.rc = &s_rc[0][threadIdx.x];
             if (FAST) {
                 const D3 o = load3(orig, r), d = load3(dirs, r);
-                if (ray_safe(P, o, d))
+                // f32 rays (|o|, |d| < 3.5e38) cannot reach ray_safe's 1e300 bound
+                // unless near/far are beyond 1e250 (P.f32_safe, set on the host)
+                if ((sizeof(RT) == 4 && P.f32_safe) || ray_safe(P, o, d))
                     walk_fast<M>(P, s, orig, dirs, r, err);
                 else
                     walk_dense<M>(P, s, o, d, err);
@@ -903,11 +914,11 @@ __global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
             kept = s.n_kept;
             emit_local += s.n_cand;
             if (FWD) {  // every kept sample was composited (rays over kWalkCap too)
-                fo.color[3 * r] = AT(s.acc[1 * kAccStride]);
-                fo.color[3 * r + 1] = AT(s.acc[2 * kAccStride]);
-                fo.color[3 * r + 2] = AT(s.acc[3 * kAccStride]);
-                fo.opacity[r] = AT(s.acc[4 * kAccStride]);
-                fo.depth[r] = AT(s.acc[5 * kAccStride]);
+                fo.color[3 * r] = AT(WACC(1));
+                fo.color[3 * r + 1] = AT(WACC(2));
+                fo.color[3 * r + 2] = AT(WACC(3));
+                fo.opacity[r] = AT(WACC(4));
+                fo.depth[r] = AT(WACC(5));
             }
         }
         // the chunk's sample total: the packing scans these (32x fewer than rays)
@@ -968,12 +979,6 @@ constexpr size_t kExpandSmem =
     size_t(kExpandWarps) * (kWalkCap * 32 * (2 * sizeof(uint32_t) + sizeof(uint16_t)) + 2 * sizeof(uint64_t));
 constexpr uint32_t kMaxAlphaTable = 1024;  // the fused backward's constant-density alpha table
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 // (an explicit minBlocksPerSM, even 1, changes the register allocation and costs
 // ~25 us per step here: leave it unset unless tuning with -DVMB_EXPAND_MINB)
@@ -1524,6 +1529,7 @@ int march_params(const vmb_grid* g, const vmb_rays* rays, const vmb_march_config
     // fp32 fast walk: lattice indices and step-range conversions stay well inside
     // fp32 resolution for lattices up to 2^20 steps.
     P->fast = P->skip && P->n_steps < (1ull << 20) && P->n_steps > 0 && g->res <= 1024;
+    P->f32_safe = fmax(fabs(P->near_), fabs(P->far_)) < 1e250;
     P->step_f = float(P->step);
     P->m0_f = float(P->near_ + 0.5 * P->step);
     P->inv_step_f = float(1.0 / P->step);
