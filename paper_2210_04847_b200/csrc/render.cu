@@ -21,7 +21,10 @@
 // are not contiguous (arbitrary user offsets) use per-lane global reads.
 // Sample positions are 32-bit: packed offsets are u32 by construction (pack()
 // rejects more than 2^32-1 samples, core_types.cpp:33-36).
+#include <type_traits>
+
 #include "vm_internal.h"
+#include "vm_bulk.cuh"
 
 namespace vmb {
 namespace {
@@ -44,15 +47,23 @@ struct FwdSmem {
     T sig[Tile<T>::CH];
 };
 
-template <typename T>
-struct BwdSmem {
-    double ts[Tile<T>::CH];
-    double te[Tile<T>::CH];
+// PAD (k_backward_hy, dynamic shared memory): room for a bulk copy that starts at
+// the 16-byte boundary at or below a group's first sample and ends at the one at or
+// above its last, and the copies' mbarrier
+struct BulkBar {
+    unsigned long long bar;   // the bulk copies' mbarrier
+};
+struct NoBar {};
+template <typename T, int PAD = 0>
+struct BwdSmem : std::conditional_t<(PAD > 0), BulkBar, NoBar> {
+    alignas(16) double ts[Tile<T>::CH + PAD];
+    alignas(16) double te[Tile<T>::CH + PAD];
     double al[Tile<T>::CH];
     double tr[Tile<T>::CH];   // transmittance before each sample
-    T rgb[3 * Tile<T>::CH];   // input rgb, then d_rgb
-    T sig[Tile<T>::CH];       // input sigma, then d_sigma
+    alignas(16) T rgb[3 * Tile<T>::CH + PAD];   // input rgb, then d_rgb
+    alignas(16) T sig[Tile<T>::CH + PAD];       // input sigma, then d_sigma
 };
+constexpr int kBulkPad = 8;
 
 struct RayRange {
     uint64_t r;
@@ -128,6 +139,56 @@ __device__ __forceinline__ void stage_in(S& sm, int lane, uint32_t cs, uint32_t 
         }
     }
     __syncwarp();
+}
+
+// k_backward_hy's staging by the bulk-copy engine: lane 0 issues one
+// cp.async.bulk per array (t_starts, t_ends, sigma, rgb) of the group's samples
+// [cs, cs + n), each from the 16-byte boundary at or below its first byte to the one
+// at or above its end, completed on the warp's mbarrier; the group's sample i then
+// sits at index i + shift of the array's tile (TileView). Returns false (nothing
+// issued) when a pointer is not 16-byte aligned or a rounded span would pass
+// n_samples: the caller stages that group with stage_in.
+template <typename T>
+struct TileView {
+    double* ts;
+    double* te;
+    T* rgb;
+    T* sig;
+};
+template <typename T>
+__device__ __forceinline__ bool stage_bulk(BwdSmem<T, kBulkPad>& sm, int lane, uint32_t cs, uint32_t n, uint64_t n_samples,
+                                           const double* __restrict__ ts, const double* __restrict__ te,
+                                           const T* __restrict__ rgb, const T* __restrict__ sig, uint32_t& phase,
+                                           TileView<T>& v) {
+#ifndef VMB_BWD_BULK
+#define VMB_BWD_BULK 1
+#endif
+    if (!VMB_BWD_BULK) return false;
+    const uint64_t a_t0 = reinterpret_cast<uint64_t>(ts), a_t1 = reinterpret_cast<uint64_t>(te);
+    const uint64_t a_c = reinterpret_cast<uint64_t>(rgb), a_s = reinterpret_cast<uint64_t>(sig);
+    if (((a_t0 | a_t1 | a_c | a_s) & 15u) != 0u) return false;
+    // byte spans [lo, hi) relative to each array, 16-byte aligned
+    const uint64_t t_lo = (8ull * cs) & ~15ull, t_hi = (8ull * (cs + n) + 15ull) & ~15ull;
+    const uint64_t c_lo = (3ull * sizeof(T) * cs) & ~15ull, c_hi = (3ull * sizeof(T) * (cs + n) + 15ull) & ~15ull;
+    const uint64_t s_lo = (uint64_t(sizeof(T)) * cs) & ~15ull, s_hi = (uint64_t(sizeof(T)) * (cs + n) + 15ull) & ~15ull;
+    if (t_hi > 8ull * n_samples || c_hi > 3ull * sizeof(T) * n_samples || s_hi > uint64_t(sizeof(T)) * n_samples)
+        return false;
+    __syncwarp();  // every lane's accesses of the tile so far precede the copies
+    if (lane == 0) {
+        fence_proxy_async();
+        mbar_expect(&sm.bar, uint32_t(2 * (t_hi - t_lo) + (c_hi - c_lo) + (s_hi - s_lo)));
+        bulk_g2s(sm.ts, reinterpret_cast<const char*>(ts) + t_lo, uint32_t(t_hi - t_lo), &sm.bar);
+        bulk_g2s(sm.te, reinterpret_cast<const char*>(te) + t_lo, uint32_t(t_hi - t_lo), &sm.bar);
+        bulk_g2s(sm.rgb, reinterpret_cast<const char*>(rgb) + c_lo, uint32_t(c_hi - c_lo), &sm.bar);
+        bulk_g2s(sm.sig, reinterpret_cast<const char*>(sig) + s_lo, uint32_t(s_hi - s_lo), &sm.bar);
+    }
+    v.ts = sm.ts + (8ull * cs - t_lo) / 8;
+    v.te = sm.te + (8ull * cs - t_lo) / 8;
+    v.rgb = sm.rgb + (3ull * sizeof(T) * cs - c_lo) / sizeof(T);
+    v.sig = sm.sig + (uint64_t(sizeof(T)) * cs - s_lo) / sizeof(T);
+    mbar_wait(&sm.bar, phase);
+    phase ^= 1u;
+    return true;
 }
 
 // ------------------------------------------------------------------ forward
@@ -384,8 +445,8 @@ __device__ __forceinline__ Up load_up(const T* dc, const T* dop, const T* ddep, 
     return u;
 }
 
-template <typename T>
-__device__ __forceinline__ void write_out(BwdSmem<T>& sm, int lane, uint32_t cs, uint32_t n,
+template <typename T, typename S>
+__device__ __forceinline__ void write_out(S& sm, int lane, uint32_t cs, uint32_t n,
                                           T* __restrict__ g_rgb, T* __restrict__ g_sig) {
     constexpr int R = Tile<T>::CH / 32;
     __syncwarp();
@@ -412,8 +473,8 @@ __device__ __forceinline__ void write_out(BwdSmem<T>& sm, int lane, uint32_t cs,
 // to the association order of the scans' products and sums.
 constexpr int kCarryTiles = 32;  // one per lane: lane k holds the T carried into tile sb_start + k
 
-template <typename T>
-__device__ void bwd_long_ray(BwdSmem<T>& sm, int lane, uint32_t s0, uint32_t s1, const Up& u,
+template <typename T, typename S>
+__device__ void bwd_long_ray(S& sm, int lane, uint32_t s0, uint32_t s1, const Up& u,
                              const double* __restrict__ ts, const double* __restrict__ te,
                              const T* __restrict__ rgb, const T* __restrict__ sig,
                              T* __restrict__ g_rgb, T* __restrict__ g_sig) {
@@ -483,7 +544,7 @@ __device__ void bwd_long_ray(BwdSmem<T>& sm, int lane, uint32_t s0, uint32_t s1,
                     sm.sig[i] = T((t1 - t0) * (tr * (1.0 - a) * v - suffix));
                 }
             }
-            write_out(sm, lane, cs, n, g_rgb, g_sig);
+            write_out<T>(sm, lane, cs, n, g_rgb, g_sig);
         }
         sb_end = sb_start;
     }
@@ -527,12 +588,15 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
     const T* __restrict__ sig, const T* __restrict__ dc, const T* __restrict__ dop,
     const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig,
     uint32_t* __restrict__ long_rays, unsigned int* __restrict__ n_long) {
-    __shared__ BwdSmem<T> smem[kWarps];
+    extern __shared__ __align__(16) unsigned char bwd_dyn_smem[];  // kWarps x BwdSmem<T, kBulkPad>
     const int lane = threadIdx.x & 31;
-    BwdSmem<T>& sm = smem[threadIdx.x >> 5];
-    // owner lane of each staged sample: bytes of the sigma tile, which is free
-    // between the alpha phase (stage_in) and phase D (which writes d_sigma there)
-    uint8_t* own = reinterpret_cast<uint8_t*>(sm.sig);
+    BwdSmem<T, kBulkPad>& sm = reinterpret_cast<BwdSmem<T, kBulkPad>*>(bwd_dyn_smem)[threadIdx.x >> 5];
+    if (lane == 0) {
+        mbar_init(&sm.bar);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    uint32_t bphase = 0u;  // parity of the bulk-copy barrier's next phase
     const uint64_t n_warps = (n_rays + 31) / 32;
     for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
          w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
@@ -545,7 +609,7 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
                             __shfl_sync(0xffffffffu, u.dcz, q), __shfl_sync(0xffffffffu, u.dop, q),
                             __shfl_sync(0xffffffffu, u.ddep, q)};
                 if (__shfl_sync(0xffffffffu, int(rr.valid), q) && a < b)
-                    bwd_long_ray(sm, lane, a, b, uq, ts, te, rgb, sig, g_rgb, g_sig);
+                    bwd_long_ray<T>(sm, lane, a, b, uq, ts, te, rgb, sig, g_rgb, g_sig);
             }
             continue;
         }
@@ -572,7 +636,21 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
             const int g1 = 31 - __clz(fm);
             const uint32_t n = __shfl_sync(0xffffffffu, rr.end, g1) - base;
             if (n) {
-                stage_in<T, false>(sm, lane, base, n, ts, te, rgb, sig);
+                TileView<T> tv;
+                if (stage_bulk(sm, lane, base, n, n_samples, ts, te, rgb, sig, bphase, tv)) {
+#pragma unroll
+                    for (int k = 0; k < Tile<T>::CH / 32; ++k) {
+                        const uint32_t i = 32u * k + lane;
+                        if (i < n) sm.al[i] = 1.0 - exp(-double(tv.sig[i]) * (tv.te[i] - tv.ts[i]));
+                    }
+                    __syncwarp();
+                } else {
+                    stage_in<T, false>(sm, lane, base, n, ts, te, rgb, sig);
+                    tv = TileView<T>{sm.ts, sm.te, sm.rgb, sm.sig};
+                }
+                // owner lane of each staged sample: bytes of the sigma tile, free
+                // between the alpha phase and phase D (which writes d_sigma there)
+                uint8_t* own = reinterpret_cast<uint8_t*>(tv.sig);
                 // B (lane-serial): T before each sample, rendering.cpp:89-96 — one
                 // dependent DMUL per sample; the owner map for the parallel phase
                 if (lane >= g0 && lane <= g1) {
@@ -611,16 +689,16 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
                                 __shfl_sync(0xffffffffu, u.dcz, o), __shfl_sync(0xffffffffu, u.dop, o),
                                 __shfl_sync(0xffffffffu, u.ddep, o)};
                     if (in) {
-                        const double t0 = sm.ts[i], t1 = sm.te[i], a = sm.al[i], tr = sm.tr[i];
-                        const double v = uo.value(double(sm.rgb[3 * i]), double(sm.rgb[3 * i + 1]),
-                                                  double(sm.rgb[3 * i + 2]), 0.5 * (t0 + t1));
+                        const double t0 = tv.ts[i], t1 = tv.te[i], a = sm.al[i], tr = sm.tr[i];
+                        const double v = uo.value(double(tv.rgb[3 * i]), double(tv.rgb[3 * i + 1]),
+                                                  double(tv.rgb[3 * i + 2]), 0.5 * (t0 + t1));
                         const double wgt = tr * a;
                         T* gr = g_rgb + 3 * uint64_t(base) + 3 * i;
                         gr[0] = T(uo.dcx * wgt);
                         gr[1] = T(uo.dcy * wgt);
                         gr[2] = T(uo.dcz * wgt);
-                        sm.ts[i] = t1 - t0;
-                        sm.te[i] = wgt * v;
+                        tv.ts[i] = t1 - t0;
+                        tv.te[i] = wgt * v;
                         sm.tr[i] = tr * (1.0 - a) * v;
                     }
                 }
@@ -632,29 +710,29 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
                     uint32_t i = rr.end - base;
                     const uint32_t b = rr.off - base;
                     for (; i >= b + 4; i -= 4) {  // loads first, then the chain
-                        const double d3_ = sm.ts[i - 1], a3 = sm.tr[i - 1], w3 = sm.te[i - 1];
-                        const double d2_ = sm.ts[i - 2], a2 = sm.tr[i - 2], w2 = sm.te[i - 2];
-                        const double d1_ = sm.ts[i - 3], a1 = sm.tr[i - 3], w1 = sm.te[i - 3];
-                        const double d0_ = sm.ts[i - 4], a0 = sm.tr[i - 4], w0 = sm.te[i - 4];
-                        sm.sig[i - 1] = T(d3_ * (a3 - suffix));
+                        const double d3_ = tv.ts[i - 1], a3 = sm.tr[i - 1], w3 = tv.te[i - 1];
+                        const double d2_ = tv.ts[i - 2], a2 = sm.tr[i - 2], w2 = tv.te[i - 2];
+                        const double d1_ = tv.ts[i - 3], a1 = sm.tr[i - 3], w1 = tv.te[i - 3];
+                        const double d0_ = tv.ts[i - 4], a0 = sm.tr[i - 4], w0 = tv.te[i - 4];
+                        tv.sig[i - 1] = T(d3_ * (a3 - suffix));
                         suffix += w3;
-                        sm.sig[i - 2] = T(d2_ * (a2 - suffix));
+                        tv.sig[i - 2] = T(d2_ * (a2 - suffix));
                         suffix += w2;
-                        sm.sig[i - 3] = T(d1_ * (a1 - suffix));
+                        tv.sig[i - 3] = T(d1_ * (a1 - suffix));
                         suffix += w1;
-                        sm.sig[i - 4] = T(d0_ * (a0 - suffix));
+                        tv.sig[i - 4] = T(d0_ * (a0 - suffix));
                         suffix += w0;
                     }
                     while (i-- > b) {
-                        sm.sig[i] = T(sm.ts[i] * (sm.tr[i] - suffix));
-                        suffix += sm.te[i];
+                        tv.sig[i] = T(tv.ts[i] * (sm.tr[i] - suffix));
+                        suffix += tv.te[i];
                     }
                 }
                 __syncwarp();
                 T* psg = g_sig + base + lane;
 #pragma unroll
                 for (int k = 0; k < Tile<T>::CH / 32; ++k)
-                    if (32u * k + lane < n) psg[32 * k] = sm.sig[32 * k + lane];
+                    if (32u * k + lane < n) psg[32 * k] = tv.sig[32 * k + lane];
                 __syncwarp();
             }
             g0 = g1 + 1;
@@ -769,7 +847,13 @@ int launch_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, con
     if (!list) return VMB_CUDA;
     auto* n_long = reinterpret_cast<unsigned int*>(list);
     cudaMemsetAsync(n_long, 0, 4, ctx->stream);
-    k_backward_hy<T><<<blocks, kWarps * 32, 0, ctx->stream>>>(
+    constexpr size_t smem = kWarps * sizeof(BwdSmem<T, kBulkPad>);
+    static const bool opted = [] {  // above the 48 KB default of dynamic shared memory
+        return cudaFuncSetAttribute(k_backward_hy<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) ==
+               cudaSuccess;
+    }();
+    (void)opted;
+    k_backward_hy<T><<<blocks, kWarps * 32, smem, ctx->stream>>>(
         p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
         static_cast<const T*>(rgb), static_cast<const T*>(sig), static_cast<const T*>(dc),
         static_cast<const T*>(dop), static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig),
