@@ -8,6 +8,6 @@ for rep in 1 2; do
       > gpurun_out/ab_${n}_$rep.json 2> gpurun_out/ab_${n}_$rep.err
     python -c "
 import json,sys; d=json.loads(open('gpurun_out/ab_${n}_$rep.json').read().strip().splitlines()[-1])
-print('$n', $rep, round(d['ms_per_step'],4), {k: round(v,4) for k,v in d.get('phases_ms',{}).items()}, d['roofline']['step']['frac'] if 'roofline' in d else '')"
+print('$n', $rep, round(d['ms_per_step'],4), {k: round(v,4) for k,v in d.get('phases_ms',{}).items()}, d['roofline']['step']['frac'] if 'roofline' in d else '', 'cfg2', round(d['config2']['ms_per_step'],4) if d.get('config2') else '')"
   done
 done
