@@ -614,8 +614,11 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
             continue;
         }
         const unsigned vmask = __ballot_sync(0xffffffffu, rr.valid);  // valid lanes: a prefix
-        {  // rays longer than a tile go to k_backward_long: one list append per warp
-            const unsigned lm = __ballot_sync(0xffffffffu, rr.valid && rr.end - rr.off > uint32_t(Tile<T>::CH));
+        // Rays longer than half a tile go to k_backward_long (one warp per ray, lane
+        // scans): a group holding one or two such rays would run its recurrences on
+        // one or two lanes (the cascade's ~120-sample rays). One list append per warp.
+        const unsigned lm = __ballot_sync(0xffffffffu, rr.valid && rr.end - rr.off > uint32_t(Tile<T>::CH / 2));
+        {
             if (lm) {
                 unsigned at = 0;
                 if (lane == 0) at = atomicAdd(n_long, unsigned(__popc(lm)));
@@ -627,13 +630,15 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
         int g0 = 0;
         while (g0 < 32 && ((vmask >> g0) & 1u)) {
             const uint32_t base = __shfl_sync(0xffffffffu, rr.off, g0);
-            const bool fits = rr.valid && lane >= g0 && rr.end - base <= uint32_t(Tile<T>::CH);
-            const unsigned fm = __ballot_sync(0xffffffffu, fits);  // monotone: ends ascend
-            if (!((fm >> g0) & 1u)) {  // ray g0 alone exceeds a tile: listed above
+            if ((lm >> g0) & 1u) {  // ray g0 is listed for k_backward_long
                 ++g0;
                 continue;
             }
-            const int g1 = 31 - __clz(fm);
+            const bool fits = rr.valid && lane >= g0 && rr.end - base <= uint32_t(Tile<T>::CH);
+            const unsigned fm = __ballot_sync(0xffffffffu, fits);  // monotone: ends ascend
+            // the group: from g0 while the rays fit the tile, up to the next listed ray
+            const unsigned later_long = lm & ~((2u << g0) - 1u);
+            const int g1 = min(31 - __clz(fm), later_long ? __ffs(later_long) - 2 : 31);
             const uint32_t n = __shfl_sync(0xffffffffu, rr.end, g1) - base;
             if (n) {
                 TileView<T> tv;

@@ -351,7 +351,8 @@ def _instance(rng, n_rays, max_per_ray, contiguous=True):
 
 
 @pytest.mark.parametrize("n_rays,max_per_ray,contiguous",
-                         [(3000, 12, True), (500, 300, True), (257, 40, False), (64, 2048, True)])
+                         [(3000, 12, True), (500, 300, True), (257, 40, False), (64, 2048, True),
+                          (2000, 100, True)])  # rays around the half-tile cut (64 f32, 32 f64) in every warp
 def test_render_paths_vs_oracle(dev, orc, n_rays, max_per_ray, contiguous):
     rng = np.random.default_rng(n_rays)
     p, rgb, sig = _instance(rng, n_rays, max_per_ray, contiguous)
