@@ -126,6 +126,15 @@ struct MarchParams {
     // the outermost level is an AABB: a midpoint outside it on an axis the ray does
     // not come back along ends the walk (every later midpoint is outside every level)
     bool exit_box;
+    // empty-space skipping of walk_ext (every level an AABB grid, no growth): per
+    // level (0 = the base grid) its box origin and cells per world unit, the box of
+    // the level below in this level's cell units, and its distance map
+    bool ext_skip;
+    struct {
+        double lo[3], scale[3];
+        float in_lo[3], in_hi[3];
+    } xs[kMaxLevels];
+    const uint8_t* lv_dist[kMaxLevels - 1];
 };
 
 template <typename T>
@@ -461,6 +470,31 @@ __device__ __forceinline__ int cascade_query(const MarchParams& P, D3 p, D3 d) {
     return 0;
 }
 
+// cascade_query that also reports the deciding level (0 = base) and its cell
+__device__ __forceinline__ int cascade_locate(const MarchParams& P, D3 p, D3 d, int* lev, int64_t* cell) {
+    int64_t c = cell_of_point(P.k, P.res, p);
+    if (c >= 0) {
+        *lev = 0, *cell = c;
+        return fine_bit(P.bits, c);
+    }
+    for (uint32_t l = 0; l < P.n_lv; ++l) {
+        c = cell_of_point(P.lv_k[l], P.lv_res[l], p);
+        if (c >= 0) {
+            *lev = int(l) + 1, *cell = c;
+            return fine_bit(P.lv_bits[l], c);
+        }
+    }
+    *lev = -1;
+    if (P.exit_box) {
+        const Contract& k = P.n_lv ? P.lv_k[P.n_lv - 1] : P.k;
+        const D3 g = contract(k, p);
+        if ((g.x > 1.0 && d.x >= 0.0) || (g.x < 0.0 && d.x <= 0.0) || (g.y > 1.0 && d.y >= 0.0) ||
+            (g.y < 0.0 && d.y <= 0.0) || (g.z > 1.0 && d.z >= 0.0) || (g.z < 0.0 && d.z <= 0.0))
+            return -1;
+    }
+    return 0;
+}
+
 // Geometric step growth outside the unit ball (ray_marching.cpp:88-106).
 template <int MODE>
 __device__ void walk_growth(const MarchParams& P, Sink& s, D3 o, D3 d, DevError* err) {
@@ -505,11 +539,57 @@ __device__ void walk_ext(const MarchParams& P, Sink& s, D3 o, D3 d, DevError* er
             atomicMin(&err->key, march_err_key(s.ray, 0, ERR_NONFINITE_COORD));
             return;
         }
-        const int q = cascade_query(P, mid, d);
+        int lev;
+        int64_t cell;
+        const int q = cascade_locate(P, mid, d, &lev, &cell);
         if (q < 0) return;
         if (q && !on_candidate<MODE>(P, s, s.n_cand, t, t1, mid, err)) return;
+        const double mt0 = 0.5 * (t + t1);
         t += dt;
-        if (!P.grows) continue;
+        if (!P.grows) {
+            // Empty-space skipping: the deciding level's cell is empty with distance
+            // D >= 2 to its nearest occupied cell, so every point within D - 1 cells
+            // of this midpoint (that is still decided by this level: inside its box,
+            // outside the box of the level below) is an empty cell. The next steps
+            // whose midpoints stay within that reach are not candidates: only their
+            // t recurrence runs (t += dt, the same fp64 sequence), not their queries.
+            // Bounds in fp32 cell units with 1e-3-cell margins (the positions'
+            // rounding is ~1e-5 cells) and a 1e-4 relative shrink.
+            if (P.ext_skip && q == 0 && lev >= 0) {
+                const int D = __ldg((lev == 0 ? P.dist : P.lv_dist[lev - 1]) + cell);
+                if (D >= 2) {
+                    const auto& X = P.xs[lev];
+                    const float Rl = float(lev == 0 ? P.res : P.lv_res[lev - 1]);
+                    // cell coordinates from fp64 (a far-off box must not lose them to fp32)
+                    const float u0 = float((mid.x - X.lo[0]) * X.scale[0]), B0 = float(d.x * X.scale[0]);
+                    const float u1 = float((mid.y - X.lo[1]) * X.scale[1]), B1 = float(d.y * X.scale[1]);
+                    const float u2 = float((mid.z - X.lo[2]) * X.scale[2]), B2 = float(d.z * X.scale[2]);
+                    const float bmax = fmaxf(fmaxf(fabsf(B0), fabsf(B1)), fabsf(B2));
+                    float lim = (float(D) - 1.001f) / bmax;  // bmax == 0: +inf
+                    auto wall = [&](float u, float B) {     // stay inside this level's box
+                        if (B > 0.0f) lim = fminf(lim, (Rl - 1e-3f - u) / B);
+                        if (B < 0.0f) lim = fminf(lim, (u - 1e-3f) / -B);
+                    };
+                    wall(u0, B0), wall(u1, B1), wall(u2, B2);
+                    if (lev > 0) {  // stay outside the box of the level below (L-inf gap)
+                        const float gap = fmaxf(fmaxf(fmaxf(X.in_lo[0] - u0, u0 - X.in_hi[0]),
+                                                      fmaxf(X.in_lo[1] - u1, u1 - X.in_hi[1])),
+                                                fmaxf(X.in_lo[2] - u2, u2 - X.in_hi[2]));
+                        lim = fminf(lim, (gap - 1e-3f) / bmax);
+                    }
+                    const double reach = double(lim) * 0.9999;
+                    if (reach > 0.0) {
+                        while (t < P.far_) {
+                            if (P.cone) dt = fmin(fmax(t * P.cone_angle, P.step), P.max_step);
+                            const double t1n = min_ref(t + dt, P.far_);
+                            if (!(t1n > t) || 0.5 * (t + t1n) - mt0 > reach) break;
+                            t += dt;
+                        }
+                    }
+                }
+            }
+            continue;
+        }
         const D3 b = mid - P.ball_c;
         const double b2 = dot(b, b);
         const bool outside = P.ball_filter && b2 > P.ball_r2_hi   ? true
@@ -1648,7 +1728,26 @@ int apply_ext(const vmb_grid* g, const vmb_march_ext* x, const vmb_march_config*
         P->lv_k[l] = L->k;
         P->lv_res[l] = L->res;
         P->lv_bits[l] = L->bits;
+        P->lv_dist[l] = L->dist;
         prev = L;
+    }
+    // walk_ext's empty-space skipping: every level an AABB grid, no step growth
+    P->ext_skip = !P->grows && g->con.kind == VMB_CONTRACT_AABB;
+    for (uint32_t l = 0; P->ext_skip && l <= x->n_levels; ++l) {
+        const vmb_grid* L = l == 0 ? g : x->levels[l - 1];
+        auto& X = P->xs[l];
+        for (int a = 0; a < 3; ++a) {
+            const double sz = L->con.box_max[a] - L->con.box_min[a];
+            if (!(sz > 0.0) || !std::isfinite(sz)) P->ext_skip = false;
+            X.lo[a] = L->con.box_min[a];
+            X.scale[a] = double(L->res) / sz;
+            X.in_lo[a] = 1.0f, X.in_hi[a] = 0.0f;  // level 0: no level below (gap unused)
+            if (l > 0) {
+                const vmb_grid* B = l == 1 ? g : x->levels[l - 2];
+                X.in_lo[a] = float((B->con.box_min[a] - L->con.box_min[a]) * double(L->res) / sz);
+                X.in_hi[a] = float((B->con.box_max[a] - L->con.box_min[a]) * double(L->res) / sz);
+            }
+        }
     }
     P->n_lv = x->n_levels;
     P->cone = x->cone != 0;
