@@ -483,8 +483,10 @@ __device__ void bwd_long_ray(S& sm, int lane, uint32_t s0, uint32_t s1, const Up
     double carryS = 0.0;  // sum of w v over the samples after the current round
     for (uint32_t sb_end = nt; sb_end > 0;) {
         const uint32_t sb_start = sb_end > uint32_t(kCarryTiles) ? sb_end - kCarryTiles : 0u;
-        double carryT = 1.0, my_carry = 1.0;  // forward sweep: T carried into every tile
-        for (uint32_t t = 0; t < sb_end; ++t) {
+        // forward sweep: T carried into every tile of the super-block (the last tile's
+        // own product is never needed: a ray within one tile has no forward sweep)
+        double carryT = 1.0, my_carry = 1.0;
+        for (uint32_t t = 0; t + 1 < sb_end; ++t) {
             if (t >= sb_start && uint32_t(lane) == t - sb_start) my_carry = carryT;
             const uint32_t cs = s0 + t * CH, n = min(CH, s1 - cs);
             stage_in<T, false>(sm, lane, cs, n, ts, te, static_cast<const T*>(nullptr), sig);
@@ -496,6 +498,7 @@ __device__ void bwd_long_ray(S& sm, int lane, uint32_t s0, uint32_t s1, const Up
             }
             __syncwarp();
         }
+        if (uint32_t(lane) == sb_end - 1 - sb_start) my_carry = carryT;
         __syncwarp();
         for (uint32_t t = sb_end; t-- > sb_start;) {
             const uint32_t cs = s0 + t * CH, n = min(CH, s1 - cs);
