@@ -623,7 +623,15 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
     const float Rf = float(P.res);
     // Only fp32 state stays live in the loops; the fp64 ray is re-read from
     // global memory (L1) by the rare exact paths.
-    float A[3], B[3], of[3], df[3];
+    float A[3], B[3], Q[3];
+    // SolidSphere: the squared distance to the centre along the ray as a quadratic
+    // in the midpoint parameter, |o + d m - c|^2 = a m^2 + b m + c0 (coefficients in
+    // fp64, evaluated in fp32 by two FMAs), with its error bound sph_err:
+    //   the midpoint's fp32 error |dm| <= 6 2^-24 M (M = max(|near|, |far|)) moves the
+    //   quadratic by <= (2 a M + |b|) |dm|; the coefficients' rounding, the two FMAs'
+    //   and r^2's add <= 4 2^-24 (a M^2 + |b| M + c0 + r^2); the reference's fp64
+    //   evaluation is within ~1e-15 of it; a factor 4 of headroom on top.
+    float sph_err = 0.0f;
     {
         const D3 o = load3(orig, r), d = load3(dirs, r);
         A[0] = float((o.x - P.k.lo.x) * P.scale[0]);
@@ -632,16 +640,22 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
         B[0] = float(d.x * P.scale[0]);
         B[1] = float(d.y * P.scale[1]);
         B[2] = float(d.z * P.scale[2]);
-        of[0] = float(o.x), of[1] = float(o.y), of[2] = float(o.z);
-        df[0] = float(d.x), df[1] = float(d.y), df[2] = float(d.z);
+        Q[0] = Q[1] = Q[2] = 0.0f;
+        if (P.sphere_fast) {
+            const D3 oc = o - d3(P.f.center[0], P.f.center[1], P.f.center[2]);
+            const double qa = dot(d, d), qb = 2.0 * dot(oc, d), qc = dot(oc, oc);
+            const double M = double(P.Mf), r2 = P.f.radius * P.f.radius;
+            const double bound = (2.0 * qa * M + fabs(qb)) * 6.0 * M + 4.0 * (qa * M * M + fabs(qb) * M + qc + r2);
+            Q[0] = float(qa), Q[1] = float(qb), Q[2] = float(qc);
+            sph_err = float(4.0 * 0x1p-24 * bound * (1.0 + 1e-6)) + 1e-12f;
+        }
     }
     if (mrsm(MODE)) {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             WRC(a) = A[a];
             WRC(3 + a) = B[a];
-            WRC(6 + a) = of[a];
-            WRC(9 + a) = df[a];
+            WRC(6 + a) = Q[a];
         }
     }
     // the constants where they are used: from the shared slot (RSMM) or registers
@@ -651,17 +665,6 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
     // (scalings by powers of two are exact: x * 2^-22 == ldexpf(x, -22))
     const float E = (2.0f * amax + 5.0f * bmax * P.Mf) * 0x1p-22f + 1e-6f;
     const bool fast_ok = E < 0.05f;
-    // Error bound of the fp32 |p - c|^2 (see the filtered sphere test below):
-    // per-axis position error e <= 2^-24 (3|o| + 7|d| M + 2|c|) (rounding of o, d, c,
-    // of the fp32 midpoint and of the FMA/subtraction), squared-distance error
-    // <= 3 2^-24 r^2 + 2 sqrt(3) r e + 3 e^2; a factor 4 of headroom on top.
-    float sph_err = 0.0f;
-    if (P.sphere_fast) {
-        float omax = fmaxf(fmaxf(fabsf(of[0]), fabsf(of[1])), fabsf(of[2]));
-        float dmax = fmaxf(fmaxf(fabsf(df[0]), fabsf(df[1])), fabsf(df[2]));
-        float e = (3.0f * omax + 7.0f * dmax * P.Mf + 2.0f * P.sph_cmax) * 0x1p-24f;
-        sph_err = 4.0f * ((3.0f * P.sph_r2) * 0x1p-24f + 3.5f * P.sph_r * e + 3.0f * e * e) + 1e-12f;
-    }
     const float EPSD = 1e-3f + 4.0f * E;  // guard for the fp32 clip
     // ray_aabb_intersect against the guarded bounding box of the occupied cells
     // (inside the domain [0, R]^3): every lattice step outside it is an empty cell
@@ -740,12 +743,10 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
         // occupied cell: a candidate, with the reference's exact interval
         const double dj = double(j);  // double(j + 1) == dj + 1.0 exactly (j < 2^20): one I2F
         if (P.sphere_fast && s.filtering) {
-            // Filtered SolidSphere test (fields.cpp:45): |p - c|^2 in fp32 with the
-            // bound sph_err; decided cases skip the fp64 midpoint + sqrt.
-            float qx = fmaf(VM_RC(9, df[0]), m, VM_RC(6, of[0])) - P.sph_c[0];
-            float qy = fmaf(VM_RC(10, df[1]), m, VM_RC(7, of[1])) - P.sph_c[1];
-            float qz = fmaf(VM_RC(11, df[2]), m, VM_RC(8, of[2])) - P.sph_c[2];
-            float d2 = fmaf(qx, qx, fmaf(qy, qy, qz * qz));
+            // Filtered SolidSphere test (fields.cpp:45): |p - c|^2 in fp32 from the
+            // ray's quadratic, within sph_err; decided cases skip the fp64 midpoint
+            // + sqrt.
+            const float d2 = fmaf(fmaf(VM_RC(6, Q[0]), m, VM_RC(7, Q[1])), m, VM_RC(8, Q[2]));
             if (d2 > P.sph_r2 + sph_err || d2 < P.sph_r2 - sph_err) {
                 if (s.n_cand >= P.max_cand) return;  // candidate cap
                 uint32_t ci = s.n_cand++;
