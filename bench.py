@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--workload", default="config5", choices=["config5", "config3", "config1"],
                     help="config3: the multi-level grid + cone-step workload alone; config1: the 4096-ray "
                          "batch as a CUDA graph (one JSON line each)")
+    ap.add_argument("--config4", type=int, default=1,
+                    help="N=1: also time BASELINE config 4 (2^20 rays, grid update every 16 steps) -> `config4`")
     ap.add_argument("--config1", type=int, default=1,
                     help="N=1: also time BASELINE config 1 (4096 rays, CUDA graph) in a sub-run -> `config1`")
     ap.add_argument("--field", default="sphere", choices=["sphere", "checker", "voxel"],
@@ -908,8 +910,28 @@ def main():
             cfg2["samples"] = c2["config"]["samples_per_gpu"]
             cfg2["roofline_step_frac"] = c2["roofline"]["step"]["frac"]
             cfg2["e2e"] = {k: c2["e2e"].get(k) for k in ("value", "unit", "ms_per_step")}
+            cfg2["clocks"] = c2.get("clocks")
         except Exception as ex:  # pragma: no cover
             cfg2 = {"error": repr(ex)}
+
+    cfg4 = None
+    if dist.rank == 0 and dist.world == 1 and args.config4 and args.width == 2048:
+        try:  # BASELINE config 4 (training loop shape): 2^20 rays per step, a grid EMA update every 16 steps
+            steps4 = max(args.steps, 32)
+            out = subprocess.run([sys.executable, os.path.abspath(__file__), "--width", "1024", "--grid-update-every",
+                                  "16", "--steps", str(steps4), "--warmup", str(args.warmup), "--cpu-baseline", "0",
+                                  "--config1", "0", "--config2", "0", "--config3", "0", "--config4", "0",
+                                  "--fields", "0", "--phases", "0"],
+                                 capture_output=True, text=True, timeout=600)
+            c4 = json.loads(out.stdout.strip().splitlines()[-1])
+            cfg4 = {k: c4[k] for k in ("value", "unit", "ms_per_step", "samples_per_s", "clocks", "grid_update_ms")}
+            cfg4["workload"] = (f"config 4: 1048576 orbit-camera rays per step (W=1024), 128^3 grid, an occupancy-grid "
+                                f"EMA update (probe + EMA + threshold + distance map) every 16 steps inside the timed "
+                                f"loop ({steps4} steps), SolidSphere field")
+            cfg4["samples"] = c4["config"]["samples_per_gpu"]
+            cfg4["roofline_step_frac"] = c4["roofline"]["step"]["frac"]
+        except Exception as ex:  # pragma: no cover
+            cfg4 = {"error": repr(ex)}
 
     fields = None
     if dist.rank == 0 and dist.world == 1 and args.fields and args.field == "sphere" and args.width == 2048:
@@ -918,7 +940,8 @@ def main():
             try:  # the same step with a general field: no constant-density shortcuts
                 out = subprocess.run([sys.executable, os.path.abspath(__file__), "--field", kind, "--steps",
                                       str(args.steps), "--warmup", str(args.warmup), "--cpu-baseline", "0",
-                                      "--config1", "0", "--config2", "0", "--config3", "0", "--fields", "0"],
+                                      "--config1", "0", "--config2", "0", "--config3", "0", "--config4", "0",
+                                      "--fields", "0"],
                                      capture_output=True, text=True, timeout=900)
                 fl = json.loads(out.stdout.strip().splitlines()[-1])
                 fields[kind] = {k: fl[k] for k in ("value", "unit", "ms_per_step", "samples_per_s", "phases_ms",
@@ -988,7 +1011,7 @@ def main():
                 "pipeline": pipe_info,
                 "phases_ms": phase, "grid_update_ms": grid_update_ms,
                 "roofline": roof, "e2e": e2e, "e2e_camera": e2e_cam, "cpu_baseline": cpu, "clocks": clk,
-                "config1": cfg1, "config2": cfg2, "config3": cfg3, "fields": fields,
+                "config1": cfg1, "config2": cfg2, "config3": cfg3, "config4": cfg4, "fields": fields,
                 "gpu_launches": (KERNELS_PER_STEP - {"none": 0, "shade": 1, "forward": 2}[args.fusion])
                 * args.steps * (pipe.K if pipe else 1)}
         print(json.dumps(line), flush=True)
