@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--workload", default="config5", choices=["config5", "config3", "config1"],
                     help="config3: the multi-level grid + cone-step workload alone; config1: the 4096-ray "
                          "batch as a CUDA graph (one JSON line each)")
+    ap.add_argument("--res256", type=int, default=1,
+                    help="N=1: also time config 5 over a 256^3 grid in a sub-run -> `grid256`")
     ap.add_argument("--config4", type=int, default=1,
                     help="N=1: also time BASELINE config 4 (2^20 rays, grid update every 16 steps) -> `config4`")
     ap.add_argument("--config1", type=int, default=1,
@@ -914,6 +916,23 @@ def main():
         except Exception as ex:  # pragma: no cover
             cfg2 = {"error": repr(ex)}
 
+    res256 = None
+    if dist.rank == 0 and dist.world == 1 and args.res256 and args.width == 2048 and args.resolution == 128:
+        try:  # BASELINE config 5's second grid size: the same step over a 256^3 grid
+            out = subprocess.run([sys.executable, os.path.abspath(__file__), "--resolution", "256", "--steps",
+                                  str(args.steps), "--warmup", str(args.warmup), "--cpu-baseline", "0",
+                                  "--config1", "0", "--config2", "0", "--config3", "0", "--config4", "0",
+                                  "--fields", "0", "--res256", "0"],
+                                 capture_output=True, text=True, timeout=900)
+            c5 = json.loads(out.stdout.strip().splitlines()[-1])
+            res256 = {k: c5[k] for k in ("value", "unit", "ms_per_step", "samples_per_s", "phases_ms", "clocks")}
+            res256["workload"] = c5["config"]["workload"]
+            res256["samples"] = c5["config"]["samples_per_gpu"]
+            res256["roofline_step_frac"] = c5["roofline"]["step"]["frac"]
+            res256["roofline_march_frac"] = c5["roofline"]["frac"]
+        except Exception as ex:  # pragma: no cover
+            res256 = {"error": repr(ex)}
+
     cfg4 = None
     if dist.rank == 0 and dist.world == 1 and args.config4 and args.width == 2048:
         try:  # BASELINE config 4 (training loop shape): 2^20 rays per step, a grid EMA update every 16 steps
@@ -921,7 +940,7 @@ def main():
             out = subprocess.run([sys.executable, os.path.abspath(__file__), "--width", "1024", "--grid-update-every",
                                   "16", "--steps", str(steps4), "--warmup", str(args.warmup), "--cpu-baseline", "0",
                                   "--config1", "0", "--config2", "0", "--config3", "0", "--config4", "0",
-                                  "--fields", "0", "--phases", "0"],
+                                  "--fields", "0", "--phases", "0", "--res256", "0"],
                                  capture_output=True, text=True, timeout=600)
             c4 = json.loads(out.stdout.strip().splitlines()[-1])
             cfg4 = {k: c4[k] for k in ("value", "unit", "ms_per_step", "samples_per_s", "clocks", "grid_update_ms")}
@@ -941,7 +960,7 @@ def main():
                 out = subprocess.run([sys.executable, os.path.abspath(__file__), "--field", kind, "--steps",
                                       str(args.steps), "--warmup", str(args.warmup), "--cpu-baseline", "0",
                                       "--config1", "0", "--config2", "0", "--config3", "0", "--config4", "0",
-                                      "--fields", "0"],
+                                      "--fields", "0", "--res256", "0"],
                                      capture_output=True, text=True, timeout=900)
                 fl = json.loads(out.stdout.strip().splitlines()[-1])
                 fields[kind] = {k: fl[k] for k in ("value", "unit", "ms_per_step", "samples_per_s", "phases_ms",
@@ -1011,7 +1030,7 @@ def main():
                 "pipeline": pipe_info,
                 "phases_ms": phase, "grid_update_ms": grid_update_ms,
                 "roofline": roof, "e2e": e2e, "e2e_camera": e2e_cam, "cpu_baseline": cpu, "clocks": clk,
-                "config1": cfg1, "config2": cfg2, "config3": cfg3, "config4": cfg4, "fields": fields,
+                "config1": cfg1, "config2": cfg2, "config3": cfg3, "config4": cfg4, "grid256": res256, "fields": fields,
                 "gpu_launches": (KERNELS_PER_STEP - {"none": 0, "shade": 1, "forward": 2}[args.fusion])
                 * args.steps * (pipe.K if pipe else 1)}
         print(json.dumps(line), flush=True)

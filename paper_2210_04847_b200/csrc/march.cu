@@ -650,10 +650,15 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
             sph_err = float(4.0 * 0x1p-24 * bound * (1.0 + 1e-6)) + 1e-12f;
         }
     }
+    // the loop evaluates v = u - 1/2 (cell coordinate minus one half): the cell is
+    // rint(v), decided when every |v - rint(v)| <= 1/2 - E (one max, one compare)
+    float Ah[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) Ah[a] = A[a] - 0.5f;
     if (mrsm(MODE)) {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            WRC(a) = A[a];
+            WRC(a) = Ah[a];
             WRC(3 + a) = B[a];
             WRC(6 + a) = Q[a];
         }
@@ -663,8 +668,10 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
     const float amax = fmaxf(fmaxf(fabsf(A[0]), fabsf(A[1])), fabsf(A[2]));
     const float bmax = fmaxf(fmaxf(fabsf(B[0]), fabsf(B[1])), fabsf(B[2]));
     // (scalings by powers of two are exact: x * 2^-22 == ldexpf(x, -22))
-    const float E = (2.0f * amax + 5.0f * bmax * P.Mf) * 0x1p-22f + 1e-6f;
+    // (+ 2^-24 (amax + 1): the rounding of A - 1/2)
+    const float E = (2.0f * amax + 5.0f * bmax * P.Mf) * 0x1p-22f + (amax + 1.0f) * 0x1p-24f + 1e-6f;
     const bool fast_ok = E < 0.05f;
+    const float half_E = 0.5f - E;
     const float EPSD = 1e-3f + 4.0f * E;  // guard for the fp32 clip
     // ray_aabb_intersect against the guarded bounding box of the occupied cells
     // (inside the domain [0, R]^3): every lattice step outside it is an empty cell
@@ -707,12 +714,12 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
     bool alive = true;
     while (j <= jend) {
         const float m = fmaf(float(j), P.step_f, P.m0_f);
-        const float u0 = fmaf(VM_RC(3, B[0]), m, VM_RC(0, A[0]));
-        const float u1 = fmaf(VM_RC(4, B[1]), m, VM_RC(1, A[1]));
-        const float u2 = fmaf(VM_RC(5, B[2]), m, VM_RC(2, A[2]));
+        const float v0 = fmaf(VM_RC(3, B[0]), m, VM_RC(0, Ah[0]));
+        const float v1 = fmaf(VM_RC(4, B[1]), m, VM_RC(1, Ah[1]));
+        const float v2 = fmaf(VM_RC(5, B[2]), m, VM_RC(2, Ah[2]));
         // |u| stays within a few cells of the domain here (the loop range is the
         // clipped lattice), so the float->int floor is exact and in range
-        const int i0 = __float2int_rd(u0), i1 = __float2int_rd(u1), i2 = __float2int_rd(u2);
+        const int i0 = __float2int_rn(v0), i1 = __float2int_rn(v1), i2 = __float2int_rn(v2);
         const bool inside = unsigned(i0) < unsigned(Ri) && unsigned(i1) < unsigned(Ri) && unsigned(i2) < unsigned(Ri);
         int D = kDistCap;
         uint32_t cell = 0;
@@ -727,8 +734,8 @@ __device__ void walk_fast(const MarchParams& P, Sink& s, const RT* __restrict__ 
         }
         bool exact = !fast_ok || j == last;
         if (!exact) {
-            const float r0 = u0 - float(i0), r1 = u1 - float(i1), r2 = u2 - float(i2);
-            exact = r0 < E || r0 > 1.0f - E || r1 < E || r1 > 1.0f - E || r2 < E || r2 > 1.0f - E;
+            const float r0 = v0 - float(i0), r1 = v1 - float(i1), r2 = v2 - float(i2);
+            exact = fmaxf(fmaxf(fabsf(r0), fabsf(r1)), fabsf(r2)) > half_E;
         }
         if (exact) {
             if (!eval_step<MODE>(P, s, load3(orig, r), load3(dirs, r), uint64_t(j), err, &alive))
