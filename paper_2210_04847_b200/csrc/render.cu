@@ -620,7 +620,11 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
         // Rays longer than half a tile go to k_backward_long (one warp per ray, lane
         // scans): a group holding one or two such rays would run its recurrences on
         // one or two lanes (the cascade's ~120-sample rays). One list append per warp.
-        const unsigned lm = __ballot_sync(0xffffffffu, rr.valid && rr.end - rr.off > uint32_t(Tile<T>::CH / 2));
+#ifndef VMB_BWD_SERIAL_DIV
+#define VMB_BWD_SERIAL_DIV 2  // rays above CH / this go to k_backward_long (config 2, 27-sample rays: /2 0.211 ms, /4 0.210, /8 0.237)
+#endif
+        const unsigned lm =
+            __ballot_sync(0xffffffffu, rr.valid && rr.end - rr.off > uint32_t(Tile<T>::CH / VMB_BWD_SERIAL_DIV));
         {
             if (lm) {
                 unsigned at = 0;
