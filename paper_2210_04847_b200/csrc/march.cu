@@ -1055,7 +1055,7 @@ struct ShadeOut {
 // lane holds its own ray; a sample's ray is handed to its lane by shuffles. The
 // per-sample work touches registers/smem only, plus the coalesced output writes.
 #ifndef VMB_EXPAND_WARPS
-#define VMB_EXPAND_WARPS 16  // one 122 KB CTA per SM: 0.769 ms/step vs 0.780 (8), 0.820 (4), 0.774 (20)
+#define VMB_EXPAND_WARPS 12  // one CTA per SM; r2 sweep (config 5 step): 12 0.7077 ms, 16 0.7113, 14 0.7104, 10 0.7118, 6 0.7121
 #endif
 constexpr int kExpandWarps = VMB_EXPAND_WARPS;
 #ifndef VMB_EXPAND_UNROLL

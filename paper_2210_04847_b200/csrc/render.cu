@@ -30,7 +30,7 @@ namespace vmb {
 namespace {
 
 #ifndef VMB_RENDER_WARPS
-#define VMB_RENDER_WARPS 8
+#define VMB_RENDER_WARPS 4  // r2 (config 5 step, with 8 CTAs/SM): 4 warps 0.694 ms, 8 warps 0.707
 #endif
 constexpr int kWarps = VMB_RENDER_WARPS;  // threads per CTA / 32
 
@@ -213,7 +213,7 @@ struct Fwd {
 constexpr uint32_t kFwdLaneAvg = VMB_FWD_LANE_AVG;
 
 template <typename T>
-__global__ void __launch_bounds__(kWarps * 32, 4) k_forward(
+__global__ void __launch_bounds__(kWarps * 32, 24 / kWarps) k_forward(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays, uint64_t n_samples,
     const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
     const T* __restrict__ sig, T* __restrict__ color, T* __restrict__ opacity, T* __restrict__ depth) {
@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_backward_long(
 // each group is staged once and every lane runs the reference's exact forward-T /
 // reverse-suffix recurrence (rendering.cpp:85-108) from shared memory.
 #ifndef VMB_BWD_MINB
-#define VMB_BWD_MINB 4
+#define VMB_BWD_MINB 8
 #endif
 
 
@@ -754,7 +754,7 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
 
 // ------------------------------------------------------------------ transmittance
 template <typename T>
-__global__ void __launch_bounds__(kWarps * 32, 4) k_transmittance(
+__global__ void __launch_bounds__(kWarps * 32, 32 / kWarps) k_transmittance(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_rays, uint64_t n_samples,
     const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ sig,
     T* __restrict__ out) {
@@ -839,7 +839,7 @@ int launched(const char* where) {
 }
 
 #ifndef VMB_RENDER_CTAS
-#define VMB_RENDER_CTAS 16
+#define VMB_RENDER_CTAS 32
 #endif
 #ifndef VMB_FWD_WIN_CTAS
 #define VMB_FWD_WIN_CTAS 6  // windowed forward CTAs per SM (r1 sweep: 6 best)
@@ -870,7 +870,7 @@ int launch_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, con
         static_cast<const T*>(rgb), static_cast<const T*>(sig), static_cast<const T*>(dc),
         static_cast<const T*>(dop), static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig),
         list + 4, n_long);
-    k_backward_long<T><<<ctx->num_sms * 4, kWarps * 32, 0, ctx->stream>>>(
+    k_backward_long<T><<<ctx->num_sms * (32 / kWarps), kWarps * 32, 0, ctx->stream>>>(
         p->d_offsets, p->d_counts, p->n_samples, p->d_t_starts, p->d_t_ends, static_cast<const T*>(rgb),
         static_cast<const T*>(sig), static_cast<const T*>(dc), static_cast<const T*>(dop),
         static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig), list + 4, n_long);
@@ -901,7 +901,7 @@ int backward_listed(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, con
                     const unsigned int* n_list, int dtype) {
     auto go = [&](auto* t) {
         using T = std::remove_pointer_t<decltype(t)>;
-        k_backward_long<T><<<ctx->num_sms * 4, kWarps * 32, 0, ctx->stream>>>(
+        k_backward_long<T><<<ctx->num_sms * (32 / kWarps), kWarps * 32, 0, ctx->stream>>>(
             p->d_offsets, p->d_counts, p->n_samples, p->d_t_starts, p->d_t_ends, static_cast<const T*>(rgb),
             static_cast<const T*>(sig), static_cast<const T*>(dc), static_cast<const T*>(dop),
             static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig), list, n_list);
