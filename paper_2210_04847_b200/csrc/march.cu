@@ -39,7 +39,10 @@ namespace {
 // BUFFER_FWD = BUFFER + the render_forward compositing of each kept sample, done
 // in filter_sample as the sample is kept (vmb_march_render_field).
 enum Mode { COUNT = 0, FILL = 1, BUFFER = 2, BUFFER_FWD = 3 };
-constexpr int kAccStride = 128;  // = the walk kernel's block size
+#ifndef VMB_WALK_THREADS
+#define VMB_WALK_THREADS 128
+#endif
+constexpr int kAccStride = VMB_WALK_THREADS;  // = the walk kernel's block size
 // k_march_walk's per-thread shared-memory slots, at namespace scope so every access
 // is indexed by threadIdx.x (two generic pointers held in the Sink cost registers and
 // spills under the 64-register cap): the six fused-forward accumulators (k = Tf, r,
@@ -896,7 +899,7 @@ constexpr int kClaim = VMB_WALK_CLAIM;
 // FAST instantiates only walk_fast (+ its exact fallback and the dense walk for
 // unsafe rays), so its register allocation is not the union of every walk.
 #ifndef VMB_WALK_MINB
-#define VMB_WALK_MINB 8
+#define VMB_WALK_MINB (1024 / VMB_WALK_THREADS)  // 32 warps per SM: 64 registers
 #endif
 // Fused render_forward (vmb_march_render_field): for an analytic field the
 // compositing of rendering.cpp:47-58 runs over exactly the kept samples, in order,
@@ -943,7 +946,7 @@ struct FwdOut {
 // FAST instantiates only walk_fast (+ its exact fallback and the dense walk for
 // unsafe rays), so its register allocation is not the union of every walk.
 template <typename RT, bool FAST, typename AT, bool FWD, bool VOX, bool ATAB = false, bool ATTR = false>
-__global__ void __launch_bounds__(128, VMB_WALK_MINB) k_march_walk(
+__global__ void __launch_bounds__(kAccStride, VMB_WALK_MINB) k_march_walk(
     MarchParams P, const RT* __restrict__ orig, const RT* __restrict__ dirs, uint64_t n_rays,
     uint32_t* __restrict__ counts, uint32_t* __restrict__ kept_idx, unsigned int* chunk_counter,
     uint64_t n_chunks, unsigned long long* emitted, DevError* err, FwdOut<AT> fo,
@@ -1955,9 +1958,9 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
     auto launch_walk = [&](auto kernel, auto* o, auto* d, auto fo) {
         int per_sm = 0;
         const size_t dyn = size_t(P.atab_n) * 2 * sizeof(double);  // read only by ATAB kernels: alpha, midpoint
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, dyn);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kAccStride, dyn);
         if (per_sm < 1) per_sm = 4;
-        kernel<<<ctx->num_sms * per_sm, 128, dyn, ctx->stream>>>(
+        kernel<<<ctx->num_sms * per_sm, kAccStride, dyn, ctx->stream>>>(
             P, o, d, n, out->d_counts, kept_idx, counters, n_chunks, emitted, ctx->d_err, fo, chunk_tot, kept_attr);
     };
     auto walk_vox = [&](auto* o, auto* d, auto VOXC) {
