@@ -1451,7 +1451,7 @@ __global__ void k_march_fixup(MarchParams P, const RT* __restrict__ orig, const 
 // 10.27 -> 9.86 ms (8 CTAs / 64 registers: 10.10 ms; later A/B at 9.30 ms: 5 CTAs
 // 9.71, 7 CTAs 9.40).
 #ifndef VMB_MARCH_MINB
-#define VMB_MARCH_MINB 6
+#define VMB_MARCH_MINB 8  // 64 registers; config 3 (cascade, two-pass walk): 8.97 ms vs 9.04 (6), 9.58 (4)
 #endif
 #define VMB_MARCH_LB __launch_bounds__(128, VMB_MARCH_MINB)
 template <typename RT, int MODE>
