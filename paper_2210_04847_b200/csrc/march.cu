@@ -68,6 +68,9 @@ __host__ __device__ constexpr bool mrsm(int m) { return (m & RSMM) != 0; }
 // in its own k_march instantiations so the other walks keep their register budget
 constexpr int EXTM = 32;
 __host__ __device__ constexpr bool mext(int m) { return (m & EXTM) != 0; }
+// bit 7 (FILL, k_march): the slab pass of a long-ray walk (k_march's comment)
+constexpr int SLABM = 128;
+__host__ __device__ constexpr bool mslab(int m) { return (m & SLABM) != 0; }
 // bit 6 (BUFFER_FWD): each kept sample's rgb/sigma, rounded to the attribute dtype,
 // also go to the walk's scratch beside its lattice index, so the expansion copies
 // them instead of evaluating a non-constant field a second time (Sink::attr)
@@ -1461,32 +1464,58 @@ __global__ void VMB_MARCH_LB k_march(MarchParams P, const RT* __restrict__ orig,
                                                const uint32_t* __restrict__ offsets,
                                                double* __restrict__ ts, double* __restrict__ te,
                                                uint32_t* __restrict__ idx, uint64_t cap,
-                                               unsigned long long* emitted, DevError* err) {
+                                               unsigned long long* emitted, DevError* err, uint32_t slab_cap = 0) {
+    // SLABM (FILL): one pass instead of count + fill for long-ray walks — each ray
+    // writes its first slab_cap kept intervals to its own slab [r slab_cap, (r + 1)
+    // slab_cap) of ts/te/idx and its kept count; k_slab_gather packs them after the
+    // scan. FILL with slab_cap > 0: the packed fill of the rays above slab_cap only.
+    constexpr bool SLAB = mslab(MODE);
     unsigned long long emit_local = 0;
     __shared__ double stg[mbase(MODE) == FILL ? 8 * kStgStride : 1];
     const bool vec = ((reinterpret_cast<uintptr_t>(ts) | reinterpret_cast<uintptr_t>(te) |
                        reinterpret_cast<uintptr_t>(idx)) & 15) == 0;
     for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rays;
          r += uint64_t(gridDim.x) * blockDim.x) {
+        if (mbase(MODE) == FILL && !SLAB && slab_cap && counts[r] <= slab_cap) continue;
         Sink s;
         s.ray = r;
         if (mbase(MODE) == FILL) {
             s.ts = ts;
             s.te = te;
             s.idx = idx;
-            s.base = offsets[r];
-            s.cap = cap;
+            s.base = SLAB ? r * slab_cap : offsets[r];
+            s.cap = SLAB ? (r + 1) * slab_cap : cap;
             s.stg = stg + threadIdx.x;
             s.vec = vec;
         }
-        walk<MODE>(P, s, orig, dirs, r, err);
+        walk<MODE & ~SLABM>(P, s, orig, dirs, r, err);
         if (mbase(MODE) == FILL) s.flush_tail();
-        if (mbase(MODE) == COUNT) counts[r] = s.n_kept;
+        if (mbase(MODE) == COUNT || SLAB) counts[r] = s.n_kept;
         emit_local += s.n_cand;
     }
-    if (mbase(MODE) == COUNT && emitted) {
+    if ((mbase(MODE) == COUNT || SLAB) && emitted) {
         for (int off = 16; off > 0; off >>= 1) emit_local += __shfl_xor_sync(0xffffffffu, emit_local, off);
         if ((threadIdx.x & 31) == 0 && emit_local) atomicAdd(emitted, emit_local);
+    }
+}
+
+// The slab pass's packing: warp per ray, its min(count, slab_cap) intervals copied
+// coalesced from the slab to the packed arrays at the ray's offset, with its index.
+__global__ void k_slab_gather(const uint32_t* __restrict__ counts, const uint32_t* __restrict__ offsets,
+                              uint64_t n_rays, uint32_t slab_cap, const double* __restrict__ sts,
+                              const double* __restrict__ ste, double* __restrict__ ts, double* __restrict__ te,
+                              uint32_t* __restrict__ idx, uint64_t cap) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t r = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < n_rays;
+         r += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const uint32_t n = min(__ldg(counts + r), slab_cap);
+        const uint64_t o = __ldg(offsets + r), src = r * slab_cap;
+        for (uint32_t k = uint32_t(lane); k < n; k += 32)
+            if (o + k < cap) {
+                ts[o + k] = __ldg(sts + src + k);
+                te[o + k] = __ldg(ste + src + k);
+                idx[o + k] = uint32_t(r);
+            }
     }
 }
 
@@ -1630,26 +1659,70 @@ int march_params(const vmb_grid* g, const vmb_rays* rays, const vmb_march_config
     return VMB_OK;
 }
 
+// The slab pass of a two-pass walk (k_march slab_mode): per-ray capacity and buffers
+struct Slab {
+    uint32_t cap = 0;  // 0: count + fill
+    int mode = 0;      // 1: the slab pass (SLABM), 2: the fill of the rays above cap
+    double* ts = nullptr;
+    double* te = nullptr;
+    uint32_t* idx = nullptr;
+};
+
 template <int MODE>
 void launch_march(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, uint32_t* counts,
-                  const uint32_t* offsets, vmb_samples* out, unsigned long long* emitted);
+                  const uint32_t* offsets, vmb_samples* out, unsigned long long* emitted, Slab sl = Slab{});
 
 template <int MODE>
 void launch_march_rt(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, uint32_t* counts,
-                     const uint32_t* offsets, vmb_samples* out, unsigned long long* emitted) {
+                     const uint32_t* offsets, vmb_samples* out, unsigned long long* emitted, Slab sl) {
     int blocks = grid_blocks(ctx, rays->n_rays, 128, 16);
+    double* ts = sl.mode == 1 ? sl.ts : out ? out->d_t_starts : nullptr;
+    double* te = sl.mode == 1 ? sl.te : out ? out->d_t_ends : nullptr;
+    uint32_t* ix = sl.mode == 1 ? sl.idx : out ? out->d_ray_indices : nullptr;
+    const uint64_t cap = out ? out->capacity : 0;
     if (rays->dtype == VMB_F32)
         k_march<float, MODE><<<blocks, 128, 0, ctx->stream>>>(
             P, static_cast<const float*>(rays->d_origins), static_cast<const float*>(rays->d_directions),
-            rays->n_rays, counts, offsets, out ? out->d_t_starts : nullptr,
-            out ? out->d_t_ends : nullptr, out ? out->d_ray_indices : nullptr, out ? out->capacity : 0,
-            emitted, ctx->d_err);
+            rays->n_rays, counts, offsets, ts, te, ix, cap, emitted, ctx->d_err, sl.cap);
     else
         k_march<double, MODE><<<blocks, 128, 0, ctx->stream>>>(
-            P, static_cast<const double*>(rays->d_origins),
-            static_cast<const double*>(rays->d_directions), rays->n_rays, counts, offsets,
-            out ? out->d_t_starts : nullptr, out ? out->d_t_ends : nullptr,
-            out ? out->d_ray_indices : nullptr, out ? out->capacity : 0, emitted, ctx->d_err);
+            P, static_cast<const double*>(rays->d_origins), static_cast<const double*>(rays->d_directions),
+            rays->n_rays, counts, offsets, ts, te, ix, cap, emitted, ctx->d_err, sl.cap);
+}
+
+// Long-ray walks (accumulated t: cascades, cone stepping, growth) pack in one walk:
+// the slab pass, the scan, k_slab_gather, and a fill of the rays above the slab
+// capacity only, instead of a count walk and a fill walk. Up to 256 intervals per
+// ray and 4 GiB of slab; otherwise (or for short-ray walks) count + fill.
+Slab make_slab(vmb_ctx* ctx, const MarchParams& P, uint64_t n_rays) {
+#ifndef VMB_SLAB
+#define VMB_SLAB 1
+#endif
+    Slab sl;
+    if (!VMB_SLAB || !(P.accum || P.grows) || n_rays == 0) return sl;
+    const uint64_t budget = 4ull << 30;
+    uint64_t cap = budget / (n_rays * 16);
+    cap = cap > 256 ? 256 : cap & ~uint64_t(3);
+    if (cap < 64) return sl;
+    auto* b = static_cast<double*>(scratch(ctx, SCRATCH_SLAB, n_rays * cap * (2 * sizeof(double) + 4)));
+    if (!b) {
+        cudaGetLastError();  // fall back to count + fill
+        return sl;
+    }
+    sl.cap = uint32_t(cap);
+    sl.ts = b;
+    sl.te = b + n_rays * cap;
+    sl.idx = reinterpret_cast<uint32_t*>(b + 2 * n_rays * cap);
+    return sl;
+}
+
+void slab_pack(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out, Slab sl) {
+    const int blocks = grid_blocks(ctx, rays->n_rays * 32, 256, 8);
+    k_slab_gather<<<blocks, 256, 0, ctx->stream>>>(out->d_counts, out->d_offsets, rays->n_rays, sl.cap, sl.ts,
+                                                   sl.te, out->d_t_starts, out->d_t_ends, out->d_ray_indices,
+                                                   out->capacity);
+    sl.mode = 2;
+    launch_march<FILL>(ctx, P, rays, out->d_counts, out->d_offsets, out, nullptr, sl);
 }
 
 // walk_skip reads the grid's coarse bits: the paths that may take it build them first
@@ -1659,16 +1732,27 @@ int ensure_skip_structures(vmb_ctx* ctx, const MarchParams& P) {
 
 template <int MODE>
 void launch_march(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, uint32_t* counts,
-                  const uint32_t* offsets, vmb_samples* out, unsigned long long* emitted) {
+                  const uint32_t* offsets, vmb_samples* out, unsigned long long* emitted, Slab sl) {
     if (ensure_skip_structures(ctx, P)) return;
+    if (MODE == FILL && sl.mode == 1) {  // the slab pass: long-ray (accumulated-t / growth) walks only
+        if (P.accum && P.f.kind == VMB_FIELD_VOXEL)
+            launch_march_rt<FILL | SLABM | VOXM | EXTM>(ctx, P, rays, counts, offsets, out, emitted, sl);
+        else if (P.accum)
+            launch_march_rt<FILL | SLABM | EXTM>(ctx, P, rays, counts, offsets, out, emitted, sl);
+        else if (P.f.kind == VMB_FIELD_VOXEL)
+            launch_march_rt<FILL | SLABM | VOXM>(ctx, P, rays, counts, offsets, out, emitted, sl);
+        else
+            launch_march_rt<FILL | SLABM>(ctx, P, rays, counts, offsets, out, emitted, sl);
+        return;
+    }
     if (P.accum && P.f.kind == VMB_FIELD_VOXEL)
-        launch_march_rt<MODE | VOXM | EXTM>(ctx, P, rays, counts, offsets, out, emitted);
+        launch_march_rt<MODE | VOXM | EXTM>(ctx, P, rays, counts, offsets, out, emitted, sl);
     else if (P.accum)
-        launch_march_rt<MODE | EXTM>(ctx, P, rays, counts, offsets, out, emitted);
+        launch_march_rt<MODE | EXTM>(ctx, P, rays, counts, offsets, out, emitted, sl);
     else if (P.f.kind == VMB_FIELD_VOXEL)
-        launch_march_rt<MODE | VOXM>(ctx, P, rays, counts, offsets, out, emitted);
+        launch_march_rt<MODE | VOXM>(ctx, P, rays, counts, offsets, out, emitted, sl);
     else
-        launch_march_rt<MODE>(ctx, P, rays, counts, offsets, out, emitted);
+        launch_march_rt<MODE>(ctx, P, rays, counts, offsets, out, emitted, sl);
 }
 
 std::string march_error_text(const DevError& e) {
@@ -2044,7 +2128,12 @@ int march_packed(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
         if (total > out->capacity) return fail(VMB_CAPACITY, "march: sample capacity too small");
         return VMB_OK;
     }
-    if (rays->n_rays) launch_march<COUNT>(ctx, P, rays, out->d_counts, nullptr, nullptr, stats ? ctx->d_u64 + 1 : nullptr);
+    Slab sl = make_slab(ctx, P, rays->n_rays);
+    sl.mode = 1;
+    if (sl.cap)
+        launch_march<FILL>(ctx, P, rays, out->d_counts, nullptr, out, stats ? ctx->d_u64 + 1 : nullptr, sl);
+    else if (rays->n_rays)
+        launch_march<COUNT>(ctx, P, rays, out->d_counts, nullptr, nullptr, stats ? ctx->d_u64 + 1 : nullptr);
     rc = scan_counts(ctx, out->d_counts, rays->n_rays, out->d_offsets, ctx->d_u64);
     if (rc) return rc;
     cudaMemcpyAsync(ctx->h_u64, ctx->d_u64, 16, cudaMemcpyDeviceToHost, ctx->stream);
@@ -2058,7 +2147,10 @@ int march_packed(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
     }
     if (total > 0xffffffffull) return fail(VMB_INVALID_ARGUMENT, "pack: sample count exceeds 32-bit index range");
     if (total > out->capacity) return fail(VMB_CAPACITY, "march: sample capacity too small");
-    if (total) launch_march<FILL>(ctx, P, rays, out->d_counts, out->d_offsets, out, nullptr);
+    if (total && sl.cap)
+        slab_pack(ctx, P, rays, out, sl);
+    else if (total)
+        launch_march<FILL>(ctx, P, rays, out->d_counts, out->d_offsets, out, nullptr);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "march fill");
     if (sr.on && sr.fwd && total) {  // long-ray batches: one shade + composite pass
@@ -2174,11 +2266,19 @@ int vmb_march_field_async(vmb_ctx* ctx, const vmb_grid* g, const vmb_rays* rays,
     if (use_fused(P))
         return launch_fused(ctx, P, rays, out, reinterpret_cast<unsigned long long*>(d_n), nullptr,
                             ShadeReq{});
-    if (rays->n_rays) launch_march<COUNT>(ctx, P, rays, out->d_counts, nullptr, nullptr, nullptr);
+    Slab sl = make_slab(ctx, P, rays->n_rays);
+    sl.mode = 1;
+    if (sl.cap)
+        launch_march<FILL>(ctx, P, rays, out->d_counts, nullptr, out, nullptr, sl);
+    else if (rays->n_rays)
+        launch_march<COUNT>(ctx, P, rays, out->d_counts, nullptr, nullptr, nullptr);
     rc = scan_counts(ctx, out->d_counts, rays->n_rays, out->d_offsets,
                      reinterpret_cast<unsigned long long*>(d_n));
     if (rc) return rc;
-    if (rays->n_rays) launch_march<FILL>(ctx, P, rays, out->d_counts, out->d_offsets, out, nullptr);
+    if (rays->n_rays && sl.cap)
+        slab_pack(ctx, P, rays, out, sl);
+    else if (rays->n_rays)
+        launch_march<FILL>(ctx, P, rays, out->d_counts, out->d_offsets, out, nullptr);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? VMB_OK : cuda_fail(e, "march async");
 }

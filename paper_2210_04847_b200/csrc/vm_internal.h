@@ -51,8 +51,8 @@ struct vmb_ctx {
     vmb::DevError* h_err = nullptr;     // pinned mirror
     unsigned long long* d_u64 = nullptr;  // 8 device scalars (totals, counters)
     unsigned long long* h_u64 = nullptr;  // pinned mirror
-    void* scratch[6] = {};          // per-purpose growable device scratch (see scratch(), SCRATCH_SLOTS)
-    size_t scratch_bytes[6] = {};
+    void* scratch[7] = {};          // per-purpose growable device scratch (see scratch(), SCRATCH_SLOTS)
+    size_t scratch_bytes[7] = {};
     cudaEvent_t events[32] = {};
     // NCCL (dlopen'ed lazily; see comm.cpp)
     void* nccl_comm = nullptr;
@@ -98,7 +98,7 @@ int cuda_fail(cudaError_t e, const char* where);
 // Growable device scratch, one buffer per slot so nested users never alias:
 // slot 0 = scan tile sums, 1 = march / candidates temporaries, 2 = grid update,
 // 3 = validation / misc. Growing synchronizes the stream before freeing.
-enum { SCRATCH_SCAN = 0, SCRATCH_MARCH = 1, SCRATCH_GRID = 2, SCRATCH_MISC = 3, SCRATCH_VOXGRAD = 4, SCRATCH_RENDER = 5, SCRATCH_SLOTS = 6 };
+enum { SCRATCH_SCAN = 0, SCRATCH_MARCH = 1, SCRATCH_GRID = 2, SCRATCH_MISC = 3, SCRATCH_VOXGRAD = 4, SCRATCH_RENDER = 5, SCRATCH_SLAB = 6, SCRATCH_SLOTS = 7 };
 static_assert(sizeof(vmb_ctx::scratch) / sizeof(void*) == SCRATCH_SLOTS, "one scratch buffer per slot");
 void* scratch(vmb_ctx* ctx, int slot, size_t bytes);
 inline int grid_blocks(vmb_ctx* ctx, uint64_t work, int threads, int per_sm = 8) {

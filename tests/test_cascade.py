@@ -152,14 +152,14 @@ class _DevRays:
         self.rays = api.device_rays(dev, *self.keep, near, far)
 
 
-def _march(dev, cas, o, d, near, far, field, cfg, cone=None, max_step=1e10):
+def _march(dev, cas, o, d, near, far, field, cfg, cone=None, max_step=1e10, per_ray=64):
     from paper_2210_04847_b200 import api
     from paper_2210_04847_b200._lib import MarchConfig, MarchStats
     rays = _DevRays(dev, o, d, near, far)
     st = MarchStats()
     c = MarchConfig(cfg.step_size, cfg.early_stop_eps, cfg.alpha_thre, cfg.max_samples_per_ray,
                     cfg.unbounded_step_growth)
-    out = api.DevicePacked.allocate(dev, len(o), 64 * len(o))
+    out = api.DevicePacked.allocate(dev, len(o), per_ray * len(o))
     api.march_cascade_device(dev, cas, rays.rays, _api_field(field), c, out, cone, max_step, st)
     return out.to_host(), st
 
@@ -271,3 +271,22 @@ def test_cascade_errors(dev):
         api.march_cascade_device(dev, bad, rays.rays, _api_field(BOX), MarchConfig(1e-2, 1e-4, 1e-2, 64, 1.0),
                                  out, 0.01)
     assert Contraction is not None
+
+
+@pytest.mark.gpu
+def test_device_cascade_long_rays_past_the_slab_match_port(dev):
+    """Long-ray walks pack in one walk (a per-ray slab of 256 intervals, then a fill of
+    the rays above it): rays with no transmittance cut through a dense field keep
+    hundreds of samples each, so both the slab gather and the overflow fill run."""
+    port = Oracle("port")
+    dense = O.Field.box((-9.0, -9.0, -9.0), (9.0, 9.0, 1.0), sigma=20.0, rgb=(0.5, 0.5, 0.5))
+    pgrids = port_cascade(port, 32, 3, dense, SEEDS)
+    cas = _device_cascade(dev, 32, 3, _api_field(dense), SEEDS)
+    o, d = rays_inside(1024, 21)
+    cfg = O.MarchConfig(1.6914558667664816e-3, 0.0, 1e-4, 100000, 1.0)
+    want = port.march_cascade(o, d, 0.01, 100.0, pgrids[0], pgrids[1:], dense, cfg, 1.0 / 256, 0.02)
+    got, st = _march(dev, cas, o, d, 0.01, 100.0, dense, cfg, 1.0 / 256, 0.02, per_ray=int(want.counts.max()) + 1)
+    assert want.counts.max() > 256 and (want.counts <= 256).any()
+    for k in ("offsets", "counts", "t_starts", "t_ends", "ray_indices"):
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+    assert st.samples_emitted == want.samples_emitted and st.samples_kept == want.samples_kept
