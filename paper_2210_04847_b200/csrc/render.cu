@@ -555,7 +555,7 @@ __device__ void bwd_long_ray(S& sm, int lane, uint32_t s0, uint32_t s1, const Up
 
 // The rays k_backward_hy set aside (longer than a tile), one warp each.
 template <typename T>
-__global__ void __launch_bounds__(kWarps * 32) k_backward_long(
+__global__ void __launch_bounds__(kWarps * 32, 32 / kWarps) k_backward_long(
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ counts, uint64_t n_samples,
     const double* __restrict__ ts, const double* __restrict__ te, const T* __restrict__ rgb,
     const T* __restrict__ sig, const T* __restrict__ dc, const T* __restrict__ dop,
@@ -565,14 +565,36 @@ __global__ void __launch_bounds__(kWarps * 32) k_backward_long(
     const int lane = threadIdx.x & 31;
     BwdSmem<T>& sm = smem[threadIdx.x >> 5];
     const unsigned int n = *n_long;
-    for (uint64_t k = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; k < n;
-         k += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
-        const uint64_t r = long_rays[k];
-        const uint64_t ns = n_samples < 0xffffffffull ? n_samples : 0xffffffffull;
-        const uint64_t o = offsets[r], e = o + counts[r];
-        const Up u = load_up(dc, dop, ddep, r, true);
+    const uint64_t ns = n_samples < 0xffffffffull ? n_samples : 0xffffffffull;
+    const uint64_t stride = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    // Software pipeline over the warp's rays: the next ray's offset, count and upstream
+    // gradients, and the index of the one after, are in flight while a ray is processed
+    // (its chain was list -> offsets -> samples, three dependent global round trips).
+    uint64_t k = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    struct Meta {
+        uint32_t o = 0, c = 0;
+        T u[5] = {};
+    };
+    auto ray_at = [&](uint64_t q) { return q < n ? __ldg(long_rays + q) : 0u; };
+    auto fetch = [&](uint64_t q, uint32_t r, Meta& m) {
+        if (q >= n) return;
+        m.o = __ldg(offsets + r), m.c = __ldg(counts + r);
+        m.u[0] = dc[3 * uint64_t(r)], m.u[1] = dc[3 * uint64_t(r) + 1], m.u[2] = dc[3 * uint64_t(r) + 2];
+        m.u[3] = dop[r], m.u[4] = ddep[r];
+    };
+    Meta cur;
+    fetch(k, ray_at(k), cur);
+    uint32_t r_next = ray_at(k + stride);
+    for (; k < n; k += stride) {
+        const uint32_t r_after = ray_at(k + 2 * stride);
+        Meta nxt;
+        fetch(k + stride, r_next, nxt);
+        const uint64_t o = cur.o, e = o + cur.c;
+        const Up u{double(cur.u[0]), double(cur.u[1]), double(cur.u[2]), double(cur.u[3]), double(cur.u[4])};
         bwd_long_ray(sm, lane, uint32_t(o < ns ? o : ns), uint32_t(e < ns ? e : ns), u,
                      ts, te, rgb, sig, g_rgb, g_sig);
+        cur = nxt;
+        r_next = r_after;
     }
 }
 
