@@ -94,7 +94,7 @@ def parse():
     ap.add_argument("--chunks", type=int, default=2,
                     help="resident step: the batch is marched as this many sub-batches (2x2 measured best, r1)")
     ap.add_argument("--e2e-streams", type=int, default=2)
-    ap.add_argument("--e2e-chunks", type=int, default=4)  # 2x4 measured best on B200 (r1)
+    ap.add_argument("--e2e-chunks", type=int, default=8)  # 2x8 best in the r2 sweep (profiles/r2/ab/e2e_*)
     ap.add_argument("--e2e-async", type=int, default=1, help="async march (no per-chunk host sync)")
     # device-generated rays leave PCIe to the gradients: more, smaller chunks pay (4x8 best on B200, r1)
     ap.add_argument("--e2e-camera-streams", type=int, default=4)
@@ -323,52 +323,71 @@ def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev
     host_in = [o32, d32] + list(ups)            # per-ray: 12, 12, 12, 4, 4 bytes
     widths = [3, 3, 3, 1, 1]
     first_in = 2 if cam is not None else 0      # camera mode: rays made on the device
-    pinned = []
-    for arr in host_in:
-        p = C.c_void_p()
-        check(L.vmb_host_alloc(arr.nbytes, C.byref(p)))
-        C.memmove(p.value, arr.ctypes.data, arr.nbytes)
-        pinned.append(p)
-    out_w = [3, 1, 1]
-    p_out = []
-    for w in out_w:
-        p = C.c_void_p()
-        check(L.vmb_host_alloc(N * w * 4, C.byref(p)))
-        p_out.append(p)
+    # The host keeps each chunk's inputs as one block [origins | directions | d_color |
+    # d_opacity | d_depth] (camera mode: the three gradients only) and receives its
+    # outputs as one block [color | opacity | depth]: one H2D and one D2H copy per
+    # chunk instead of five and three (the layout of the user's buffers; filled before
+    # the timed region).
+    in_w, out_w = widths[first_in:], [3, 1, 1]
+    win, wout = sum(in_w), sum(out_w)           # floats per ray
+    p_in, p_out = C.c_void_p(), C.c_void_p()
+    check(L.vmb_host_alloc(N * win * 4, C.byref(p_in)))
+    check(L.vmb_host_alloc(N * wout * 4, C.byref(p_out)))
+    h_in = np.ctypeslib.as_array((C.c_float * (N * win)).from_address(p_in.value))
+    for b, e in bounds:
+        at = b * win
+        for arr, w in zip(host_in[first_in:], in_w):
+            h_in[at:at + (e - b) * w] = arr.reshape(-1)[b * w:e * w]
+            at += (e - b) * w
     ctxs = [dev] + [api.Device(dist.local) for _ in range(n_ctx - 1)]
     ccap = cap  # the full batch's capacity bounds any chunk's sample count
     bufs = []
     for cx in ctxs:
-        ins = [cx.empty(cmax * w, np.float32) for w in widths]
-        outs = [cx.empty(cmax * w, np.float32) for w in out_w]
-        bufs.append(dict(ins=ins, outs=outs, packed=api.DevicePacked.allocate(cx, cmax, ccap),
+        d_in = cx.empty(cmax * win, np.float32)
+        d_out = cx.empty(cmax * wout, np.float32)
+        bufs.append(dict(d_in=d_in, d_out=d_out, o=cx.empty(cmax * 3, np.float32), d=cx.empty(cmax * 3, np.float32),
+                         packed=api.DevicePacked.allocate(cx, cmax, ccap),
                          n_dev=cx.zeros(n_chunk, np.uint64),
                          rgb=cx.empty(ccap * 3, np.float32), sig=cx.empty(ccap, np.float32),
                          grgb=cx.empty(ccap * 3, np.float32), gsig=cx.empty(ccap, np.float32)))
 
+    class Ptr:  # a device pointer with the DeviceArray interface the api needs
+        def __init__(self, ptr):
+            self.ptr = ptr
+
     def run_chunk(ci, b, e):
         cx, bf = ctxs[ci], bufs[ci]
         n = e - b
-        for arr, p, w in list(zip(bf["ins"], pinned, widths))[first_in:]:
-            check(L.vmb_memcpy_h2d(cx.h, arr.ptr, p.value + b * w * 4, n * w * 4))
-        rays = Rays(bf["ins"][0].ptr, bf["ins"][1].ptr, VMB_F32, 0, n, 0.2, 1.0)
+        check(L.vmb_memcpy_h2d(cx.h, bf["d_in"].ptr, p_in.value + b * win * 4, n * win * 4))
+        views, at = [], bf["d_in"].ptr
+        for w in in_w:  # the block's arrays on the device
+            views.append(Ptr(at))
+            at += n * w * 4
+        if cam is None:
+            o_ptr, d_ptr, ups_dev = views[0].ptr, views[1].ptr, views[2:]
+        else:
+            o_ptr, d_ptr, ups_dev = bf["o"].ptr, bf["d"].ptr, views
+        outs, at = [], bf["d_out"].ptr
+        for w in out_w:
+            outs.append(Ptr(at))
+            at += n * w * 4
+        rays = Rays(o_ptr, d_ptr, VMB_F32, 0, n, 0.2, 1.0)
         if cam is not None:
-            check(L.vmb_generate_rays_range(cx.h, C.byref(cam), 0.2, 1.0, VMB_F32, pixel0 + b, n, bf["ins"][0].ptr,
-                                            bf["ins"][1].ptr, C.byref(rays)))
+            check(L.vmb_generate_rays_range(cx.h, C.byref(cam), 0.2, 1.0, VMB_F32, pixel0 + b, n, o_ptr, d_ptr,
+                                            C.byref(rays)))
         pk = bf["packed"]
         if args.e2e_async:  # no host round trip: the sample total stays on the device
             smp = pk.samples_struct()
             check(L.vmb_march_render_field_async(cx.h, grid.h, C.byref(rays), C.byref(field), C.byref(cfg),
-                                                 C.byref(smp), bf["rgb"].ptr, bf["sig"].ptr, bf["outs"][0].ptr,
-                                                 bf["outs"][1].ptr, bf["outs"][2].ptr, VMB_F32, 0.0,
+                                                 C.byref(smp), bf["rgb"].ptr, bf["sig"].ptr, outs[0].ptr,
+                                                 outs[1].ptr, outs[2].ptr, VMB_F32, 0.0,
                                                  bf["n_dev"].ptr + 8 * chunk_id[0]))
             pk.n_samples = pk.capacity
         else:
-            api.march_render_device(cx, grid, rays, field, cfg, pk, bf["rgb"], bf["sig"], *bf["outs"])
-        api.render_backward_device(cx, pk, bf["rgb"], bf["sig"], *bf["ins"][2:], bf["grgb"], bf["gsig"])
+            api.march_render_device(cx, grid, rays, field, cfg, pk, bf["rgb"], bf["sig"], *outs)
+        api.render_backward_device(cx, pk, bf["rgb"], bf["sig"], *ups_dev, bf["grgb"], bf["gsig"])
         d2h = L.vmb_memcpy_d2h_async if args.e2e_async else L.vmb_memcpy_d2h  # async: synced at the end
-        for arr, p, w in zip(bf["outs"], p_out, out_w):
-            check(d2h(cx.h, p.value + b * w * 4, arr.ptr, n * w * 4))
+        check(d2h(cx.h, p_out.value + b * wout * 4, bf["d_out"].ptr, n * wout * 4))
 
     def worker(ci, steps, err):
         try:
@@ -416,11 +435,16 @@ def e2e_pipeline(args, dist, api, dev, grid, field, cfg, o32, d32, ups, cap, dev
             assert int(bf["n_dev"].numpy().max()) <= ccap, "e2e chunk exceeded its sample capacity"
     # the pipelined result must equal the resident single-stream step's
     same = True
-    for p, w, darr in zip(p_out, out_w, dev_out):
-        h = np.empty(N * w, np.float32)
-        C.memmove(h.ctypes.data, p.value, h.nbytes)
-        same &= bool(np.array_equal(h, darr.numpy(N * w)))
-    for p in pinned + p_out:
+    h_out = np.ctypeslib.as_array((C.c_float * (N * wout)).from_address(p_out.value)).copy()
+    got = [[], [], []]
+    for b, e in bounds:
+        at = b * wout
+        for j, w in enumerate(out_w):
+            got[j].append(h_out[at:at + (e - b) * w])
+            at += (e - b) * w
+    for parts, w, darr in zip(got, out_w, dev_out):
+        same &= bool(np.array_equal(np.concatenate(parts), darr.numpy(N * w)))
+    for p in (p_in, p_out):
         L.vmb_host_free(p)
     for cx in ctxs[1:]:
         cx.sync()
