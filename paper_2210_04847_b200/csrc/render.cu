@@ -35,7 +35,10 @@ namespace {
 constexpr int kWarps = VMB_RENDER_WARPS;  // threads per CTA / 32
 
 template <typename T> struct Tile;
-template <> struct Tile<float> { static constexpr int CH = 128; };
+#ifndef VMB_TILE_F32
+#define VMB_TILE_F32 128  // r2 A/B: 192 and 256 slower (config 5 0.706 / 0.796 ms), config 2 no better
+#endif
+template <> struct Tile<float> { static constexpr int CH = VMB_TILE_F32; };
 template <> struct Tile<double> { static constexpr int CH = 64; };
 
 template <typename T>
