@@ -629,3 +629,38 @@ def test_distance_map_is_exact_capped_chebyshev(dev, res, density):
         assert list(box) == [x.min(), y.min(), z.min(), x.max() + 1, y.max() + 1, z.max() + 1]
     else:
         assert all(box[a] >= box[3 + a] for a in range(3))
+
+
+def test_render_backward_unaligned_buffers_match_aligned(dev, orc):
+    """k_backward_hy stages groups with 16-byte bulk copies when every buffer is 16-byte
+    aligned; buffers that are not (views into larger arrays at odd element offsets)
+    take the per-element cp.async staging. Both agree bit for bit, and with the
+    reference."""
+    import ctypes as C
+    from paper_2210_04847_b200._lib import VMB_F32, PackedView, check
+    rng = np.random.default_rng(77)
+    p, rgb, sig = _instance(rng, 3000, 40)
+    n, s = p.n_rays, p.n_samples
+    dc, do, dd = (rng.uniform(-1, 1, (n, 3)).astype(np.float32), rng.uniform(-1, 1, n).astype(np.float32),
+                  rng.uniform(-1, 1, n).astype(np.float32))
+    r32, s32 = rgb.astype(np.float32), sig.astype(np.float32)
+
+    def run(shift):  # shift = elements of padding in front of every per-sample array
+        pad = lambda a: np.concatenate([np.zeros(shift * (a.size // max(len(a), 1) if a.ndim > 1 else 1), a.dtype),
+                                        a.reshape(-1)])  # noqa: E731
+        off, cnt = dev.upload(p.offsets.astype(np.uint32)), dev.upload(p.counts.astype(np.uint32))
+        ts, te = dev.upload(pad(p.t_starts)), dev.upload(pad(p.t_ends))
+        dr, ds = dev.upload(pad(r32)), dev.upload(pad(s32))
+        ups = [dev.upload(x.reshape(-1)) for x in (dc, do, dd)]
+        gr, gs = dev.zeros((s + shift) * 3, np.float32), dev.zeros(s + shift, np.float32)
+        v = PackedView(off.ptr, cnt.ptr, n, ts.ptr + 8 * shift, te.ptr + 8 * shift, s)
+        check(dev.lib.vmb_render_backward(dev.h, C.byref(v), dr.ptr + 12 * shift, ds.ptr + 4 * shift,
+                                          ups[0].ptr, ups[1].ptr, ups[2].ptr, gr.ptr + 12 * shift,
+                                          gs.ptr + 4 * shift, VMB_F32))
+        return gr.numpy((s + shift) * 3)[3 * shift:].reshape(s, 3), gs.numpy(s + shift)[shift:]
+
+    a_rgb, a_sig = run(0)
+    u_rgb, u_sig = run(1)
+    assert np.array_equal(a_rgb, u_rgb) and np.array_equal(a_sig, u_sig)
+    ref_r, ref_s = orc.render_backward(p, r32.astype(np.float64), s32.astype(np.float64), dc, do, dd)
+    close(a_rgb, ref_r), close(a_sig, ref_s)
