@@ -1069,17 +1069,23 @@ constexpr int kExpandWarps = VMB_EXPAND_WARPS;
 #endif
 constexpr int kExpandUnroll = VMB_EXPAND_UNROLL;  // rounds per iteration of the constant-shading path
 // per warp: two kept-index row buffers, the owner map, and the rows' two mbarriers
-constexpr size_t kExpandSmem =
-    size_t(kExpandWarps) * (kWalkCap * 32 * (2 * sizeof(uint32_t) + sizeof(uint16_t)) + 2 * sizeof(uint64_t));
+__host__ __device__ constexpr size_t expand_smem_of(int warps) {
+    return size_t(warps) * (kWalkCap * 32 * (2 * sizeof(uint32_t) + sizeof(uint16_t)) + 2 * sizeof(uint64_t));
+}
+constexpr size_t kExpandSmem = expand_smem_of(kExpandWarps);
+// Warps per expansion CTA: the variants that evaluate the field per sample (rays by
+// shuffles, e.g. the Checker) are compute-heavier and run 16 (r2: Checker step
+// 1.44 -> 1.37 ms); constant / copied attributes run kExpandWarps (12).
+__host__ __device__ constexpr int expand_warps(bool shade, bool cst, bool attr) { return shade && !cst && !attr ? 16 : kExpandWarps; }
 constexpr uint32_t kMaxAlphaTable = 1024;  // the fused backward's constant-density alpha table
 
 
 // (an explicit minBlocksPerSM, even 1, changes the register allocation and costs
 // ~25 us per step here: leave it unset unless tuning with -DVMB_EXPAND_MINB)
 #ifdef VMB_EXPAND_MINB
-#define VMB_EXPAND_BOUNDS __launch_bounds__(32 * kExpandWarps, VMB_EXPAND_MINB)
+#define VMB_EXPAND_BOUNDS __launch_bounds__(32 * expand_warps(SHADE, CONST, ATTR), VMB_EXPAND_MINB)
 #else
-#define VMB_EXPAND_BOUNDS __launch_bounds__(32 * kExpandWarps)
+#define VMB_EXPAND_BOUNDS __launch_bounds__(32 * expand_warps(SHADE, CONST, ATTR))
 #endif
 // Fused training step (vmb_march_render_backward_field_async): the expansion also
 // runs render_backward (rendering.cpp:67-112) on the samples it has just written —
@@ -1122,6 +1128,7 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
     uint32_t* __restrict__ overflow, unsigned int* n_overflow, ShadeOut<RT, AT, VOX> sh, BwdOut<AT> bo,
     const void* __restrict__ kept_attr) {
     constexpr bool RAYS = SHADE && !CONST && !ATTR;  // the per-sample shading needs the ray
+    constexpr int EW = expand_warps(SHADE, CONST, ATTR);
     using AT4 = std::conditional_t<sizeof(AT) == 4, float4, double4>;
     const AT4* attr = static_cast<const AT4*>(kept_attr);
     // dynamic shared memory (kExpandSmem): per warp, two kept-index row buffers and
@@ -1129,7 +1136,7 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
     extern __shared__ __align__(16) uint32_t expand_smem[];
     uint32_t(*s_idx)[2][kWalkCap * 32] = reinterpret_cast<uint32_t(*)[2][kWalkCap * 32]>(expand_smem);
     uint16_t(*s_map)[kWalkCap * 32] =
-        reinterpret_cast<uint16_t(*)[kWalkCap * 32]>(expand_smem + kExpandWarps * 2 * kWalkCap * 32);
+        reinterpret_cast<uint16_t(*)[kWalkCap * 32]>(expand_smem + EW * 2 * kWalkCap * 32);
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const uint64_t n_chunks = (n_rays + 31) / 32;
@@ -1142,8 +1149,8 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
     }
     // the row buffers' mbarriers, then (BWD && CONST) alpha per lattice step
     unsigned long long* rbar = reinterpret_cast<unsigned long long*>(
-        expand_smem + kExpandWarps * (2 * kWalkCap * 32 + kWalkCap * 16)) + 2 * wib;
-    double* atab = reinterpret_cast<double*>(expand_smem + kExpandWarps * (2 * kWalkCap * 32 + kWalkCap * 16 + 4));
+        expand_smem + EW * (2 * kWalkCap * 32 + kWalkCap * 16)) + 2 * wib;
+    double* atab = reinterpret_cast<double*>(expand_smem + EW * (2 * kWalkCap * 32 + kWalkCap * 16 + 4));
     if (BWD && CONST) {
         for (uint32_t j = threadIdx.x; j < bo.atab_n; j += blockDim.x) {
             const double dj = double(j);
@@ -1903,14 +1910,13 @@ FwdOut<AT> fwd_out(const ShadeReq& sr) {
 // Resident CTAs per SM of one expansion kernel (persistent grid), after opting it
 // in to kExpandSmem of dynamic shared memory — once per kernel (the kernel is the
 // template argument: instantiations share one function type).
-constexpr size_t kExpandSmemBwd = kExpandSmem + kMaxAlphaTable * sizeof(double);  // + alpha table (8 B aligned)
 
-template <auto K, size_t SMEM = kExpandSmem>
+template <auto K, size_t SMEM, int W>
 int expand_per_sm() {
     static const int n = [] {
         cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM));
         int m = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, K, 32 * kExpandWarps, SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, K, 32 * W, SMEM);
         return m < 1 ? 2 : m;
     }();
     return n;
@@ -1942,11 +1948,18 @@ void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* ray
                         reinterpret_cast<unsigned int*>(bwd_list), 0u, double(AT(sr.f.sigma))};
         bo.atab_n = P.n_steps <= kMaxAlphaTable ? uint32_t(P.n_steps) : 0u;
     }
-    auto launch = [&](auto kernel, int per_sm, size_t smem) {
-        kernel<<<grid_blocks(ctx, n_chunks * 32, 32 * kExpandWarps, per_sm), 32 * kExpandWarps, smem,
-                 ctx->stream>>>(P.near_, P.far_, P.step, out->d_counts, chunk_off, out->d_offsets, kept_idx, rays->n_rays,
+    auto launch = [&](auto kernel, int per_sm, size_t smem, int w) {
+        kernel<<<grid_blocks(ctx, n_chunks * 32, 32 * w, per_sm), 32 * w, smem, ctx->stream>>>(P.near_, P.far_, P.step, out->d_counts, chunk_off, out->d_offsets, kept_idx, rays->n_rays,
                                 out->d_t_starts, out->d_t_ends, out->d_ray_indices, out->capacity, overflow,
                                 n_overflow, sh, bo, kept_attr);
+    };
+    // one expansion variant: its warps per CTA and dynamic shared memory (+ the
+    // constant-density alpha table for the fused backward)
+    auto go = [&](auto kernel, auto CST, auto BWDC, auto ATTRC) {
+        constexpr bool C = decltype(CST)::value, B = decltype(BWDC)::value, A = decltype(ATTRC)::value;
+        constexpr int W = expand_warps(SHADE, C, A);
+        constexpr size_t SM = expand_smem_of(W) + (B && C ? kMaxAlphaTable * sizeof(double) : 0);
+        launch(kernel, expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, C, B, A>, SM, W>(), SM, W);
     };
     const bool cst = SHADE && !VOX && const_shading(P, sr);
     bool plain = true;
@@ -1955,26 +1968,24 @@ void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* ray
             plain = false;
             cudaMemsetAsync(bwd_list, 0, 4, ctx->stream);
             if (cst)
-                launch(k_march_expand<RT, AT, SHADE, VOX, true, true>,
-                       expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, true, true>, kExpandSmemBwd>(), kExpandSmemBwd);
+                go(k_march_expand<RT, AT, SHADE, VOX, true, true>, std::true_type{}, std::true_type{},
+                   std::false_type{});
             else if (kept_attr)
-                launch(k_march_expand<RT, AT, SHADE, VOX, false, true, true>,
-                       expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, false, true, true>>(), kExpandSmem);
+                go(k_march_expand<RT, AT, SHADE, VOX, false, true, true>, std::false_type{}, std::true_type{},
+                   std::true_type{});
             else
-                launch(k_march_expand<RT, AT, SHADE, VOX, false, true>,
-                       expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, false, true>>(), kExpandSmem);
+                go(k_march_expand<RT, AT, SHADE, VOX, false, true>, std::false_type{}, std::true_type{},
+                   std::false_type{});
         } else if (kept_attr) {
             plain = false;
-            launch(k_march_expand<RT, AT, SHADE, VOX, false, false, true>,
-                   expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, false, false, true>>(), kExpandSmem);
+            go(k_march_expand<RT, AT, SHADE, VOX, false, false, true>, std::false_type{}, std::false_type{},
+               std::true_type{});
         }
     }
     if (plain && cst)
-        launch(k_march_expand<RT, AT, SHADE, VOX, true>, expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, true>>(),
-               kExpandSmem);
+        go(k_march_expand<RT, AT, SHADE, VOX, true>, std::true_type{}, std::false_type{}, std::false_type{});
     else if (plain)
-        launch(k_march_expand<RT, AT, SHADE, VOX, false>, expand_per_sm<k_march_expand<RT, AT, SHADE, VOX, false>>(),
-               kExpandSmem);
+        go(k_march_expand<RT, AT, SHADE, VOX, false>, std::false_type{}, std::false_type{}, std::false_type{});
     k_march_fixup<RT, AT, SHADE, FWD, VOX><<<ctx->num_sms * 2, 128, 0, ctx->stream>>>(
         P, sh.orig, sh.dirs, out->d_offsets, out->d_t_starts, out->d_t_ends, out->d_ray_indices,
         out->capacity, overflow, n_overflow, ctx->d_err, sh, fwd_out<AT>(sr));
