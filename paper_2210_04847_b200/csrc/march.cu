@@ -954,6 +954,7 @@ __global__ void __launch_bounds__(kAccStride, VMB_WALK_MINB) k_march_walk(
     uint32_t* __restrict__ counts, uint32_t* __restrict__ kept_idx, unsigned int* chunk_counter,
     uint64_t n_chunks, unsigned long long* emitted, DevError* err, FwdOut<AT> fo,
     uint32_t* __restrict__ chunk_tot, void* __restrict__ kept_attr) {
+    griddep_wait();
     const int lane = threadIdx.x & 31;
     unsigned long long emit_local = 0;
     if (ATAB) {  // alpha per lattice step for the constant interior density (sphere)
@@ -1127,6 +1128,7 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
     double* __restrict__ ts, double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,
     uint32_t* __restrict__ overflow, unsigned int* n_overflow, ShadeOut<RT, AT, VOX> sh, BwdOut<AT> bo,
     const void* __restrict__ kept_attr) {
+    griddep_wait();
     constexpr bool RAYS = SHADE && !CONST && !ATTR;  // the per-sample shading needs the ray
     constexpr int EW = expand_warps(SHADE, CONST, ATTR);
     using AT4 = std::conditional_t<sizeof(AT) == 4, float4, double4>;
@@ -1434,6 +1436,7 @@ __global__ void k_march_fixup(MarchParams P, const RT* __restrict__ orig, const 
                               double* __restrict__ te, uint32_t* __restrict__ idx, uint64_t cap,
                               const uint32_t* __restrict__ overflow, const unsigned int* n_overflow,
                               DevError* err, ShadeOut<RT, AT, VOX> sh, FwdOut<AT> fo) {
+    griddep_wait();
     const unsigned int n = *n_overflow;
     for (unsigned int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         uint64_t r = overflow[k];
@@ -1949,9 +1952,10 @@ void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* ray
         bo.atab_n = P.n_steps <= kMaxAlphaTable ? uint32_t(P.n_steps) : 0u;
     }
     auto launch = [&](auto kernel, int per_sm, size_t smem, int w) {
-        kernel<<<grid_blocks(ctx, n_chunks * 32, 32 * w, per_sm), 32 * w, smem, ctx->stream>>>(P.near_, P.far_, P.step, out->d_counts, chunk_off, out->d_offsets, kept_idx, rays->n_rays,
-                                out->d_t_starts, out->d_t_ends, out->d_ray_indices, out->capacity, overflow,
-                                n_overflow, sh, bo, kept_attr);
+        launch_pdl(kernel, dim3(grid_blocks(ctx, n_chunks * 32, 32 * w, per_sm)), dim3(32 * w), smem, ctx->stream,
+                   P.near_, P.far_, P.step, out->d_counts, chunk_off, out->d_offsets, kept_idx, rays->n_rays,
+                   out->d_t_starts, out->d_t_ends, out->d_ray_indices, out->capacity, overflow, n_overflow, sh, bo,
+                   kept_attr);
     };
     // one expansion variant: its warps per CTA and dynamic shared memory (+ the
     // constant-density alpha table for the fused backward)
@@ -1986,9 +1990,9 @@ void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* ray
         go(k_march_expand<RT, AT, SHADE, VOX, true>, std::true_type{}, std::false_type{}, std::false_type{});
     else if (plain)
         go(k_march_expand<RT, AT, SHADE, VOX, false>, std::false_type{}, std::false_type{}, std::false_type{});
-    k_march_fixup<RT, AT, SHADE, FWD, VOX><<<ctx->num_sms * 2, 128, 0, ctx->stream>>>(
-        P, sh.orig, sh.dirs, out->d_offsets, out->d_t_starts, out->d_t_ends, out->d_ray_indices,
-        out->capacity, overflow, n_overflow, ctx->d_err, sh, fwd_out<AT>(sr));
+    launch_pdl(k_march_fixup<RT, AT, SHADE, FWD, VOX>, dim3(ctx->num_sms * 2), dim3(128), 0, ctx->stream, P, sh.orig,
+               sh.dirs, out->d_offsets, out->d_t_starts, out->d_t_ends, out->d_ray_indices, out->capacity, overflow,
+               n_overflow, ctx->d_err, sh, fwd_out<AT>(sr));
     if (sr.bwd) {  // the rays of chunks with a ray above kWalkCap samples, after the fixup
         vmb_packed_view v{out->d_offsets, out->d_counts, rays->n_rays, out->d_t_starts, out->d_t_ends, out->capacity};
         backward_listed(ctx, &v, sr.rgb, sr.sig, sr.dc, sr.dop, sr.ddep, sr.g_rgb, sr.g_sig, bwd_list + 4,
@@ -2055,8 +2059,8 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
         const size_t dyn = size_t(P.atab_n) * 2 * sizeof(double);  // read only by ATAB kernels: alpha, midpoint
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kAccStride, dyn);
         if (per_sm < 1) per_sm = 4;
-        kernel<<<ctx->num_sms * per_sm, kAccStride, dyn, ctx->stream>>>(
-            P, o, d, n, out->d_counts, kept_idx, counters, n_chunks, emitted, ctx->d_err, fo, chunk_tot, kept_attr);
+        launch_pdl(kernel, dim3(ctx->num_sms * per_sm), dim3(kAccStride), dyn, ctx->stream, P, o, d, n, out->d_counts,
+                   kept_idx, counters, n_chunks, emitted, ctx->d_err, fo, chunk_tot, kept_attr);
     };
     auto walk_vox = [&](auto* o, auto* d, auto VOXC) {
         using RT = std::remove_const_t<std::remove_pointer_t<decltype(o)>>;

@@ -565,6 +565,7 @@ __global__ void __launch_bounds__(kWarps * 32, 32 / kWarps) k_backward_long(
     const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig,
     const uint32_t* __restrict__ long_rays, const unsigned int* __restrict__ n_long) {
     __shared__ BwdSmem<T> smem[kWarps];
+    griddep_wait();
     const int lane = threadIdx.x & 31;
     BwdSmem<T>& sm = smem[threadIdx.x >> 5];
     const unsigned int n = *n_long;
@@ -617,6 +618,7 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
     const T* __restrict__ ddep, T* __restrict__ g_rgb, T* __restrict__ g_sig,
     uint32_t* __restrict__ long_rays, unsigned int* __restrict__ n_long) {
     extern __shared__ __align__(16) unsigned char bwd_dyn_smem[];  // kWarps x BwdSmem<T, kBulkPad>
+    griddep_wait();
     const int lane = threadIdx.x & 31;
     BwdSmem<T, kBulkPad>& sm = reinterpret_cast<BwdSmem<T, kBulkPad>*>(bwd_dyn_smem)[threadIdx.x >> 5];
     if (lane == 0) {
@@ -890,15 +892,14 @@ int launch_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, con
                cudaSuccess;
     }();
     (void)opted;
-    k_backward_hy<T><<<blocks, kWarps * 32, smem, ctx->stream>>>(
-        p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
-        static_cast<const T*>(rgb), static_cast<const T*>(sig), static_cast<const T*>(dc),
-        static_cast<const T*>(dop), static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig),
-        list + 4, n_long);
-    k_backward_long<T><<<ctx->num_sms * (32 / kWarps), kWarps * 32, 0, ctx->stream>>>(
-        p->d_offsets, p->d_counts, p->n_samples, p->d_t_starts, p->d_t_ends, static_cast<const T*>(rgb),
-        static_cast<const T*>(sig), static_cast<const T*>(dc), static_cast<const T*>(dop),
-        static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig), list + 4, n_long);
+    launch_pdl(k_backward_hy<T>, dim3(blocks), dim3(kWarps * 32), smem, ctx->stream, p->d_offsets, p->d_counts,
+               p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends, static_cast<const T*>(rgb),
+               static_cast<const T*>(sig), static_cast<const T*>(dc), static_cast<const T*>(dop),
+               static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig), list + 4, n_long);
+    launch_pdl(k_backward_long<T>, dim3(ctx->num_sms * (32 / kWarps)), dim3(kWarps * 32), 0, ctx->stream,
+               p->d_offsets, p->d_counts, p->n_samples, p->d_t_starts, p->d_t_ends, static_cast<const T*>(rgb),
+               static_cast<const T*>(sig), static_cast<const T*>(dc), static_cast<const T*>(dop),
+               static_cast<const T*>(ddep), static_cast<T*>(g_rgb), static_cast<T*>(g_sig), list + 4, n_long);
     return launched("render_backward");
 }
 

@@ -22,6 +22,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_tiles(const In* __restrict__ 
                                                          unsigned long long* __restrict__ tile_sums) {
     __shared__ uint32_t sm[kTile + kTile / 32];
     __shared__ unsigned long long warp_tot[kThreads / 32];
+    griddep_wait();
     const uint64_t base = uint64_t(blockIdx.x) * kTile;
     const int t = threadIdx.x;
 #pragma unroll
@@ -72,6 +73,7 @@ __global__ void __launch_bounds__(1024) k_scan_sums(unsigned long long* sums, ui
                                                     unsigned long long* d_total) {
     __shared__ unsigned long long warp_tot[32];
     __shared__ unsigned long long carry;
+    griddep_wait();
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     if (t == 0) carry = 0;
     __syncthreads();
@@ -101,6 +103,7 @@ __global__ void __launch_bounds__(1024) k_scan_sums(unsigned long long* sums, ui
 
 __global__ void k_scan_add(uint32_t* __restrict__ out, uint64_t n,
                            const unsigned long long* __restrict__ sums) {
+    griddep_wait();
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x)
         out[i] += uint32_t(sums[i / kTile]);
@@ -116,9 +119,9 @@ int scan_impl(vmb_ctx* ctx, const In* in, uint64_t n, uint32_t* out,
     uint64_t tiles = (n + kTile - 1) / kTile;
     auto* sums = static_cast<unsigned long long*>(scratch(ctx, SCRATCH_SCAN, tiles * sizeof(unsigned long long)));
     if (!sums) return VMB_CUDA;
-    k_scan_tiles<In><<<unsigned(tiles), kThreads, 0, ctx->stream>>>(in, n, out, sums);
-    k_scan_sums<<<1, 1024, 0, ctx->stream>>>(sums, tiles, d_total);
-    if (tiles > 1) k_scan_add<<<grid_blocks(ctx, n, 256), 256, 0, ctx->stream>>>(out, n, sums);
+    launch_pdl(k_scan_tiles<In>, dim3(unsigned(tiles)), dim3(kThreads), 0, ctx->stream, in, n, out, sums);
+    launch_pdl(k_scan_sums, dim3(1), dim3(1024), 0, ctx->stream, sums, tiles, d_total);
+    if (tiles > 1) launch_pdl(k_scan_add, dim3(grid_blocks(ctx, n, 256)), dim3(256), 0, ctx->stream, out, n, sums);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? VMB_OK : cuda_fail(e, "scan");
 }

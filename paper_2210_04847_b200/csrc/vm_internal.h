@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "../../include/vmb200.h"
 #include "vm_exact.cuh"
@@ -101,6 +102,28 @@ int cuda_fail(cudaError_t e, const char* where);
 enum { SCRATCH_SCAN = 0, SCRATCH_MARCH = 1, SCRATCH_GRID = 2, SCRATCH_MISC = 3, SCRATCH_VOXGRAD = 4, SCRATCH_RENDER = 5, SCRATCH_SLAB = 6, SCRATCH_SLOTS = 7 };
 static_assert(sizeof(vmb_ctx::scratch) / sizeof(void*) == SCRATCH_SLOTS, "one scratch buffer per slot");
 void* scratch(vmb_ctx* ctx, int slot, size_t bytes);
+// Programmatic dependent launch (PDL): the kernel may be scheduled while the previous
+// kernel on the stream drains (its launch latency hidden behind that kernel's tail);
+// every kernel launched this way calls griddep_wait() before touching memory.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+#endif
+
 inline int grid_blocks(vmb_ctx* ctx, uint64_t work, int threads, int per_sm = 8) {
     uint64_t b = (work + threads - 1) / threads;
     uint64_t cap = uint64_t(ctx->num_sms) * per_sm;
