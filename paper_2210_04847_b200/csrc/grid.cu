@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(256) k_update_fused(GridDev g, vmb_field f, Ti
                                                       bool has_seed, uint64_t seed, double decay,
                                                       double* __restrict__ cache,
                                                       uint32_t* __restrict__ bits, uint64_t n_words) {
+    griddep_wait();
     const int lane = threadIdx.x & 31;
     const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -149,6 +150,7 @@ __global__ void __launch_bounds__(256) k_apply(GridDev g, const double* __restri
 // bits from cache only (constructor, seed_occupancy)
 __global__ void __launch_bounds__(256) k_refresh(GridDev g, const double* __restrict__ cache,
                                                  uint32_t* __restrict__ bits, uint64_t n_words) {
+    griddep_wait();
     const int lane = threadIdx.x & 31;
     const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -381,6 +383,7 @@ __device__ __forceinline__ uint64_t bits64(const uint32_t* __restrict__ bits, in
 // nearest set bit on each side by clz / ffs.
 __global__ void k_dist_x(const uint32_t* __restrict__ bits, uint32_t res, uint64_t n, uint64_t n_words,
                          uint8_t* __restrict__ out) {
+    griddep_wait();
     constexpr int W = kDistCap - 1;
     for (uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < n;
          c += uint64_t(gridDim.x) * blockDim.x) {
@@ -406,6 +409,7 @@ __global__ void k_dist_x(const uint32_t* __restrict__ bits, uint32_t res, uint64
 __global__ void k_dist_axis_tiled(const uint8_t* __restrict__ in, uint32_t res, uint64_t stride,
                                   uint64_t ostride, uint8_t* __restrict__ out) {
     extern __shared__ uint8_t tile[];  // [res][32]
+    griddep_wait();
     const uint32_t ntx = (res + 31) / 32;
     const uint32_t other = blockIdx.x / ntx, x0 = (blockIdx.x % ntx) * 32;
     const int lane = threadIdx.x & 31, row = threadIdx.x >> 5, rows = blockDim.x >> 5;
@@ -445,7 +449,7 @@ int grid_ensure_coarse(vmb_ctx* ctx, const vmb_grid* cg) {
 int grid_rebuild_coarse(vmb_ctx* ctx, vmb_grid* g) {
     g->coarse_valid = false;
     const int blocks = grid_blocks(ctx, g->n_cells, 256);
-    k_dist_x<<<blocks, 256, 0, ctx->stream>>>(g->bits, g->res, g->n_cells, g->n_words, g->dist);
+    launch_pdl(k_dist_x, dim3(blocks), dim3(256), 0, ctx->stream, g->bits, g->res, g->n_cells, g->n_words, g->dist);
     const uint64_t r = g->res, plane = r * r;
     const uint32_t tiles = uint32_t(r * ((r + 31) / 32));
     const size_t smem = size_t(r) * 32;  // one line of 32 columns
@@ -454,8 +458,8 @@ int grid_rebuild_coarse(vmb_ctx* ctx, vmb_grid* g) {
                cudaSuccess;
     }();
     (void)opted;
-    k_dist_axis_tiled<<<tiles, 256, smem, ctx->stream>>>(g->dist, g->res, r, plane, g->dist_tmp);      // y
-    k_dist_axis_tiled<<<tiles, 256, smem, ctx->stream>>>(g->dist_tmp, g->res, plane, r, g->dist);      // z
+    launch_pdl(k_dist_axis_tiled, dim3(tiles), dim3(256), smem, ctx->stream, g->dist, g->res, r, plane, g->dist_tmp);
+    launch_pdl(k_dist_axis_tiled, dim3(tiles), dim3(256), smem, ctx->stream, g->dist_tmp, g->res, plane, r, g->dist);
     cudaMemsetAsync(g->bbox, 0xff, 3 * sizeof(uint32_t), ctx->stream);
     cudaMemsetAsync(g->bbox + 3, 0, 3 * sizeof(uint32_t), ctx->stream);
     k_bbox<<<grid_blocks(ctx, g->n_words, 256, 4), 256, 0, ctx->stream>>>(g->bits, g->res, g->n_words, g->bbox);
@@ -463,7 +467,7 @@ int grid_rebuild_coarse(vmb_ctx* ctx, vmb_grid* g) {
 }
 
 int grid_refresh(vmb_ctx* ctx, vmb_grid* g) {
-    k_refresh<<<grid_blocks(ctx, g->n_words * 32, 256), 256, 0, ctx->stream>>>(dev_of(g), g->cache,
+    launch_pdl(k_refresh, dim3(grid_blocks(ctx, g->n_words * 32, 256)), dim3(256), 0, ctx->stream, dev_of(g), g->cache,
                                                                                 g->bits, g->n_words);
     int rc = launch_check("grid refresh");
     return rc ? rc : grid_rebuild_coarse(ctx, g);
@@ -606,8 +610,9 @@ int vmb_grid_update_field(vmb_ctx* ctx, vmb_grid* g, const vmb_field* f, const d
         k_apply<<<grid_blocks(ctx, g->n_words * 32, 256), 256, 0, ctx->stream>>>(
             gd, g->probed, decay, g->cache, g->bits, g->n_words);
     } else {
-        (f->kind == VMB_FIELD_VOXEL ? k_update_fused<true> : k_update_fused<false>)<<<grid_blocks(ctx, g->n_words * 32, 256), 256, 0, ctx->stream>>>(
-            gd, *f, ts, has_seed != 0, seed, decay, g->cache, g->bits, g->n_words);
+        launch_pdl(f->kind == VMB_FIELD_VOXEL ? k_update_fused<true> : k_update_fused<false>,
+                   dim3(grid_blocks(ctx, g->n_words * 32, 256)), dim3(256), 0, ctx->stream, gd, *f, ts, has_seed != 0,
+                   seed, decay, g->cache, g->bits, g->n_words);
     }
     rc = launch_check("grid update");
     return rc ? rc : grid_rebuild_coarse(ctx, g);

@@ -1480,6 +1480,7 @@ __global__ void VMB_MARCH_LB k_march(MarchParams P, const RT* __restrict__ orig,
     // slab_cap) of ts/te/idx and its kept count; k_slab_gather packs them after the
     // scan. FILL with slab_cap > 0: the packed fill of the rays above slab_cap only.
     constexpr bool SLAB = mslab(MODE);
+    griddep_wait();
     unsigned long long emit_local = 0;
     __shared__ double stg[mbase(MODE) == FILL ? 8 * kStgStride : 1];
     const bool vec = ((reinterpret_cast<uintptr_t>(ts) | reinterpret_cast<uintptr_t>(te) |
@@ -1515,6 +1516,7 @@ __global__ void k_slab_gather(const uint32_t* __restrict__ counts, const uint32_
                               uint64_t n_rays, uint32_t slab_cap, const double* __restrict__ sts,
                               const double* __restrict__ ste, double* __restrict__ ts, double* __restrict__ te,
                               uint32_t* __restrict__ idx, uint64_t cap) {
+    griddep_wait();
     const int lane = threadIdx.x & 31;
     for (uint64_t r = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < n_rays;
          r += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
@@ -1691,13 +1693,13 @@ void launch_march_rt(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, u
     uint32_t* ix = sl.mode == 1 ? sl.idx : out ? out->d_ray_indices : nullptr;
     const uint64_t cap = out ? out->capacity : 0;
     if (rays->dtype == VMB_F32)
-        k_march<float, MODE><<<blocks, 128, 0, ctx->stream>>>(
-            P, static_cast<const float*>(rays->d_origins), static_cast<const float*>(rays->d_directions),
-            rays->n_rays, counts, offsets, ts, te, ix, cap, emitted, ctx->d_err, sl.cap);
+        launch_pdl(k_march<float, MODE>, dim3(blocks), dim3(128), 0, ctx->stream, P,
+                   static_cast<const float*>(rays->d_origins), static_cast<const float*>(rays->d_directions),
+                   rays->n_rays, counts, offsets, ts, te, ix, cap, emitted, ctx->d_err, sl.cap);
     else
-        k_march<double, MODE><<<blocks, 128, 0, ctx->stream>>>(
-            P, static_cast<const double*>(rays->d_origins), static_cast<const double*>(rays->d_directions),
-            rays->n_rays, counts, offsets, ts, te, ix, cap, emitted, ctx->d_err, sl.cap);
+        launch_pdl(k_march<double, MODE>, dim3(blocks), dim3(128), 0, ctx->stream, P,
+                   static_cast<const double*>(rays->d_origins), static_cast<const double*>(rays->d_directions),
+                   rays->n_rays, counts, offsets, ts, te, ix, cap, emitted, ctx->d_err, sl.cap);
 }
 
 // Long-ray walks (accumulated t: cascades, cone stepping, growth) pack in one walk:
@@ -1728,9 +1730,8 @@ Slab make_slab(vmb_ctx* ctx, const MarchParams& P, uint64_t n_rays) {
 
 void slab_pack(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_samples* out, Slab sl) {
     const int blocks = grid_blocks(ctx, rays->n_rays * 32, 256, 8);
-    k_slab_gather<<<blocks, 256, 0, ctx->stream>>>(out->d_counts, out->d_offsets, rays->n_rays, sl.cap, sl.ts,
-                                                   sl.te, out->d_t_starts, out->d_t_ends, out->d_ray_indices,
-                                                   out->capacity);
+    launch_pdl(k_slab_gather, dim3(blocks), dim3(256), 0, ctx->stream, out->d_counts, out->d_offsets, rays->n_rays,
+               sl.cap, sl.ts, sl.te, out->d_t_starts, out->d_t_ends, out->d_ray_indices, out->capacity);
     sl.mode = 2;
     launch_march<FILL>(ctx, P, rays, out->d_counts, out->d_offsets, out, nullptr, sl);
 }

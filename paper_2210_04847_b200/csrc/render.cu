@@ -353,6 +353,7 @@ __global__ void __launch_bounds__(kWinWarps * 32) k_shade_forward_win(
     const double* __restrict__ ts, const double* __restrict__ te, T* __restrict__ rgb, T* __restrict__ sig,
     T* __restrict__ color, T* __restrict__ opacity, T* __restrict__ depth) {
     __shared__ WinSmem<T> smem[kWinWarps];
+    griddep_wait();
     const int lane = threadIdx.x & 31;
     constexpr int kWinW = Win<T>::W, kRq = 32 / kWinW;
     const int half = lane / kWinW, j = lane % kWinW;
@@ -908,12 +909,11 @@ void launch_shade_forward(vmb_ctx* ctx, const vmb_rays* rays, const vmb_field* f
                           const vmb_packed_view* p, void* rgb, void* sig, void* color, void* opacity,
                           void* depth) {
     const int wb = grid_blocks(ctx, (p->n_rays + 31) / 32 * 32, kWinWarps * 32, VMB_FWD_WIN_CTAS);
-    (f->kind == VMB_FIELD_VOXEL ? k_shade_forward_win<RT, T, true> : k_shade_forward_win<RT, T, false>)
-        <<<wb, kWinWarps * 32, 0, ctx->stream>>>(
-            static_cast<const RT*>(rays->d_origins), static_cast<const RT*>(rays->d_directions), *f, time,
-            p->d_offsets, p->d_counts, p->n_rays, p->n_samples, p->d_t_starts, p->d_t_ends,
-            static_cast<T*>(rgb), static_cast<T*>(sig), static_cast<T*>(color), static_cast<T*>(opacity),
-            static_cast<T*>(depth));
+    launch_pdl(f->kind == VMB_FIELD_VOXEL ? k_shade_forward_win<RT, T, true> : k_shade_forward_win<RT, T, false>,
+               dim3(wb), dim3(kWinWarps * 32), 0, ctx->stream, static_cast<const RT*>(rays->d_origins),
+               static_cast<const RT*>(rays->d_directions), *f, time, p->d_offsets, p->d_counts, p->n_rays,
+               p->n_samples, p->d_t_starts, p->d_t_ends, static_cast<T*>(rgb), static_cast<T*>(sig),
+               static_cast<T*>(color), static_cast<T*>(opacity), static_cast<T*>(depth));
 }
 
 }  // namespace
