@@ -1971,7 +1971,7 @@ void launch_expand_fixup(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* ray
     if constexpr (FWD && SHADE) {
         if (sr.bwd) {
             plain = false;
-            cudaMemsetAsync(bwd_list, 0, 4, ctx->stream);
+            zero_words_async(ctx, bwd_list, 1);
             if (cst)
                 go(k_march_expand<RT, AT, SHADE, VOX, true, true>, std::true_type{}, std::true_type{},
                    std::false_type{});
@@ -2048,7 +2048,7 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
     auto* chunk_tot = reinterpret_cast<uint32_t*>(rest + n * 4);  // per-chunk totals
     auto* chunk_off = chunk_tot + n_chunks;                       // and their scan
     auto* bwd_list = chunk_off + n_chunks;  // fused backward: [count, pad x3, rays...]
-    cudaMemsetAsync(base, 0, head, ctx->stream);
+    zero_words_async(ctx, base, int(head / 4));
     if (n == 0) {
         cudaMemsetAsync(d_total, 0, 8, ctx->stream);
         cudaError_t e = cudaGetLastError();

@@ -886,7 +886,7 @@ int launch_backward(vmb_ctx* ctx, const vmb_packed_view* p, const void* rgb, con
     auto* list = static_cast<uint32_t*>(scratch(ctx, SCRATCH_RENDER, 16 + 4 * p->n_rays));
     if (!list) return VMB_CUDA;
     auto* n_long = reinterpret_cast<unsigned int*>(list);
-    cudaMemsetAsync(n_long, 0, 4, ctx->stream);
+    zero_words_async(ctx, n_long, 1);
     constexpr size_t smem = kWarps * sizeof(BwdSmem<T, kBulkPad>);
     static const bool opted = [] {  // above the 48 KB default of dynamic shared memory
         return cudaFuncSetAttribute(k_backward_hy<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) ==

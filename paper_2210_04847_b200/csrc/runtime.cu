@@ -24,6 +24,19 @@ int cuda_fail(cudaError_t e, const char* where) {
     return VMB_CUDA;
 }
 
+namespace {
+__global__ void k_zero_words(uint32_t* __restrict__ p, int n) {
+    griddep_wait();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0u;
+}
+}  // namespace
+
+// A few counters zeroed by a one-warp kernel in the PDL chain (a memset node between
+// two kernels would serialise the next kernel's launch behind it).
+void zero_words_async(vmb_ctx* ctx, void* p, int n_words) {
+    launch_pdl(k_zero_words, dim3(1), dim3(32), 0, ctx->stream, static_cast<uint32_t*>(p), n_words);
+}
+
 void* scratch(vmb_ctx* ctx, int slot, size_t bytes) {
     if (bytes == 0) bytes = 16;
     if (ctx->scratch_bytes[slot] >= bytes) return ctx->scratch[slot];

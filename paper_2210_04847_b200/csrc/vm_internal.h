@@ -102,6 +102,7 @@ int cuda_fail(cudaError_t e, const char* where);
 enum { SCRATCH_SCAN = 0, SCRATCH_MARCH = 1, SCRATCH_GRID = 2, SCRATCH_MISC = 3, SCRATCH_VOXGRAD = 4, SCRATCH_RENDER = 5, SCRATCH_SLAB = 6, SCRATCH_SLOTS = 7 };
 static_assert(sizeof(vmb_ctx::scratch) / sizeof(void*) == SCRATCH_SLOTS, "one scratch buffer per slot");
 void* scratch(vmb_ctx* ctx, int slot, size_t bytes);
+void zero_words_async(vmb_ctx* ctx, void* p, int n_words);  // runtime.cu
 // Programmatic dependent launch (PDL): the kernel may be scheduled while the previous
 // kernel on the stream drains (its launch latency hidden behind that kernel's tail);
 // every kernel launched this way calls griddep_wait() before touching memory.
