@@ -1713,7 +1713,7 @@ Slab make_slab(vmb_ctx* ctx, const MarchParams& P, uint64_t n_rays) {
     Slab sl;
     if (!VMB_SLAB || !(P.accum || P.grows) || n_rays == 0) return sl;
     const uint64_t budget = 4ull << 30;
-    uint64_t cap = budget / (n_rays * 16);
+    uint64_t cap = budget / (n_rays * (2 * sizeof(double) + 4));  // t0, t1, index per slot
     cap = cap > 256 ? 256 : cap & ~uint64_t(3);
     if (cap < 64) return sl;
     auto* b = static_cast<double*>(scratch(ctx, SCRATCH_SLAB, n_rays * cap * (2 * sizeof(double) + 4)));
