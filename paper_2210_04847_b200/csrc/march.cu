@@ -1705,14 +1705,14 @@ void launch_march_rt(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, u
 // Long-ray walks (accumulated t: cascades, cone stepping, growth) pack in one walk:
 // the slab pass, the scan, k_slab_gather, and a fill of the rays above the slab
 // capacity only, instead of a count walk and a fill walk. Up to 256 intervals per
-// ray and 4 GiB of slab; otherwise (or for short-ray walks) count + fill.
+// ray and 6 GiB of slab; otherwise (or for short-ray walks) count + fill.
 Slab make_slab(vmb_ctx* ctx, const MarchParams& P, uint64_t n_rays) {
 #ifndef VMB_SLAB
 #define VMB_SLAB 1
 #endif
     Slab sl;
     if (!VMB_SLAB || !(P.accum || P.grows) || n_rays == 0) return sl;
-    const uint64_t budget = 4ull << 30;
+    const uint64_t budget = 6ull << 30;  // 256 slots for up to 1.26M rays
     uint64_t cap = budget / (n_rays * (2 * sizeof(double) + 4));  // t0, t1, index per slot
     cap = cap > 256 ? 256 : cap & ~uint64_t(3);
     if (cap < 64) return sl;
