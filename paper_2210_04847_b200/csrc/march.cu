@@ -2029,7 +2029,11 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
     if (int rc = ensure_skip_structures(ctx, P)) return rc;
     const uint64_t n = rays->n_rays;
     const uint64_t n_chunks = (n + 31) / 32;
-    const size_t head = 16;
+    // head: [chunk claim, overflow count, scan ticket, pad] + the single-pass scan's
+    // status words (one per tile of chunk totals), all zeroed before the walk
+    const uint64_t scan_tiles = scan_onepass_tiles(n_chunks);
+    const bool onepass = scan_tiles <= 1024;
+    const size_t head = onepass ? (16 + 8 * scan_tiles + 15) / 16 * 16 : 16;
     const size_t idx_bytes = n_chunks * kWalkCap * 32 * sizeof(uint32_t);
     // the walk keeps each kept sample's rgb/sigma for the stored voxel field (ATTRM):
     // 16-32 B of scratch per sample instead of a second trilinear stencil (voxel
@@ -2040,7 +2044,8 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
     const size_t misc = n * 4 + 8 * n_chunks + (sr.bwd ? 16 + 4 * n : 0) + 64;
     char* base = static_cast<char*>(scratch(ctx, SCRATCH_MARCH, head + idx_bytes + attr_bytes + misc + 256));
     if (!base) return VMB_CUDA;
-    auto* counters = reinterpret_cast<unsigned int*>(base);  // [chunk, overflow]
+    auto* counters = reinterpret_cast<unsigned int*>(base);  // [chunk, overflow, scan ticket]
+    auto* scan_status = reinterpret_cast<unsigned long long*>(base + 16);
     auto* kept_idx = reinterpret_cast<uint32_t*>(base + head);
     void* kept_attr = attr_on ? static_cast<void*>(base + head + idx_bytes) : nullptr;  // 16 B aligned
     char* rest = base + head + idx_bytes + attr_bytes;
@@ -2106,7 +2111,8 @@ int launch_fused(vmb_ctx* ctx, const MarchParams& P, const vmb_rays* rays, vmb_s
         walk_rt(static_cast<const double*>(rays->d_origins), static_cast<const double*>(rays->d_directions));
     // offsets: the scan of the walk's per-chunk totals, then within each chunk the
     // expansion's warp scan (it writes out->d_offsets)
-    int rc = scan_counts(ctx, chunk_tot, n_chunks, chunk_off, d_total);
+    int rc = onepass ? scan_counts_onepass(ctx, chunk_tot, n_chunks, chunk_off, d_total, counters + 2, scan_status)
+                     : scan_counts(ctx, chunk_tot, n_chunks, chunk_off, d_total);
     if (rc) return rc;
     if (rays->dtype == VMB_F32)
         dispatch_expand<float>(ctx, P, rays, out, kept_idx, overflow, counters + 1, n_chunks, sr, chunk_off, bwd_list,

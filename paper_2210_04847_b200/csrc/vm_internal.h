@@ -146,6 +146,9 @@ int read_error(vmb_ctx* ctx, DevError* out);  // synchronizes
 // Exclusive scan of u32 counts into u32 offsets; device total (u64) at d_total.
 int scan_counts(vmb_ctx* ctx, const uint32_t* counts, uint64_t n, uint32_t* offsets,
                 unsigned long long* d_total);
+uint64_t scan_onepass_tiles(uint64_t n);  // scan.cu: single-pass scan of the march's chunk totals
+int scan_counts_onepass(vmb_ctx* ctx, const uint32_t* counts, uint64_t n, uint32_t* offsets,
+                        unsigned long long* d_total, unsigned int* ticket, unsigned long long* status);
 // Exclusive scan of u8 flags into u32 positions (compaction), device total at d_total.
 int scan_flags(vmb_ctx* ctx, const uint8_t* flags, uint64_t n, uint32_t* pos,
                unsigned long long* d_total);
