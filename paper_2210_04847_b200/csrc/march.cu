@@ -1073,7 +1073,6 @@ constexpr int kExpandUnroll = VMB_EXPAND_UNROLL;  // rounds per iteration of the
 __host__ __device__ constexpr size_t expand_smem_of(int warps) {
     return size_t(warps) * (kWalkCap * 32 * (2 * sizeof(uint32_t) + sizeof(uint16_t)) + 2 * sizeof(uint64_t));
 }
-constexpr size_t kExpandSmem = expand_smem_of(kExpandWarps);
 // Warps per expansion CTA: the variants that evaluate the field per sample (rays by
 // shuffles, e.g. the Checker) are compute-heavier and run 16 (r2: Checker step
 // 1.44 -> 1.37 ms); constant / copied attributes run kExpandWarps (12).
@@ -1133,7 +1132,7 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
     constexpr int EW = expand_warps(SHADE, CONST, ATTR);
     using AT4 = std::conditional_t<sizeof(AT) == 4, float4, double4>;
     const AT4* attr = static_cast<const AT4*>(kept_attr);
-    // dynamic shared memory (kExpandSmem): per warp, two kept-index row buffers and
+    // dynamic shared memory (expand_smem_of(EW)): per warp, two kept-index row buffers and
     // the owner map of the chunk's output slots (lane | (k << 5), k = rank in the ray)
     extern __shared__ __align__(16) uint32_t expand_smem[];
     uint32_t(*s_idx)[2][kWalkCap * 32] = reinterpret_cast<uint32_t(*)[2][kWalkCap * 32]>(expand_smem);
@@ -1912,7 +1911,7 @@ FwdOut<AT> fwd_out(const ShadeReq& sr) {
 }
 
 // Resident CTAs per SM of one expansion kernel (persistent grid), after opting it
-// in to kExpandSmem of dynamic shared memory — once per kernel (the kernel is the
+// in to its dynamic shared memory — once per kernel (the kernel is the
 // template argument: instantiations share one function type).
 
 template <auto K, size_t SMEM, int W>
