@@ -42,9 +42,9 @@ from paper_2210_04847_b200.pipeline import ResidentPipeline  # noqa: E402
 
 BASELINE_METRIC = "rays/sec & samples/sec (march+render fwd+bwd) at 1/2/4/8 B200; % HBM roofline"
 SCENE = dict(center=(0.5, 0.5, 0.5), radius=0.2, sigma=200.0, rgb=(0.8, 0.25, 0.25))
-# march = k_zero_words + k_march_walk + k_scan_tiles + k_scan_sums + k_scan_add + k_march_expand +
-# k_march_fixup; then k_shade, k_forward, k_zero_words + k_backward_hy + k_backward_long
-KERNELS_PER_STEP = 12
+# march = k_zero_words + k_march_walk + k_scan_onepass + k_march_expand + k_march_fixup; then k_shade,
+# k_forward (not launched when fused), k_zero_words + k_backward_hy + k_backward_long
+KERNELS_PER_STEP = 10
 
 
 def parse():
@@ -185,8 +185,7 @@ class Clocks:
                 "reasons": reasons, "samples": len(sm)}
 
 
-PHASE_KERNELS = {"march": ["k_march_walk", "k_scan_tiles", "k_scan_sums", "k_scan_add",
-                           "k_march_expand", "k_march_fixup"],
+PHASE_KERNELS = {"march": ["k_march_walk", "k_scan_onepass", "k_march_expand", "k_march_fixup"],
                  "shade": ["k_shade"], "render_forward": ["k_forward"],
                  "render_backward": ["k_backward_hy", "k_backward_long"]}
 
