@@ -924,12 +924,9 @@ def main():
     cfg2 = None
     if dist.rank == 0 and dist.world == 1 and args.config2 and args.width == 2048:
         try:  # BASELINE config 2 (NeRF-Synthetic-shaped batch), same step, its own process
-            # 3 streams x 3 sub-batches: the small batch's kernels overlap better (r2 sweep:
-            # 0.176 vs 0.179 ms for 2 x 2, profiles/r2/ab)
             out = subprocess.run([sys.executable, os.path.abspath(__file__), "--width", "512", "--step-size",
                                   repr(math.sqrt(3.0) / 1024), "--steps", str(max(args.steps, 20)), "--warmup",
-                                  str(args.warmup), "--cpu-baseline", "0", "--config2", "0", "--phases", "0",
-                                  "--streams", "3", "--chunks", "3"],
+                                  str(args.warmup), "--cpu-baseline", "0", "--config2", "0", "--phases", "0"],
                                  capture_output=True, text=True, timeout=600)
             c2 = json.loads(out.stdout.strip().splitlines()[-1])
             cfg2 = {k: c2[k] for k in ("value", "unit", "ms_per_step", "samples_per_s")}
