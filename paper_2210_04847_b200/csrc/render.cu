@@ -632,6 +632,7 @@ __global__ void __launch_bounds__(kWarps * 32, VMB_BWD_MINB) k_backward_hy(
     for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n_warps;
          w += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
         const RayRange rr = ray_range(offsets, counts, n_rays, n_samples, w, lane);
+        if (rr.contiguous && rr.s0 == rr.s1) continue;  // no sample in the chunk (half of config 5's)
         const Up u = load_up(dc, dop, ddep, rr.r, rr.valid);
         if (!rr.contiguous) {  // rays not stored one after the other: each by the whole warp
             for (int q = 0; q < 32; ++q) {
