@@ -1240,6 +1240,15 @@ __global__ void VMB_EXPAND_BOUNDS k_march_expand(
 
         const uint64_t r = chunk * 32 + lane;
         const bool valid = r < n_rays;
+        if (!__any_sync(0xffffffffu, cur.cnt != 0u)) {  // no kept sample in the chunk: its offsets only
+            if (valid) offsets[r] = cur.off;
+            mbar_wait(&rbar[buf], (rphase >> buf) & 1u);  // the chunk's (empty) row stage
+            rphase ^= 1u << buf;
+            __syncwarp();
+            cur = nxt;
+            nxt = nn;
+            continue;
+        }
         const uint32_t cnt = cur.cnt;
         uint32_t incl = cnt;  // inclusive warp scan of the counts
 #pragma unroll
